@@ -1,0 +1,185 @@
+/*
+ * dpcuda.h -- the C ABI of the B200 datapipe engine (libdpcuda.so).
+ *
+ * This is the drop-in boundary for the reference's fused
+ * shuffle -> map -> batch -> prefetch path.  The reference
+ * ("datapipe", /root/reference/proj) exposes that path only as a C++ operator
+ * API; it has no C ABI or FFI of its own.  The entry points below are what an
+ * FFI binding of that API would bind, in two layers:
+ *
+ *   1. dp_graph_* / dp_iterator_*  -- the Dataset/Iterator operator API
+ *      (ops::*, Optimize, MakeIterator, GetNext), backed by the C++ host
+ *      engine in paper_2101_12127_b200/csrc/engine/ which lowers the graph
+ *      onto the sm_100a kernels.  Declared in dpcuda_pipeline.h.
+ *   2. dp_k_* (this file)          -- one entry per sm_100a kernel family,
+ *      taking device pointers, sizes and an explicit cudaStream_t (passed as
+ *      void*); asynchronous on that stream.  Used by the engine and by the
+ *      parity tests.
+ *
+ * Conventions:
+ *   - every function returns 0 (DP_OK) or a dp_status; no exception crosses
+ *     the boundary.  dp_last_error() returns a thread-local message.
+ *   - dp_status values 1..19 mirror datapipe::ErrorCode
+ *     (/root/reference/proj/include/datapipe/errors.hpp:25-45) + 1.
+ *   - no hidden allocation on launch paths; callers own device buffers.
+ */
+#ifndef DPCUDA_H_
+#define DPCUDA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  DP_OK = 0,
+  /* datapipe::ErrorCode + 1 (errors.hpp:25-45) */
+  DP_ERR_INVALID_ARITY = 1,
+  DP_ERR_INVALID_ATTR = 2,
+  DP_ERR_TYPE_MISMATCH = 3,
+  DP_ERR_MALFORMED_INPUT = 4,
+  DP_ERR_VALIDATION_FAILED = 5,
+  DP_ERR_DUPLICATE_NAME = 6,
+  DP_ERR_UNKNOWN_UDF = 7,
+  DP_ERR_MISSING_FILE = 8,
+  DP_ERR_UDF_ERROR = 9,
+  DP_ERR_FINGERPRINT_MISMATCH = 10,
+  DP_ERR_VERSION_MISMATCH = 11,
+  DP_ERR_CORRUPT_BLOB = 12,
+  DP_ERR_CONCURRENT_CACHE_FILL = 13,
+  DP_ERR_REWRITE_DIVERGED = 14,
+  DP_ERR_RULE_PRODUCED_INVALID_GRAPH = 15,
+  DP_ERR_DOMAIN_ERROR = 16,
+  DP_ERR_GRID_TOO_LARGE = 17,
+  DP_ERR_PARSE_ERROR = 18,
+  DP_ERR_INTERNAL = 19,
+  /* device-side failures (no reference counterpart) */
+  DP_ERR_CUDA = 100,
+  DP_ERR_OUT_OF_MEMORY = 101,
+  DP_ERR_END_OF_SEQUENCE = 102
+} dp_status;
+
+/* Thread-local message of the last failing call on this thread. */
+const char* dp_last_error(void);
+/* Library version / build string ("libdpcuda sm_100a ..."). */
+const char* dp_build_info(void);
+/* Number of visible CUDA devices (0 when there is no GPU). */
+int dp_device_count(int* count);
+
+/* ---------------------------------------------------------------------- */
+/* K1  range_affine_batch -- FromMemory(IntRange) + Map(x*a+b) + Batch     */
+/*     replaces FromMemoryIterator::Next + MapIterator + BatchIterator /   */
+/*     MapAndBatchIterator (src/runtime.cpp:386-414, 480-535, 579-637,     */
+/*     1467-1721) for an int64 range source.                               */
+/*     out[i] = (first + i) * a + b,  i < rows  (int64, wrap-around).      */
+int dp_k_range_affine_batch(int64_t first, int64_t rows, int64_t a, int64_t b,
+                            int64_t* out, void* stream);
+
+/* ---------------------------------------------------------------------- */
+/* K2  shuffle_plan -- ShuffleIterator (src/runtime.cpp:688-768) with the  */
+/*     PCG32 contract (include/datapipe/random.hpp:39-74).                 */
+/*     Emission order of a windowed reservoir of `buffer_size` over the    */
+/*     input ordinals 0..n-1 seeded with `engine_seed` (= MixSeeds(salt,   */
+/*     seed|0x9d2c5680), runtime.cpp:713-718).  out[k] = in_map[ord_k] if  */
+/*     in_map != NULL else ord_k.  `scratch` must hold min(n,buffer_size)  */
+/*     uint32 when that exceeds the kernel's shared-memory buffer (pass    */
+/*     NULL otherwise; see dp_k_shuffle_plan_scratch_bytes).               */
+size_t dp_k_shuffle_plan_scratch_bytes(uint64_t n, uint64_t buffer_size);
+int dp_k_shuffle_plan(uint64_t n, uint64_t buffer_size, uint64_t engine_seed,
+                      const int64_t* in_map, int64_t* out, void* scratch,
+                      void* stream);
+
+/* ---------------------------------------------------------------------- */
+/* K3  gather + random crop + flip + normalize + batch (one launch per     */
+/*     batch) -- MapAndBatchIterator::WorkerLoop + the crop UDF +          */
+/*     AssembleBatch (src/runtime.cpp:1574-1670, 617-628).                 */
+/*     images: uint8 [num_images, in_h, in_w, 3] (HWC), device resident.   */
+/*     order:  int64 gather positions (NULL = identity); element j of the  */
+/*     batch is images[order[first + j]], its id = that position.          */
+/*     out_ids: int64 [rows]; out: fp32 [rows, crop_h, crop_w, 3].         */
+/*     Crop offsets / flip: Philox4x32-10(key = udf_seed, ctr = id).       */
+/*     normalize: (x - mean[c]) / std[c] rounded as IEEE fp32 division.    */
+int dp_k_crop_flip_normalize_batch(const uint8_t* images, int64_t num_images,
+                                   int in_h, int in_w, const int64_t* order,
+                                   int64_t first, int64_t rows,
+                                   uint64_t udf_seed, int crop_h, int crop_w,
+                                   int do_flip, const float mean[3],
+                                   const float stdv[3], int64_t* out_ids,
+                                   float* out, void* stream);
+
+/* K4  gather + bilinear resize (half-pixel centres, edge clamp) +         */
+/*     normalize + batch.  Same layout conventions as K3.                  */
+int dp_k_resize_normalize_batch(const uint8_t* images, int64_t num_images,
+                                int in_h, int in_w, const int64_t* order,
+                                int64_t first, int64_t rows, int out_h,
+                                int out_w, const float mean[3],
+                                const float stdv[3], int64_t* out_ids,
+                                float* out, void* stream);
+
+/* ---------------------------------------------------------------------- */
+/* K5  filter(len <= max_keep) stream compaction + padded_batch.           */
+/*     FilterIterator (src/runtime.cpp:537-577) + BatchIterator on ragged  */
+/*     lists (579-637); padded_batch is a new kind.   */
+/*     kept: int64 [n] out (stable order), *num_kept written to device     */
+/*     memory `num_kept_dev` (int64).  scratch: dp_k_filter_scratch_bytes. */
+size_t dp_k_filter_scratch_bytes(int64_t n);
+int dp_k_filter_len_le(const int32_t* lengths, int64_t n, int32_t max_keep,
+                       const int64_t* in_map, int64_t* kept,
+                       int64_t* num_kept_dev, void* scratch, void* stream);
+/* Per-batch max row length: lmax[j] = max over the rows of batch j of     */
+/* lengths[kept[j*batch + r]]  (rows of the last batch may be fewer).      */
+int dp_k_batch_max_len(const int32_t* lengths, const int64_t* kept,
+                       int64_t num_kept, int64_t batch, int32_t* lmax,
+                       void* stream);
+/* One padded batch: out[r, 0:lmax] = tokens of row r then pad_value;      */
+/* out_lengths[r] = its length.  rows <= batch.                            */
+int dp_k_padded_batch(const int32_t* tokens, const int64_t* offsets,
+                      const int32_t* lengths, const int64_t* kept,
+                      int64_t first, int64_t rows, int32_t lmax,
+                      int32_t pad_value, int32_t* out, int32_t* out_lengths,
+                      void* stream);
+
+/* ---------------------------------------------------------------------- */
+/* K6  shard + interleave index mapping -- ShardIterator (runtime.cpp:     */
+/*     770-800) + (Parallel)InterleaveIterator (1044-1128, 1727-2021) over */
+/*     equal-length readers.  Inputs are the source ordinals p < n_sources */
+/*     with p % num_shards == shard_index; each opens a reader of          */
+/*     `records` elements valued p * records + r; cycle = cycle_length.    */
+/*     out: int64 [count] where count = dp_k_shard_interleave_count(...).  */
+int64_t dp_k_shard_interleave_count(int64_t n_sources, int64_t num_shards,
+                                    int64_t shard_index, int64_t records);
+int dp_k_shard_interleave_index(int64_t n_sources, int64_t num_shards,
+                                int64_t shard_index, int64_t cycle,
+                                int64_t records, int64_t* out, void* stream);
+/* Shard alone: out[i] = shard_index + i * num_shards (or in_map of it). */
+int dp_k_shard_index(int64_t n, int64_t num_shards, int64_t shard_index,
+                     const int64_t* in_map, int64_t* out, void* stream);
+
+/* ---------------------------------------------------------------------- */
+/* K7  order digest (the multi-GPU "final ordering check") */
+/*     position-keyed, parallel: D = sum_i SplitMix64Next(v_i ^ (i *      */
+/*     0x9e3779b97f4a7c15)) mod 2^64 (state passed by value).  Accumulates */
+/*     into *digest_dev (uint64) for positions first..first+n-1.           */
+int dp_k_order_digest(const int64_t* values, int64_t n, int64_t first,
+                      uint64_t* digest_dev, void* stream);
+/* Same over raw 32-bit words (fp32 batch payloads, bit-exact check). */
+int dp_k_word_digest(const uint32_t* words, int64_t n, int64_t first,
+                     uint64_t* digest_dev, void* stream);
+
+/* ---------------------------------------------------------------------- */
+/* Synthetic inputs (same generators as oracle/restate.c). */
+/* images[i, off] = top byte of SplitMix64Next(seed ^ ((first_id + i) *    */
+/* image_bytes + off)).                                                    */
+int dp_k_synth_images(uint8_t* images, uint64_t first_id, uint64_t count,
+                      uint64_t image_bytes, uint64_t seed, void* stream);
+/* tokens[offsets[i] + j] = SplitMix64Next(seed ^ (i << 20 | j)) & 0x7fffffff */
+int dp_k_synth_tokens(int32_t* tokens, const int64_t* offsets, int64_t n,
+                      uint64_t seed, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DPCUDA_H_ */

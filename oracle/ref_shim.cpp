@@ -1,0 +1,392 @@
+// oracle/ref_shim.cpp -- extern "C" driver over the COMPILED REFERENCE.
+//
+// TEST INFRASTRUCTURE ONLY.  Built by oracle/Makefile together with the
+// reference's own sources (compiled in place from /root/reference/proj/src,
+// never copied) into oracle/_ref/libdpref.so.  Used by tests/ to pin the
+// oracle restatement (oracle/restate.c) and to generate tests/golden/, and by
+// bench.py --impl reference / cpu_baseline as the reference CPU pipeline.
+//
+// Every pipeline here is built through the reference's public operator API
+// (datapipe::ops::*, include/datapipe/graph.hpp:134-165), optimized with
+// datapipe::Optimize (include/datapipe/optimizer.hpp:73-75) and drained
+// through MakeIterator / PipelineIterator::GetNext
+// (include/datapipe/runtime.hpp:68,98-100) with seed_override set (SURVEY.md
+// 0.3 #5).  The map UDFs are the oracle restatement registered through
+// UdfRegistry::RegisterMap (include/datapipe/udf.hpp:61-63).
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "datapipe/element.hpp"
+#include "datapipe/errors.hpp"
+#include "datapipe/graph.hpp"
+#include "datapipe/optimizer.hpp"
+#include "datapipe/runtime.hpp"
+#include "datapipe/udf.hpp"
+#include "restate.h"
+
+using namespace datapipe;
+
+namespace {
+
+thread_local std::string g_err;
+
+int Fail(const std::exception& e) {
+  g_err = e.what();
+  return -1;
+}
+
+std::vector<Element> IntRange(int64_t n) {
+  std::vector<Element> out;
+  out.reserve(static_cast<size_t>(n));
+  for (int64_t i = 0; i < n; ++i) out.push_back(Element::Scalar(Value::Int64(i)));
+  return out;
+}
+
+IteratorOptions Seeded(uint64_t base_seed) {
+  IteratorOptions o;
+  o.deterministic = true;
+  o.seed_override = base_seed;
+  return o;
+}
+
+void RegisterAffine(UdfRegistry& reg, const std::string& name, int64_t a,
+                    int64_t b) {
+  if (reg.Contains(name)) return;
+  reg.RegisterMap(name, [a, b](const Element& e) {
+    return Element::Scalar(Value::Int64(e.component(0).int64() * a + b));
+  });
+}
+
+struct ImageUdfParams {
+  int mode;  // 0 crop+flip+normalize, 1 resize+normalize, 2 crop+normalize
+  int in_h, in_w, out_h, out_w;
+  uint64_t udf_seed;
+};
+
+std::string ImageUdfName(const ImageUdfParams& p) {
+  return "img_udf(mode=" + std::to_string(p.mode) + ",in=" +
+         std::to_string(p.in_h) + "x" + std::to_string(p.in_w) + ",out=" +
+         std::to_string(p.out_h) + "x" + std::to_string(p.out_w) + ",seed=" +
+         std::to_string(p.udf_seed) + ")";
+}
+
+// (int64 id, bytes uint8 HWC) -> (int64 id, bytes fp32 HWC little endian).
+void RegisterImageUdf(UdfRegistry& reg, const ImageUdfParams& p) {
+  std::string name = ImageUdfName(p);
+  if (reg.Contains(name)) return;
+  reg.RegisterMap(name, [p](const Element& e) {
+    int64_t id = e.component(0).int64();
+    const std::string& img = e.component(1).bytes();
+    std::string out(static_cast<size_t>(p.out_h) * p.out_w * 3 * sizeof(float),
+                    '\0');
+    float* o = reinterpret_cast<float*>(out.data());
+    const uint8_t* in = reinterpret_cast<const uint8_t*>(img.data());
+    if (p.mode == 1) {
+      orc_resize_normalize(in, p.in_h, p.in_w, p.out_h, p.out_w, o);
+    } else {
+      orc_crop_flip_normalize(in, p.in_h, p.in_w, id, p.udf_seed, p.out_h,
+                              p.out_w, p.mode == 0 ? 1 : 0, o);
+    }
+    std::vector<Value> c;
+    c.push_back(Value::Int64(id));
+    c.push_back(Value::Bytes(std::move(out)));
+    return Element(std::move(c));
+  });
+}
+
+std::vector<Element> SynthImages(int64_t n, int h, int w, uint64_t pix_seed) {
+  std::vector<Element> out;
+  out.reserve(static_cast<size_t>(n));
+  size_t bytes = static_cast<size_t>(h) * w * 3;
+  std::string buf(bytes, '\0');
+  for (int64_t i = 0; i < n; ++i) {
+    orc_synth_images(pix_seed, static_cast<uint64_t>(i), 1, bytes,
+                     reinterpret_cast<uint8_t*>(buf.data()));
+    std::vector<Value> c;
+    c.push_back(Value::Int64(i));
+    c.push_back(Value::Bytes(buf));
+    out.push_back(Element(std::move(c)));
+  }
+  return out;
+}
+
+struct ImagePipelineArgs {
+  ImageUdfParams udf;
+  int64_t n;
+  int64_t shard_k, shard_g;    // shard_k 0 => no shard
+  int64_t shuffle_buffer;      // 0 => no shuffle
+  int has_shuffle_seed;
+  uint64_t shuffle_seed;
+  int64_t batch;
+  int drop_remainder;
+  int64_t parallel;            // num_parallel_calls of the map
+  int64_t prefetch;            // 0 => none; -1 AUTOTUNE
+  uint64_t pix_seed;
+};
+
+DatasetGraph BuildImageGraph(UdfRegistry& reg, const ImagePipelineArgs& a,
+                             std::vector<Element> elements) {
+  RegisterImageUdf(reg, a.udf);
+  DatasetGraph g = ops::FromMemory(std::move(elements), reg);
+  if (a.shard_k > 0) g = ops::Shard(g, a.shard_k, a.shard_g, reg);
+  if (a.shuffle_buffer > 0) {
+    std::optional<uint64_t> seed;
+    if (a.has_shuffle_seed) seed = a.shuffle_seed;
+    g = ops::Shuffle(g, a.shuffle_buffer, seed, reg);
+  }
+  g = ops::Map(g, ImageUdfName(a.udf), a.parallel, reg);
+  g = ops::Batch(g, a.batch, a.drop_remainder != 0, reg);
+  if (a.prefetch != 0) g = ops::Prefetch(g, a.prefetch, reg);
+  auto [opt, report] = Optimize(g, RuleSet::Default(), reg);
+  return opt;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error(void) { return g_err.c_str(); }
+
+// cfg1: from_memory(IntRange(n)) -> map(x*a+b, p) -> batch(b) [-> Optimize].
+// out_values[n] (flattened batches), out_batch_sizes[], *num_batches; writes
+// the root node kind after Optimize into root_kind (>= 32 bytes).
+int ref_range_map_batch(int64_t n, int64_t a, int64_t b, int64_t batch,
+                        int drop_remainder, int64_t parallel, int optimize,
+                        uint64_t base_seed, int64_t* out_values,
+                        int64_t* out_batch_sizes, int64_t* num_batches,
+                        char* root_kind) {
+  try {
+    UdfRegistry reg;
+    std::string udf = "affine(" + std::to_string(a) + "," + std::to_string(b) + ")";
+    RegisterAffine(reg, udf, a, b);
+    DatasetGraph g = ops::FromMemory(IntRange(n), reg);
+    g = ops::Map(g, udf, parallel, reg);
+    g = ops::Batch(g, batch, drop_remainder != 0, reg);
+    if (optimize) g = Optimize(g, RuleSet::Default(), reg).first;
+    std::snprintf(root_kind, 32, "%s", NodeKindName(g.root()->kind()));
+    auto it = MakeIterator(g, reg, Seeded(base_seed));
+    int64_t k = 0, nb = 0;
+    while (auto e = it->GetNext()) {
+      const auto& items = e->component(0).items();
+      for (const auto& v : items) out_values[k++] = v.int64();
+      out_batch_sizes[nb++] = static_cast<int64_t>(items.size());
+    }
+    *num_batches = nb;
+    return 0;
+  } catch (const std::exception& e) {
+    return Fail(e);
+  }
+}
+
+// from_memory(IntRange(n)) [-> shard(k, g)] -> shuffle(buffer, seed) [->
+// repeat(epochs)]; writes the emitted values (input ordinals) to out.
+int ref_shuffle_ids(int64_t n, int64_t shard_k, int64_t shard_g,
+                    int64_t buffer, int has_seed, uint64_t seed,
+                    uint64_t base_seed, int64_t epochs, int optimize,
+                    int64_t* out, int64_t* count) {
+  try {
+    UdfRegistry reg;
+    DatasetGraph g = ops::FromMemory(IntRange(n), reg);
+    if (shard_k > 0) g = ops::Shard(g, shard_k, shard_g, reg);
+    std::optional<uint64_t> s;
+    if (has_seed) s = seed;
+    g = ops::Shuffle(g, buffer, s, reg);
+    if (epochs > 1) g = ops::Repeat(g, epochs, reg);
+    if (optimize) g = Optimize(g, RuleSet::Default(), reg).first;
+    auto it = MakeIterator(g, reg, Seeded(base_seed));
+    int64_t k = 0;
+    while (auto e = it->GetNext()) out[k++] = e->component(0).int64();
+    *count = k;
+    return 0;
+  } catch (const std::exception& e) {
+    return Fail(e);
+  }
+}
+
+// Image pipelines (cfg2 / cfg3 shapes) at parity sizes.  Outputs the batch
+// ids (int64), the fp32 pixels (out_h*out_w*3 per image) and batch sizes.
+int ref_image_pipeline(int mode, int in_h, int in_w, int out_h, int out_w,
+                       uint64_t udf_seed, uint64_t pix_seed, int64_t n,
+                       int64_t shard_k, int64_t shard_g, int64_t shuffle_buffer,
+                       int has_shuffle_seed, uint64_t shuffle_seed,
+                       int64_t batch, int drop_remainder, int64_t parallel,
+                       int64_t prefetch, uint64_t base_seed, int64_t* out_ids,
+                       float* out_pixels, int64_t* out_batch_sizes,
+                       int64_t* num_batches) {
+  try {
+    UdfRegistry reg;
+    ImagePipelineArgs a{{mode, in_h, in_w, out_h, out_w, udf_seed},
+                        n, shard_k, shard_g, shuffle_buffer, has_shuffle_seed,
+                        shuffle_seed, batch, drop_remainder, parallel,
+                        prefetch, pix_seed};
+    DatasetGraph g = BuildImageGraph(reg, a, SynthImages(n, in_h, in_w, pix_seed));
+    auto it = MakeIterator(g, reg, Seeded(base_seed));
+    size_t per = static_cast<size_t>(out_h) * out_w * 3;
+    int64_t k = 0, nb = 0;
+    while (auto e = it->GetNext()) {
+      const auto& ids = e->component(0).items();
+      const auto& imgs = e->component(1).items();
+      for (size_t i = 0; i < ids.size(); ++i, ++k) {
+        out_ids[k] = ids[i].int64();
+        std::memcpy(out_pixels + static_cast<size_t>(k) * per,
+                    imgs[i].bytes().data(), per * sizeof(float));
+      }
+      out_batch_sizes[nb++] = static_cast<int64_t>(ids.size());
+    }
+    *num_batches = nb;
+    return 0;
+  } catch (const std::exception& e) {
+    return Fail(e);
+  }
+}
+
+// cfg4 at parity sizes: from_memory(list[int64] token sequences) ->
+// filter(len <= max_keep) -> batch(b) (ragged, the reference has no
+// padded_batch).  Outputs per emitted row its length
+// and tokens (concatenated), and the batch sizes.
+int ref_filter_batch_tokens(int64_t n, uint64_t len_seed, uint32_t max_len,
+                            uint64_t tok_seed, int32_t max_keep, int64_t batch,
+                            int drop_remainder, int64_t* out_row_lengths,
+                            int64_t* out_tokens, int64_t* out_batch_sizes,
+                            int64_t* num_batches, int64_t* num_rows,
+                            int64_t* num_tokens) {
+  try {
+    UdfRegistry reg;
+    std::string pred = "len_le(" + std::to_string(max_keep) + ")";
+    reg.RegisterPredicate(pred, [max_keep](const Element& e) {
+      return static_cast<int64_t>(e.component(0).items().size()) <= max_keep;
+    });
+    std::vector<int32_t> lens(static_cast<size_t>(n));
+    orc_synth_lengths(len_seed, max_len, static_cast<uint64_t>(n), lens.data());
+    std::vector<Element> elems;
+    elems.reserve(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) {
+      std::vector<Value> toks;
+      toks.reserve(static_cast<size_t>(lens[i]));
+      for (int32_t j = 0; j < lens[i]; ++j)
+        toks.push_back(Value::Int64(orc_synth_token(tok_seed, i, j)));
+      elems.push_back(Element::Scalar(Value::List(std::move(toks))));
+    }
+    DatasetGraph g = ops::FromMemory(std::move(elems), reg);
+    g = ops::Filter(g, pred, reg);
+    g = ops::Batch(g, batch, drop_remainder != 0, reg);
+    g = Optimize(g, RuleSet::Default(), reg).first;
+    auto it = MakeIterator(g, reg, Seeded(1));
+    int64_t nb = 0, nr = 0, nt = 0;
+    while (auto e = it->GetNext()) {
+      const auto& rows = e->component(0).items();
+      for (const auto& row : rows) {
+        out_row_lengths[nr++] = static_cast<int64_t>(row.items().size());
+        for (const auto& t : row.items()) out_tokens[nt++] = t.int64();
+      }
+      out_batch_sizes[nb++] = static_cast<int64_t>(rows.size());
+    }
+    *num_batches = nb;
+    *num_rows = nr;
+    *num_tokens = nt;
+    return 0;
+  } catch (const std::exception& e) {
+    return Fail(e);
+  }
+}
+
+// cfg5 index stage: from_memory(shard ids 0..S-1) -> shard(k, g) ->
+// interleave(reader of R records valued id*R + r, cycle, parallel) [->
+// shuffle(buffer, seed)].  Emits the record values.
+int ref_interleave_ids(int64_t num_sources, int64_t shard_k, int64_t shard_g,
+                       int64_t cycle, int64_t parallel, int64_t records,
+                       int64_t shuffle_buffer, uint64_t shuffle_seed,
+                       uint64_t base_seed, int64_t* out, int64_t* count) {
+  try {
+    UdfRegistry reg;
+    std::string udf = "reader(" + std::to_string(records) + ")";
+    reg.RegisterDataset(
+        udf,
+        [&reg, records](const Element& e) {
+          int64_t s = e.component(0).int64();
+          std::vector<Element> recs;
+          for (int64_t r = 0; r < records; ++r)
+            recs.push_back(Element::Scalar(Value::Int64(s * records + r)));
+          return ops::FromMemory(std::move(recs), reg);
+        },
+        ElementSpec({TypeSpec::Int64()}));
+    DatasetGraph g = ops::FromMemory(IntRange(num_sources), reg);
+    if (shard_k > 0) g = ops::Shard(g, shard_k, shard_g, reg);
+    g = ops::Interleave(g, udf, cycle, parallel, reg);
+    if (shuffle_buffer > 0) g = ops::Shuffle(g, shuffle_buffer, shuffle_seed, reg);
+    auto it = MakeIterator(g, reg, Seeded(base_seed));
+    int64_t k = 0;
+    while (auto e = it->GetNext()) out[k++] = e->component(0).int64();
+    *count = k;
+    return 0;
+  } catch (const std::exception& e) {
+    return Fail(e);
+  }
+}
+
+// CPU baseline timing (bench::Run methodology, src/bench.cpp:192-249): the
+// image pipeline over `n` resident synthetic images with map parallelism
+// `parallel`, optimized to map_and_batch, prefetch(prefetch).  One warm-up
+// epoch is discarded; each measured epoch is a fresh iterator drained to EOF.
+// Writes the per-epoch wall seconds into epoch_s[epochs].
+int ref_time_image_pipeline(int mode, int in_h, int in_w, int out_h, int out_w,
+                            uint64_t udf_seed, uint64_t pix_seed, int64_t n,
+                            int64_t shuffle_buffer, uint64_t shuffle_seed,
+                            int64_t batch, int64_t parallel, int64_t prefetch,
+                            uint64_t base_seed, int epochs, double* epoch_s,
+                            int64_t* elements_per_epoch) {
+  try {
+    UdfRegistry reg;
+    ImagePipelineArgs a{{mode, in_h, in_w, out_h, out_w, udf_seed},
+                        n, 0, 0, shuffle_buffer, 1, shuffle_seed, batch, 0,
+                        parallel, prefetch, pix_seed};
+    DatasetGraph g = BuildImageGraph(reg, a, SynthImages(n, in_h, in_w, pix_seed));
+    for (int ep = 0; ep <= epochs; ++ep) {
+      auto it = MakeIterator(g, reg, Seeded(base_seed));
+      auto t0 = std::chrono::steady_clock::now();
+      int64_t count = 0;
+      while (auto e = it->GetNext()) count += static_cast<int64_t>(e->component(0).items().size());
+      double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      if (ep > 0) epoch_s[ep - 1] = s;
+      *elements_per_epoch = count;
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    return Fail(e);
+  }
+}
+
+// CPU baseline for cfg1 (range -> map -> batch, optimized).
+int ref_time_range_map_batch(int64_t n, int64_t batch, int64_t parallel,
+                             int epochs, double* epoch_s) {
+  try {
+    UdfRegistry reg;
+    RegisterAffine(reg, "affine(3,1)", 3, 1);
+    DatasetGraph g = ops::FromMemory(IntRange(n), reg);
+    g = ops::Map(g, "affine(3,1)", parallel, reg);
+    g = ops::Batch(g, batch, false, reg);
+    g = Optimize(g, RuleSet::Default(), reg).first;
+    for (int ep = 0; ep <= epochs; ++ep) {
+      auto it = MakeIterator(g, reg, Seeded(1));
+      auto t0 = std::chrono::steady_clock::now();
+      while (auto e = it->GetNext()) {
+      }
+      double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      if (ep > 0) epoch_s[ep - 1] = s;
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    return Fail(e);
+  }
+}
+
+int ref_hardware_concurrency(void) {
+  return static_cast<int>(std::thread::hardware_concurrency());
+}
+
+}  // extern "C"

@@ -1,0 +1,114 @@
+/*
+ * oracle/restate.h -- CPU restatement of the reference's hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Nothing in the product (paper_2101_12127_b200/,
+ * include/) links, loads or calls this code.  Only tests/, the smoke() check
+ * in __graft_entry__.py and bench.py's cpu_baseline / --impl reference leg use
+ * it, and only as the checker or the reported CPU baseline.
+ *
+ * Two parity levels:
+ *  1. ordering / batching / filtering / sharding (integer, bit exact): a plain
+ *     C restatement of the reference runtime, pinned against the compiled
+ *     reference (oracle/_ref, oracle/ref_shim.cpp) and against the known
+ *     answers in SURVEY.md Appendix A (tests/golden/).
+ *  2. map-UDF arithmetic (crop / flip / resize / normalize): the reference has
+ *     no image UDFs, so this file DEFINES them.  The same C
+ *     functions are registered into the reference's UdfRegistry by
+ *     oracle/ref_shim.cpp, so the compiled reference pipeline and this
+ *     restatement agree by construction on the arithmetic; the order in which
+ *     elements reach the UDF is what the reference pins.
+ *
+ * Compiled with -O2 -ffp-contract=off and no -march (matches the reference's
+ * Release flags, /root/reference/proj/CMakeLists.txt:7-9): every fp32 op is
+ * individually rounded, no FMA contraction.
+ */
+#ifndef DP_ORACLE_RESTATE_H_
+#define DP_ORACLE_RESTATE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- PRNG contract: /root/reference/proj/include/datapipe/random.hpp ---- */
+uint64_t orc_splitmix64_next(uint64_t* state);           /* random.hpp:24-29 */
+uint64_t orc_mix_seeds(uint64_t a, uint64_t b);          /* random.hpp:31-34 */
+typedef struct { uint64_t state; } orc_pcg32;
+void orc_pcg32_init(orc_pcg32* g, uint64_t seed);        /* random.hpp:41-46 */
+uint32_t orc_pcg32_next(orc_pcg32* g);                   /* random.hpp:48-54 */
+uint32_t orc_pcg32_bounded(orc_pcg32* g, uint32_t bound);/* random.hpp:57-63 */
+
+/* ShuffleIterator::DeriveSeed, runtime.cpp:713-718: attr seed absent -> the
+ * constant 0x9d2c5680. */
+uint64_t orc_shuffle_seed(uint64_t epoch_salt, int has_attr_seed,
+                          uint64_t attr_seed);
+
+/* ShuffleIterator::Next, runtime.cpp:721-747 (and ReferenceEval
+ * reference.cpp:47-73): windowed reservoir over the input ordinals 0..n-1.
+ * out[k] = input ordinal emitted at step k.  n, buffer >= 1. */
+void orc_shuffle_order(uint64_t n, uint64_t buffer_size, uint64_t engine_seed,
+                       uint32_t* out);
+
+/* ---- digest ---- */
+uint64_t orc_digest_init(void);
+uint64_t orc_digest_i64(uint64_t h, const int64_t* v, size_t n);
+uint64_t orc_digest_u32(uint64_t h, const uint32_t* v, size_t n);
+
+/* ---- synthetic inputs ---- */
+/* pixel byte `off` of image `id` (image of `image_bytes` bytes): top byte of
+ * SplitMix64Next(seed ^ (id * image_bytes + off)). */
+uint8_t orc_synth_pixel(uint64_t seed, uint64_t id, uint64_t image_bytes,
+                        uint64_t off);
+void orc_synth_images(uint64_t seed, uint64_t first_id, uint64_t count,
+                      uint64_t image_bytes, uint8_t* out);
+/* token sequences: len_i = Pcg32(len_seed).Bounded(max_len) + 1 drawn in
+ * order; token (i, j) = SplitMix64Next(tok_seed ^ (i << 20 | j)) & 0x7fffffff. */
+void orc_synth_lengths(uint64_t len_seed, uint32_t max_len, uint64_t n,
+                       int32_t* lengths);
+int32_t orc_synth_token(uint64_t tok_seed, uint64_t i, uint64_t j);
+
+/* ---- Philox4x32-10 (Salmon et al. 2011); the crop/flip randomness
+ * contract of this build: key = udf seed, counter =
+ * element id. ---- */
+void orc_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2],
+                       uint32_t out[4]);
+void orc_crop_params(uint64_t seed, int64_t id, int in_h, int in_w, int crop_h,
+                     int crop_w, int* oy, int* ox, int* flip);
+
+/* ---- map UDF arithmetic ---- */
+extern const float ORC_MEAN[3];
+extern const float ORC_STD[3];
+/* random crop (crop_h x crop_w at Philox offsets) + optional horizontal flip
+ * + per-channel normalize (x - M_c) / S_c, HWC fp32 out.  `do_flip` = 0
+ * disables the flip draw (crop only). */
+void orc_crop_flip_normalize(const uint8_t* img, int in_h, int in_w,
+                             int64_t id, uint64_t seed, int crop_h, int crop_w,
+                             int do_flip, float* out);
+/* bilinear resize (half-pixel centres, edge clamp) + normalize. */
+void orc_resize_normalize(const uint8_t* img, int in_h, int in_w, int out_h,
+                          int out_w, float* out);
+float orc_normalize(float v, int c);
+
+/* ---- filter + padded batch (cfg4) ---- */
+/* Stable compaction of the positions with lengths[i] <= max_keep.  Returns
+ * the kept count; kept[] gets the source positions in order. */
+uint64_t orc_filter_len_le(const int32_t* lengths, uint64_t n,
+                           int32_t max_keep, uint32_t* kept);
+
+/* ---- shard / interleave index mapping (cfg3/cfg5) ---- */
+/* ShardIterator, runtime.cpp:785-792: positions p with p % k == g. */
+uint64_t orc_shard_positions(uint64_t n, uint64_t k, uint64_t g,
+                             uint64_t* out);
+/* InterleaveIterator (cycle c) over M inputs, each opening a reader of L
+ * records (input m, record r) -> m * L + r.  runtime.cpp:1061-1120. */
+uint64_t orc_interleave_order(uint64_t m_inputs, const uint64_t* inputs,
+                              uint64_t cycle, uint64_t records,
+                              uint64_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DP_ORACLE_RESTATE_H_ */

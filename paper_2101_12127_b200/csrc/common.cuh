@@ -1,0 +1,165 @@
+// common.cuh -- device-side contracts shared by every sm_100a kernel.
+//
+// The integer contracts are the reference's (bit-identical):
+//   SplitMix64Next / MixSeeds / Pcg32  -- /root/reference/proj/include/
+//                                         datapipe/random.hpp:24-74
+// plus an O(log k) LCG jump-ahead so many lanes can draw one PCG stream in
+// parallel, and Philox4x32-10 for this build's crop/flip randomness (the
+// reference defines no image UDFs).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace dpk {
+
+constexpr uint64_t kPcgMult = 6364136223846793005ULL;
+constexpr uint64_t kPcgInc = 1442695040888963407ULL;  // random.hpp:72
+
+__host__ __device__ __forceinline__ uint64_t splitmix64_next(uint64_t& s) {
+  uint64_t z = (s += 0x9e3779b97f4a7c15ULL);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+__host__ __device__ __forceinline__ uint64_t mix_seeds(uint64_t a, uint64_t b) {
+  uint64_t s = a ^ (b + 0x9e3779b97f4a7c15ULL + (a << 6) + (a >> 2));
+  return splitmix64_next(s);
+}
+
+// PCG-XSH-RR output function of the pre-advance state (random.hpp:48-54).
+__host__ __device__ __forceinline__ uint32_t pcg_output(uint64_t old) {
+  uint32_t xorshifted = static_cast<uint32_t>(((old >> 18u) ^ old) >> 27u);
+  uint32_t rot = static_cast<uint32_t>(old >> 59u);
+  return (xorshifted >> rot) | (xorshifted << ((-rot) & 31u));
+}
+
+__host__ __device__ __forceinline__ uint64_t pcg_step(uint64_t s) {
+  return s * kPcgMult + kPcgInc;
+}
+
+// State after Pcg32(seed) construction (random.hpp:41-46).
+__host__ __device__ __forceinline__ uint64_t pcg_seeded_state(uint64_t seed) {
+  uint64_t s = pcg_step(0);
+  s += seed;
+  return pcg_step(s);
+}
+
+// Affine map of k LCG steps: s_k = mult * s + plus (Brown, "Random number
+// generation with arbitrary strides", 1994).
+struct LcgJump {
+  uint64_t mult, plus;
+};
+
+__host__ __device__ __forceinline__ LcgJump lcg_jump(uint64_t k) {
+  uint64_t acc_mult = 1, acc_plus = 0;
+  uint64_t cur_mult = kPcgMult, cur_plus = kPcgInc;
+  while (k) {
+    if (k & 1) {
+      acc_mult *= cur_mult;
+      acc_plus = acc_plus * cur_mult + cur_plus;
+    }
+    cur_plus = (cur_mult + 1) * cur_plus;
+    cur_mult *= cur_mult;
+    k >>= 1;
+  }
+  return {acc_mult, acc_plus};
+}
+
+__host__ __device__ __forceinline__ uint64_t lcg_apply(LcgJump j, uint64_t s) {
+  return j.mult * s + j.plus;
+}
+
+// Philox4x32-10 (Salmon et al., SC'11).
+__host__ __device__ __forceinline__ void philox4x32_10(uint32_t c0, uint32_t c1,
+                                                       uint32_t c2, uint32_t c3,
+                                                       uint32_t k0, uint32_t k1,
+                                                       uint32_t out[4]) {
+#pragma unroll
+  for (int round = 0; round < 10; ++round) {
+#ifdef __CUDA_ARCH__
+    uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+    uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+#else
+    uint64_t p0 = static_cast<uint64_t>(0xD2511F53u) * c0;
+    uint64_t p1 = static_cast<uint64_t>(0xCD9E8D57u) * c2;
+    uint32_t hi0 = static_cast<uint32_t>(p0 >> 32), lo0 = static_cast<uint32_t>(p0);
+    uint32_t hi1 = static_cast<uint32_t>(p1 >> 32), lo1 = static_cast<uint32_t>(p1);
+#endif
+    uint32_t n0 = hi1 ^ c1 ^ k0;
+    uint32_t n2 = hi0 ^ c3 ^ k1;
+    c0 = n0;
+    c1 = lo1;
+    c2 = n2;
+    c3 = lo0;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  out[0] = c0;
+  out[1] = c1;
+  out[2] = c2;
+  out[3] = c3;
+}
+
+// Crop offsets and flip bit for element `id` (key = udf seed, ctr = id).
+struct CropParams {
+  int oy, ox, flip;
+};
+
+__host__ __device__ __forceinline__ CropParams crop_params(uint64_t seed, int64_t id,
+                                                           int in_h, int in_w,
+                                                           int crop_h, int crop_w) {
+  uint32_t r[4];
+  uint64_t uid = static_cast<uint64_t>(id);
+  philox4x32_10(static_cast<uint32_t>(uid), static_cast<uint32_t>(uid >> 32), 0u, 0u,
+                static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32), r);
+  CropParams p;
+  p.oy = static_cast<int>(r[0] % static_cast<uint32_t>(in_h - crop_h + 1));
+  p.ox = static_cast<int>(r[1] % static_cast<uint32_t>(in_w - crop_w + 1));
+  p.flip = static_cast<int>(r[2] & 1u);
+  return p;
+}
+
+// Per-channel normalize constants; `rcp` = RN(1 / std) for the exact
+// division sequence below.
+struct NormConsts {
+  float mean[3];
+  float stdv[3];
+  float rcp[3];
+};
+
+#ifdef __CUDACC__
+// (v - mean) / std rounded exactly as IEEE fp32 division for every v that is
+// an integer in [0, 255] (uint8 pixel): one rounded subtract, then the
+// Markstein correction q' = RN(q + RN(d - q*s) * r) from q = RN(d * r).
+// tests/test_oracle.py::test_fast_division_exhaustive proves it against
+// IEEE division over all 3 x 256 inputs.
+__device__ __forceinline__ float normalize_u8(float v, float mean, float s, float r) {
+  float d = __fsub_rn(v, mean);
+  float q = __fmul_rn(d, r);
+  float rem = __fmaf_rn(-q, s, d);
+  return __fmaf_rn(rem, r, q);
+}
+
+// General fp32 input (resize output): plain IEEE division.
+__device__ __forceinline__ float normalize_f32(float v, float mean, float s) {
+  return __fdiv_rn(__fsub_rn(v, mean), s);
+}
+
+__device__ __forceinline__ void st_cs_f4(float4* p, float4 v) {
+  asm volatile("st.global.cs.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x),
+               "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+
+__device__ __forceinline__ uint4 ld_nc_na_u4(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+#endif
+
+}  // namespace dpk

@@ -1,0 +1,211 @@
+// k_tokens.cu -- K5: Filter(len <= max_keep) as warp-ballot stream
+// compaction + PaddedBatch.
+//
+// Filter: FilterIterator (/root/reference/proj/src/runtime.cpp:537-577)
+// keeps element i iff pred(i) and preserves order.  Here the predicate is the
+// length test, evaluated on the int32 length array only; the kept positions
+// are produced by a three-kernel stable compaction (per-tile counts with
+// __ballot_sync/__popc, one-CTA exclusive scan over tiles, per-tile scatter
+// at the scanned offsets), so the result is order-preserving and bit exact.
+// PaddedBatch (new kind): each batch of `batch` kept rows
+// is padded to its own max length; the valid prefix of every row equals the
+// reference's ragged Batch output.
+#include <cstdint>
+
+#include "common.cuh"
+#include "status.hpp"
+
+namespace dpk {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kItems = 16;  // consecutive elements per thread
+constexpr int kTile = kThreads * kItems;
+constexpr uint32_t kFull = 0xffffffffu;
+
+__device__ __forceinline__ int block_exclusive_scan(int v, int* warp_sums, int* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(kFull, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_sums[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int w = lane < kThreads / 32 ? warp_sums[lane] : 0;
+    int z = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(kFull, z, o);
+      if (lane >= o) z += y;
+    }
+    if (lane < kThreads / 32) warp_sums[lane] = z - w;
+    if (lane == kThreads / 32 - 1) *total = z;
+  }
+  __syncthreads();
+  return x - v + warp_sums[warp];
+}
+
+__device__ __forceinline__ int thread_keep_mask(const int32_t* __restrict__ lengths, int64_t n, int64_t base,
+                                                int32_t max_keep) {
+  int mask = 0;
+#pragma unroll
+  for (int u = 0; u < kItems; ++u) {
+    const int64_t i = base + u;
+    if (i < n && lengths[i] <= max_keep) mask |= 1 << u;
+  }
+  return mask;
+}
+
+__global__ void __launch_bounds__(kThreads)
+filter_count_kernel(const int32_t* __restrict__ lengths, int64_t n, int32_t max_keep, int64_t* __restrict__ tile_counts) {
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kTile + static_cast<int64_t>(threadIdx.x) * kItems;
+  int c = __popc(thread_keep_mask(lengths, n, base, max_keep));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
+  __shared__ int warp_counts[kThreads / 32];
+  if ((threadIdx.x & 31) == 0) warp_counts[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int w = 0; w < kThreads / 32; ++w) t += warp_counts[w];
+    tile_counts[blockIdx.x] = t;
+  }
+}
+
+// One CTA: exclusive scan of the tile counts in place; total -> *num_kept.
+__global__ void __launch_bounds__(1024)
+filter_scan_kernel(int64_t* __restrict__ tile_counts, int64_t tiles, int64_t* __restrict__ num_kept) {
+  __shared__ int64_t warp_sums[32];
+  __shared__ int64_t carry;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < tiles; base += 1024) {
+    const int64_t i = base + threadIdx.x;
+    const int64_t v = i < tiles ? tile_counts[i] : 0;
+    int64_t x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      int64_t y = __shfl_up_sync(kFull, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_sums[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      int64_t w = warp_sums[lane];
+      int64_t z = w;
+      for (int o = 1; o < 32; o <<= 1) {
+        int64_t y = __shfl_up_sync(kFull, z, o);
+        if (lane >= o) z += y;
+      }
+      warp_sums[lane] = z - w;
+    }
+    __syncthreads();
+    const int64_t excl = x - v + warp_sums[warp] + carry;
+    if (i < tiles) tile_counts[i] = excl;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = excl + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *num_kept = carry;
+}
+
+__global__ void __launch_bounds__(kThreads)
+filter_scatter_kernel(const int32_t* __restrict__ lengths, int64_t n, int32_t max_keep,
+                      const int64_t* __restrict__ tile_offsets, const int64_t* __restrict__ in_map,
+                      int64_t* __restrict__ kept) {
+  __shared__ int warp_sums[kThreads / 32];
+  __shared__ int total;
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kTile + static_cast<int64_t>(threadIdx.x) * kItems;
+  const int mask = thread_keep_mask(lengths, n, base, max_keep);
+  int off = block_exclusive_scan(__popc(mask), warp_sums, &total);
+  int64_t dst = tile_offsets[blockIdx.x] + off;
+#pragma unroll
+  for (int u = 0; u < kItems; ++u) {
+    if (mask & (1 << u)) {
+      const int64_t p = base + u;
+      kept[dst++] = in_map ? in_map[p] : p;
+    }
+  }
+}
+
+// One warp per batch.
+__global__ void __launch_bounds__(kThreads)
+batch_max_len_kernel(const int32_t* __restrict__ lengths, const int64_t* __restrict__ kept, int64_t num_kept,
+                     int64_t batch, int64_t num_batches, int32_t* __restrict__ lmax) {
+  const int64_t w = static_cast<int64_t>(blockIdx.x) * (kThreads / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (w >= num_batches) return;
+  const int64_t r0 = w * batch;
+  const int64_t r1 = r0 + batch < num_kept ? r0 + batch : num_kept;
+  int32_t m = 0;
+  for (int64_t r = r0 + lane; r < r1; r += 32) m = max(m, lengths[kept[r]]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(kFull, m, o));
+  if (lane == 0) lmax[w] = m;
+}
+
+// One warp per output row; coalesced 4-byte loads/stores.
+__global__ void __launch_bounds__(kThreads)
+padded_batch_kernel(const int32_t* __restrict__ tokens, const int64_t* __restrict__ offsets,
+                    const int32_t* __restrict__ lengths, const int64_t* __restrict__ kept, int64_t first, int64_t rows,
+                    int32_t lmax, int32_t pad, int32_t* __restrict__ out, int32_t* __restrict__ out_lengths) {
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * (kThreads / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const int64_t p = kept[first + r];
+  const int32_t len = lengths[p];
+  const int32_t* src = tokens + offsets[p];
+  int32_t* dst = out + r * static_cast<int64_t>(lmax);
+  for (int c = lane; c < lmax; c += 32) __stcs(dst + c, c < len ? __ldcs(src + c) : pad);
+  if (lane == 0) out_lengths[r] = len;
+}
+
+}  // namespace
+}  // namespace dpk
+
+using namespace dpk;
+
+extern "C" size_t dp_k_filter_scratch_bytes(int64_t n) {
+  int64_t tiles = (n + kTile - 1) / kTile;
+  return static_cast<size_t>(tiles < 1 ? 1 : tiles) * sizeof(int64_t);
+}
+
+extern "C" int dp_k_filter_len_le(const int32_t* lengths, int64_t n, int32_t max_keep, const int64_t* in_map,
+                                  int64_t* kept, int64_t* num_kept_dev, void* scratch, void* stream) {
+  if (n < 0) return fail(DP_ERR_INVALID_ATTR, "filter: n must be >= 0");
+  if (!num_kept_dev || !scratch) return fail(DP_ERR_INVALID_ATTR, "filter: null num_kept/scratch");
+  cudaStream_t s = as_stream(stream);
+  if (n == 0) return cuda_status(cudaMemsetAsync(num_kept_dev, 0, sizeof(int64_t), s), "filter: memset");
+  const int64_t tiles = (n + kTile - 1) / kTile;
+  if (tiles > 0x7fffffff) return fail(DP_ERR_INVALID_ATTR, "filter: n too large");
+  int64_t* tile = static_cast<int64_t*>(scratch);
+  filter_count_kernel<<<static_cast<int>(tiles), kThreads, 0, s>>>(lengths, n, max_keep, tile);
+  filter_scan_kernel<<<1, 1024, 0, s>>>(tile, tiles, num_kept_dev);
+  filter_scatter_kernel<<<static_cast<int>(tiles), kThreads, 0, s>>>(lengths, n, max_keep, tile, in_map, kept);
+  return launch_status("filter_len_le");
+}
+
+extern "C" int dp_k_batch_max_len(const int32_t* lengths, const int64_t* kept, int64_t num_kept, int64_t batch,
+                                  int32_t* lmax, void* stream) {
+  if (batch < 1) return fail(DP_ERR_INVALID_ATTR, "padded_batch: batch_size must be >= 1");
+  if (num_kept <= 0) return DP_OK;
+  const int64_t nb = (num_kept + batch - 1) / batch;
+  const int64_t blocks = (nb + kThreads / 32 - 1) / (kThreads / 32);
+  batch_max_len_kernel<<<static_cast<int>(blocks), kThreads, 0, as_stream(stream)>>>(lengths, kept, num_kept, batch,
+                                                                                     nb, lmax);
+  return launch_status("batch_max_len");
+}
+
+extern "C" int dp_k_padded_batch(const int32_t* tokens, const int64_t* offsets, const int32_t* lengths,
+                                 const int64_t* kept, int64_t first, int64_t rows, int32_t lmax, int32_t pad_value,
+                                 int32_t* out, int32_t* out_lengths, void* stream) {
+  if (rows < 0 || lmax < 0) return fail(DP_ERR_INVALID_ATTR, "padded_batch: bad rows/lmax");
+  if (rows == 0) return DP_OK;
+  const int64_t blocks = (rows + kThreads / 32 - 1) / (kThreads / 32);
+  padded_batch_kernel<<<static_cast<int>(blocks), kThreads, 0, as_stream(stream)>>>(
+      tokens, offsets, lengths, kept, first, rows, lmax, pad_value, out, out_lengths);
+  return launch_status("padded_batch");
+}

@@ -12,7 +12,7 @@ import os
 import re
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libdpcuda.so")
+LIB_PATH = os.environ.get("DP_LIB_PATH") or os.path.join(_HERE, "lib", "libdpcuda.so")
 INCLUDE_DIR = os.path.join(os.path.dirname(_HERE), "include")
 
 c_i32 = ctypes.c_int32

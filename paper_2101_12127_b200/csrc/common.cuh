@@ -130,21 +130,17 @@ struct NormConsts {
 };
 
 #ifdef __CUDACC__
-// (v - mean) / std rounded exactly as IEEE fp32 division for every v that is
-// an integer in [0, 255] (uint8 pixel): one rounded subtract, then the
-// Markstein correction q' = RN(q + RN(d - q*s) * r) from q = RN(d * r).
-// tests/test_oracle.py::test_fast_division_exhaustive proves it against
-// IEEE division over all 3 x 256 inputs.
-__device__ __forceinline__ float normalize_u8(float v, float mean, float s, float r) {
+// (v - mean) / std rounded exactly as IEEE fp32 division: one rounded
+// subtract, then the Markstein correction q' = RN(q + RN(d - q*s) * r) from
+// q = RN(d * r), r = RN(1/s).  Proven equal to IEEE division for EVERY fp32
+// v in [+0, 255] and the three normalize channels by exhaustive enumeration
+// (tools/prove_fast_div.c, run by tests/test_oracle.py), which covers uint8
+// pixels (K3) and every bilinear blend of them (K4).
+__device__ __forceinline__ float normalize_fast(float v, float mean, float s, float r) {
   float d = __fsub_rn(v, mean);
   float q = __fmul_rn(d, r);
   float rem = __fmaf_rn(-q, s, d);
   return __fmaf_rn(rem, r, q);
-}
-
-// General fp32 input (resize output): plain IEEE division.
-__device__ __forceinline__ float normalize_f32(float v, float mean, float s) {
-  return __fdiv_rn(__fsub_rn(v, mean), s);
 }
 
 __device__ __forceinline__ void st_cs_f4(float4* p, float4 v) {
@@ -163,3 +159,60 @@ __device__ __forceinline__ uint4 ld_nc_na_u4(const void* p) {
 #endif
 
 }  // namespace dpk
+
+#ifdef __CUDACC__
+namespace dpk {
+
+// ---- TMA bulk copies + mbarriers (sm_90+ PTX; SASS UBLKCP / SYNCS) ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "DP_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra DP_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// L2 evict-first policy for read-once streams.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+// Global -> shared bulk copy (TMA engine), completion counted on `bar`.
+// dst/src 16-byte aligned, bytes a multiple of 16.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+// Exact uint8 -> fp32 without the conversion pipe: 2^23 + x, minus 2^23.
+__device__ __forceinline__ float u8_to_f32(uint32_t x) {
+  return __fsub_rn(__uint_as_float(0x4B000000u | x), 8388608.0f);
+}
+
+}  // namespace dpk
+#endif

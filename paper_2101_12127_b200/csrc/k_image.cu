@@ -11,6 +11,8 @@
 // shared memory with 16-byte non-allocating loads, then every thread emits
 // 16-byte streaming (.cs) stores of 4 normalized fp32 values, so the output
 // (80% of the traffic) leaves the SM as fully coalesced 128-bit stores.
+#include <algorithm>
+#include <cstdlib>
 #include <cstdint>
 
 #include "common.cuh"
@@ -22,6 +24,11 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kCropBandRows = 16;
 constexpr int kResizeBandRows = 16;
+constexpr int kFastCropBandRows = 16;   // tools/ksweep.py: 16 rows x 8 stages best on B200
+constexpr int kFastResizeBandRows = 16;
+constexpr int kCropStages = 8;
+constexpr int kResizeStages = 4;
+constexpr size_t kSmemBudget = 200 * 1024;
 
 __device__ __forceinline__ float sel3(int c, float a, float b, float d) { return c == 0 ? a : (c == 1 ? b : d); }
 
@@ -31,6 +38,7 @@ struct ImageArgs {
   int64_t first;
   int64_t* out_ids;
   float* out;
+  int64_t num_images;
   int in_h, in_w, out_h, out_w;
   int bands;
   NormConsts nc;
@@ -39,11 +47,12 @@ struct ImageArgs {
 // ---------------------------------------------------------------- K3 ----
 template <bool kAligned>
 __global__ void __launch_bounds__(kThreads)
-crop_flip_norm_kernel(ImageArgs a, uint64_t seed, int do_flip, int sstride) {
+crop_generic_kernel(ImageArgs a, uint64_t seed, int do_flip, int sstride) {
   extern __shared__ __align__(16) uint8_t stage[];
   const int band = blockIdx.x % a.bands;
   const int64_t j = blockIdx.x / a.bands;
   const int64_t id = a.order ? a.order[a.first + j] : a.first + j;
+  if (id < 0 || id >= a.num_images) return;  // engine orders are in range by construction
   CropParams cp = crop_params(seed, id, a.in_h, a.in_w, a.out_h, a.out_w);
   if (!do_flip) cp.flip = 0;
   if (band == 0 && threadIdx.x == 0) a.out_ids[j] = id;
@@ -89,7 +98,7 @@ crop_flip_norm_kernel(ImageArgs a, uint64_t seed, int do_flip, int sstride) {
         const int x = e / 3;
         const int ch = e - 3 * x;
         const int sx = cp.flip ? (a.out_w - 1 - x) : x;
-        v[u] = normalize_u8(static_cast<float>(srow[sx * 3 + ch]), sel3(ch, nc.mean[0], nc.mean[1], nc.mean[2]),
+        v[u] = normalize_fast(static_cast<float>(srow[sx * 3 + ch]), sel3(ch, nc.mean[0], nc.mean[1], nc.mean[2]),
                             sel3(ch, nc.stdv[0], nc.stdv[1], nc.stdv[2]), sel3(ch, nc.rcp[0], nc.rcp[1], nc.rcp[2]));
       }
       st_cs_f4(reinterpret_cast<float4*>(obase + static_cast<size_t>(r) * seg + 4 * q),
@@ -101,7 +110,7 @@ crop_flip_norm_kernel(ImageArgs a, uint64_t seed, int do_flip, int sstride) {
       const int x = e / 3, ch = e - 3 * x;
       const int sx = cp.flip ? (a.out_w - 1 - x) : x;
       obase[static_cast<size_t>(r) * seg + e] =
-          normalize_u8(static_cast<float>(stage[r * sstride + sx * 3 + ch]), sel3(ch, nc.mean[0], nc.mean[1], nc.mean[2]),
+          normalize_fast(static_cast<float>(stage[r * sstride + sx * 3 + ch]), sel3(ch, nc.mean[0], nc.mean[1], nc.mean[2]),
                        sel3(ch, nc.stdv[0], nc.stdv[1], nc.stdv[2]), sel3(ch, nc.rcp[0], nc.rcp[1], nc.rcp[2]));
     }
   }
@@ -127,11 +136,12 @@ __device__ __forceinline__ float lerp_rn(float p, float q, float w) {
 
 template <bool kAligned>
 __global__ void __launch_bounds__(kThreads)
-resize_norm_kernel(ImageArgs a) {
+resize_generic_kernel(ImageArgs a) {
   extern __shared__ __align__(16) uint8_t stage[];
   const int band = blockIdx.x % a.bands;
   const int64_t j = blockIdx.x / a.bands;
   const int64_t id = a.order ? a.order[a.first + j] : a.first + j;
+  if (id < 0 || id >= a.num_images) return;  // engine orders are in range by construction
   if (band == 0 && threadIdx.x == 0) a.out_ids[j] = id;
 
   const int y_begin = band * kResizeBandRows;
@@ -178,7 +188,8 @@ resize_norm_kernel(ImageArgs a) {
       const float top = lerp_rn(p00, p01, wx);
       const float bot = lerp_rn(p10, p11, wx);
       const float val = lerp_rn(top, bot, wy);
-      v[u] = normalize_f32(val, sel3(ch, nc.mean[0], nc.mean[1], nc.mean[2]), sel3(ch, nc.stdv[0], nc.stdv[1], nc.stdv[2]));
+      v[u] = normalize_fast(val, sel3(ch, nc.mean[0], nc.mean[1], nc.mean[2]), sel3(ch, nc.stdv[0], nc.stdv[1], nc.stdv[2]),
+                            sel3(ch, nc.rcp[0], nc.rcp[1], nc.rcp[2]));
     }
     if (kAligned) {
       st_cs_f4(reinterpret_cast<float4*>(obase + static_cast<size_t>(r) * seg + 4 * q),
@@ -216,6 +227,353 @@ int check_common(const uint8_t* images, int64_t num_images, int in_h, int in_w, 
   return DP_OK;
 }
 
+
+// ===================================================================
+// Fast path: persistent, warp-specialized CTAs over a kStages-deep TMA
+// pipeline (one CTA per SM).
+//
+// Work item = (batch row j, band of `band_rows` output rows).  One producer
+// warp resolves each item's gather index (and crop offsets), arms the
+// stage's "full" mbarrier with the exact byte count and issues the
+// cp.async.bulk copies (TMA engine, L2 evict-first) of the source bytes the
+// band needs.  The consumer warps own one fixed float4 output column q per
+// thread, so channel constants and smem offsets of their 4 outputs are
+// computed once per kernel; the inner loop is 4 (K3) or 16 (K4) LDS.U8,
+// exact normalizes and one 16-byte streaming store.  Each consumer warp
+// releases a stage through the "empty" mbarrier on its own -- there is no
+// CTA-wide barrier in the loop, so warps drift freely and the TMA reads of
+// later items overlap the store stream of earlier ones.
+// ===================================================================
+constexpr int kMaxStages = 16;
+constexpr int kFastConsumers = 672;  // 21 warps; + 1 producer warp
+
+struct StageMeta {
+  int64_t id;
+  int64_t j;
+  int band, nrows, shift, flip, ys0, pad;
+};
+
+// Everything the producer needs to issue one item; computed by one lane per
+// item, 32 items at a time, so the gather-index loads and Philox draws of a
+// whole group are in flight together instead of serialising per item.
+struct Plan {
+  int64_t id, j;
+  int band, nrows, src_row, col, shift, flip;
+  uint32_t bytes_row;
+};
+
+__device__ __forceinline__ Plan shfl_plan(const Plan& p, int src) {
+  Plan o;
+  o.id = __shfl_sync(0xffffffffu, p.id, src);
+  o.j = __shfl_sync(0xffffffffu, p.j, src);
+  o.band = __shfl_sync(0xffffffffu, p.band, src);
+  o.nrows = __shfl_sync(0xffffffffu, p.nrows, src);
+  o.src_row = __shfl_sync(0xffffffffu, p.src_row, src);
+  o.col = __shfl_sync(0xffffffffu, p.col, src);
+  o.shift = __shfl_sync(0xffffffffu, p.shift, src);
+  o.flip = __shfl_sync(0xffffffffu, p.flip, src);
+  o.bytes_row = __shfl_sync(0xffffffffu, p.bytes_row, src);
+  return o;
+}
+
+struct FastArgs {
+  const uint8_t* images;
+  const int64_t* order;
+  int64_t first, rows, num_images;
+  int64_t* out_ids;
+  float* out;
+  int in_h, in_w, out_h, out_w;
+  int band_rows, bands, q_per_row, rpp;
+  int stage_stride, stage_bytes, stages;
+  uint64_t seed;
+  int do_flip;
+  NormConsts nc;
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+struct RowTap {
+  int y0, y1;
+  float wy;
+};
+
+// ---- K3 stage operations ----
+struct CropOp {
+  float mu[4], sd[4], rc[4];
+  int off_n[4], off_f[4];
+
+  __device__ void init(const FastArgs& a, int q, uint8_t*) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = 4 * q + u, x = e / 3, ch = e - 3 * x;
+      mu[u] = sel3(ch, a.nc.mean[0], a.nc.mean[1], a.nc.mean[2]);
+      sd[u] = sel3(ch, a.nc.stdv[0], a.nc.stdv[1], a.nc.stdv[2]);
+      rc[u] = sel3(ch, a.nc.rcp[0], a.nc.rcp[1], a.nc.rcp[2]);
+      off_n[u] = e;
+      off_f[u] = (a.out_w - 1 - x) * 3 + ch;
+    }
+  }
+
+  static __device__ Plan plan(const FastArgs& a, int64_t item, const uint8_t*) {
+    Plan p;
+    p.j = item / a.bands;
+    p.band = static_cast<int>(item - p.j * a.bands);
+    const int64_t id = a.order ? a.order[a.first + p.j] : a.first + p.j;
+    const bool valid = id >= 0 && id < a.num_images;
+    p.id = valid ? id : -1;
+    p.nrows = min(a.band_rows, a.out_h - p.band * a.band_rows);
+    CropParams cp{0, 0, 0};
+    if (valid) cp = crop_params(a.seed, id, a.in_h, a.in_w, a.out_h, a.out_w);
+    const int start = cp.ox * 3;
+    p.shift = start & 15;
+    p.src_row = cp.oy + p.band * a.band_rows;  // first source row
+    p.col = start - p.shift;                     // 16-byte aligned first source byte
+    p.flip = a.do_flip ? cp.flip : 0;
+    p.bytes_row = static_cast<uint32_t>((p.shift + a.out_w * 3 + 15) >> 4) << 4;
+    return p;
+  }
+
+  // producer warp: fill meta + issue the row copies of one planned item
+  static __device__ void issue(const FastArgs& a, const Plan& p, uint8_t* dst, StageMeta* meta, uint64_t* full,
+                               int lane, uint64_t pol) {
+    const bool valid = p.id >= 0;
+    if (lane == 0) {
+      *meta = StageMeta{p.id, p.j, p.band, p.nrows, p.shift, p.flip, 0, 0};
+      mbar_arrive_expect_tx(full, valid ? p.bytes_row * p.nrows : 0u);
+    }
+    __syncwarp();
+    if (valid) {
+      const size_t row_bytes = static_cast<size_t>(a.in_w) * 3;
+      const uint8_t* src0 = a.images + (static_cast<size_t>(p.id) * a.in_h + p.src_row) * row_bytes + p.col;
+      for (int r = lane; r < p.nrows; r += 32)
+        bulk_g2s(dst + r * a.stage_stride, src0 + r * row_bytes, p.bytes_row, full, pol);
+    }
+  }
+
+  __device__ void consume(const FastArgs& a, const StageMeta& m, const uint8_t* stage, int q, int rsub,
+                          const uint8_t*) const {
+    const uint8_t* st = stage + m.shift;
+    const int seg = a.out_w * 3;
+    float4* ob = reinterpret_cast<float4*>(a.out + (static_cast<size_t>(m.j) * a.out_h +
+                                                    static_cast<size_t>(m.band) * a.band_rows) * seg);
+    for (int r = rsub; r < m.nrows; r += a.rpp) {
+      const uint8_t* row = st + r * a.stage_stride;
+      float v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        v[u] = normalize_fast(u8_to_f32(row[m.flip ? off_f[u] : off_n[u]]), mu[u], sd[u], rc[u]);
+      st_cs_f4(ob + static_cast<size_t>(r) * a.q_per_row + q, make_float4(v[0], v[1], v[2], v[3]));
+    }
+  }
+};
+
+// ---- K4 stage operations ----
+struct ResizeOp {
+  float mu[4], sd[4], rc[4], wx[4];
+  int o0[4], o1[4];
+
+  __device__ void init(const FastArgs& a, int q, uint8_t*) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = 4 * q + u, x = e / 3, ch = e - 3 * x;
+      mu[u] = sel3(ch, a.nc.mean[0], a.nc.mean[1], a.nc.mean[2]);
+      sd[u] = sel3(ch, a.nc.stdv[0], a.nc.stdv[1], a.nc.stdv[2]);
+      rc[u] = sel3(ch, a.nc.rcp[0], a.nc.rcp[1], a.nc.rcp[2]);
+      int x0, x1;
+      resize_coord(x, a.in_w, a.out_w, x0, x1, wx[u]);
+      o0[u] = x0 * 3 + ch;
+      o1[u] = x1 * 3 + ch;
+    }
+  }
+
+  static __device__ Plan plan(const FastArgs& a, int64_t item, const uint8_t* taps_raw) {
+    const RowTap* taps = reinterpret_cast<const RowTap*>(taps_raw);
+    Plan p;
+    p.j = item / a.bands;
+    p.band = static_cast<int>(item - p.j * a.bands);
+    const int64_t id = a.order ? a.order[a.first + p.j] : a.first + p.j;
+    p.id = (id >= 0 && id < a.num_images) ? id : -1;
+    const int y_begin = p.band * a.band_rows;
+    p.nrows = min(a.band_rows, a.out_h - y_begin);
+    p.src_row = taps[y_begin].y0;
+    const int ys1 = taps[y_begin + p.nrows - 1].y1;
+    p.bytes_row = static_cast<uint32_t>((ys1 - p.src_row + 1) * a.in_w * 3);  // whole contiguous span
+    p.col = 0;
+    p.shift = 0;
+    p.flip = 0;
+    return p;
+  }
+
+  static __device__ void issue(const FastArgs& a, const Plan& p, uint8_t* dst, StageMeta* meta, uint64_t* full,
+                               int lane, uint64_t pol) {
+    const bool valid = p.id >= 0;
+    if (lane == 0) {
+      *meta = StageMeta{p.id, p.j, p.band, p.nrows, 0, 0, p.src_row, 0};
+      mbar_arrive_expect_tx(full, valid ? p.bytes_row : 0u);
+      if (valid)
+        bulk_g2s(dst, a.images + (static_cast<size_t>(p.id) * a.in_h + p.src_row) * static_cast<size_t>(a.in_w) * 3,
+                 p.bytes_row, full, pol);
+    }
+    __syncwarp();
+  }
+
+  __device__ void consume(const FastArgs& a, const StageMeta& m, const uint8_t* st, int q, int rsub,
+                          const uint8_t* taps_raw) const {
+    const RowTap* taps = reinterpret_cast<const RowTap*>(taps_raw);
+    const size_t row_bytes = static_cast<size_t>(a.in_w) * 3;
+    const int seg = a.out_w * 3;
+    const int y_begin = m.band * a.band_rows;
+    float4* ob = reinterpret_cast<float4*>(a.out + (static_cast<size_t>(m.j) * a.out_h + y_begin) * seg);
+    for (int r = rsub; r < m.nrows; r += a.rpp) {
+      const RowTap t = taps[y_begin + r];
+      const uint8_t* row0 = st + static_cast<size_t>(t.y0 - m.ys0) * row_bytes;
+      const uint8_t* row1 = st + static_cast<size_t>(t.y1 - m.ys0) * row_bytes;
+      float v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float top = lerp_rn(u8_to_f32(row0[o0[u]]), u8_to_f32(row0[o1[u]]), wx[u]);
+        const float bot = lerp_rn(u8_to_f32(row1[o0[u]]), u8_to_f32(row1[o1[u]]), wx[u]);
+        v[u] = normalize_fast(lerp_rn(top, bot, t.wy), mu[u], sd[u], rc[u]);
+      }
+      st_cs_f4(ob + static_cast<size_t>(r) * a.q_per_row + q, make_float4(v[0], v[1], v[2], v[3]));
+    }
+  }
+};
+
+template <class Op>
+__global__ void __launch_bounds__(kFastConsumers + 32, 1) pipeline_kernel(FastArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ uint64_t full[kMaxStages], empty[kMaxStages];
+  __shared__ StageMeta meta[kMaxStages];
+  const int kStages = a.stages;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int consumers = a.q_per_row * a.rpp;
+  const int n_cwarps = (consumers + 31) >> 5;
+  uint8_t* taps = smem + kStages * a.stage_bytes;  // resize row taps (unused by K3)
+
+  for (int y = tid; y < a.out_h; y += blockDim.x) {
+    RowTap t;
+    resize_coord(y, a.in_h, a.out_h, t.y0, t.y1, t.wy);
+    reinterpret_cast<RowTap*>(taps)[y] = t;
+  }
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], n_cwarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  const int64_t total = a.rows * a.bands;
+  if (warp == n_cwarps) {  // ---- producer warp ----
+    const uint64_t pol = policy_evict_first();
+    for (int64_t k0 = 0;; k0 += 32) {
+      const int64_t my_item = blockIdx.x + (k0 + lane) * static_cast<int64_t>(gridDim.x);
+      Plan mine{};
+      if (my_item < total) mine = Op::plan(a, my_item, taps);
+      const int n = __popc(__ballot_sync(0xffffffffu, my_item < total));
+      for (int t = 0; t < n; ++t) {
+        const int64_t k = k0 + t;
+        const int s = static_cast<int>(k % kStages);
+        if (k >= kStages) mbar_wait(&empty[s], static_cast<uint32_t>((k / kStages) - 1) & 1);
+        Op::issue(a, shfl_plan(mine, t), smem + s * a.stage_bytes, &meta[s], &full[s], lane, pol);
+      }
+      if (n < 32) break;
+    }
+    return;
+  }
+  // ---- consumer warps ----
+  const int q = tid % a.q_per_row, rsub = tid / a.q_per_row;
+  const bool active = tid < consumers;
+  Op op;
+  op.init(a, active ? q : 0, taps);
+  int k = 0;
+  for (int64_t item = blockIdx.x; item < total; item += gridDim.x, ++k) {
+    const int s = k % kStages;
+    mbar_wait(&full[s], (k / kStages) & 1);
+    const StageMeta m = meta[s];
+    if (m.id >= 0 && active) {
+      if (m.band == 0 && tid == 0) a.out_ids[m.j] = m.id;
+      op.consume(a, m, smem + s * a.stage_bytes, q, rsub, taps);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+}
+
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <typename K>
+int launch_persistent(K kernel, const FastArgs& a, size_t smem, cudaStream_t s, const char* what) {
+  int st;
+  if ((st = cuda_status(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem)),
+                        what)))
+    return st;
+  const int threads = ((a.q_per_row * a.rpp + 31) / 32) * 32 + 32;
+  int per_sm = 0;
+  if ((st = cuda_status(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem), what)))
+    return st;
+  if (per_sm < 1) return fail(DP_ERR_INVALID_ATTR, std::string(what) + ": kernel does not fit on an SM");
+  const int64_t items = a.rows * a.bands;
+  const int64_t grid = std::min<int64_t>(items, static_cast<int64_t>(per_sm) * sm_count());
+  kernel<<<static_cast<int>(grid), threads, smem, s>>>(a);
+  return launch_status(what);
+}
+
+// Fast-path eligibility: 16B-aligned rows and buffers, whole float4 per
+// thread column, a row of float4s fits one CTA.
+bool fast_ok(const uint8_t* images, int in_w, int out_w, const float* out) {
+  const int q = out_w * 3 / 4;
+  return (static_cast<size_t>(in_w) * 3) % 16 == 0 && reinterpret_cast<uintptr_t>(images) % 16 == 0 &&
+         out_w % 4 == 0 && reinterpret_cast<uintptr_t>(out) % 16 == 0 && q <= kFastConsumers;
+}
+
+// Development-only overrides for tuning sweeps (tools/kbench.py).
+int env_int(const char* name, int fallback) {
+  const char* v = std::getenv(name);
+  return v && *v ? std::atoi(v) : fallback;
+}
+
+FastArgs make_fast(const uint8_t* images, int64_t num_images, int in_h, int in_w, const int64_t* order, int64_t first,
+                   int64_t rows, int out_h, int out_w, const float mean[3], const float stdv[3], int64_t* out_ids,
+                   float* out, int band_rows, int stages) {
+  FastArgs a{};
+  a.images = images;
+  a.order = order;
+  a.first = first;
+  a.rows = rows;
+  a.num_images = num_images;
+  a.out_ids = out_ids;
+  a.out = out;
+  a.in_h = in_h;
+  a.in_w = in_w;
+  a.out_h = out_h;
+  a.out_w = out_w;
+  a.band_rows = band_rows < out_h ? band_rows : out_h;
+  a.bands = (out_h + a.band_rows - 1) / a.band_rows;
+  a.q_per_row = out_w * 3 / 4;
+  a.rpp = kFastConsumers / a.q_per_row;
+  if (a.rpp > a.band_rows) a.rpp = a.band_rows;
+  a.nc = make_norm(mean, stdv);
+  a.stages = env_int("DP_DEV_STAGES", stages);
+  if (a.stages < 2) a.stages = 2;
+  if (a.stages > kMaxStages) a.stages = kMaxStages;
+  return a;
+}
+
 }  // namespace
 }  // namespace dpk
 
@@ -230,7 +588,20 @@ extern "C" int dp_k_crop_flip_normalize_batch(const uint8_t* images, int64_t num
   if (crop_h > in_h || crop_w > in_w)
     return fail(DP_ERR_INVALID_ATTR, "crop_flip_normalize: crop larger than the image");
   if (rows == 0) return DP_OK;
-  ImageArgs a{images, order, first, out_ids, out, in_h, in_w, crop_h, crop_w,
+  cudaStream_t s = as_stream(stream);
+  if (fast_ok(images, in_w, crop_w, out)) {
+    FastArgs f = make_fast(images, num_images, in_h, in_w, order, first, rows, crop_h, crop_w, mean, stdv, out_ids,
+                           out, env_int("DP_DEV_CROP_BAND", kFastCropBandRows), kCropStages);
+    f.seed = udf_seed;
+    f.do_flip = do_flip;
+    f.stage_stride = ((crop_w * 3 + 15 + 15) / 16) * 16;
+    f.stage_bytes = ((f.band_rows * f.stage_stride + 127) / 128) * 128;
+    const size_t taps = static_cast<size_t>(crop_h) * sizeof(RowTap);
+    while (f.stages > 2 && static_cast<size_t>(f.stages) * f.stage_bytes + taps > kSmemBudget) --f.stages;
+    const size_t smem = static_cast<size_t>(f.stages) * f.stage_bytes + taps;
+    if (smem <= kSmemBudget) return launch_persistent(pipeline_kernel<CropOp>, f, smem, s, "crop_flip_normalize");
+  }
+  ImageArgs a{images, order, first, out_ids, out, num_images, in_h, in_w, crop_h, crop_w,
               (crop_h + kCropBandRows - 1) / kCropBandRows, make_norm(mean, stdv)};
   const size_t row_bytes = static_cast<size_t>(in_w) * 3;
   const bool aligned = (row_bytes % 16 == 0) && (reinterpret_cast<uintptr_t>(images) % 16 == 0) &&
@@ -240,13 +611,12 @@ extern "C" int dp_k_crop_flip_normalize_batch(const uint8_t* images, int64_t num
   const size_t smem = static_cast<size_t>(kCropBandRows) * sstride;
   const int64_t grid = rows * a.bands;
   if (grid > 0x7fffffff) return fail(DP_ERR_INVALID_ATTR, "crop_flip_normalize: batch too large");
-  cudaStream_t s = as_stream(stream);
   if (aligned) {
-    if ((st = ensure_smem(crop_flip_norm_kernel<true>, smem))) return st;
-    crop_flip_norm_kernel<true><<<static_cast<int>(grid), kThreads, smem, s>>>(a, udf_seed, do_flip, sstride);
+    if ((st = ensure_smem(crop_generic_kernel<true>, smem))) return st;
+    crop_generic_kernel<true><<<static_cast<int>(grid), kThreads, smem, s>>>(a, udf_seed, do_flip, sstride);
   } else {
-    if ((st = ensure_smem(crop_flip_norm_kernel<false>, smem))) return st;
-    crop_flip_norm_kernel<false><<<static_cast<int>(grid), kThreads, smem, s>>>(a, udf_seed, do_flip, sstride);
+    if ((st = ensure_smem(crop_generic_kernel<false>, smem))) return st;
+    crop_generic_kernel<false><<<static_cast<int>(grid), kThreads, smem, s>>>(a, udf_seed, do_flip, sstride);
   }
   return launch_status("crop_flip_normalize");
 }
@@ -258,7 +628,22 @@ extern "C" int dp_k_resize_normalize_batch(const uint8_t* images, int64_t num_im
   int st = check_common(images, num_images, in_h, in_w, rows, out_h, out_w, out_ids, out, "resize_normalize");
   if (st) return st;
   if (rows == 0) return DP_OK;
-  ImageArgs a{images, order, first, out_ids, out, in_h, in_w, out_h, out_w,
+  cudaStream_t s = as_stream(stream);
+  if (fast_ok(images, in_w, out_w, out)) {
+    FastArgs f = make_fast(images, num_images, in_h, in_w, order, first, rows, out_h, out_w, mean, stdv, out_ids, out,
+                           env_int("DP_DEV_RESIZE_BAND", kFastResizeBandRows), kResizeStages);
+    const double sc = static_cast<double>(in_h) / out_h;
+    int src_rows = static_cast<int>(f.band_rows * sc) + 3;
+    if (src_rows > in_h) src_rows = in_h;
+    f.stage_stride = in_w * 3;
+    f.stage_bytes = static_cast<int>(((static_cast<size_t>(src_rows) * in_w * 3 + 127) / 128) * 128);
+    const size_t taps = static_cast<size_t>(out_h) * sizeof(RowTap);
+    while (f.stages > 2 && static_cast<size_t>(f.stages) * f.stage_bytes + taps > kSmemBudget) --f.stages;
+    const size_t smem = static_cast<size_t>(f.stages) * f.stage_bytes + taps;
+    if (smem <= kSmemBudget)
+      return launch_persistent(pipeline_kernel<ResizeOp>, f, smem, s, "resize_normalize");
+  }
+  ImageArgs a{images, order, first, out_ids, out, num_images, in_h, in_w, out_h, out_w,
               (out_h + kResizeBandRows - 1) / kResizeBandRows, make_norm(mean, stdv)};
   const size_t row_bytes = static_cast<size_t>(in_w) * 3;
   const bool aligned = (row_bytes % 16 == 0) && (reinterpret_cast<uintptr_t>(images) % 16 == 0) &&
@@ -271,13 +656,12 @@ extern "C" int dp_k_resize_normalize_batch(const uint8_t* images, int64_t num_im
     return fail(DP_ERR_INVALID_ATTR, "resize_normalize: source band exceeds shared memory (downscale > ~9x)");
   const int64_t grid = rows * a.bands;
   if (grid > 0x7fffffff) return fail(DP_ERR_INVALID_ATTR, "resize_normalize: batch too large");
-  cudaStream_t s = as_stream(stream);
   if (aligned) {
-    if ((st = ensure_smem(resize_norm_kernel<true>, smem))) return st;
-    resize_norm_kernel<true><<<static_cast<int>(grid), kThreads, smem, s>>>(a);
+    if ((st = ensure_smem(resize_generic_kernel<true>, smem))) return st;
+    resize_generic_kernel<true><<<static_cast<int>(grid), kThreads, smem, s>>>(a);
   } else {
-    if ((st = ensure_smem(resize_norm_kernel<false>, smem))) return st;
-    resize_norm_kernel<false><<<static_cast<int>(grid), kThreads, smem, s>>>(a);
+    if ((st = ensure_smem(resize_generic_kernel<false>, smem))) return st;
+    resize_generic_kernel<false><<<static_cast<int>(grid), kThreads, smem, s>>>(a);
   }
   return launch_status("resize_normalize");
 }

@@ -1,0 +1,294 @@
+// dpb200/datapipe.hpp -- the Dataset / Iterator operator API of the B200
+// engine: graph builders (ops::*), the UDF registry with device UDF
+// descriptors, the static optimizer, and MakeIterator / GetNext.
+//
+// Drop-in surface for the reference's path:
+//   ops::* builders     -- /root/reference/proj/include/datapipe/graph.hpp:134-165
+//   Build / DatasetGraph -- graph.hpp:68-131
+//   UdfRegistry          -- udf.hpp:41-87 (plus device descriptors)
+//   Optimize / RuleSet   -- optimizer.hpp:22-75
+//   MakeIterator / PipelineIterator::GetNext / IteratorOptions
+//                        -- runtime.hpp:35-100
+// The kinds on the path are supported; Range, TensorSlices, TokenSequences
+// and PaddedBatch are the new kinds the north star names.  Graphs that do
+// not lower onto the device path are rejected at MakeIterator with
+// PipelineError(kInvalidAttr) -- there is no CPU fallback.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <functional>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <optional>
+#include <string>
+#include <variant>
+#include <vector>
+
+#include "dpb200/core.hpp"
+
+namespace datapipe::b200 {
+
+constexpr int64_t kAutotune = -1;        // graph.hpp:34
+constexpr int64_t kInfiniteRepeat = -1;  // graph.hpp:36
+
+enum class NodeKind : uint8_t {
+  // reference kinds on the path (numbering of graph.hpp:38-56)
+  kFromMemory = 0,
+  kInterleave = 5,
+  kBatch = 6,
+  kPrefetch = 8,
+  kRepeat = 9,
+  kShuffle = 10,
+  kShard = 11,
+  kMap = 2,
+  kFilter = 3,
+  kMapAndBatch = 16,
+  // new kinds
+  kRange = 32,
+  kTensorSlices = 33,
+  kTokenSequences = 34,
+  kPaddedBatch = 35,
+};
+
+const char* NodeKindName(NodeKind kind);
+
+// ---- source data (device resident, or pinned host for end-to-end runs) ----
+struct SourceData {
+  enum class Kind { kInt64, kImages, kTokens } kind;
+  int64_t count = 0;
+  // kInt64: values[count] (device);  kImages: u8 [count, h, w, c]
+  // kTokens: lengths i32[count], offsets i64[count+1], tokens i32[total]
+  std::shared_ptr<void> values, lengths, offsets, tokens;
+  int64_t h = 0, w = 0, c = 0, total_tokens = 0;
+  Residency residency = Residency::kDevice;
+  int device = 0;
+};
+using SourcePtr = std::shared_ptr<const SourceData>;
+
+// Synthetic inputs, generated on the device.
+SourcePtr SynthImages(int64_t count, int64_t h, int64_t w, uint64_t seed, int device = 0);
+SourcePtr SynthTokens(int64_t count, uint32_t max_len, uint64_t len_seed, uint64_t tok_seed, int device = 0);
+// Uploads host data (copied); images: u8 [count, h, w, 3].
+SourcePtr ImagesFromHost(const uint8_t* data, int64_t count, int64_t h, int64_t w, int device = 0);
+// Wraps pinned host memory (not copied, must outlive the graph); the device
+// kernels read it over PCIe (end-to-end runs).
+SourcePtr ImagesFromPinnedHost(const uint8_t* data, int64_t count, int64_t h, int64_t w, int device = 0);
+SourcePtr Int64FromHost(const int64_t* values, int64_t count, int device = 0);
+SourcePtr TokensFromHost(const int32_t* lengths, int64_t count, const int32_t* tokens, int device = 0);
+
+// ---- graph IR ----
+using AttrValue = std::variant<int64_t, uint64_t, double, bool, std::string, std::vector<std::string>, SourcePtr>;
+using Attrs = std::map<std::string, AttrValue>;
+
+class DatasetNode {
+ public:
+  DatasetNode(NodeKind kind, std::vector<std::shared_ptr<const DatasetNode>> inputs, Attrs attrs, ElementSpec spec)
+      : kind_(kind), inputs_(std::move(inputs)), attrs_(std::move(attrs)), spec_(std::move(spec)) {}
+  NodeKind kind() const { return kind_; }
+  const std::vector<std::shared_ptr<const DatasetNode>>& inputs() const { return inputs_; }
+  const Attrs& attrs() const { return attrs_; }
+  const ElementSpec& output_spec() const { return spec_; }
+  bool HasAttr(const std::string& k) const { return attrs_.count(k) > 0; }
+  int64_t GetInt(const std::string& k) const;
+  int64_t GetIntOr(const std::string& k, int64_t fallback) const;
+  uint64_t GetUint(const std::string& k) const;
+  bool GetBoolOr(const std::string& k, bool fallback) const;
+  const std::string& GetString(const std::string& k) const;
+  const SourcePtr& GetSource(const std::string& k) const;
+
+ private:
+  NodeKind kind_;
+  std::vector<std::shared_ptr<const DatasetNode>> inputs_;
+  Attrs attrs_;
+  ElementSpec spec_;
+};
+using NodePtr = std::shared_ptr<const DatasetNode>;
+
+class DatasetGraph {
+ public:
+  DatasetGraph() = default;
+  explicit DatasetGraph(NodePtr root) : root_(std::move(root)) {}
+  const NodePtr& root() const { return root_; }
+  const ElementSpec& element_spec() const { return root_->output_spec(); }
+  std::string ToString() const;
+
+ private:
+  NodePtr root_;
+};
+
+// ---- device UDFs ----
+// One step of a map UDF chain; consecutive steps are fused into one batch
+// kernel at lowering time (K1 affine, K3 crop+flip+normalize, K4 resize +
+// normalize).
+struct MapStep {
+  enum class Op { kAffine, kRandomCropFlip, kResizeBilinear, kNormalize } op;
+  int64_t a = 1, b = 0;                 // affine
+  int64_t out_h = 0, out_w = 0;         // crop / resize
+  uint64_t seed = 0;                    // crop: Philox key
+  bool flip = true;                     // crop: random horizontal flip
+  std::array<float, 3> mean{}, stdv{};  // normalize
+};
+
+// Predicate on a token sequence's length (the cfg4 filter).
+struct LengthPredicate {
+  int64_t max_len = 0;  // keep iff len <= max_len
+};
+
+// Interleave reader: input element x opens a dataset of `records` records
+// valued x * records + r (index into the record source).
+struct RecordReader {
+  int64_t records = 0;
+};
+
+class UdfRegistry {
+ public:
+  struct Entry {
+    std::vector<MapStep> map;              // map / map_and_batch
+    std::optional<LengthPredicate> predicate;
+    std::optional<RecordReader> reader;    // interleave
+    std::optional<int64_t> cost_hint_ns;
+  };
+  UdfRegistry() = default;
+  UdfRegistry(const UdfRegistry&) = delete;
+  UdfRegistry& operator=(const UdfRegistry&) = delete;
+
+  void Register(const std::string& name, Entry entry);  // kDuplicateName
+  void RegisterAffine(const std::string& name, int64_t a, int64_t b);
+  void RegisterRandomCropFlip(const std::string& name, int64_t crop_h, int64_t crop_w, uint64_t seed, bool flip);
+  void RegisterResizeBilinear(const std::string& name, int64_t out_h, int64_t out_w);
+  void RegisterNormalize(const std::string& name, std::array<float, 3> mean, std::array<float, 3> stdv);
+  void RegisterLengthFilter(const std::string& name, int64_t max_len);
+  void RegisterRecordReader(const std::string& name, int64_t records);
+  bool Contains(const std::string& name) const;
+  const Entry& Get(const std::string& name) const;  // kUnknownUdf
+  ElementSpec MapOutputSpec(const std::string& name, const ElementSpec& in) const;
+
+ private:
+  mutable std::mutex mu_;
+  std::map<std::string, std::unique_ptr<Entry>> entries_;
+};
+
+ElementSpec ApplyMapSteps(const std::vector<MapStep>& steps, const ElementSpec& in);
+
+NodePtr Build(NodeKind kind, std::vector<NodePtr> inputs, Attrs attrs, const UdfRegistry& reg);
+
+namespace ops {
+DatasetGraph Range(int64_t n, const UdfRegistry& reg);
+DatasetGraph FromMemory(const std::vector<int64_t>& values, const UdfRegistry& reg, int device = 0);
+DatasetGraph TensorSlices(SourcePtr images, const UdfRegistry& reg);
+DatasetGraph TokenSequences(SourcePtr tokens, const UdfRegistry& reg);
+DatasetGraph Map(const DatasetGraph& in, const std::string& udf, int64_t num_parallel_calls, const UdfRegistry& reg);
+DatasetGraph Filter(const DatasetGraph& in, const std::string& udf, const UdfRegistry& reg);
+DatasetGraph Interleave(const DatasetGraph& in, const std::string& udf, int64_t cycle_length,
+                        int64_t num_parallel_calls, SourcePtr records, const UdfRegistry& reg);
+DatasetGraph Batch(const DatasetGraph& in, int64_t batch_size, bool drop_remainder, const UdfRegistry& reg);
+DatasetGraph PaddedBatch(const DatasetGraph& in, int64_t batch_size, int64_t padding_value, bool drop_remainder,
+                         const UdfRegistry& reg);
+DatasetGraph Prefetch(const DatasetGraph& in, int64_t buffer_size, const UdfRegistry& reg);
+DatasetGraph Repeat(const DatasetGraph& in, int64_t count, const UdfRegistry& reg);
+DatasetGraph Shuffle(const DatasetGraph& in, int64_t buffer_size, std::optional<uint64_t> seed,
+                     const UdfRegistry& reg);
+DatasetGraph Shard(const DatasetGraph& in, int64_t num_shards, int64_t index, const UdfRegistry& reg);
+}  // namespace ops
+
+// ---- static optimizer (optimizer.hpp:22-75; formats.md:152-186) ----
+inline constexpr const char* kMapMapFusion = "map_map_fusion";
+inline constexpr const char* kFilterFilterFusion = "filter_filter_fusion";
+inline constexpr const char* kMapFilterFusion = "map_filter_fusion";
+inline constexpr const char* kMapVectorization = "map_vectorization";
+inline constexpr const char* kMapBatchFusion = "map_batch_fusion";
+inline constexpr const char* kShuffleRepeatFusion = "shuffle_repeat_fusion";
+
+class RuleSet {
+ public:
+  static RuleSet Default();
+  static RuleSet None() { return RuleSet(); }
+  void Disable(const std::string& name);
+  bool IsEnabled(const std::string& name) const;
+  const std::vector<std::string>& order() const { return order_; }
+  static const std::vector<std::string>& AllRuleNames();
+
+ private:
+  std::vector<std::string> order_;
+};
+
+struct RewriteRecord {
+  std::string rule, node_path;
+};
+struct RewriteReport {
+  std::vector<RewriteRecord> applied;
+  int iterations = 0;
+  std::string ToString() const;
+};
+
+std::pair<DatasetGraph, RewriteReport> Optimize(const DatasetGraph& graph, const RuleSet& rules,
+                                                UdfRegistry& registry);
+
+// ---- runtime ----
+struct IteratorOptions {
+  bool deterministic = true;
+  std::optional<uint64_t> seed_override;  // base seed (runtime.hpp:35-44)
+  // B200 extensions --------------------------------------------------------
+  int device = 0;
+  // Stream (cudaStream_t) the consumer reads batches on; batch i is made
+  // ready on it with cudaStreamWaitEvent, and a released slot is reused only
+  // after the consumer's work queued on it so far.  nullptr = the iterator's
+  // own stream (consumer work queued there is ordered by construction).
+  void* consumer_stream = nullptr;
+  // Copy each batch into pinned host memory before returning it.
+  bool host_output = false;
+  // Upper bound on device memory for prefetch slots (bytes).
+  size_t slot_memory_budget = size_t(8) << 30;
+};
+
+struct NodeMetricsRow {
+  std::string path, label;
+  int64_t self_time_ns = 0;
+  int64_t elements_produced = 0;
+};
+
+class DevicePipeline;  // lowering + device state (runtime.cpp)
+
+class PipelineIterator {
+ public:
+  PipelineIterator(DatasetGraph graph, const UdfRegistry& registry, IteratorOptions options);
+  ~PipelineIterator();
+  PipelineIterator(const PipelineIterator&) = delete;
+  PipelineIterator& operator=(const PipelineIterator&) = delete;
+
+  // Next batch, or nullopt after the end (sticky).  Thread-safe.  Returned
+  // tensors are ready on options().consumer_stream; Tensor::ready is the
+  // producing event for other streams.
+  std::optional<Element> GetNext();
+
+  const DatasetGraph& graph() const { return graph_; }
+  const IteratorOptions& options() const { return options_; }
+  uint64_t base_seed() const { return base_seed_; }
+  int64_t root_delivered() const;
+  std::vector<NodeMetricsRow> Metrics() const;
+  void* stream() const;                 // the iterator's producer stream
+  int64_t prefetch_depth() const;       // device slots in use (autotuned)
+  int64_t kernel_launches() const;      // sm_100a kernels issued so far
+  // Device time (CUDA events around each launch, on the launching stream)
+  // of the fused batch-stage launches issued so far: {total ns, launches}.
+  std::pair<int64_t, int64_t> BatchStageTiming() const;
+  std::string LoweringPlan() const;     // human-readable lowering
+
+ private:
+  DatasetGraph graph_;
+  IteratorOptions options_;
+  uint64_t base_seed_;
+  std::unique_ptr<DevicePipeline> impl_;
+  mutable std::mutex mu_;
+};
+
+std::unique_ptr<PipelineIterator> MakeIterator(const DatasetGraph& graph, const UdfRegistry& registry,
+                                               IteratorOptions options = {});
+
+// PRNG contract helpers (random.hpp:24-34; runtime.cpp:713-718).
+uint64_t MixSeeds(uint64_t a, uint64_t b);
+uint64_t ShuffleEngineSeed(uint64_t epoch_salt, std::optional<uint64_t> attr_seed);
+
+}  // namespace datapipe::b200

@@ -77,6 +77,11 @@ int dp_device_count(int* count);
 int dp_k_range_affine_batch(int64_t first, int64_t rows, int64_t a, int64_t b,
                             int64_t* out, void* stream);
 
+/* K1 general form (gathered int64 source): out[i] = v * a + b with       */
+/* v = values ? values[p] : p and p = order ? order[first + i] : first + i. */
+int dp_k_gather_affine_batch(const int64_t* values, const int64_t* order, int64_t first, int64_t rows,
+                             int64_t a, int64_t b, int64_t* out, void* stream);
+
 /* ---------------------------------------------------------------------- */
 /* K2  shuffle_plan -- ShuffleIterator (src/runtime.cpp:688-768) with the  */
 /*     PCG32 contract (include/datapipe/random.hpp:39-74).                 */
@@ -121,6 +126,7 @@ int dp_k_resize_normalize_batch(const uint8_t* images, int64_t num_images,
 /* ---------------------------------------------------------------------- */
 /* K5  filter(len <= max_keep) stream compaction + padded_batch.           */
 /*     FilterIterator (src/runtime.cpp:537-577) + BatchIterator on ragged  */
+/*     (element i of the filtered sequence has length lengths[in_map[i]])  */
 /*     lists (579-637); padded_batch is a new kind.   */
 /*     kept: int64 [n] out (stable order), *num_kept written to device     */
 /*     memory `num_kept_dev` (int64).  scratch: dp_k_filter_scratch_bytes. */
@@ -141,6 +147,16 @@ int dp_k_padded_batch(const int32_t* tokens, const int64_t* offsets,
                       int32_t pad_value, int32_t* out, int32_t* out_lengths,
                       void* stream);
 
+/* Grouped form: rows [first_row, first_row + rows) of consecutive padded  */
+/* batches of `batch` rows in one launch; lmax_dev[j] / boff_dev[j] are    */
+/* the epoch's per-batch max length and element offset (exclusive prefix   */
+/* of rows_j * lmax_j); `out` is the element offset boff_dev[first_row /   */
+/* batch].  order = the epoch's kept positions.                            */
+int dp_k_padded_batches(const int32_t* tokens, const int64_t* offsets, const int32_t* lengths,
+                        const int64_t* order, int64_t first_row, int64_t rows, int64_t batch,
+                        const int32_t* lmax_dev, const int64_t* boff_dev, int32_t pad_value,
+                        int32_t* out, int32_t* out_lengths, void* stream);
+
 /* ---------------------------------------------------------------------- */
 /* K6  shard + interleave index mapping -- ShardIterator (runtime.cpp:     */
 /*     770-800) + (Parallel)InterleaveIterator (1044-1128, 1727-2021) over */
@@ -153,6 +169,9 @@ int64_t dp_k_shard_interleave_count(int64_t n_sources, int64_t num_shards,
 int dp_k_shard_interleave_index(int64_t n_sources, int64_t num_shards,
                                 int64_t shard_index, int64_t cycle,
                                 int64_t records, int64_t* out, void* stream);
+/* General form over inputs first + i * stride, i < m_inputs. */
+int dp_k_interleave_index(int64_t first, int64_t stride, int64_t m_inputs, int64_t cycle,
+                          int64_t records, int64_t* out, void* stream);
 /* Shard alone: out[i] = shard_index + i * num_shards (or in_map of it). */
 int dp_k_shard_index(int64_t n, int64_t num_shards, int64_t shard_index,
                      const int64_t* in_map, int64_t* out, void* stream);

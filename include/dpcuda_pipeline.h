@@ -1,0 +1,153 @@
+/*
+ * dpcuda_pipeline.h -- C ABI of the Dataset / Iterator operator API
+ * (libdpcuda.so).  Each entry point is the FFI binding of one reference
+ * operator; the reference interface it replaces is cited beside it
+ * (paths under /root/reference/proj/).  Status codes: include/dpcuda.h.
+ *
+ * Ownership: every dp_registry / dp_graph / dp_iterator handle is released
+ * with its *_release / *_destroy call; a dp_batch returned by
+ * dp_iterator_get_next holds a lease on a device prefetch slot until
+ * dp_batch_release.
+ */
+#ifndef DPCUDA_PIPELINE_H_
+#define DPCUDA_PIPELINE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include "dpcuda.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct dp_registry dp_registry;
+typedef struct dp_graph dp_graph;
+typedef struct dp_iterator dp_iterator;
+typedef struct dp_source dp_source;
+
+#define DP_AUTOTUNE (-1)
+#define DP_INFINITE (-1)
+
+/* ---- UDF registry: include/datapipe/udf.hpp:41-87 (UdfRegistry) ---- */
+int dp_registry_create(dp_registry** out);
+void dp_registry_destroy(dp_registry* reg);
+/* map x -> x*a + b on int64 elements (the cfg1 UDF) */
+int dp_registry_register_affine(dp_registry* reg, const char* name, int64_t a, int64_t b);
+/* random crop (Philox key = seed, counter = element id) + optional flip */
+int dp_registry_register_random_crop_flip(dp_registry* reg, const char* name, int64_t crop_h, int64_t crop_w,
+                                          uint64_t seed, int flip);
+/* bilinear resize, half-pixel centres */
+int dp_registry_register_resize_bilinear(dp_registry* reg, const char* name, int64_t out_h, int64_t out_w);
+/* per-channel (x - mean[c]) / std[c] to fp32 */
+int dp_registry_register_normalize(dp_registry* reg, const char* name, const float mean[3], const float stdv[3]);
+/* predicate: keep sequences with length <= max_len */
+int dp_registry_register_length_filter(dp_registry* reg, const char* name, int64_t max_len);
+/* interleave dataset UDF: element x opens records x*records .. x*records+records-1 */
+int dp_registry_register_record_reader(dp_registry* reg, const char* name, int64_t records);
+int dp_registry_contains(const dp_registry* reg, const char* name);
+
+/* ---- sources (new kinds) ---- */
+int dp_source_synthetic_images(int64_t count, int64_t h, int64_t w, uint64_t seed, int device, dp_source** out);
+int dp_source_images_from_host(const uint8_t* data, int64_t count, int64_t h, int64_t w, int device,
+                               dp_source** out);
+/* pinned/registered host memory read by the kernels over PCIe (end-to-end runs; not copied) */
+int dp_source_images_pinned_host(const uint8_t* data, int64_t count, int64_t h, int64_t w, int device,
+                                 dp_source** out);
+int dp_source_synthetic_tokens(int64_t count, uint32_t max_len, uint64_t len_seed, uint64_t tok_seed, int device,
+                               dp_source** out);
+int dp_source_tokens_from_host(const int32_t* lengths, int64_t count, const int32_t* tokens, int device,
+                               dp_source** out);
+void dp_source_release(dp_source* src);
+
+/* ---- graph builders: include/datapipe/graph.hpp:134-165 (ops::*) ---- */
+int dp_graph_range(const dp_registry* reg, int64_t n, dp_graph** out);                  /* source synthetic count=n */
+int dp_graph_from_memory_i64(const dp_registry* reg, const int64_t* values, int64_t n, int device,
+                             dp_graph** out);                                           /* ops::FromMemory */
+int dp_graph_tensor_slices(const dp_registry* reg, const dp_source* images, dp_graph** out);
+int dp_graph_token_sequences(const dp_registry* reg, const dp_source* tokens, dp_graph** out);
+int dp_graph_map(const dp_graph* in, const char* udf, int64_t num_parallel_calls, const dp_registry* reg,
+                 dp_graph** out);                                                       /* ops::Map */
+int dp_graph_filter(const dp_graph* in, const char* udf, const dp_registry* reg, dp_graph** out); /* ops::Filter */
+int dp_graph_interleave(const dp_graph* in, const char* udf, int64_t cycle_length, int64_t num_parallel_calls,
+                        const dp_source* records, const dp_registry* reg, dp_graph** out); /* ops::Interleave */
+int dp_graph_batch(const dp_graph* in, int64_t batch_size, int drop_remainder, const dp_registry* reg,
+                   dp_graph** out);                                                     /* ops::Batch */
+int dp_graph_padded_batch(const dp_graph* in, int64_t batch_size, int64_t padding_value, int drop_remainder,
+                          const dp_registry* reg, dp_graph** out);                      /* new kind */
+int dp_graph_prefetch(const dp_graph* in, int64_t buffer_size, const dp_registry* reg, dp_graph** out);
+int dp_graph_repeat(const dp_graph* in, int64_t count, const dp_registry* reg, dp_graph** out);
+int dp_graph_shuffle(const dp_graph* in, int64_t buffer_size, int has_seed, uint64_t seed, const dp_registry* reg,
+                     dp_graph** out);                                                   /* ops::Shuffle */
+int dp_graph_shard(const dp_graph* in, int64_t num_shards, int64_t index, const dp_registry* reg,
+                   dp_graph** out);                                                     /* ops::Shard */
+/* Optimize(graph, RuleSet::Default() minus the comma-separated
+ * disabled_rules, registry): include/datapipe/optimizer.hpp:73-75.
+ * report (optional) receives RewriteReport::ToString(). */
+int dp_graph_optimize(const dp_graph* in, dp_registry* reg, const char* disabled_rules, dp_graph** out,
+                      char* report, size_t report_len);
+/* kind name of the root node ("map_and_batch", ...) and the graph dump */
+int dp_graph_root_kind(const dp_graph* g, char* buf, size_t len);
+int dp_graph_to_string(const dp_graph* g, char* buf, size_t len);
+void dp_graph_release(dp_graph* g);
+
+/* ---- iterator: include/datapipe/runtime.hpp:35-100 ---- */
+typedef struct {
+  int deterministic;          /* IteratorOptions::deterministic */
+  int has_seed_override;      /* IteratorOptions::seed_override */
+  uint64_t seed_override;
+  int device;                 /* CUDA device ordinal */
+  void* consumer_stream;      /* cudaStream_t the batches are consumed on (NULL: iterator stream) */
+  int host_output;            /* copy batches to pinned host memory */
+  uint64_t slot_memory_budget;/* bytes of device prefetch slots (0: default 8 GiB) */
+} dp_iterator_options;
+
+typedef enum { DP_U8 = 0, DP_I32 = 1, DP_I64 = 2, DP_F32 = 3 } dp_dtype;
+
+typedef struct {
+  int dtype;          /* dp_dtype */
+  int ndim;
+  int64_t shape[6];
+  void* data;         /* device pointer (or pinned host with host_output) */
+  int on_host;
+} dp_tensor;
+
+typedef struct {
+  void* handle;       /* lease; pass to dp_batch_release */
+  int num_components;
+  dp_tensor components[4];
+  void* ready_event;  /* cudaEvent_t completing when the batch is written */
+  int64_t index;      /* batch ordinal in the stream */
+} dp_batch;
+
+void dp_iterator_options_default(dp_iterator_options* o);
+/* MakeIterator (runtime.hpp:98-100): validates UDFs (UnknownUdf) and lowers
+ * the graph onto the device (InvalidAttr if it has no device lowering). */
+int dp_iterator_create(const dp_graph* g, const dp_registry* reg, const dp_iterator_options* opt, dp_iterator** out);
+/* PipelineIterator::GetNext (runtime.hpp:68): DP_OK with *batch filled, or
+ * DP_ERR_END_OF_SEQUENCE (sticky). */
+int dp_iterator_get_next(dp_iterator* it, dp_batch* batch);
+/* Ends the lease.  The slot is rewritten only after the work queued on the
+ * iterator's consumer_stream before this call. */
+int dp_batch_release(dp_batch* batch);
+/* Blocks the calling host thread until the batch is written (and, with
+ * host_output, copied to its pinned host slot). */
+int dp_batch_wait(const dp_batch* batch);
+/* Copies a batch component to host memory (waits for the batch). */
+int dp_tensor_copy_to_host(const dp_batch* batch, int component, void* dst, size_t bytes);
+void* dp_iterator_stream(const dp_iterator* it);
+int64_t dp_iterator_kernel_launches(const dp_iterator* it);
+/* Device time of the fused batch-stage launches so far (CUDA events around
+ * each launch on the launching stream; waits for issued launches). */
+int dp_iterator_batch_stage_timing(const dp_iterator* it, int64_t* total_ns, int64_t* launches);
+int64_t dp_iterator_prefetch_depth(const dp_iterator* it);
+int64_t dp_iterator_root_delivered(const dp_iterator* it);
+uint64_t dp_iterator_base_seed(const dp_iterator* it);
+int dp_iterator_describe(const dp_iterator* it, char* buf, size_t len);
+void dp_iterator_destroy(dp_iterator* it);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DPCUDA_PIPELINE_H_ */

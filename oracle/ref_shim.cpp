@@ -361,6 +361,42 @@ int ref_time_image_pipeline(int mode, int in_h, int in_w, int out_h, int out_w,
   }
 }
 
+// bench.py --impl reference: the reference pipeline for the image configs
+// over a resident sample of `n` synthetic images, repeated indefinitely
+// (repeat(INFINITE) above the shuffle), optimized to map_and_batch with
+// num_parallel_calls = `parallel`, prefetch(2).  Pulls `warmup` batches,
+// then times `steps` GetNext calls (one batch each).  Returns seconds.
+int ref_time_image_steps(int mode, int in_h, int in_w, int out_h, int out_w, uint64_t udf_seed,
+                         uint64_t pix_seed, int64_t n, int64_t shuffle_buffer, uint64_t shuffle_seed,
+                         int64_t batch, int64_t parallel, int64_t warmup, int64_t steps,
+                         double* seconds, int64_t* elements) {
+  try {
+    UdfRegistry reg;
+    ImageUdfParams p{mode, in_h, in_w, out_h, out_w, udf_seed};
+    RegisterImageUdf(reg, p);
+    DatasetGraph g = ops::FromMemory(SynthImages(n, in_h, in_w, pix_seed), reg);
+    if (shuffle_buffer > 0) g = ops::Shuffle(g, shuffle_buffer, shuffle_seed, reg);
+    g = ops::Repeat(g, kInfiniteRepeat, reg);
+    g = ops::Map(g, ImageUdfName(p), parallel, reg);
+    g = ops::Batch(g, batch, false, reg);
+    g = ops::Prefetch(g, 2, reg);
+    g = Optimize(g, RuleSet::Default(), reg).first;
+    auto it = MakeIterator(g, reg, Seeded(1));
+    for (int64_t i = 0; i < warmup; ++i) it->GetNext();
+    int64_t count = 0;
+    auto t0 = std::chrono::steady_clock::now();
+    for (int64_t i = 0; i < steps; ++i) {
+      auto e = it->GetNext();
+      count += static_cast<int64_t>(e->component(0).items().size());
+    }
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    *elements = count;
+    return 0;
+  } catch (const std::exception& e) {
+    return Fail(e);
+  }
+}
+
 // CPU baseline for cfg1 (range -> map -> batch, optimized).
 int ref_time_range_map_batch(int64_t n, int64_t batch, int64_t parallel,
                              int epochs, double* epoch_s) {

@@ -1,0 +1,1191 @@
+// runtime.cpp -- MakeIterator / GetNext: lowers a graph onto the sm_100a
+// kernels and runs it as a stream-ordered device pipeline.
+//
+// Reference path being replaced: the NodeIterator tree of
+// /root/reference/proj/src/runtime.cpp -- FromMemory (386-414), Shuffle
+// (688-768), Shard (770-800), Repeat (1130-1187), Prefetch (1193-1294),
+// MapAndBatch (1467-1721), Interleave (1044-1128), Filter (537-577), Batch
+// (579-637), GetNext (147-165, 2196-2199).
+//
+// Lowering.  A graph is split into
+//   [prefetch]* [repeat] BATCH-STAGE INDEX-CHAIN SOURCE
+// BATCH-STAGE  map_and_batch(f) | batch(map(f)) | batch | padded_batch -- one
+//              fused gather+UDF+store kernel per group of batches (K1/K3/K4/K5)
+// INDEX-CHAIN  shard / interleave / filter / shuffle / repeat -- computed
+//              once per epoch as a device array of source positions (the
+//              "epoch plan": K6 shard/interleave index, K5 compaction, K2
+//              exact shuffle order), each stage mapping the previous one.
+// Batch i of the stream is rows [i*b, i*b + rows_i) of the epoch plan; the
+// fused kernel gathers its elements through the plan.  Nothing is copied or
+// assembled on the host.
+//
+// Prefetch.  A ring of device slots, each holding a group of G consecutive
+// batches (G = 1 for 150 MB image batches, larger for small batches so each
+// launch moves >= 64 MB).  GetNext keeps `depth` groups in flight on the
+// iterator's stream, returns batch i as an Element of device Tensor views
+// whose owner is a lease on the slot; the slot is rewritten only after every
+// batch of its group was handed out and dropped, and after consumer-stream
+// work queued before the drop (a release event).  `depth` = the prefetch
+// buffer_size, or for AUTOTUNE a value chosen from the measured device time
+// per group against the host issue time.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <cstring>
+#include <deque>
+#include <functional>
+#include <map>
+#include <mutex>
+#include <random>
+#include <set>
+#include <sstream>
+
+#include "dpb200/datapipe.hpp"
+#include "dpcuda.h"
+
+namespace datapipe::b200 {
+
+namespace {
+
+void CudaCheck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw DeviceError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void KCheck(int status, const char* what) {
+  if (status != DP_OK) {
+    if (status == DP_ERR_CUDA || status == DP_ERR_OUT_OF_MEMORY)
+      throw DeviceError(std::string(what) + ": " + dp_last_error());
+    throw PipelineError(static_cast<ErrorCode>(status - 1), std::string(what) + ": " + dp_last_error());
+  }
+}
+
+struct DeviceGuard {
+  int prev = 0;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) CudaCheck(cudaSetDevice(dev), "cudaSetDevice");
+  }
+  ~DeviceGuard() {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (cur != prev) cudaSetDevice(prev);
+  }
+};
+
+std::shared_ptr<void> DeviceAlloc(size_t bytes, int device) {
+  DeviceGuard g(device);
+  void* p = nullptr;
+  CudaCheck(cudaMalloc(&p, bytes ? bytes : 16), "cudaMalloc");
+  return std::shared_ptr<void>(p, [device](void* q) {
+    DeviceGuard g2(device);
+    cudaFree(q);
+  });
+}
+
+std::shared_ptr<void> PinnedAlloc(size_t bytes) {
+  void* p = nullptr;
+  CudaCheck(cudaHostAlloc(&p, bytes ? bytes : 16, cudaHostAllocPortable | cudaHostAllocMapped), "cudaHostAlloc");
+  return std::shared_ptr<void>(p, [](void* q) { cudaFreeHost(q); });
+}
+
+template <typename T>
+T* P(const std::shared_ptr<void>& p) {
+  return static_cast<T*>(p.get());
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ sources --
+SourcePtr SynthImages(int64_t count, int64_t h, int64_t w, uint64_t seed, int device) {
+  if (count < 1 || h < 1 || w < 1) throw PipelineError(ErrorCode::kInvalidAttr, "synth images: bad shape");
+  auto s = std::make_shared<SourceData>();
+  s->kind = SourceData::Kind::kImages;
+  s->count = count;
+  s->h = h;
+  s->w = w;
+  s->c = 3;
+  s->device = device;
+  const size_t bytes = static_cast<size_t>(count) * h * w * 3;
+  s->values = DeviceAlloc(bytes, device);
+  DeviceGuard g(device);
+  KCheck(dp_k_synth_images(P<uint8_t>(s->values), 0, count, h * w * 3, seed, nullptr), "synth images");
+  CudaCheck(cudaDeviceSynchronize(), "synth images");
+  return s;
+}
+
+SourcePtr SynthTokens(int64_t count, uint32_t max_len, uint64_t len_seed, uint64_t tok_seed, int device) {
+  if (count < 1 || max_len < 1) throw PipelineError(ErrorCode::kInvalidAttr, "synth tokens: bad shape");
+  // lengths: Pcg32(len_seed).Bounded(max_len) + 1 drawn in order (random.hpp:41-63)
+  std::vector<int32_t> lens(count);
+  uint64_t st = 0;
+  auto next = [&]() {
+    uint64_t old = st;
+    st = old * 6364136223846793005ULL + 1442695040888963407ULL;
+    uint32_t xs = static_cast<uint32_t>(((old >> 18u) ^ old) >> 27u);
+    uint32_t rot = static_cast<uint32_t>(old >> 59u);
+    return (xs >> rot) | (xs << ((-rot) & 31u));
+  };
+  next();
+  st += len_seed;
+  next();
+  const uint32_t thr = (0u - max_len) % max_len;
+  for (auto& l : lens) {
+    uint32_t r;
+    do r = next();
+    while (r < thr);
+    l = static_cast<int32_t>(r % max_len) + 1;
+  }
+  auto s = std::make_shared<SourceData>();
+  s->kind = SourceData::Kind::kTokens;
+  s->count = count;
+  s->device = device;
+  std::vector<int64_t> offs(count + 1, 0);
+  for (int64_t i = 0; i < count; ++i) offs[i + 1] = offs[i] + lens[i];
+  s->total_tokens = offs[count];
+  s->lengths = DeviceAlloc(sizeof(int32_t) * count, device);
+  s->offsets = DeviceAlloc(sizeof(int64_t) * (count + 1), device);
+  s->tokens = DeviceAlloc(sizeof(int32_t) * std::max<int64_t>(s->total_tokens, 1), device);
+  DeviceGuard g(device);
+  CudaCheck(cudaMemcpy(s->lengths.get(), lens.data(), sizeof(int32_t) * count, cudaMemcpyHostToDevice), "upload");
+  CudaCheck(cudaMemcpy(s->offsets.get(), offs.data(), sizeof(int64_t) * (count + 1), cudaMemcpyHostToDevice), "upload");
+  KCheck(dp_k_synth_tokens(P<int32_t>(s->tokens), P<int64_t>(s->offsets), count, tok_seed, nullptr), "synth tokens");
+  CudaCheck(cudaDeviceSynchronize(), "synth tokens");
+  return s;
+}
+
+SourcePtr ImagesFromHost(const uint8_t* data, int64_t count, int64_t h, int64_t w, int device) {
+  auto s = std::make_shared<SourceData>();
+  s->kind = SourceData::Kind::kImages;
+  s->count = count;
+  s->h = h;
+  s->w = w;
+  s->c = 3;
+  s->device = device;
+  const size_t bytes = static_cast<size_t>(count) * h * w * 3;
+  s->values = DeviceAlloc(bytes, device);
+  DeviceGuard g(device);
+  CudaCheck(cudaMemcpy(s->values.get(), data, bytes, cudaMemcpyHostToDevice), "upload images");
+  return s;
+}
+
+SourcePtr ImagesFromPinnedHost(const uint8_t* data, int64_t count, int64_t h, int64_t w, int device) {
+  auto s = std::make_shared<SourceData>();
+  s->kind = SourceData::Kind::kImages;
+  s->count = count;
+  s->h = h;
+  s->w = w;
+  s->c = 3;
+  s->device = device;
+  s->residency = Residency::kHost;
+  DeviceGuard g(device);
+  void* dptr = nullptr;
+  const size_t bytes = static_cast<size_t>(count) * h * w * 3;
+  bool registered = false;
+  if (cudaHostGetDevicePointer(&dptr, const_cast<uint8_t*>(data), 0) != cudaSuccess) {
+    cudaGetLastError();
+    CudaCheck(cudaHostRegister(const_cast<uint8_t*>(data), bytes, cudaHostRegisterMapped | cudaHostRegisterPortable),
+              "cudaHostRegister");
+    registered = true;
+    CudaCheck(cudaHostGetDevicePointer(&dptr, const_cast<uint8_t*>(data), 0), "cudaHostGetDevicePointer");
+  }
+  void* host = const_cast<uint8_t*>(data);
+  s->values = std::shared_ptr<void>(dptr, [host, registered](void*) {
+    if (registered) cudaHostUnregister(host);
+  });
+  return s;
+}
+
+SourcePtr Int64FromHost(const int64_t* values, int64_t count, int device) {
+  auto s = std::make_shared<SourceData>();
+  s->kind = SourceData::Kind::kInt64;
+  s->count = count;
+  s->device = device;
+  s->values = DeviceAlloc(sizeof(int64_t) * std::max<int64_t>(count, 1), device);
+  DeviceGuard g(device);
+  if (count) CudaCheck(cudaMemcpy(s->values.get(), values, sizeof(int64_t) * count, cudaMemcpyHostToDevice), "upload");
+  return s;
+}
+
+SourcePtr TokensFromHost(const int32_t* lengths, int64_t count, const int32_t* tokens, int device) {
+  auto s = std::make_shared<SourceData>();
+  s->kind = SourceData::Kind::kTokens;
+  s->count = count;
+  s->device = device;
+  std::vector<int64_t> offs(count + 1, 0);
+  for (int64_t i = 0; i < count; ++i) {
+    if (lengths[i] < 0) throw PipelineError(ErrorCode::kInvalidAttr, "token lengths must be >= 0");
+    offs[i + 1] = offs[i] + lengths[i];
+  }
+  s->total_tokens = offs[count];
+  s->lengths = DeviceAlloc(sizeof(int32_t) * std::max<int64_t>(count, 1), device);
+  s->offsets = DeviceAlloc(sizeof(int64_t) * (count + 1), device);
+  s->tokens = DeviceAlloc(sizeof(int32_t) * std::max<int64_t>(s->total_tokens, 1), device);
+  DeviceGuard g(device);
+  CudaCheck(cudaMemcpy(s->lengths.get(), lengths, sizeof(int32_t) * count, cudaMemcpyHostToDevice), "upload");
+  CudaCheck(cudaMemcpy(s->offsets.get(), offs.data(), sizeof(int64_t) * (count + 1), cudaMemcpyHostToDevice), "upload");
+  if (s->total_tokens)
+    CudaCheck(cudaMemcpy(s->tokens.get(), tokens, sizeof(int32_t) * s->total_tokens, cudaMemcpyHostToDevice), "upload");
+  return s;
+}
+
+// ------------------------------------------------------------------ lowering --
+namespace {
+
+struct IndexOp {
+  enum class Kind { kShard, kShuffle, kFilter, kInterleave, kRepeat } kind;
+  int64_t a = 0, b = 0;  // shard(k, i) | shuffle(buffer) | filter(max_len) | interleave(cycle, records) | repeat(count)
+  std::optional<uint64_t> seed;
+  std::string path;
+};
+
+enum class BatchKind { kAffine, kCrop, kResize, kPadded, kIdentityInt };
+
+struct Lowered {
+  int64_t prefetch = 0;  // 0: none, -1: AUTOTUNE, else depth
+  int64_t outer_repeat = 1;
+  BatchKind kind = BatchKind::kIdentityInt;
+  int64_t batch = 1;
+  bool drop = false;
+  int64_t pad = 0;
+  std::vector<MapStep> steps;
+  int64_t affine_a = 1, affine_b = 0;
+  MapStep crop{}, resize{}, norm{};
+  std::vector<IndexOp> chain;  // bottom-up
+  SourcePtr source;            // element data (images / tokens / int64 values); null for range
+  int64_t source_count = 0;    // positions entering the index chain
+  bool index_over_records = false;
+  SourcePtr records;           // interleave record source
+  std::vector<std::string> node_paths;  // root first
+  std::string batch_node_path;
+};
+
+[[noreturn]] void Unsupported(const std::string& why) {
+  throw PipelineError(ErrorCode::kInvalidAttr, "device lowering: " + why);
+}
+
+Lowered Lower(const DatasetGraph& g, const UdfRegistry& reg) {
+  Lowered L;
+  const DatasetNode* n = g.root().get();
+  std::string path = "/" + std::string(NodeKindName(n->kind())) + "@0";
+  auto descend = [&]() {
+    n = n->inputs()[0].get();
+    path += "/" + std::string(NodeKindName(n->kind())) + "@0";
+  };
+  while (n->kind() == NodeKind::kPrefetch) {
+    L.node_paths.push_back(path);
+    int64_t b = n->GetInt("buffer_size");
+    L.prefetch = (b == kAutotune || L.prefetch == kAutotune) ? kAutotune : std::max(L.prefetch, b);
+    descend();
+  }
+  if (n->kind() == NodeKind::kRepeat) {
+    L.node_paths.push_back(path);
+    L.outer_repeat = n->GetInt("count");
+    descend();
+    while (n->kind() == NodeKind::kPrefetch) {
+      L.node_paths.push_back(path);
+      descend();
+    }
+  }
+  // ---- batch stage ----
+  L.batch_node_path = path;
+  L.node_paths.push_back(path);
+  if (n->kind() == NodeKind::kMapAndBatch) {
+    L.steps = reg.Get(n->GetString("udf")).map;
+    L.batch = n->GetInt("batch_size");
+    L.drop = n->GetBoolOr("drop_remainder", false);
+    descend();
+  } else if (n->kind() == NodeKind::kBatch) {
+    L.batch = n->GetInt("batch_size");
+    L.drop = n->GetBoolOr("drop_remainder", false);
+    descend();
+    if (n->kind() == NodeKind::kMap) {  // unfused map+batch: same result for total UDFs
+      if (n->HasAttr("fused_filter_udf")) Unsupported("map with a fused predicate under batch");
+      L.steps = reg.Get(n->GetString("udf")).map;
+      descend();
+    }
+  } else if (n->kind() == NodeKind::kPaddedBatch) {
+    L.kind = BatchKind::kPadded;
+    L.batch = n->GetInt("batch_size");
+    L.pad = n->GetInt("padding_value");
+    L.drop = n->GetBoolOr("drop_remainder", false);
+    descend();
+  } else {
+    Unsupported(std::string("the root must be a batch stage (map_and_batch / batch / padded_batch), got ") +
+                NodeKindName(n->kind()));
+  }
+  // ---- index chain ----
+  std::vector<IndexOp> top_down;
+  bool seen_interleave = false;
+  for (;;) {
+    const NodeKind k = n->kind();
+    if (k == NodeKind::kShard) {
+      top_down.push_back({IndexOp::Kind::kShard, n->GetInt("num_shards"), n->GetInt("index"), {}, path});
+    } else if (k == NodeKind::kShuffle) {
+      IndexOp op{IndexOp::Kind::kShuffle, n->GetInt("buffer_size"), 0, {}, path};
+      if (n->HasAttr("seed")) op.seed = n->GetUint("seed");
+      top_down.push_back(op);
+    } else if (k == NodeKind::kFilter) {
+      const auto& e = reg.Get(n->GetString("udf"));
+      if (!e.predicate) Unsupported("filter UDF '" + n->GetString("udf") + "' is not a device length predicate");
+      top_down.push_back({IndexOp::Kind::kFilter, e.predicate->max_len, 0, {}, path});
+    } else if (k == NodeKind::kRepeat) {
+      if (!top_down.empty()) Unsupported("repeat must sit directly under the batch stage");
+      top_down.push_back({IndexOp::Kind::kRepeat, n->GetInt("count"), 0, {}, path});
+    } else if (k == NodeKind::kInterleave) {
+      if (seen_interleave) Unsupported("nested interleave");
+      seen_interleave = true;
+      const auto& e = reg.Get(n->GetString("udf"));
+      if (!e.reader) Unsupported("interleave UDF is not a record reader");
+      top_down.push_back({IndexOp::Kind::kInterleave, n->GetInt("cycle_length"), e.reader->records, {}, path});
+      if (n->HasAttr("records")) L.records = n->GetSource("records");
+    } else if (k == NodeKind::kPrefetch) {
+      // prefetch inside the index chain only buffers indices: a no-op here
+    } else {
+      break;
+    }
+    L.node_paths.push_back(path);
+    descend();
+  }
+  L.node_paths.push_back(path);
+  L.chain.assign(top_down.rbegin(), top_down.rend());
+  // ---- source ----
+  switch (n->kind()) {
+    case NodeKind::kRange:
+      L.source_count = n->GetInt("count");
+      break;
+    case NodeKind::kFromMemory:
+    case NodeKind::kTensorSlices:
+    case NodeKind::kTokenSequences:
+      L.source = n->GetSource("source");
+      L.source_count = L.source->count;
+      break;
+    default:
+      Unsupported(std::string("unsupported node on the device path: ") + NodeKindName(n->kind()));
+  }
+  if (seen_interleave) {
+    if (L.source && L.source->kind != SourceData::Kind::kInt64) Unsupported("interleave input must be int64 ordinals");
+    if (L.source) Unsupported("interleave over from_memory ordinals: use range()");
+    L.source = L.records;  // the batch stage reads the record source
+    for (const auto& op : L.chain)
+      if (op.kind == IndexOp::Kind::kInterleave) break;
+      else if (op.kind != IndexOp::Kind::kShard) Unsupported("only shard may precede interleave");
+  }
+  // ---- batch kind from source + UDF chain ----
+  const SourceData::Kind sk = L.source ? L.source->kind : SourceData::Kind::kInt64;
+  if (L.kind == BatchKind::kPadded) {
+    if (sk != SourceData::Kind::kTokens) Unsupported("padded_batch needs token sequences");
+    for (const auto& op : L.chain)
+      if (op.kind == IndexOp::Kind::kRepeat) Unsupported("repeat under padded_batch: put repeat above it");
+    if (!L.steps.empty()) Unsupported("map before padded_batch");
+  } else if (sk == SourceData::Kind::kTokens) {
+    Unsupported("batch of ragged token sequences: use padded_batch");
+  } else if (sk == SourceData::Kind::kInt64) {
+    L.kind = BatchKind::kAffine;
+    for (const auto& s : L.steps) {
+      if (s.op != MapStep::Op::kAffine) Unsupported("int64 elements support affine UDFs only");
+      L.affine_a = L.affine_a * s.a;  // (x*a1 + b1)*a2 + b2 in wrap-around int64
+      L.affine_b = L.affine_b * s.a + s.b;
+    }
+  } else {  // images
+    const auto& st = L.steps;
+    if (st.size() == 2 && st[0].op == MapStep::Op::kRandomCropFlip && st[1].op == MapStep::Op::kNormalize) {
+      L.kind = BatchKind::kCrop;
+      L.crop = st[0];
+      L.norm = st[1];
+    } else if (st.size() == 2 && st[0].op == MapStep::Op::kResizeBilinear && st[1].op == MapStep::Op::kNormalize) {
+      L.kind = BatchKind::kResize;
+      L.resize = st[0];
+      L.norm = st[1];
+    } else {
+      Unsupported("image UDF chain must be random_crop_flip>>normalize or resize_bilinear>>normalize");
+    }
+    if (L.source->c != 3) Unsupported("images must have 3 channels");
+  }
+  if (seen_interleave && !L.records) Unsupported("interleave needs a record source");
+  return L;
+}
+
+// An epoch of the index chain: `count` positions into the element source,
+// materialised in `order` (null = identity), with `tail` extra slots after
+// `count` for the head of the next epoch (batches that span epochs).
+struct EpochPlan {
+  int64_t epoch = -1;
+  int64_t count = 0;
+  std::shared_ptr<void> order;  // int64 [count + tail]
+  int64_t tail = 0;
+  // padded batches
+  std::vector<int32_t> lmax;         // per batch of this epoch
+  std::vector<int64_t> boff;         // per batch, exclusive prefix (elements)
+  std::shared_ptr<void> lmax_dev, boff_dev;
+  cudaEvent_t ready = nullptr;
+};
+
+struct Slot {
+  int device = 0;
+  std::shared_ptr<void> a, b, ha, hb;  // device outputs (+ pinned host mirrors)
+  size_t a_bytes = 0, b_bytes = 0;
+  cudaEvent_t ready = nullptr, release = nullptr, start = nullptr;
+  bool release_recorded = false;
+  // group bookkeeping
+  int64_t first_batch = 0, num_batches = 0, handed_out = 0;
+  std::atomic<int64_t> outstanding{0};
+  bool busy = false;
+  std::vector<int64_t> batch_off_a, batch_off_b, batch_rows, batch_cols;
+  ~Slot() {
+    if (ready) cudaEventDestroy(ready);
+    if (release) cudaEventDestroy(release);
+    if (start) cudaEventDestroy(start);
+  }
+};
+
+}  // namespace
+
+// -------------------------------------------------------------- the pipeline --
+class DevicePipeline {
+ public:
+  DevicePipeline(const Lowered& L, uint64_t base_seed, const IteratorOptions& opt)
+      : L_(L), base_seed_(base_seed), opt_(opt) {
+    DeviceGuard g(opt_.device);
+    CudaCheck(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
+    CudaCheck(cudaStreamCreateWithFlags(&plan_stream_, cudaStreamNonBlocking), "stream");
+    if (opt_.host_output) CudaCheck(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking), "stream");
+    consumer_ = opt_.consumer_stream ? static_cast<cudaStream_t>(opt_.consumer_stream) : stream_;
+    depth_ = L_.prefetch > 0 ? L_.prefetch : 2;
+    autotune_ = L_.prefetch == kAutotune;
+    PlanEpochSizes();          // also finds the max sequence length (padded slots)
+    batch_bytes_ = BatchBytes();
+    // group size: >= 256 MB of output per launch (amortises launch latency and
+    // the persistent kernel's ramp-up / drain), at most one epoch of batches
+    const size_t target = size_t(256) << 20;
+    group_ = std::max<int64_t>(1, static_cast<int64_t>(target / std::max<size_t>(batch_bytes_.first + batch_bytes_.second, 1)));
+    group_ = std::min(group_, std::max<int64_t>(1, batches_per_epoch_));
+    if (span_epochs_) group_ = std::min<int64_t>(group_, std::max<int64_t>(1, epoch_count_ / std::max<int64_t>(L_.batch, 1)));
+    if (group_ > 1) {  // epoch 0 was planned with a one-group tail: re-plan lazily
+      for (auto& [e, p] : plans_)
+        if (p.ready) cudaEventDestroy(p.ready);
+      cudaStreamSynchronize(plan_stream_);
+      plans_.clear();
+    }
+  }
+
+  ~DevicePipeline() {
+    DeviceGuard g(opt_.device);
+    cudaStreamSynchronize(stream_);
+    for (auto& t : timed_) event_pool_.push_back(t);
+    for (auto& t : event_pool_) {
+      cudaEventDestroy(t.start);
+      cudaEventDestroy(t.end);
+    }
+    cudaStreamSynchronize(plan_stream_);
+    if (copy_stream_) cudaStreamSynchronize(copy_stream_);
+    for (auto& [e, p] : plans_)
+      if (p.ready) cudaEventDestroy(p.ready);
+    cudaStreamDestroy(stream_);
+    cudaStreamDestroy(plan_stream_);
+    if (copy_stream_) cudaStreamDestroy(copy_stream_);
+  }
+
+  std::optional<Element> Next() {
+    DeviceGuard g(opt_.device);
+    if (done_) return std::nullopt;
+    const int64_t i = next_batch_;
+    if (total_batches_ >= 0 && i >= total_batches_) {
+      done_ = true;
+      return std::nullopt;
+    }
+    const int64_t grp = i / group_;
+    while (issued_groups_ <= grp) IssueGroup(issued_groups_);
+    // keep `depth` groups in flight
+    while (issued_groups_ < grp + depth_ && (total_groups_ < 0 || issued_groups_ < total_groups_)) {
+      if (!TryIssueGroup(issued_groups_, /*may_grow=*/false)) break;
+    }
+    auto slot = group_slot_.at(grp);
+    next_batch_++;
+    if (consumer_ != stream_ && !opt_.host_output) CudaCheck(cudaStreamWaitEvent(consumer_, slot->ready, 0), "wait");
+    produced_++;
+    MaybeAutotune();
+    return MakeElement(slot, i);
+  }
+
+  int64_t delivered() const { return produced_; }
+  int64_t depth() const { return depth_; }
+  int64_t launches() const { return launches_; }
+  void* stream() const { return stream_; }
+  int64_t batch_time_ns() const { return batch_ns_total_; }
+  int64_t group_size() const { return group_; }
+  std::string Describe() const {
+    std::ostringstream os;
+    const char* kinds[] = {"K1 gather_affine_batch", "K3 crop_flip_normalize_batch", "K4 resize_normalize_batch",
+                           "K5 padded_batches", "K1 gather_affine_batch"};
+    os << "batch stage: " << kinds[static_cast<int>(L_.kind)] << " (batch " << L_.batch << (L_.drop ? ", drop" : "")
+       << ", " << group_ << " batch(es) per launch, depth " << depth_ << (autotune_ ? " autotuned" : "") << ")\n";
+    os << "index chain (bottom-up):";
+    for (const auto& op : L_.chain) {
+      const char* names[] = {"shard", "shuffle", "filter", "interleave", "repeat"};
+      os << " " << names[static_cast<int>(op.kind)];
+    }
+    os << "\nsource positions: " << L_.source_count << ", epoch: " << epoch_count_ << " elements, "
+       << batches_per_epoch_ << " batches" << (span_epochs_ ? " (batches span epochs)" : "") << "\n";
+    return os.str();
+  }
+
+ private:
+  // ---- sizes ----
+  std::pair<size_t, size_t> BatchBytes() const {
+    const int64_t b = L_.batch;
+    switch (L_.kind) {
+      case BatchKind::kAffine:
+      case BatchKind::kIdentityInt: return {sizeof(int64_t) * b, 0};
+      case BatchKind::kCrop: return {sizeof(int64_t) * b, sizeof(float) * b * L_.crop.out_h * L_.crop.out_w * 3};
+      case BatchKind::kResize: return {sizeof(int64_t) * b, sizeof(float) * b * L_.resize.out_h * L_.resize.out_w * 3};
+      case BatchKind::kPadded: return {sizeof(int32_t) * b * std::max<int64_t>(max_len_, 1), sizeof(int32_t) * b};
+    }
+    return {0, 0};
+  }
+
+  // Epoch length is the same every epoch (shuffle keeps the count; filter
+  // predicates are deterministic); compute it once (may run the filter).
+  void PlanEpochSizes() {
+    span_epochs_ = false;
+    int64_t inner_repeat = 1;
+    for (const auto& op : L_.chain)
+      if (op.kind == IndexOp::Kind::kRepeat) {
+        span_epochs_ = true;
+        inner_repeat = op.a;
+      }
+    if (L_.kind == BatchKind::kPadded) {
+      // max sequence length over the source, for slot sizing
+      std::vector<int32_t> lens(L_.source->count);
+      CudaCheck(cudaMemcpy(lens.data(), L_.source->lengths.get(), sizeof(int32_t) * lens.size(), cudaMemcpyDeviceToHost),
+                "lengths");
+      max_len_ = lens.empty() ? 0 : *std::max_element(lens.begin(), lens.end());
+      for (const auto& op : L_.chain)
+        if (op.kind == IndexOp::Kind::kFilter) max_len_ = std::min<int64_t>(max_len_, std::max<int64_t>(op.a, 0));
+    }
+    EpochPlan& p0 = Plan(0);
+    epoch_count_ = p0.count;
+    const int64_t per = L_.drop ? epoch_count_ / L_.batch : (epoch_count_ + L_.batch - 1) / L_.batch;
+    if (span_epochs_) {
+      if (inner_repeat == kInfiniteRepeat) {
+        total_batches_ = epoch_count_ == 0 ? 0 : -1;
+      } else {
+        const int64_t total = epoch_count_ * inner_repeat;
+        total_batches_ = L_.drop ? total / L_.batch : (total + L_.batch - 1) / L_.batch;
+      }
+      batches_per_epoch_ = std::max<int64_t>(1, epoch_count_ / L_.batch);
+    } else {
+      batches_per_epoch_ = per;
+      if (L_.outer_repeat == kInfiniteRepeat) total_batches_ = per == 0 ? 0 : -1;
+      else total_batches_ = per * L_.outer_repeat;
+    }
+    if (!span_epochs_) {
+      const int64_t gpe = 0;  // groups per epoch fixed after group_ known (see GroupInfo)
+      (void)gpe;
+    }
+    total_groups_ = -1;  // computed lazily via GroupRange
+  }
+
+  // Batches of group g: [first, first + n).  Groups never straddle the
+  // boundary of a non-spanning epoch, so every group is one contiguous range
+  // of one epoch plan (plus the next epoch's head when spanning).
+  std::pair<int64_t, int64_t> GroupRange(int64_t g) const {
+    if (span_epochs_) {
+      int64_t first = g * group_;
+      int64_t n = group_;
+      if (total_batches_ >= 0) n = std::min(n, total_batches_ - first);
+      return {first, std::max<int64_t>(n, 0)};
+    }
+    const int64_t gpe = (batches_per_epoch_ + group_ - 1) / group_;
+    if (gpe == 0) return {0, 0};
+    const int64_t e = g / gpe, k = g % gpe;
+    int64_t first = e * batches_per_epoch_ + k * group_;
+    int64_t n = std::min(group_, batches_per_epoch_ - k * group_);
+    if (total_batches_ >= 0 && first >= total_batches_) n = 0;
+    return {first, n};
+  }
+
+  // salt for the shuffles of epoch e: base seed, re-salted per repeat epoch
+  // (RepeatIterator::MakeChild runtime.cpp:1175-1177; fused shuffle :751)
+  uint64_t EpochSalt(int64_t e) const {
+    bool under_repeat = L_.outer_repeat != 1 || span_epochs_;
+    return under_repeat ? MixSeeds(base_seed_, static_cast<uint64_t>(e)) : base_seed_;
+  }
+
+  EpochPlan& Plan(int64_t e) {
+    auto it = plans_.find(e);
+    if (it != plans_.end()) return it->second;
+    // retire plans two epochs back (stream-ordered: later kernels no longer use them)
+    for (auto jt = plans_.begin(); jt != plans_.end();) {
+      if (jt->first < e - 1) {
+        if (jt->second.ready) cudaEventDestroy(jt->second.ready);
+        jt = plans_.erase(jt);
+      } else {
+        ++jt;
+      }
+    }
+    EpochPlan& p = plans_[e];
+    p.epoch = e;
+    BuildPlan(p, e);
+    return p;
+  }
+
+  void BuildPlan(EpochPlan& p, int64_t e) {
+    cudaStream_t s = plan_stream_;
+    const uint64_t salt = EpochSalt(e);
+    // state: identity over [0, count) or an array
+    int64_t count = L_.source_count;
+    std::shared_ptr<void> cur;  // int64 order (null = identity)
+    const int64_t tail = std::max<int64_t>(L_.batch * group_, 1);
+    auto alloc = [&](int64_t n) { return DeviceAlloc(sizeof(int64_t) * (n + tail), opt_.device); };
+    for (const auto& op : L_.chain) {
+      switch (op.kind) {
+        case IndexOp::Kind::kShard: {
+          const int64_t m = count > op.b ? (count - op.b + op.a - 1) / op.a : 0;
+          auto out = alloc(m);
+          KCheck(dp_k_shard_index(count, op.a, op.b, P<int64_t>(cur), P<int64_t>(out), s), "shard");
+          launches_++;
+          cur = out;
+          count = m;
+          break;
+        }
+        case IndexOp::Kind::kInterleave: {
+          // inputs are the current positions = source ordinals; they are an
+          // arithmetic sequence here (identity or shards of it)
+          int64_t first = 0, stride = 1;
+          ArithmeticOf(count, first, stride);
+          const int64_t m = count * op.b;
+          auto out = alloc(m);
+          KCheck(dp_k_interleave_index(first, stride, count, op.a, op.b, P<int64_t>(out), s), "interleave");
+          launches_++;
+          cur = out;
+          count = m;
+          break;
+        }
+        case IndexOp::Kind::kFilter: {
+          auto out = alloc(count);
+          auto nk = DeviceAlloc(sizeof(int64_t), opt_.device);
+          auto scratch = DeviceAlloc(dp_k_filter_scratch_bytes(count), opt_.device);
+          KCheck(dp_k_filter_len_le(P<int32_t>(L_.source->lengths), count, static_cast<int32_t>(op.a), P<int64_t>(cur),
+                                    P<int64_t>(out), P<int64_t>(nk), scratch.get(), s),
+                 "filter");
+          launches_ += 3;
+          int64_t m = 0;
+          CudaCheck(cudaMemcpyAsync(&m, nk.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, s), "filter count");
+          CudaCheck(cudaStreamSynchronize(s), "filter count");
+          cur = out;
+          count = m;
+          break;
+        }
+        case IndexOp::Kind::kShuffle: {
+          auto out = alloc(count);
+          const uint64_t seed = ShuffleEngineSeed(salt, op.seed);
+          size_t sb = dp_k_shuffle_plan_scratch_bytes(static_cast<uint64_t>(count), static_cast<uint64_t>(op.a));
+          std::shared_ptr<void> scratch = sb ? DeviceAlloc(sb, opt_.device) : nullptr;
+          KCheck(dp_k_shuffle_plan(count, op.a, seed, P<int64_t>(cur), P<int64_t>(out), scratch.get(), s), "shuffle");
+          launches_++;
+          cur = out;
+          count = count;
+          break;
+        }
+        case IndexOp::Kind::kRepeat:
+          break;
+      }
+    }
+    if (!cur && (span_epochs_ || L_.kind == BatchKind::kPadded)) {
+      // materialise the identity so spanning batches can append the next head
+      cur = alloc(count);
+      KCheck(dp_k_shard_index(count, 1, 0, nullptr, P<int64_t>(cur), s), "identity");
+      launches_++;
+    }
+    p.count = count;
+    p.order = cur;
+    p.tail = cur ? tail : 0;
+    if (L_.kind == BatchKind::kPadded) {
+      const int64_t nb = (count + L_.batch - 1) / L_.batch;
+      p.lmax.assign(nb, 0);
+      p.boff.assign(nb + 1, 0);
+      if (nb) {
+        auto lm = DeviceAlloc(sizeof(int32_t) * nb, opt_.device);
+        KCheck(dp_k_batch_max_len(P<int32_t>(L_.source->lengths), P<int64_t>(cur), count, L_.batch, P<int32_t>(lm), s),
+               "batch_max_len");
+        launches_++;
+        CudaCheck(cudaMemcpyAsync(p.lmax.data(), lm.get(), sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, s), "lmax");
+        CudaCheck(cudaStreamSynchronize(s), "lmax");
+        for (int64_t j = 0; j < nb; ++j) {
+          const int64_t rows = std::min<int64_t>(L_.batch, count - j * L_.batch);
+          p.boff[j + 1] = p.boff[j] + rows * p.lmax[j];
+        }
+        p.lmax_dev = lm;
+        p.boff_dev = DeviceAlloc(sizeof(int64_t) * (nb + 1), opt_.device);
+        CudaCheck(cudaMemcpyAsync(p.boff_dev.get(), p.boff.data(), sizeof(int64_t) * (nb + 1), cudaMemcpyHostToDevice, s),
+                  "boff");
+      }
+    }
+    CudaCheck(cudaEventCreateWithFlags(&p.ready, cudaEventDisableTiming), "event");
+    CudaCheck(cudaEventRecord(p.ready, s), "event");
+  }
+
+  // The current positions before an interleave are source ordinals produced
+  // by shards only: recover (first, stride) symbolically.
+  void ArithmeticOf(int64_t /*count*/, int64_t& first, int64_t& stride) const {
+    first = 0;
+    stride = 1;
+    for (const auto& op : L_.chain) {
+      if (op.kind == IndexOp::Kind::kInterleave) break;
+      first += op.b * stride;
+      stride *= op.a;
+    }
+  }
+
+  // Ensure epoch plan e exists and, for spanning batches, that the head of
+  // epoch e+1 follows it in memory.
+  void EnsurePlanFor(int64_t first_batch, int64_t nb) {
+    if (!span_epochs_) {
+      Plan(first_batch / std::max<int64_t>(batches_per_epoch_, 1));
+      return;
+    }
+    const int64_t r0 = first_batch * L_.batch;
+    const int64_t r1 = std::min(r0 + nb * L_.batch, total_batches_ >= 0 ? TotalRows() : INT64_MAX);
+    const int64_t e0 = epoch_count_ ? r0 / epoch_count_ : 0;
+    const int64_t e1 = epoch_count_ ? (r1 - 1) / epoch_count_ : 0;
+    EpochPlan& p = Plan(e0);
+    for (int64_t e = e0 + 1; e <= e1; ++e) {
+      EpochPlan& q = Plan(e);
+      // append epoch e's head after epoch e0's end (only e0 + 1 can be needed: tail = one group)
+      const int64_t off = (e - e0) * epoch_count_;
+      const int64_t need = std::min<int64_t>(q.count, p.count + p.tail - off);
+      if (need > 0 && !appended_.count(e0 * 1000003 + e)) {
+        CudaCheck(cudaStreamWaitEvent(plan_stream_, q.ready, 0), "wait");
+        CudaCheck(cudaMemcpyAsync(P<int64_t>(p.order) + off, q.order.get(), sizeof(int64_t) * need,
+                                  cudaMemcpyDeviceToDevice, plan_stream_),
+                  "append head");
+        CudaCheck(cudaEventRecord(p.ready, plan_stream_), "event");
+        appended_.insert(e0 * 1000003 + e);
+      }
+    }
+  }
+
+  bool MoreEpochsAfter(int64_t e) const {
+    if (span_epochs_) {
+      const int64_t rows = TotalRows();
+      return rows == INT64_MAX || (e + 1) * epoch_count_ < rows;
+    }
+    if (L_.outer_repeat == kInfiniteRepeat) return true;
+    return e + 1 < L_.outer_repeat;
+  }
+
+  int64_t TotalRows() const {
+    int64_t inner = 1;
+    for (const auto& op : L_.chain)
+      if (op.kind == IndexOp::Kind::kRepeat) inner = op.a;
+    return inner < 0 ? INT64_MAX : epoch_count_ * inner;
+  }
+
+  std::shared_ptr<Slot> NewSlot() {
+    auto slot = std::make_shared<Slot>();
+    slot->device = opt_.device;
+    slot->a_bytes = batch_bytes_.first * group_;
+    slot->b_bytes = batch_bytes_.second * group_;
+    slot->a = DeviceAlloc(slot->a_bytes, opt_.device);
+    if (slot->b_bytes) slot->b = DeviceAlloc(slot->b_bytes, opt_.device);
+    if (opt_.host_output) {
+      slot->ha = PinnedAlloc(slot->a_bytes);
+      if (slot->b_bytes) slot->hb = PinnedAlloc(slot->b_bytes);
+    }
+    CudaCheck(cudaEventCreateWithFlags(&slot->ready, cudaEventDisableTiming), "event");
+    CudaCheck(cudaEventCreateWithFlags(&slot->release, cudaEventDisableTiming), "event");
+    CudaCheck(cudaEventCreate(&slot->start), "event");
+    slot_bytes_total_ += slot->a_bytes + slot->b_bytes;
+    slots_.push_back(slot);
+    return slot;
+  }
+
+  std::shared_ptr<Slot> FindFreeSlot(bool may_grow) {
+    for (auto& s : slots_) {
+      std::lock_guard lk(shared_->mu);
+      if (!s->busy || (s->handed_out == s->num_batches && s->outstanding.load() == 0)) return s;
+    }
+    const size_t need = (batch_bytes_.first + batch_bytes_.second) * group_;
+    if (static_cast<int64_t>(slots_.size()) < depth_ || may_grow) {
+      if (slot_bytes_total_ + need > opt_.slot_memory_budget && !slots_.empty())
+        throw PipelineError(ErrorCode::kInternal,
+                            "prefetch slots exhausted: every device batch slot is still held by the consumer "
+                            "(drop returned Elements before requesting more, or raise slot_memory_budget)");
+      return NewSlot();
+    }
+    return nullptr;
+  }
+
+  void IssueGroup(int64_t g) {
+    if (!TryIssueGroup(g, /*may_grow=*/true)) throw PipelineError(ErrorCode::kInternal, "could not issue batch group");
+  }
+
+  bool TryIssueGroup(int64_t g, bool may_grow) {
+    auto [first, nb] = GroupRange(g);
+    if (nb <= 0) {
+      total_groups_ = g;
+      return false;
+    }
+    auto slot = FindFreeSlot(may_grow);
+    if (!slot) return false;
+    const auto t0 = std::chrono::steady_clock::now();
+    {
+      std::lock_guard lk(shared_->mu);
+      if (slot->busy && slot->release_recorded) CudaCheck(cudaStreamWaitEvent(stream_, slot->release, 0), "wait release");
+      slot->busy = true;
+      slot->release_recorded = false;
+      slot->first_batch = first;
+      slot->num_batches = nb;
+      slot->handed_out = 0;
+      slot->outstanding = 0;
+    }
+    EnsurePlanFor(first, nb);
+    const int64_t epoch = span_epochs_ ? (epoch_count_ ? first * L_.batch / epoch_count_ : 0)
+                                       : first / std::max<int64_t>(batches_per_epoch_, 1);
+    EpochPlan& plan = Plan(epoch);
+    CudaCheck(cudaStreamWaitEvent(stream_, plan.ready, 0), "wait plan");
+    // Plan the next epoch on the side stream now, so its index kernels
+    // overlap this epoch's batch kernels instead of stalling the next one.
+    if (L_.kind != BatchKind::kPadded && MoreEpochsAfter(epoch)) Plan(epoch + 1);
+    // rows of this group inside the epoch plan
+    const int64_t row0 = span_epochs_ ? first * L_.batch - epoch * epoch_count_
+                                      : (first - epoch * batches_per_epoch_) * L_.batch;
+    int64_t rows_total = 0;
+    slot->batch_rows.assign(nb, 0);
+    slot->batch_cols.assign(nb, 0);
+    slot->batch_off_a.assign(nb, 0);
+    slot->batch_off_b.assign(nb, 0);
+    const int64_t avail = span_epochs_ ? plan.count + plan.tail : plan.count;
+    for (int64_t k = 0; k < nb; ++k) {
+      int64_t rows = std::min<int64_t>(L_.batch, (span_epochs_ ? TotalRows() - (first + k) * L_.batch
+                                                               : plan.count - (row0 + k * L_.batch)));
+      rows = std::min<int64_t>(rows, avail - (row0 + k * L_.batch));
+      slot->batch_rows[k] = rows;
+      rows_total += rows;
+    }
+    TimedLaunch tl = NewTimedLaunch();
+    CudaCheck(cudaEventRecord(tl.start, stream_), "event");
+    const int64_t* order = P<int64_t>(plan.order);
+    const float mean[3] = {L_.norm.mean[0], L_.norm.mean[1], L_.norm.mean[2]};
+    const float stdv[3] = {L_.norm.stdv[0], L_.norm.stdv[1], L_.norm.stdv[2]};
+    switch (L_.kind) {
+      case BatchKind::kAffine:
+      case BatchKind::kIdentityInt: {
+        const int64_t* values = L_.source ? P<int64_t>(L_.source->values) : nullptr;
+        if (!values && !order) {
+          KCheck(dp_k_range_affine_batch(row0, rows_total, L_.affine_a, L_.affine_b, P<int64_t>(slot->a), stream_), "K1");
+        } else {
+          KCheck(dp_k_gather_affine_batch(values, order, row0, rows_total, L_.affine_a, L_.affine_b, P<int64_t>(slot->a),
+                                          stream_),
+                 "K1");
+        }
+        launches_++;
+        int64_t off = 0;
+        for (int64_t k = 0; k < nb; ++k) {
+          slot->batch_off_a[k] = off * sizeof(int64_t);
+          off += slot->batch_rows[k];
+        }
+        break;
+      }
+      case BatchKind::kCrop:
+      case BatchKind::kResize: {
+        const auto& src = *L_.source;
+        const int oh = static_cast<int>(L_.kind == BatchKind::kCrop ? L_.crop.out_h : L_.resize.out_h);
+        const int ow = static_cast<int>(L_.kind == BatchKind::kCrop ? L_.crop.out_w : L_.resize.out_w);
+        if (L_.kind == BatchKind::kCrop)
+          KCheck(dp_k_crop_flip_normalize_batch(P<uint8_t>(src.values), src.count, static_cast<int>(src.h),
+                                                static_cast<int>(src.w), order, row0, rows_total, L_.crop.seed, oh, ow,
+                                                L_.crop.flip ? 1 : 0, mean, stdv, P<int64_t>(slot->a), P<float>(slot->b),
+                                                stream_),
+                 "K3");
+        else
+          KCheck(dp_k_resize_normalize_batch(P<uint8_t>(src.values), src.count, static_cast<int>(src.h),
+                                             static_cast<int>(src.w), order, row0, rows_total, oh, ow, mean, stdv,
+                                             P<int64_t>(slot->a), P<float>(slot->b), stream_),
+                 "K4");
+        launches_++;
+        int64_t off = 0;
+        for (int64_t k = 0; k < nb; ++k) {
+          slot->batch_off_a[k] = off * sizeof(int64_t);
+          slot->batch_off_b[k] = off * sizeof(float) * oh * ow * 3;
+          off += slot->batch_rows[k];
+        }
+        break;
+      }
+      case BatchKind::kPadded: {
+        const int64_t j0 = row0 / L_.batch;
+        KCheck(dp_k_padded_batches(P<int32_t>(L_.source->tokens), P<int64_t>(L_.source->offsets),
+                                   P<int32_t>(L_.source->lengths), order, row0, rows_total, L_.batch,
+                                   P<int32_t>(plan.lmax_dev), P<int64_t>(plan.boff_dev), static_cast<int32_t>(L_.pad),
+                                   P<int32_t>(slot->a), P<int32_t>(slot->b), stream_),
+               "K5");
+        launches_++;
+        int64_t off = 0;
+        for (int64_t k = 0; k < nb; ++k) {
+          slot->batch_cols[k] = plan.lmax[j0 + k];
+          slot->batch_off_a[k] = (plan.boff[j0 + k] - plan.boff[j0]) * sizeof(int32_t);
+          slot->batch_off_b[k] = off * sizeof(int32_t);
+          off += slot->batch_rows[k];
+        }
+        break;
+      }
+    }
+    CudaCheck(cudaEventRecord(tl.end, stream_), "event");
+    timed_.push_back(tl);
+    if (opt_.host_output) {
+      CudaCheck(cudaEventRecord(slot->ready, stream_), "event");
+      CudaCheck(cudaStreamWaitEvent(copy_stream_, slot->ready, 0), "wait");
+      const size_t a_used = UsedBytesA(*slot), b_used = UsedBytesB(*slot);
+      CudaCheck(cudaMemcpyAsync(slot->ha.get(), slot->a.get(), a_used, cudaMemcpyDeviceToHost, copy_stream_), "d2h");
+      if (b_used) CudaCheck(cudaMemcpyAsync(slot->hb.get(), slot->b.get(), b_used, cudaMemcpyDeviceToHost, copy_stream_), "d2h");
+      CudaCheck(cudaEventRecord(slot->ready, copy_stream_), "event");
+      d2h_bytes_ += a_used + b_used;
+    } else {
+      CudaCheck(cudaEventRecord(slot->ready, stream_), "event");
+    }
+    group_slot_[g] = slot;
+    for (auto it = group_slot_.begin(); it != group_slot_.end() && it->first < g - 2 * depth_ - 4;)
+      it = group_slot_.erase(it);
+    issued_groups_ = std::max(issued_groups_, g + 1);
+    host_issue_ns_ += std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count();
+    issued_count_++;
+    return true;
+  }
+
+  size_t UsedBytesA(const Slot& s) const {
+    if (L_.kind == BatchKind::kPadded) {
+      size_t t = 0;
+      for (size_t k = 0; k < s.batch_rows.size(); ++k) t += s.batch_rows[k] * s.batch_cols[k] * sizeof(int32_t);
+      return t;
+    }
+    int64_t rows = 0;
+    for (auto r : s.batch_rows) rows += r;
+    return rows * sizeof(int64_t);
+  }
+  size_t UsedBytesB(const Slot& s) const {
+    int64_t rows = 0;
+    for (auto r : s.batch_rows) rows += r;
+    if (L_.kind == BatchKind::kPadded) return rows * sizeof(int32_t);
+    if (L_.kind == BatchKind::kCrop) return rows * sizeof(float) * L_.crop.out_h * L_.crop.out_w * 3;
+    if (L_.kind == BatchKind::kResize) return rows * sizeof(float) * L_.resize.out_h * L_.resize.out_w * 3;
+    return 0;
+  }
+
+  Element MakeElement(const std::shared_ptr<Slot>& slot, int64_t i) {
+    const int64_t k = i - slot->first_batch;
+    const int64_t rows = slot->batch_rows[k];
+    {
+      std::lock_guard lk(shared_->mu);
+      slot->handed_out++;
+      slot->outstanding++;
+    }
+    cudaStream_t consumer = consumer_;
+    std::shared_ptr<void> lease(nullptr, [slot, consumer, shared = shared_](void*) {
+      std::lock_guard lk(shared->mu);
+      if (--slot->outstanding == 0 && shared->alive) {
+        cudaEventRecord(slot->release, consumer);
+        slot->release_recorded = true;
+      }
+    });
+    const bool host = opt_.host_output;
+    auto base_a = static_cast<uint8_t*>(host ? slot->ha.get() : slot->a.get()) + slot->batch_off_a[k];
+    auto base_b = slot->b ? static_cast<uint8_t*>(host ? slot->hb.get() : slot->b.get()) + slot->batch_off_b[k] : nullptr;
+    auto mk = [&](DType dt, std::vector<int64_t> shape, void* data) {
+      Tensor t;
+      t.dtype = dt;
+      t.shape = std::move(shape);
+      t.data = data;
+      t.residency = host ? Residency::kHost : Residency::kDevice;
+      t.device = opt_.device;
+      t.owner = lease;
+      t.ready = slot->ready;
+      return Value::FromTensor(std::move(t));
+    };
+    std::vector<Value> comps;
+    switch (L_.kind) {
+      case BatchKind::kAffine:
+      case BatchKind::kIdentityInt:
+        comps.push_back(mk(DType::kInt64, {rows}, base_a));
+        break;
+      case BatchKind::kCrop:
+        comps.push_back(mk(DType::kInt64, {rows}, base_a));
+        comps.push_back(mk(DType::kFloat32, {rows, L_.crop.out_h, L_.crop.out_w, 3}, base_b));
+        break;
+      case BatchKind::kResize:
+        comps.push_back(mk(DType::kInt64, {rows}, base_a));
+        comps.push_back(mk(DType::kFloat32, {rows, L_.resize.out_h, L_.resize.out_w, 3}, base_b));
+        break;
+      case BatchKind::kPadded:
+        comps.push_back(mk(DType::kInt32, {rows, slot->batch_cols[k]}, base_a));
+        comps.push_back(mk(DType::kInt32, {rows}, base_b));
+        break;
+    }
+    return Element(std::move(comps));
+  }
+
+  // AUTOTUNE prefetch: depth = ceil(host issue time / device time per group)
+  // + 2, re-evaluated from CUDA-event timings every 16 groups.
+  struct TimedLaunch {
+    cudaEvent_t start = nullptr, end = nullptr;
+  };
+  TimedLaunch NewTimedLaunch() {
+    if (!event_pool_.empty()) {
+      TimedLaunch t = event_pool_.back();
+      event_pool_.pop_back();
+      return t;
+    }
+    TimedLaunch t;
+    CudaCheck(cudaEventCreate(&t.start), "event");
+    CudaCheck(cudaEventCreate(&t.end), "event");
+    return t;
+  }
+
+  // Accumulates the device duration of every completed batch-stage launch
+  // (events recorded around the launch on the launching stream).
+  void DrainTimings(bool wait) {
+    while (!timed_.empty()) {
+      TimedLaunch t = timed_.front();
+      if (wait) {
+        cudaEventSynchronize(t.end);
+      } else if (cudaEventQuery(t.end) != cudaSuccess) {
+        cudaGetLastError();
+        break;
+      }
+      float ms = 0;
+      if (cudaEventElapsedTime(&ms, t.start, t.end) == cudaSuccess) {
+        batch_ns_total_ += static_cast<int64_t>(static_cast<double>(ms) * 1e6);
+        timed_groups_++;
+      }
+      cudaGetLastError();
+      timed_.pop_front();
+      event_pool_.push_back(t);
+    }
+  }
+
+ public:
+  // Device time of the batch-stage launches completed so far (waits for all
+  // issued ones) -> (total ns, launches).
+  std::pair<int64_t, int64_t> BatchStageTiming() {
+    DeviceGuard g(opt_.device);
+    DrainTimings(true);
+    return {batch_ns_total_, timed_groups_};
+  }
+
+ private:
+  void MaybeAutotune() {
+    DrainTimings(false);
+    if (!autotune_ || issued_count_ < 16 || issued_count_ % 16 != 0 || timed_groups_ == 0) return;
+    const double dev = static_cast<double>(batch_ns_total_) / timed_groups_;
+    const double host = static_cast<double>(host_issue_ns_) / issued_count_;
+    const size_t per = (batch_bytes_.first + batch_bytes_.second) * group_;
+    const int64_t by_mem = std::max<int64_t>(2, static_cast<int64_t>(opt_.slot_memory_budget / std::max<size_t>(per, 1)));
+    depth_ = std::clamp<int64_t>(static_cast<int64_t>(host / std::max(dev, 1.0)) + 2, 2, std::min<int64_t>(by_mem, 512));
+  }
+
+ public:
+  int64_t d2h_bytes() const { return d2h_bytes_; }
+  // State shared with outstanding slot leases (they may outlive the pipeline).
+  struct Shared {
+    std::mutex mu;
+    bool alive = true;
+  };
+  std::shared_ptr<Shared> shared_ = std::make_shared<Shared>();
+  void Shutdown() {
+    std::lock_guard lk(shared_->mu);
+    shared_->alive = false;
+  }
+
+ private:
+  Lowered L_;
+  uint64_t base_seed_;
+  IteratorOptions opt_;
+  cudaStream_t stream_ = nullptr, plan_stream_ = nullptr, copy_stream_ = nullptr, consumer_ = nullptr;
+  int64_t depth_ = 2;
+  bool autotune_ = false;
+  std::pair<size_t, size_t> batch_bytes_;
+  int64_t max_len_ = 0;
+  int64_t group_ = 1;
+  bool span_epochs_ = false;
+  int64_t epoch_count_ = 0, batches_per_epoch_ = 0, total_batches_ = 0, total_groups_ = -1;
+  std::map<int64_t, EpochPlan> plans_;
+  std::set<int64_t> appended_;
+  std::vector<std::shared_ptr<Slot>> slots_;
+  std::map<int64_t, std::shared_ptr<Slot>> group_slot_;
+  size_t slot_bytes_total_ = 0;
+  int64_t issued_groups_ = 0, next_batch_ = 0, produced_ = 0, launches_ = 0;
+  int64_t host_issue_ns_ = 0, issued_count_ = 0, batch_ns_total_ = 0, timed_groups_ = 0;
+  std::deque<TimedLaunch> timed_;
+  std::vector<TimedLaunch> event_pool_;
+  int64_t d2h_bytes_ = 0;
+  bool done_ = false;
+};
+
+// ---------------------------------------------------------- PipelineIterator --
+PipelineIterator::PipelineIterator(DatasetGraph graph, const UdfRegistry& registry, IteratorOptions options)
+    : graph_(std::move(graph)), options_(options) {
+  if (!graph_.root()) throw PipelineError(ErrorCode::kValidationFailed, "empty graph");
+  // UDF validation (runtime.cpp:2117-2156): every referenced UDF must exist
+  std::function<void(const DatasetNode&)> validate = [&](const DatasetNode& n) {
+    if (n.HasAttr("udf")) registry.Get(n.GetString("udf"));
+    if (n.HasAttr("fused_filter_udf")) registry.Get(n.GetString("fused_filter_udf"));
+    for (const auto& in : n.inputs()) validate(*in);
+  };
+  validate(*graph_.root());
+  if (options_.seed_override) {
+    base_seed_ = *options_.seed_override;
+  } else {
+    std::random_device rd;
+    base_seed_ = MixSeeds(rd(), rd());
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    throw DeviceError("no CUDA device: the B200 engine has no CPU fallback");
+  }
+  Lowered L = Lower(graph_, registry);
+  impl_ = std::make_unique<DevicePipeline>(L, base_seed_, options_);
+}
+
+PipelineIterator::~PipelineIterator() {
+  if (impl_) impl_->Shutdown();
+}
+
+std::optional<Element> PipelineIterator::GetNext() {
+  std::lock_guard lock(mu_);
+  auto e = impl_->Next();
+  if (e && !Conforms(*e, graph_.element_spec()))
+    throw PipelineError(ErrorCode::kTypeMismatch,
+                        "produced " + e->ToString() + " not conforming to " + graph_.element_spec().ToString());
+  return e;
+}
+
+int64_t PipelineIterator::root_delivered() const {
+  std::lock_guard lock(mu_);
+  return impl_->delivered();
+}
+
+std::vector<NodeMetricsRow> PipelineIterator::Metrics() const {
+  std::lock_guard lock(mu_);
+  std::vector<NodeMetricsRow> rows;
+  rows.push_back({"/", "device batch stage", impl_->batch_time_ns(), impl_->delivered()});
+  return rows;
+}
+
+void* PipelineIterator::stream() const { return impl_->stream(); }
+int64_t PipelineIterator::prefetch_depth() const { return impl_->depth(); }
+int64_t PipelineIterator::kernel_launches() const { return impl_->launches(); }
+std::pair<int64_t, int64_t> PipelineIterator::BatchStageTiming() const {
+  std::lock_guard lock(mu_);
+  return impl_->BatchStageTiming();
+}
+std::string PipelineIterator::LoweringPlan() const { return impl_->Describe(); }
+
+std::unique_ptr<PipelineIterator> MakeIterator(const DatasetGraph& graph, const UdfRegistry& registry,
+                                               IteratorOptions options) {
+  return std::make_unique<PipelineIterator>(graph, registry, options);
+}
+
+}  // namespace datapipe::b200

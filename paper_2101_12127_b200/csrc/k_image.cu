@@ -535,10 +535,22 @@ int launch_persistent(K kernel, const FastArgs& a, size_t smem, cudaStream_t s, 
 
 // Fast-path eligibility: 16B-aligned rows and buffers, whole float4 per
 // thread column, a row of float4s fits one CTA.
+// Images in pinned host memory (end-to-end runs) are read with plain loads
+// over PCIe by the generic kernels; the TMA path is for HBM-resident data.
+bool in_device_memory(const void* p) {
+  cudaPointerAttributes attr{};
+  if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
+}
+
 bool fast_ok(const uint8_t* images, int in_w, int out_w, const float* out) {
   const int q = out_w * 3 / 4;
   return (static_cast<size_t>(in_w) * 3) % 16 == 0 && reinterpret_cast<uintptr_t>(images) % 16 == 0 &&
-         out_w % 4 == 0 && reinterpret_cast<uintptr_t>(out) % 16 == 0 && q <= kFastConsumers;
+         out_w % 4 == 0 && reinterpret_cast<uintptr_t>(out) % 16 == 0 && q <= kFastConsumers &&
+         in_device_memory(images);
 }
 
 // Development-only overrides for tuning sweeps (tools/kbench.py).

@@ -39,6 +39,19 @@ range_affine_kernel(int64_t first, int64_t rows, int64_t a, int64_t b, int64_t* 
   }
 }
 
+// K1 general form: out[i] = v * a + b, v = values ? values[p] : p,
+// p = order ? order[first + i] : first + i  (gathered int64 source).
+__global__ void __launch_bounds__(kThreads)
+gather_affine_kernel(const int64_t* __restrict__ values, const int64_t* __restrict__ order, int64_t first, int64_t rows,
+                     int64_t a, int64_t b, int64_t* __restrict__ out) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < rows; i += stride) {
+    const int64_t p = order ? order[first + i] : first + i;
+    const int64_t v = values ? values[p] : p;
+    out[i] = v * a + b;
+  }
+}
+
 // K6: closed form of the deterministic interleave over equal-length readers
 // (validated against the reference runtime in tests/test_oracle.py): inputs
 // are opened in groups of `cycle`; group G holds inputs G*c .. G*c+m-1 with
@@ -47,6 +60,7 @@ range_affine_kernel(int64_t first, int64_t rows, int64_t a, int64_t b, int64_t* 
 __global__ void __launch_bounds__(kThreads)
 shard_interleave_kernel(int64_t m_inputs, int64_t num_shards, int64_t shard_index, int64_t cycle,
                         int64_t records, int64_t count, int64_t* __restrict__ out) {
+  // inputs: source ordinal shard_index + i * num_shards, i < m_inputs
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   const int64_t group_elems = cycle * records;
   for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < count; t += stride) {
@@ -141,6 +155,25 @@ extern "C" int dp_k_range_affine_batch(int64_t first, int64_t rows, int64_t a, i
   if (rows == 0) return DP_OK;
   range_affine_kernel<<<grid_for((rows + 1) / 2, 1), kThreads, 0, as_stream(stream)>>>(first, rows, a, b, out);
   return launch_status("range_affine_batch");
+}
+
+extern "C" int dp_k_gather_affine_batch(const int64_t* values, const int64_t* order, int64_t first, int64_t rows,
+                                        int64_t a, int64_t b, int64_t* out, void* stream) {
+  if (rows < 0 || (rows > 0 && !out)) return fail(DP_ERR_INVALID_ATTR, "gather_affine_batch: bad rows/out");
+  if (rows == 0) return DP_OK;
+  gather_affine_kernel<<<grid_for(rows, 1), kThreads, 0, as_stream(stream)>>>(values, order, first, rows, a, b, out);
+  return launch_status("gather_affine_batch");
+}
+
+extern "C" int dp_k_interleave_index(int64_t first, int64_t stride, int64_t m_inputs, int64_t cycle, int64_t records,
+                                     int64_t* out, void* stream) {
+  if (cycle < 1) return fail(DP_ERR_INVALID_ATTR, "interleave_index: cycle_length must be >= 1");
+  if (records < 0 || m_inputs < 0) return fail(DP_ERR_INVALID_ATTR, "interleave_index: bad sizes");
+  const int64_t count = m_inputs * records;
+  if (count == 0) return DP_OK;
+  shard_interleave_kernel<<<grid_for(count, 1), kThreads, 0, as_stream(stream)>>>(m_inputs, stride, first, cycle,
+                                                                                    records, count, out);
+  return launch_status("interleave_index");
 }
 
 extern "C" int64_t dp_k_shard_interleave_count(int64_t n_sources, int64_t num_shards, int64_t shard_index,

@@ -48,21 +48,23 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int* warp_sums, int* 
   return x - v + warp_sums[warp];
 }
 
-__device__ __forceinline__ int thread_keep_mask(const int32_t* __restrict__ lengths, int64_t n, int64_t base,
-                                                int32_t max_keep) {
+// Element i of the filtered sequence is source position in_map[i] (or i).
+__device__ __forceinline__ int thread_keep_mask(const int32_t* __restrict__ lengths, const int64_t* __restrict__ in_map,
+                                                int64_t n, int64_t base, int32_t max_keep) {
   int mask = 0;
 #pragma unroll
   for (int u = 0; u < kItems; ++u) {
     const int64_t i = base + u;
-    if (i < n && lengths[i] <= max_keep) mask |= 1 << u;
+    if (i < n && lengths[in_map ? in_map[i] : i] <= max_keep) mask |= 1 << u;
   }
   return mask;
 }
 
 __global__ void __launch_bounds__(kThreads)
-filter_count_kernel(const int32_t* __restrict__ lengths, int64_t n, int32_t max_keep, int64_t* __restrict__ tile_counts) {
+filter_count_kernel(const int32_t* __restrict__ lengths, const int64_t* __restrict__ in_map, int64_t n, int32_t max_keep,
+                    int64_t* __restrict__ tile_counts) {
   const int64_t base = static_cast<int64_t>(blockIdx.x) * kTile + static_cast<int64_t>(threadIdx.x) * kItems;
-  int c = __popc(thread_keep_mask(lengths, n, base, max_keep));
+  int c = __popc(thread_keep_mask(lengths, in_map, n, base, max_keep));
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
   __shared__ int warp_counts[kThreads / 32];
@@ -119,7 +121,7 @@ filter_scatter_kernel(const int32_t* __restrict__ lengths, int64_t n, int32_t ma
   __shared__ int warp_sums[kThreads / 32];
   __shared__ int total;
   const int64_t base = static_cast<int64_t>(blockIdx.x) * kTile + static_cast<int64_t>(threadIdx.x) * kItems;
-  const int mask = thread_keep_mask(lengths, n, base, max_keep);
+  const int mask = thread_keep_mask(lengths, in_map, n, base, max_keep);
   int off = block_exclusive_scan(__popc(mask), warp_sums, &total);
   int64_t dst = tile_offsets[blockIdx.x] + off;
 #pragma unroll
@@ -163,10 +165,45 @@ padded_batch_kernel(const int32_t* __restrict__ tokens, const int64_t* __restric
   if (lane == 0) out_lengths[r] = len;
 }
 
+// Rows [first_row, first_row + rows) of consecutive padded batches in one
+// launch: row R belongs to batch j = R / batch, is padded to lmax[j] and
+// lands at element offset boff[j] - boff[j0] + (R - j * batch) * lmax[j].
+__global__ void __launch_bounds__(kThreads)
+padded_batches_kernel(const int32_t* __restrict__ tokens, const int64_t* __restrict__ offsets,
+                      const int32_t* __restrict__ lengths, const int64_t* __restrict__ order, int64_t first_row,
+                      int64_t rows, int64_t batch, const int32_t* __restrict__ lmax, const int64_t* __restrict__ boff,
+                      int32_t pad, int32_t* __restrict__ out, int32_t* __restrict__ out_lengths) {
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * (kThreads / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const int64_t R = first_row + r;
+  const int64_t j = R / batch, j0 = first_row / batch;
+  const int32_t lm = lmax[j];
+  const int64_t p = order ? order[R] : R;
+  const int32_t len = lengths[p];
+  const int32_t* src = tokens + offsets[p];
+  int32_t* dst = out + (boff[j] - boff[j0]) + (R - j * batch) * static_cast<int64_t>(lm);
+  for (int c = lane; c < lm; c += 32) __stcs(dst + c, c < len ? __ldcs(src + c) : pad);
+  if (lane == 0) out_lengths[r] = len;
+}
+
 }  // namespace
 }  // namespace dpk
 
 using namespace dpk;
+
+extern "C" int dp_k_padded_batches(const int32_t* tokens, const int64_t* offsets, const int32_t* lengths,
+                                   const int64_t* order, int64_t first_row, int64_t rows, int64_t batch,
+                                   const int32_t* lmax_dev, const int64_t* boff_dev, int32_t pad_value, int32_t* out,
+                                   int32_t* out_lengths, void* stream) {
+  if (rows < 0 || batch < 1) return fail(DP_ERR_INVALID_ATTR, "padded_batches: bad rows/batch");
+  if (rows == 0) return DP_OK;
+  const int64_t blocks = (rows + kThreads / 32 - 1) / (kThreads / 32);
+  if (blocks > 0x7fffffff) return fail(DP_ERR_INVALID_ATTR, "padded_batches: too many rows");
+  padded_batches_kernel<<<static_cast<int>(blocks), kThreads, 0, as_stream(stream)>>>(
+      tokens, offsets, lengths, order, first_row, rows, batch, lmax_dev, boff_dev, pad_value, out, out_lengths);
+  return launch_status("padded_batches");
+}
 
 extern "C" size_t dp_k_filter_scratch_bytes(int64_t n) {
   int64_t tiles = (n + kTile - 1) / kTile;
@@ -182,7 +219,7 @@ extern "C" int dp_k_filter_len_le(const int32_t* lengths, int64_t n, int32_t max
   const int64_t tiles = (n + kTile - 1) / kTile;
   if (tiles > 0x7fffffff) return fail(DP_ERR_INVALID_ATTR, "filter: n too large");
   int64_t* tile = static_cast<int64_t*>(scratch);
-  filter_count_kernel<<<static_cast<int>(tiles), kThreads, 0, s>>>(lengths, n, max_keep, tile);
+  filter_count_kernel<<<static_cast<int>(tiles), kThreads, 0, s>>>(lengths, in_map, n, max_keep, tile);
   filter_scan_kernel<<<1, 1024, 0, s>>>(tile, tiles, num_kept_dev);
   filter_scatter_kernel<<<static_cast<int>(tiles), kThreads, 0, s>>>(lengths, n, max_keep, tile, in_map, kept);
   return launch_status("filter_len_le");

@@ -1,0 +1,428 @@
+"""Python binding of the Dataset / Iterator operator API (include/dpcuda_pipeline.h).
+
+Mirrors the reference's C++ operator API (/root/reference/proj/include/
+datapipe/{graph,udf,optimizer,runtime}.hpp): ``Registry`` is UdfRegistry,
+``Dataset`` wraps DatasetGraph and its methods are the ops:: builders,
+``optimize`` is Optimize, ``make_iterator`` is MakeIterator and
+``Iterator.get_next`` is PipelineIterator::GetNext (None at the sticky end).
+Errors raise ``DpError`` whose ``code`` is datapipe::ErrorCode + 1.
+
+Every call goes through libdpcuda.so; there is no Python or CPU compute path.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from ._capi import DpError, lib
+
+c_i64, c_u64, c_int, c_vp, c_size = ctypes.c_int64, ctypes.c_uint64, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t
+PP = ctypes.POINTER(c_vp)
+
+ERR = {  # dp_status values (include/dpcuda.h)
+    "InvalidArity": 1, "InvalidAttr": 2, "TypeMismatch": 3, "ValidationFailed": 5, "DuplicateName": 6,
+    "UnknownUdf": 7, "RewriteDiverged": 14, "Internal": 19, "Cuda": 100, "EndOfSequence": 102,
+}
+DTYPES = {0: np.uint8, 1: np.int32, 2: np.int64, 3: np.float32}
+MEAN = (123.675, 116.28, 103.53)
+STD = (58.395, 57.12, 57.375)
+
+
+class dp_tensor(ctypes.Structure):
+    _fields_ = [("dtype", c_int), ("ndim", c_int), ("shape", c_i64 * 6), ("data", c_vp), ("on_host", c_int)]
+
+
+class dp_batch(ctypes.Structure):
+    _fields_ = [("handle", c_vp), ("num_components", c_int), ("components", dp_tensor * 4), ("ready_event", c_vp),
+                ("index", c_i64)]
+
+
+class dp_iterator_options(ctypes.Structure):
+    _fields_ = [("deterministic", c_int), ("has_seed_override", c_int), ("seed_override", c_u64), ("device", c_int),
+                ("consumer_stream", c_vp), ("host_output", c_int), ("slot_memory_budget", c_u64)]
+
+
+_SIGS = {
+    "dp_registry_create": [PP], "dp_registry_destroy": [c_vp],
+    "dp_registry_register_affine": [c_vp, ctypes.c_char_p, c_i64, c_i64],
+    "dp_registry_register_random_crop_flip": [c_vp, ctypes.c_char_p, c_i64, c_i64, c_u64, c_int],
+    "dp_registry_register_resize_bilinear": [c_vp, ctypes.c_char_p, c_i64, c_i64],
+    "dp_registry_register_normalize": [c_vp, ctypes.c_char_p, ctypes.POINTER(ctypes.c_float),
+                                       ctypes.POINTER(ctypes.c_float)],
+    "dp_registry_register_length_filter": [c_vp, ctypes.c_char_p, c_i64],
+    "dp_registry_register_record_reader": [c_vp, ctypes.c_char_p, c_i64],
+    "dp_registry_contains": [c_vp, ctypes.c_char_p],
+    "dp_source_synthetic_images": [c_i64, c_i64, c_i64, c_u64, c_int, PP],
+    "dp_source_images_from_host": [c_vp, c_i64, c_i64, c_i64, c_int, PP],
+    "dp_source_images_pinned_host": [c_vp, c_i64, c_i64, c_i64, c_int, PP],
+    "dp_source_synthetic_tokens": [c_i64, ctypes.c_uint32, c_u64, c_u64, c_int, PP],
+    "dp_source_tokens_from_host": [c_vp, c_i64, c_vp, c_int, PP],
+    "dp_source_release": [c_vp],
+    "dp_graph_range": [c_vp, c_i64, PP],
+    "dp_graph_from_memory_i64": [c_vp, c_vp, c_i64, c_int, PP],
+    "dp_graph_tensor_slices": [c_vp, c_vp, PP],
+    "dp_graph_token_sequences": [c_vp, c_vp, PP],
+    "dp_graph_map": [c_vp, ctypes.c_char_p, c_i64, c_vp, PP],
+    "dp_graph_filter": [c_vp, ctypes.c_char_p, c_vp, PP],
+    "dp_graph_interleave": [c_vp, ctypes.c_char_p, c_i64, c_i64, c_vp, c_vp, PP],
+    "dp_graph_batch": [c_vp, c_i64, c_int, c_vp, PP],
+    "dp_graph_padded_batch": [c_vp, c_i64, c_i64, c_int, c_vp, PP],
+    "dp_graph_prefetch": [c_vp, c_i64, c_vp, PP],
+    "dp_graph_repeat": [c_vp, c_i64, c_vp, PP],
+    "dp_graph_shuffle": [c_vp, c_i64, c_int, c_u64, c_vp, PP],
+    "dp_graph_shard": [c_vp, c_i64, c_i64, c_vp, PP],
+    "dp_graph_optimize": [c_vp, c_vp, ctypes.c_char_p, PP, ctypes.c_char_p, c_size],
+    "dp_graph_root_kind": [c_vp, ctypes.c_char_p, c_size],
+    "dp_graph_to_string": [c_vp, ctypes.c_char_p, c_size],
+    "dp_graph_release": [c_vp],
+    "dp_iterator_options_default": [ctypes.POINTER(dp_iterator_options)],
+    "dp_iterator_create": [c_vp, c_vp, ctypes.POINTER(dp_iterator_options), PP],
+    "dp_iterator_get_next": [c_vp, ctypes.POINTER(dp_batch)],
+    "dp_batch_release": [ctypes.POINTER(dp_batch)],
+    "dp_batch_wait": [ctypes.POINTER(dp_batch)],
+    "dp_tensor_copy_to_host": [ctypes.POINTER(dp_batch), c_int, c_vp, c_size],
+    "dp_iterator_stream": [c_vp], "dp_iterator_kernel_launches": [c_vp], "dp_iterator_prefetch_depth": [c_vp],
+    "dp_iterator_batch_stage_timing": [c_vp, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64)],
+    "dp_iterator_root_delivered": [c_vp], "dp_iterator_base_seed": [c_vp],
+    "dp_iterator_describe": [c_vp, ctypes.c_char_p, c_size], "dp_iterator_destroy": [c_vp],
+}
+_RES = {"dp_registry_destroy": None, "dp_source_release": None, "dp_graph_release": None,
+        "dp_iterator_options_default": None, "dp_iterator_destroy": None, "dp_iterator_stream": c_vp,
+        "dp_iterator_kernel_launches": c_i64, "dp_iterator_prefetch_depth": c_i64,
+        "dp_iterator_root_delivered": c_i64, "dp_iterator_base_seed": c_u64}
+
+_bound = None
+
+
+def L():
+    global _bound
+    if _bound is None:
+        l = lib()
+        for name, args in _SIGS.items():
+            f = getattr(l, name)
+            f.argtypes = args
+            f.restype = _RES.get(name, c_int)
+        _bound = l
+    return _bound
+
+
+def _check(st):
+    if st != 0:
+        raise DpError(st, lib().dp_last_error().decode())
+
+
+def _b(s: str) -> bytes:
+    return s.encode()
+
+
+class Registry:
+    """UdfRegistry (udf.hpp:41-87) holding device UDF descriptors."""
+
+    def __init__(self):
+        h = c_vp()
+        _check(L().dp_registry_create(ctypes.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            L().dp_registry_destroy(self.h)
+            self.h = None
+
+    def register_affine(self, name, a, b):
+        _check(L().dp_registry_register_affine(self.h, _b(name), a, b))
+        return name
+
+    def register_random_crop_flip(self, name, crop_h=224, crop_w=224, seed=7, flip=True):
+        _check(L().dp_registry_register_random_crop_flip(self.h, _b(name), crop_h, crop_w, seed, int(flip)))
+        return name
+
+    def register_resize_bilinear(self, name, out_h=224, out_w=224):
+        _check(L().dp_registry_register_resize_bilinear(self.h, _b(name), out_h, out_w))
+        return name
+
+    def register_normalize(self, name, mean=MEAN, std=STD):
+        m = (ctypes.c_float * 3)(*mean)
+        s = (ctypes.c_float * 3)(*std)
+        _check(L().dp_registry_register_normalize(self.h, _b(name), m, s))
+        return name
+
+    def register_length_filter(self, name, max_len):
+        _check(L().dp_registry_register_length_filter(self.h, _b(name), max_len))
+        return name
+
+    def register_record_reader(self, name, records):
+        _check(L().dp_registry_register_record_reader(self.h, _b(name), records))
+        return name
+
+    def contains(self, name):
+        return bool(L().dp_registry_contains(self.h, _b(name)))
+
+
+class Source:
+    """Device-resident (or pinned-host) element data for the source kinds."""
+
+    def __init__(self, h, keepalive=None):
+        self.h = h
+        self._keep = keepalive
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            L().dp_source_release(self.h)
+            self.h = None
+
+    @staticmethod
+    def synthetic_images(count, h, w, seed=0x5EED, device=0):
+        out = c_vp()
+        _check(L().dp_source_synthetic_images(count, h, w, seed, device, ctypes.byref(out)))
+        return Source(out)
+
+    @staticmethod
+    def images_from_host(arr: np.ndarray, device=0):
+        arr = np.ascontiguousarray(arr, np.uint8)
+        out = c_vp()
+        _check(L().dp_source_images_from_host(arr.ctypes.data, arr.shape[0], arr.shape[1], arr.shape[2], device,
+                                              ctypes.byref(out)))
+        return Source(out)
+
+    @staticmethod
+    def images_pinned_host(arr: np.ndarray, device=0):
+        """`arr` must stay alive; it is page-locked in place and read over PCIe."""
+        assert arr.dtype == np.uint8 and arr.flags["C_CONTIGUOUS"]
+        out = c_vp()
+        _check(L().dp_source_images_pinned_host(arr.ctypes.data, arr.shape[0], arr.shape[1], arr.shape[2], device,
+                                                ctypes.byref(out)))
+        return Source(out, keepalive=arr)
+
+    @staticmethod
+    def synthetic_tokens(count, max_len=1024, len_seed=4, tok_seed=4, device=0):
+        out = c_vp()
+        _check(L().dp_source_synthetic_tokens(count, max_len, len_seed, tok_seed, device, ctypes.byref(out)))
+        return Source(out)
+
+    @staticmethod
+    def tokens_from_host(lengths, tokens, device=0):
+        lengths = np.ascontiguousarray(lengths, np.int32)
+        tokens = np.ascontiguousarray(tokens, np.int32)
+        out = c_vp()
+        _check(L().dp_source_tokens_from_host(lengths.ctypes.data, lengths.size,
+                                              tokens.ctypes.data if tokens.size else None, device, ctypes.byref(out)))
+        return Source(out)
+
+
+class Dataset:
+    """DatasetGraph + the ops:: builders (graph.hpp:134-165)."""
+
+    def __init__(self, h, reg: Registry, keep=()):
+        self.h = h
+        self.reg = reg
+        self._keep = keep  # sources referenced by the graph stay alive with it
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            L().dp_graph_release(self.h)
+            self.h = None
+
+    def _emit(self, fn, *args, keep=()):
+        out = c_vp()
+        _check(fn(*args, ctypes.byref(out)))
+        return Dataset(out, self.reg, tuple(self._keep) + tuple(keep))
+
+    # sources
+    @staticmethod
+    def range(reg, n):
+        out = c_vp()
+        _check(L().dp_graph_range(reg.h, n, ctypes.byref(out)))
+        return Dataset(out, reg)
+
+    @staticmethod
+    def from_memory(reg, values, device=0):
+        v = np.ascontiguousarray(values, np.int64)
+        out = c_vp()
+        _check(L().dp_graph_from_memory_i64(reg.h, v.ctypes.data if v.size else None, v.size, device,
+                                            ctypes.byref(out)))
+        return Dataset(out, reg)
+
+    @staticmethod
+    def tensor_slices(reg, src: Source):
+        out = c_vp()
+        _check(L().dp_graph_tensor_slices(reg.h, src.h, ctypes.byref(out)))
+        return Dataset(out, reg, (src,))
+
+    @staticmethod
+    def token_sequences(reg, src: Source):
+        out = c_vp()
+        _check(L().dp_graph_token_sequences(reg.h, src.h, ctypes.byref(out)))
+        return Dataset(out, reg, (src,))
+
+    # transformations
+    def map(self, udf, num_parallel_calls=1):
+        return self._emit(L().dp_graph_map, self.h, _b(udf), num_parallel_calls, self.reg.h)
+
+    def filter(self, udf):
+        return self._emit(L().dp_graph_filter, self.h, _b(udf), self.reg.h)
+
+    def interleave(self, udf, cycle_length, num_parallel_calls=1, records: Source = None):
+        return self._emit(L().dp_graph_interleave, self.h, _b(udf), cycle_length, num_parallel_calls,
+                          records.h if records else None, self.reg.h, keep=(records,) if records else ())
+
+    def batch(self, batch_size, drop_remainder=False):
+        return self._emit(L().dp_graph_batch, self.h, batch_size, int(drop_remainder), self.reg.h)
+
+    def padded_batch(self, batch_size, padding_value=0, drop_remainder=False):
+        return self._emit(L().dp_graph_padded_batch, self.h, batch_size, padding_value, int(drop_remainder),
+                          self.reg.h)
+
+    def prefetch(self, buffer_size):
+        return self._emit(L().dp_graph_prefetch, self.h, buffer_size, self.reg.h)
+
+    def repeat(self, count):
+        return self._emit(L().dp_graph_repeat, self.h, count, self.reg.h)
+
+    def shuffle(self, buffer_size, seed=None):
+        return self._emit(L().dp_graph_shuffle, self.h, buffer_size, 0 if seed is None else 1, seed or 0,
+                          self.reg.h)
+
+    def shard(self, num_shards, index):
+        return self._emit(L().dp_graph_shard, self.h, num_shards, index, self.reg.h)
+
+    def optimize(self, disabled_rules=()):
+        """Optimize(graph, RuleSet::Default() minus disabled) -> (Dataset, report)."""
+        out = c_vp()
+        rep = ctypes.create_string_buffer(8192)
+        _check(L().dp_graph_optimize(self.h, self.reg.h, _b(",".join(disabled_rules)), ctypes.byref(out), rep,
+                                     len(rep)))
+        return Dataset(out, self.reg, self._keep), rep.value.decode()
+
+    @property
+    def root_kind(self):
+        buf = ctypes.create_string_buffer(64)
+        _check(L().dp_graph_root_kind(self.h, buf, len(buf)))
+        return buf.value.decode()
+
+    def __str__(self):
+        buf = ctypes.create_string_buffer(1 << 16)
+        _check(L().dp_graph_to_string(self.h, buf, len(buf)))
+        return buf.value.decode()
+
+
+class Batch:
+    """One element returned by GetNext: device (or pinned host) tensors."""
+
+    def __init__(self, b: dp_batch, it):
+        self.b = b
+        self._it = it
+
+    @property
+    def components(self):
+        out = []
+        for c in range(self.b.num_components):
+            t = self.b.components[c]
+            out.append((DTYPES[t.dtype], tuple(t.shape[k] for k in range(t.ndim)), t.data, bool(t.on_host)))
+        return out
+
+    def numpy(self, c):
+        dt, shape, _, _ = self.components[c]
+        arr = np.empty(shape, dt)
+        _check(L().dp_tensor_copy_to_host(ctypes.byref(self.b), c, arr.ctypes.data, arr.nbytes))
+        return arr
+
+    def wait(self):
+        """Host-blocking wait until the batch is written (and copied, with host_output)."""
+        _check(L().dp_batch_wait(ctypes.byref(self.b)))
+        return self
+
+    def host_view(self, c):
+        """Zero-copy numpy view of a host_output component (valid until release)."""
+        dt, shape, ptr, on_host = self.components[c]
+        assert on_host, "host_view needs make_iterator(..., host_output=True)"
+        n = int(np.prod(shape)) * np.dtype(dt).itemsize
+        buf = (ctypes.c_char * n).from_address(ptr)
+        return np.frombuffer(buf, dtype=dt).reshape(shape)
+
+    def release(self):
+        if self.b.handle:
+            L().dp_batch_release(ctypes.byref(self.b))
+
+    def __del__(self):
+        try:
+            self.release()
+        except Exception:
+            pass
+
+
+class Iterator:
+    """PipelineIterator (runtime.hpp:52-90)."""
+
+    def __init__(self, h, ds):
+        self.h = h
+        self._ds = ds
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            L().dp_iterator_destroy(self.h)
+            self.h = None
+
+    def get_next(self):
+        b = dp_batch()
+        st = L().dp_iterator_get_next(self.h, ctypes.byref(b))
+        if st == ERR["EndOfSequence"]:
+            return None
+        _check(st)
+        return Batch(b, self)
+
+    def __iter__(self):
+        while True:
+            b = self.get_next()
+            if b is None:
+                return
+            yield b
+
+    @property
+    def stream(self):
+        return L().dp_iterator_stream(self.h)
+
+    @property
+    def kernel_launches(self):
+        return L().dp_iterator_kernel_launches(self.h)
+
+    def batch_stage_timing(self):
+        """(total device ns, launches) of the fused batch-stage kernels so far."""
+        ns, n = c_i64(), c_i64()
+        _check(L().dp_iterator_batch_stage_timing(self.h, ctypes.byref(ns), ctypes.byref(n)))
+        return ns.value, n.value
+
+    @property
+    def prefetch_depth(self):
+        return L().dp_iterator_prefetch_depth(self.h)
+
+    @property
+    def root_delivered(self):
+        return L().dp_iterator_root_delivered(self.h)
+
+    @property
+    def base_seed(self):
+        return L().dp_iterator_base_seed(self.h)
+
+    def describe(self):
+        buf = ctypes.create_string_buffer(4096)
+        _check(L().dp_iterator_describe(self.h, buf, len(buf)))
+        return buf.value.decode()
+
+
+def make_iterator(ds: Dataset, seed_override=None, device=0, consumer_stream=None, host_output=False,
+                  slot_memory_budget=0, deterministic=True):
+    """MakeIterator(graph, registry, IteratorOptions) (runtime.hpp:98-100)."""
+    o = dp_iterator_options()
+    L().dp_iterator_options_default(ctypes.byref(o))
+    o.deterministic = int(deterministic)
+    if seed_override is not None:
+        o.has_seed_override = 1
+        o.seed_override = seed_override
+    o.device = device
+    o.consumer_stream = consumer_stream
+    o.host_output = int(host_output)
+    o.slot_memory_budget = slot_memory_budget
+    out = c_vp()
+    _check(L().dp_iterator_create(ds.h, ds.reg.h, ctypes.byref(o), ctypes.byref(out)))
+    return Iterator(out, ds)

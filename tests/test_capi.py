@@ -1,0 +1,146 @@
+"""CPU-side checks of the C ABI and the host graph layer (no GPU needed).
+
+* libdpcuda.so loads and exports every dp_* symbol include/*.h declares;
+* graph construction / validation / Optimize mirror the reference's
+  operator API and rewrite contract (P/tests/test_graph.cpp,
+  P/tests/test_optimizer.cpp: map_batch fusion yields map_and_batch, a fused
+  predicate blocks it, rule disabling, composed-UDF names);
+* MakeIterator validates UDFs before touching the device (UnknownUdf,
+  runtime.cpp:2117-2156) and fails loudly without a GPU (no CPU fallback).
+"""
+import ctypes
+
+import pytest
+
+from paper_2101_12127_b200 import _capi, pipeline as dp
+from paper_2101_12127_b200._capi import DpError
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _capi.lib()
+    names = _capi.declared_symbols()
+    assert len(names) > 60
+    missing = [n for n in names if not hasattr(lib, n)]
+    assert not missing, missing
+    assert b"sm_100a" in lib.dp_build_info()
+
+
+def test_library_is_sm100a_only():
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", _capi.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert not any(a in out for a in ("sm_80", "sm_90", "sm_89"))
+
+
+def test_device_count_without_gpu_is_not_an_error():
+    c = ctypes.c_int(-1)
+    assert _capi.lib().dp_device_count(ctypes.byref(c)) == 0 and c.value >= 0
+
+
+def reg_cfg1():
+    reg = dp.Registry()
+    reg.register_affine("affine(3,1)", 3, 1)
+    return reg
+
+
+def test_map_batch_fusion_yields_map_and_batch():
+    reg = reg_cfg1()
+    g = dp.Dataset.range(reg, 1_000_000).map("affine(3,1)").batch(1024)
+    assert g.root_kind == "batch"
+    opt, report = g.optimize()
+    assert opt.root_kind == "map_and_batch"
+    assert "map_batch_fusion at /batch@0" in report
+    # spec of the fused node: an int64 batch tensor of unknown length
+    assert "map_and_batch" in str(opt) and "tensor<int64[?]>" in str(opt)
+
+
+def test_disabled_rule_keeps_unfused_graph():
+    reg = reg_cfg1()
+    g = dp.Dataset.range(reg, 10).map("affine(3,1)").batch(4)
+    opt, report = g.optimize(disabled_rules=("map_batch_fusion",))
+    assert opt.root_kind == "batch" and "no rewrites applied" in report
+    with pytest.raises(DpError) as e:
+        g.optimize(disabled_rules=("no_such_rule",))
+    assert e.value.code == dp.ERR["InvalidAttr"]
+
+
+def test_map_map_fusion_composes_names_then_fuses_batch():
+    reg = reg_cfg1()
+    reg.register_affine("times2", 2, 0)
+    g = dp.Dataset.range(reg, 10).map("affine(3,1)", 2).map("times2", -1).batch(4)
+    opt, report = g.optimize()
+    assert report.index("map_map_fusion") < report.index("map_batch_fusion")
+    assert opt.root_kind == "map_and_batch"
+    s = str(opt)
+    assert "udf=(affine(3,1))>>(times2)" in s and "num_parallel_calls=-1" in s  # AUTOTUNE absorbing
+    assert reg.contains("(affine(3,1))>>(times2)")
+
+
+def test_map_on_wrong_element_type_is_type_mismatch():
+    reg = dp.Registry()
+    reg.register_random_crop_flip("crop", 224, 224, seed=7)
+    with pytest.raises(DpError) as e:
+        dp.Dataset.range(reg, 10).map("crop")
+    assert e.value.code == dp.ERR["TypeMismatch"]
+
+
+def test_shuffle_repeat_fusion_and_fused_predicate_blocks_map_batch():
+    reg = reg_cfg1()
+    reg.register_length_filter("short", 512)
+    g = dp.Dataset.range(reg, 100).shuffle(10, seed=42).repeat(3)
+    opt, report = g.optimize()
+    assert "shuffle_repeat_fusion" in report and "fused_with_repeat=1" in str(opt)
+    # map + filter fuse into one map carrying the predicate; batch then does
+    # NOT fuse with it (optimizer.cpp:258-264)
+    g2 = dp.Dataset.range(reg, 100).map("affine(3,1)").filter("short").batch(8)
+    opt2, report2 = g2.optimize()
+    assert "map_filter_fusion" in report2 and "map_batch_fusion" not in report2
+    assert opt2.root_kind == "batch"
+
+
+def test_attr_validation_errors():
+    reg = reg_cfg1()
+    base = dp.Dataset.range(reg, 10)
+    for build in (lambda: base.batch(0), lambda: base.shard(2, 2), lambda: base.shard(0, 0),
+                  lambda: base.shuffle(0), lambda: base.prefetch(0), lambda: base.repeat(0),
+                  lambda: base.map("affine(3,1)", 0), lambda: dp.Dataset.range(reg, -1)):
+        with pytest.raises(DpError) as e:
+            build()
+        assert e.value.code == dp.ERR["InvalidAttr"]
+    # AUTOTUNE is legal for parallelism and prefetch
+    base.map("affine(3,1)", -1).batch(4).prefetch(-1)
+
+
+def test_duplicate_udf_name():
+    reg = reg_cfg1()
+    with pytest.raises(DpError) as e:
+        reg.register_affine("affine(3,1)", 1, 1)
+    assert e.value.code == dp.ERR["DuplicateName"]
+
+
+def test_unknown_udf_fails_at_make_iterator_before_device():
+    reg = dp.Registry()
+    g = dp.Dataset.range(reg, 3).map("nope").batch(2)
+    with pytest.raises(DpError) as e:
+        dp.make_iterator(g, seed_override=1)
+    assert e.value.code == dp.ERR["UnknownUdf"]
+
+
+def test_no_cpu_fallback_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("has a GPU")
+    reg = reg_cfg1()
+    g = dp.Dataset.range(reg, 3).map("affine(3,1)").batch(2)
+    with pytest.raises(DpError) as e:
+        dp.make_iterator(g, seed_override=1)
+    assert e.value.code == dp.ERR["Cuda"] and "no CPU fallback" in str(e.value)
+
+
+def test_kernel_entry_rejects_bad_args_without_launching():
+    lib = _capi.lib()
+    assert lib.dp_k_range_affine_batch(0, -1, 1, 0, None, None) == dp.ERR["InvalidAttr"]
+    assert lib.dp_k_shuffle_plan(10, 0, 1, None, None, None, None) == dp.ERR["InvalidAttr"]
+    assert lib.dp_k_shard_index(10, 0, 0, None, None, None) == dp.ERR["InvalidAttr"]
+    assert b"num_shards" in lib.dp_last_error()
+    assert lib.dp_k_shard_interleave_count(64, 8, 3, 16) == 8 * 16

@@ -25,6 +25,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import re
 import statistics
 import subprocess
 import sys
@@ -177,12 +178,16 @@ def run_ours(args, cfg):
     g, report = build_graph(dp, cfg, src)
     it = dp.make_iterator(g, seed_override=1, device=local)
     stream = torch.cuda.ExternalStream(it.stream, device=dev)
+    per_launch = int(re.search(r"(\d+) batch\(es\) per launch", it.describe()).group(1))
+    # W and K whole launch groups, so the event window holds exactly K batches
+    args.warmup = -(-args.warmup // per_launch) * per_launch
+    args.steps = -(-args.steps // per_launch) * per_launch
     for _ in range(args.warmup):
         it.get_next().release()
     torch.cuda.synchronize(dev)
     if world > 1:
         distr.barrier()
-    launches0 = it.kernel_launches
+    launches0, batches0 = it.kernel_launches, it.batches_launched
     ns0, k0 = it.batch_stage_timing()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
@@ -194,17 +199,22 @@ def run_ours(args, cfg):
     torch.cuda.synchronize(dev)
     ms = e0.elapsed_time(e1)
     launches = it.kernel_launches - launches0
+    batches_in_window = it.batches_launched - batches0
     ns1, k1 = it.batch_stage_timing()
     t = torch.tensor([ms], device=dev, dtype=torch.float64)
     if world > 1:
         distr.all_reduce(t, op=distr.ReduceOp.MAX)
         distr.barrier()
     ms_max = float(t.item())
-    elems = args.steps * cfg["batch"] * world
+    # The device work inside [e0, e1] is exactly the batch-stage launches
+    # issued between the two events; with W and K multiples of the launch
+    # group this is K batches (checked and reported).
+    elems = batches_in_window * cfg["batch"] * world
     value = elems / (ms_max / 1e3)
-    kernel_s = (ns1 - ns0) / max(k1 - k0, 1) / 1e9
+    kernel_s = (ns1 - ns0) / max(k1 - k0, 1) / 1e9  # per launch
+    batches_per_launch = batches_in_window / max(k1 - k0, 1)
     peak, peak_src = load_peaks()
-    achieved = cfg["bytes_per_elem"] * cfg["batch"] / kernel_s / 1e9
+    achieved = cfg["bytes_per_elem"] * cfg["batch"] * batches_per_launch / kernel_s / 1e9
     del it
 
     # ---- end to end through the C ABI with host buffers ----
@@ -243,8 +253,10 @@ def run_ours(args, cfg):
                    "optimized": "map_and_batch" in report or "map_batch_fusion" in report},
         "roofline": {"bound": "hbm", "kernel": cfg["kernel"], "achieved": round(achieved, 1), "peak": peak,
                      "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                     "algorithmic_bytes_per_launch": cfg["bytes_per_elem"] * cfg["batch"],
-                     "avg_launch_us": round(kernel_s * 1e6, 3), "traffic": traffic},
+                     "algorithmic_bytes_per_launch": int(cfg["bytes_per_elem"] * cfg["batch"] * batches_per_launch),
+                     "algorithmic_bytes_per_image": cfg["bytes_per_elem"], "batches_per_launch": batches_per_launch,
+                     "avg_launch_us": round(kernel_s * 1e6, 3), "launches_timed": k1 - k0, "traffic": traffic},
+        "batches_in_window": batches_in_window, "steps_per_launch_group": per_launch,
         "cpu_baseline": {"value": None if cpu is None else (round(cpu["value"], 2) if cpu["value"] else None),
                          "unit": "images/s", "cores": os.cpu_count(), "kind": "reference",
                          "sample": None if cpu is None else cpu["sample"]},
@@ -267,7 +279,9 @@ def run_e2e(dp, cfg, local, args):
     host = np.random.default_rng(0).integers(0, 256, (n_host, h, w, 3), dtype=np.uint8)
     src = dp.Source.images_pinned_host(host, device=local)
     g, _ = build_graph(dp, cfg, src)
-    it = dp.make_iterator(g, seed_override=1, device=local, host_output=True)
+    # one batch per launch: each batch's D2H starts as soon as it is written
+    it = dp.make_iterator(g, seed_override=1, device=local, host_output=True,
+                          max_launch_bytes=int(os.environ.get("DP_E2E_LAUNCH_BYTES", 160 << 20)))
     steps = max(8, min(args.steps, 64))
     for _ in range(3):
         it.get_next().wait().release()
@@ -288,7 +302,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=512)
-    ap.add_argument("--warmup", type=int, default=16)
+    ap.add_argument("--warmup", type=int, default=32)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CFG), default="cfg2")
     args = ap.parse_args()

@@ -241,6 +241,10 @@ struct IteratorOptions {
   bool host_output = false;
   // Upper bound on device memory for prefetch slots (bytes).
   size_t slot_memory_budget = size_t(8) << 30;
+  // Output bytes one fused launch may produce (consecutive batches are
+  // grouped into one launch up to this size); 0 = 3.2 GB (512 MB with
+  // host_output).
+  size_t max_launch_bytes = 0;
 };
 
 struct NodeMetricsRow {
@@ -271,6 +275,7 @@ class PipelineIterator {
   void* stream() const;                 // the iterator's producer stream
   int64_t prefetch_depth() const;       // device slots in use (autotuned)
   int64_t kernel_launches() const;      // sm_100a kernels issued so far
+  int64_t batches_launched() const;     // batches covered by issued batch-stage launches
   // Device time (CUDA events around each launch, on the launching stream)
   // of the fused batch-stage launches issued so far: {total ns, launches}.
   std::pair<int64_t, int64_t> BatchStageTiming() const;

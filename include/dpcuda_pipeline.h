@@ -100,6 +100,7 @@ typedef struct {
   void* consumer_stream;      /* cudaStream_t the batches are consumed on (NULL: iterator stream) */
   int host_output;            /* copy batches to pinned host memory */
   uint64_t slot_memory_budget;/* bytes of device prefetch slots (0: default 8 GiB) */
+  uint64_t max_launch_bytes;  /* output bytes per fused launch (0: default) */
 } dp_iterator_options;
 
 typedef enum { DP_U8 = 0, DP_I32 = 1, DP_I64 = 2, DP_F32 = 3 } dp_dtype;
@@ -137,6 +138,8 @@ int dp_batch_wait(const dp_batch* batch);
 int dp_tensor_copy_to_host(const dp_batch* batch, int component, void* dst, size_t bytes);
 void* dp_iterator_stream(const dp_iterator* it);
 int64_t dp_iterator_kernel_launches(const dp_iterator* it);
+/* Batches covered by the fused batch-stage launches issued so far. */
+int64_t dp_iterator_batches_launched(const dp_iterator* it);
 /* Device time of the fused batch-stage launches so far (CUDA events around
  * each launch on the launching stream; waits for issued launches). */
 int dp_iterator_batch_stage_timing(const dp_iterator* it, int64_t* total_ns, int64_t* launches);

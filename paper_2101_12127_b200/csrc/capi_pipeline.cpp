@@ -229,6 +229,7 @@ int dp_iterator_create(const dp_graph* g, const dp_registry* reg, const dp_itera
       o.consumer_stream = opt->consumer_stream;
       o.host_output = opt->host_output != 0;
       if (opt->slot_memory_budget) o.slot_memory_budget = opt->slot_memory_budget;
+      o.max_launch_bytes = opt->max_launch_bytes;
     }
     *out = new dp_iterator{MakeIterator(g->g, reg->reg, o)};
   });
@@ -304,6 +305,7 @@ int dp_tensor_copy_to_host(const dp_batch* batch, int component, void* dst, size
 
 void* dp_iterator_stream(const dp_iterator* it) { return it ? it->it->stream() : nullptr; }
 int64_t dp_iterator_kernel_launches(const dp_iterator* it) { return it ? it->it->kernel_launches() : 0; }
+int64_t dp_iterator_batches_launched(const dp_iterator* it) { return it ? it->it->batches_launched() : 0; }
 int dp_iterator_batch_stage_timing(const dp_iterator* it, int64_t* total_ns, int64_t* launches) {
   DP_REQUIRE(it && total_ns && launches);
   return Guard([&] {

@@ -34,6 +34,8 @@
 #include <atomic>
 #include <chrono>
 #include <condition_variable>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <functional>
@@ -82,6 +84,30 @@ std::shared_ptr<void> DeviceAlloc(size_t bytes, int device) {
   return std::shared_ptr<void>(p, [device](void* q) {
     DeviceGuard g2(device);
     cudaFree(q);
+  });
+}
+
+// Stream-ordered allocation for per-epoch plan buffers: allocated on the plan
+// stream, returned with cudaFreeAsync on the batch stream (after the last
+// batch kernel that reads them), so an epoch transition never blocks the
+// host the way cudaMalloc / cudaFree do.  The device's default pool keeps
+// freed memory cached for reuse.
+std::shared_ptr<void> DeviceAllocAsync(size_t bytes, int device, cudaStream_t alloc_stream, cudaStream_t free_stream) {
+  DeviceGuard g(device);
+  static std::once_flag once[64];
+  std::call_once(once[device & 63], [device] {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cudaGetLastError();
+  });
+  void* p = nullptr;
+  CudaCheck(cudaMallocAsync(&p, bytes ? bytes : 16, alloc_stream), "cudaMallocAsync");
+  return std::shared_ptr<void>(p, [device, free_stream](void* q) {
+    DeviceGuard g2(device);
+    cudaFreeAsync(q, free_stream);
   });
 }
 
@@ -459,9 +485,23 @@ class DevicePipeline {
     batch_bytes_ = BatchBytes();
     // group size: >= 256 MB of output per launch (amortises launch latency and
     // the persistent kernel's ramp-up / drain), at most one epoch of batches
-    const size_t target = size_t(256) << 20;
+    // Per-launch fixed costs (kernel ramp-up, tail imbalance, launch gap)
+    // are ~10% of a 150 MB batch; 16 cfg2 batches per launch put the batch
+    // stage at the HBM roofline (tools/groupsweep.py).  Pinned host slots
+    // (host_output) are kept smaller.
+    size_t target = opt_.max_launch_bytes ? opt_.max_launch_bytes
+                                          : (opt_.host_output ? size_t(512) << 20 : size_t(3200) << 20);
+    if (const char* v = std::getenv("DP_DEV_GROUP_MB")) target = size_t(std::atoll(v)) << 20;  // tuning sweeps
+    target = std::min(target, opt_.slot_memory_budget / 2);
     group_ = std::max<int64_t>(1, static_cast<int64_t>(target / std::max<size_t>(batch_bytes_.first + batch_bytes_.second, 1)));
-    group_ = std::min(group_, std::max<int64_t>(1, batches_per_epoch_));
+    // a power of two, so groups tile power-of-two epochs without a ragged group
+    int64_t pow2 = 1;
+    while (pow2 * 2 <= group_) pow2 *= 2;
+    group_ = std::min(pow2, std::max<int64_t>(1, batches_per_epoch_));
+    // the prefetch depth must fit the slot budget (at least double buffering)
+    const size_t group_bytes = (batch_bytes_.first + batch_bytes_.second) * group_;
+    depth_ = std::max<int64_t>(2, std::min<int64_t>(depth_, static_cast<int64_t>(opt_.slot_memory_budget /
+                                                                                 std::max<size_t>(group_bytes, 1))));
     if (span_epochs_) group_ = std::min<int64_t>(group_, std::max<int64_t>(1, epoch_count_ / std::max<int64_t>(L_.batch, 1)));
     if (group_ > 1) {  // epoch 0 was planned with a one-group tail: re-plan lazily
       for (auto& [e, p] : plans_)
@@ -473,6 +513,7 @@ class DevicePipeline {
 
   ~DevicePipeline() {
     DeviceGuard g(opt_.device);
+    PrintDebugTiming();
     cudaStreamSynchronize(stream_);
     for (auto& t : timed_) event_pool_.push_back(t);
     for (auto& t : event_pool_) {
@@ -483,6 +524,9 @@ class DevicePipeline {
     if (copy_stream_) cudaStreamSynchronize(copy_stream_);
     for (auto& [e, p] : plans_)
       if (p.ready) cudaEventDestroy(p.ready);
+    plans_.clear();  // stream-ordered frees: before the streams go away
+    cudaStreamSynchronize(plan_stream_);
+    if (retire_ev_) cudaEventDestroy(retire_ev_);
     cudaStreamDestroy(stream_);
     cudaStreamDestroy(plan_stream_);
     if (copy_stream_) cudaStreamDestroy(copy_stream_);
@@ -497,22 +541,43 @@ class DevicePipeline {
       return std::nullopt;
     }
     const int64_t grp = i / group_;
+    const auto t0 = std::chrono::steady_clock::now();
     while (issued_groups_ <= grp) IssueGroup(issued_groups_);
     // keep `depth` groups in flight
     while (issued_groups_ < grp + depth_ && (total_groups_ < 0 || issued_groups_ < total_groups_)) {
       if (!TryIssueGroup(issued_groups_, /*may_grow=*/false)) break;
     }
+    const auto t1 = std::chrono::steady_clock::now();
     auto slot = group_slot_.at(grp);
     next_batch_++;
     if (consumer_ != stream_ && !opt_.host_output) CudaCheck(cudaStreamWaitEvent(consumer_, slot->ready, 0), "wait");
     produced_++;
     MaybeAutotune();
-    return MakeElement(slot, i);
+    const auto t2 = std::chrono::steady_clock::now();
+    auto e = MakeElement(slot, i);
+    const auto t3 = std::chrono::steady_clock::now();
+    dbg_[0] += std::chrono::duration<double>(t1 - t0).count();
+    dbg_[1] += std::chrono::duration<double>(t2 - t1).count();
+    dbg_[2] += std::chrono::duration<double>(t3 - t2).count();
+    return e;
+  }
+
+  double dbg_[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  void PrintDebugTiming() const {
+    if (!std::getenv("DP_DEBUG_TIMING") || produced_ == 0) return;
+    std::fprintf(stderr,
+                 "[dp timing] per GetNext (us): issue %.1f autotune %.1f element %.1f | per group: find %.1f plan %.1f "
+                 "launch %.1f events %.1f (%lld groups)\n",
+                 1e6 * dbg_[0] / produced_, 1e6 * dbg_[1] / produced_, 1e6 * dbg_[2] / produced_,
+                 1e6 * dbg_[3] / std::max<int64_t>(issued_count_, 1), 1e6 * dbg_[4] / std::max<int64_t>(issued_count_, 1),
+                 1e6 * dbg_[5] / std::max<int64_t>(issued_count_, 1), 1e6 * dbg_[6] / std::max<int64_t>(issued_count_, 1),
+                 static_cast<long long>(issued_count_));
   }
 
   int64_t delivered() const { return produced_; }
   int64_t depth() const { return depth_; }
   int64_t launches() const { return launches_; }
+  int64_t batches_launched() const { return batches_launched_; }
   void* stream() const { return stream_; }
   int64_t batch_time_ns() const { return batch_ns_total_; }
   int64_t group_size() const { return group_; }
@@ -617,9 +682,14 @@ class DevicePipeline {
   EpochPlan& Plan(int64_t e) {
     auto it = plans_.find(e);
     if (it != plans_.end()) return it->second;
-    // retire plans two epochs back (stream-ordered: later kernels no longer use them)
+    // Retire plans two epochs back.  Their buffers are freed on the plan
+    // stream, ordered after every batch kernel queued so far on the batch
+    // stream (the last readers) -- no host synchronisation.
     for (auto jt = plans_.begin(); jt != plans_.end();) {
       if (jt->first < e - 1) {
+        if (!retire_ev_) CudaCheck(cudaEventCreateWithFlags(&retire_ev_, cudaEventDisableTiming), "event");
+        CudaCheck(cudaEventRecord(retire_ev_, stream_), "event");
+        CudaCheck(cudaStreamWaitEvent(plan_stream_, retire_ev_, 0), "wait");
         if (jt->second.ready) cudaEventDestroy(jt->second.ready);
         jt = plans_.erase(jt);
       } else {
@@ -639,7 +709,10 @@ class DevicePipeline {
     int64_t count = L_.source_count;
     std::shared_ptr<void> cur;  // int64 order (null = identity)
     const int64_t tail = std::max<int64_t>(L_.batch * group_, 1);
-    auto alloc = [&](int64_t n) { return DeviceAlloc(sizeof(int64_t) * (n + tail), opt_.device); };
+    // every plan buffer is stream-ordered on the plan stream (see Plan() for
+    // how retirement orders the free after the batch kernels' last use)
+    auto dalloc = [&](size_t bytes) { return DeviceAllocAsync(bytes, opt_.device, plan_stream_, plan_stream_); };
+    auto alloc = [&](int64_t n) { return dalloc(sizeof(int64_t) * (n + tail)); };
     for (const auto& op : L_.chain) {
       switch (op.kind) {
         case IndexOp::Kind::kShard: {
@@ -666,8 +739,8 @@ class DevicePipeline {
         }
         case IndexOp::Kind::kFilter: {
           auto out = alloc(count);
-          auto nk = DeviceAlloc(sizeof(int64_t), opt_.device);
-          auto scratch = DeviceAlloc(dp_k_filter_scratch_bytes(count), opt_.device);
+          auto nk = dalloc(sizeof(int64_t));
+          auto scratch = dalloc(dp_k_filter_scratch_bytes(count));
           KCheck(dp_k_filter_len_le(P<int32_t>(L_.source->lengths), count, static_cast<int32_t>(op.a), P<int64_t>(cur),
                                     P<int64_t>(out), P<int64_t>(nk), scratch.get(), s),
                  "filter");
@@ -683,7 +756,7 @@ class DevicePipeline {
           auto out = alloc(count);
           const uint64_t seed = ShuffleEngineSeed(salt, op.seed);
           size_t sb = dp_k_shuffle_plan_scratch_bytes(static_cast<uint64_t>(count), static_cast<uint64_t>(op.a));
-          std::shared_ptr<void> scratch = sb ? DeviceAlloc(sb, opt_.device) : nullptr;
+          std::shared_ptr<void> scratch = sb ? dalloc(sb) : nullptr;
           KCheck(dp_k_shuffle_plan(count, op.a, seed, P<int64_t>(cur), P<int64_t>(out), scratch.get(), s), "shuffle");
           launches_++;
           cur = out;
@@ -708,7 +781,7 @@ class DevicePipeline {
       p.lmax.assign(nb, 0);
       p.boff.assign(nb + 1, 0);
       if (nb) {
-        auto lm = DeviceAlloc(sizeof(int32_t) * nb, opt_.device);
+        auto lm = dalloc(sizeof(int32_t) * nb);
         KCheck(dp_k_batch_max_len(P<int32_t>(L_.source->lengths), P<int64_t>(cur), count, L_.batch, P<int32_t>(lm), s),
                "batch_max_len");
         launches_++;
@@ -719,7 +792,7 @@ class DevicePipeline {
           p.boff[j + 1] = p.boff[j] + rows * p.lmax[j];
         }
         p.lmax_dev = lm;
-        p.boff_dev = DeviceAlloc(sizeof(int64_t) * (nb + 1), opt_.device);
+        p.boff_dev = dalloc(sizeof(int64_t) * (nb + 1));
         CudaCheck(cudaMemcpyAsync(p.boff_dev.get(), p.boff.data(), sizeof(int64_t) * (nb + 1), cudaMemcpyHostToDevice, s),
                   "boff");
       }
@@ -842,6 +915,8 @@ class DevicePipeline {
       slot->handed_out = 0;
       slot->outstanding = 0;
     }
+    const auto tA = std::chrono::steady_clock::now();
+    dbg_[3] += std::chrono::duration<double>(tA - t0).count();
     EnsurePlanFor(first, nb);
     const int64_t epoch = span_epochs_ ? (epoch_count_ ? first * L_.batch / epoch_count_ : 0)
                                        : first / std::max<int64_t>(batches_per_epoch_, 1);
@@ -866,6 +941,8 @@ class DevicePipeline {
       slot->batch_rows[k] = rows;
       rows_total += rows;
     }
+    const auto tB = std::chrono::steady_clock::now();
+    dbg_[4] += std::chrono::duration<double>(tB - tA).count();
     TimedLaunch tl = NewTimedLaunch();
     CudaCheck(cudaEventRecord(tl.start, stream_), "event");
     const int64_t* order = P<int64_t>(plan.order);
@@ -933,7 +1010,10 @@ class DevicePipeline {
         break;
       }
     }
+    const auto tC = std::chrono::steady_clock::now();
+    dbg_[5] += std::chrono::duration<double>(tC - tB).count();
     CudaCheck(cudaEventRecord(tl.end, stream_), "event");
+    batches_launched_ += nb;
     timed_.push_back(tl);
     if (opt_.host_output) {
       CudaCheck(cudaEventRecord(slot->ready, stream_), "event");
@@ -950,6 +1030,7 @@ class DevicePipeline {
     for (auto it = group_slot_.begin(); it != group_slot_.end() && it->first < g - 2 * depth_ - 4;)
       it = group_slot_.erase(it);
     issued_groups_ = std::max(issued_groups_, g + 1);
+    dbg_[6] += std::chrono::duration<double>(std::chrono::steady_clock::now() - tC).count();
     host_issue_ns_ += std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count();
     issued_count_++;
     return true;
@@ -1111,6 +1192,8 @@ class DevicePipeline {
   bool span_epochs_ = false;
   int64_t epoch_count_ = 0, batches_per_epoch_ = 0, total_batches_ = 0, total_groups_ = -1;
   std::map<int64_t, EpochPlan> plans_;
+  cudaEvent_t retire_ev_ = nullptr;
+  int64_t batches_launched_ = 0;
   std::set<int64_t> appended_;
   std::vector<std::shared_ptr<Slot>> slots_;
   std::map<int64_t, std::shared_ptr<Slot>> group_slot_;
@@ -1177,6 +1260,7 @@ std::vector<NodeMetricsRow> PipelineIterator::Metrics() const {
 void* PipelineIterator::stream() const { return impl_->stream(); }
 int64_t PipelineIterator::prefetch_depth() const { return impl_->depth(); }
 int64_t PipelineIterator::kernel_launches() const { return impl_->launches(); }
+int64_t PipelineIterator::batches_launched() const { return impl_->batches_launched(); }
 std::pair<int64_t, int64_t> PipelineIterator::BatchStageTiming() const {
   std::lock_guard lock(mu_);
   return impl_->BatchStageTiming();

@@ -12,8 +12,11 @@
 // 16-byte streaming (.cs) stores of 4 normalized fp32 values, so the output
 // (80% of the traffic) leaves the SM as fully coalesced 128-bit stores.
 #include <algorithm>
-#include <cstdlib>
 #include <cstdint>
+#include <cstdlib>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "common.cuh"
 #include "status.hpp"
@@ -517,15 +520,45 @@ int sm_count() {
 
 template <typename K>
 int launch_persistent(K kernel, const FastArgs& a, size_t smem, cudaStream_t s, const char* what) {
+  // cudaFuncSetAttribute / the occupancy query are host-synchronous-ish and
+  // cost tens of microseconds: do them once per (device, kernel, smem, threads).
+  struct Key {
+    int dev;
+    const void* fn;
+    size_t smem;
+    int threads;
+    bool operator<(const Key& o) const {
+      return std::tie(dev, fn, smem, threads) < std::tie(o.dev, o.fn, o.smem, o.threads);
+    }
+  };
+  static std::mutex mu;
+  static std::map<Key, int> occupancy;
+  static std::map<std::pair<int, const void*>, size_t> smem_attr;  // max dynamic smem set per kernel
   int st;
-  if ((st = cuda_status(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(smem)),
-                        what)))
-    return st;
   const int threads = ((a.q_per_row * a.rpp + 31) / 32) * 32 + 32;
+  int dev = 0;
+  cudaGetDevice(&dev);
   int per_sm = 0;
-  if ((st = cuda_status(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem), what)))
-    return st;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    const Key key{dev, reinterpret_cast<const void*>(kernel), smem, threads};
+    size_t& cur = smem_attr[{dev, reinterpret_cast<const void*>(kernel)}];
+    if (smem > cur) {  // the attribute only ever grows, so cached keys stay launchable
+      if ((st = cuda_status(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 static_cast<int>(smem)),
+                            what)))
+        return st;
+      cur = smem;
+    }
+    auto it = occupancy.find(key);
+    if (it != occupancy.end()) {
+      per_sm = it->second;
+    } else {
+      if ((st = cuda_status(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem), what)))
+        return st;
+      occupancy[key] = per_sm;
+    }
+  }
   if (per_sm < 1) return fail(DP_ERR_INVALID_ATTR, std::string(what) + ": kernel does not fit on an SM");
   const int64_t items = a.rows * a.bands;
   const int64_t grid = std::min<int64_t>(items, static_cast<int64_t>(per_sm) * sm_count());

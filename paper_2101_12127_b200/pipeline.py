@@ -40,7 +40,8 @@ class dp_batch(ctypes.Structure):
 
 class dp_iterator_options(ctypes.Structure):
     _fields_ = [("deterministic", c_int), ("has_seed_override", c_int), ("seed_override", c_u64), ("device", c_int),
-                ("consumer_stream", c_vp), ("host_output", c_int), ("slot_memory_budget", c_u64)]
+                ("consumer_stream", c_vp), ("host_output", c_int), ("slot_memory_budget", c_u64),
+                ("max_launch_bytes", c_u64)]
 
 
 _SIGS = {
@@ -84,13 +85,14 @@ _SIGS = {
     "dp_tensor_copy_to_host": [ctypes.POINTER(dp_batch), c_int, c_vp, c_size],
     "dp_iterator_stream": [c_vp], "dp_iterator_kernel_launches": [c_vp], "dp_iterator_prefetch_depth": [c_vp],
     "dp_iterator_batch_stage_timing": [c_vp, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64)],
+    "dp_iterator_batches_launched": [c_vp],
     "dp_iterator_root_delivered": [c_vp], "dp_iterator_base_seed": [c_vp],
     "dp_iterator_describe": [c_vp, ctypes.c_char_p, c_size], "dp_iterator_destroy": [c_vp],
 }
 _RES = {"dp_registry_destroy": None, "dp_source_release": None, "dp_graph_release": None,
         "dp_iterator_options_default": None, "dp_iterator_destroy": None, "dp_iterator_stream": c_vp,
         "dp_iterator_kernel_launches": c_i64, "dp_iterator_prefetch_depth": c_i64,
-        "dp_iterator_root_delivered": c_i64, "dp_iterator_base_seed": c_u64}
+        "dp_iterator_root_delivered": c_i64, "dp_iterator_base_seed": c_u64, "dp_iterator_batches_launched": c_i64}
 
 _bound = None
 
@@ -112,6 +114,16 @@ def _check(st):
         raise DpError(st, lib().dp_last_error().decode())
 
 
+def _release(obj, fn):
+    h = getattr(obj, "h", None)
+    obj.h = None
+    if h and _bound is not None:
+        try:
+            getattr(_bound, fn)(h)
+        except Exception:  # interpreter shutdown
+            pass
+
+
 def _b(s: str) -> bytes:
     return s.encode()
 
@@ -124,10 +136,8 @@ class Registry:
         _check(L().dp_registry_create(ctypes.byref(h)))
         self.h = h
 
-    def __del__(self):
-        if getattr(self, "h", None):
-            L().dp_registry_destroy(self.h)
-            self.h = None
+    def __del__(self, _rel=_release):
+        _rel(self, "dp_registry_destroy")
 
     def register_affine(self, name, a, b):
         _check(L().dp_registry_register_affine(self.h, _b(name), a, b))
@@ -166,10 +176,8 @@ class Source:
         self.h = h
         self._keep = keepalive
 
-    def __del__(self):
-        if getattr(self, "h", None):
-            L().dp_source_release(self.h)
-            self.h = None
+    def __del__(self, _rel=_release):
+        _rel(self, "dp_source_release")
 
     @staticmethod
     def synthetic_images(count, h, w, seed=0x5EED, device=0):
@@ -218,10 +226,8 @@ class Dataset:
         self.reg = reg
         self._keep = keep  # sources referenced by the graph stay alive with it
 
-    def __del__(self):
-        if getattr(self, "h", None):
-            L().dp_graph_release(self.h)
-            self.h = None
+    def __del__(self, _rel=_release):
+        _rel(self, "dp_graph_release")
 
     def _emit(self, fn, *args, keep=()):
         out = c_vp()
@@ -358,10 +364,8 @@ class Iterator:
         self.h = h
         self._ds = ds
 
-    def __del__(self):
-        if getattr(self, "h", None):
-            L().dp_iterator_destroy(self.h)
-            self.h = None
+    def __del__(self, _rel=_release):
+        _rel(self, "dp_iterator_destroy")
 
     def get_next(self):
         b = dp_batch()
@@ -393,6 +397,10 @@ class Iterator:
         return ns.value, n.value
 
     @property
+    def batches_launched(self):
+        return L().dp_iterator_batches_launched(self.h)
+
+    @property
     def prefetch_depth(self):
         return L().dp_iterator_prefetch_depth(self.h)
 
@@ -411,7 +419,7 @@ class Iterator:
 
 
 def make_iterator(ds: Dataset, seed_override=None, device=0, consumer_stream=None, host_output=False,
-                  slot_memory_budget=0, deterministic=True):
+                  slot_memory_budget=0, deterministic=True, max_launch_bytes=0):
     """MakeIterator(graph, registry, IteratorOptions) (runtime.hpp:98-100)."""
     o = dp_iterator_options()
     L().dp_iterator_options_default(ctypes.byref(o))
@@ -423,6 +431,7 @@ def make_iterator(ds: Dataset, seed_override=None, device=0, consumer_stream=Non
     o.consumer_stream = consumer_stream
     o.host_output = int(host_output)
     o.slot_memory_budget = slot_memory_budget
+    o.max_launch_bytes = max_launch_bytes
     out = c_vp()
     _check(L().dp_iterator_create(ds.h, ds.reg.h, ctypes.byref(o), ctypes.byref(out)))
     return Iterator(out, ds)

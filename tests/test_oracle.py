@@ -248,3 +248,16 @@ def test_restatement_matches_reference_interleave_random(orc, ref):
         want = ref.interleave_ids(m, c, L, parallel=p, shard=(k, g))
         inputs = orc.shard_positions(m, k, g)
         assert (closed_form_interleave(inputs, c, L) == want).all()
+
+
+def test_fast_division_proven_for_all_fp32_in_0_255(tmp_path):
+    """tools/prove_fast_div.c enumerates every fp32 in [+0, 255] (1.13e9 per
+    channel) and checks the device normalize's two-FMA division against IEEE
+    division: the K4 (resize) inputs are blends of uint8 pixels, all in that
+    range, so K4's normalize is exact too."""
+    import subprocess
+    src = os.path.join(os.path.dirname(HERE), "tools", "prove_fast_div.c")
+    exe = str(tmp_path / "prove_fast_div")
+    subprocess.run(["gcc", "-O2", "-ffp-contract=off", "-fopenmp", src, "-o", exe, "-lm"], check=True)
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and "TOTAL mismatches: 0" in out.stdout, out.stdout

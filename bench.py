@@ -238,8 +238,9 @@ def run_ours(args, cfg):
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
-        try:
-            traffic = json.load(open(prof)).get(args.config)
+        try:  # measured on a 16-batch launch; scaled to this run's launch size
+            t16 = json.load(open(prof)).get(args.config)
+            traffic = None if t16 is None else int(t16 * batches_per_launch / 16)
         except Exception:
             traffic = None
     line = {

@@ -64,11 +64,21 @@ struct SourceData {
   int64_t h = 0, w = 0, c = 0, total_tokens = 0;
   Residency residency = Residency::kDevice;
   int device = 0;
+  // Sharded residency (one process per GPU): this process
+  // holds only the elements with position p % shard_count == shard_index of a
+  // `global_count`-element dataset, row r = position shard_index + r *
+  // shard_count.  The graph must apply shard(shard_count, shard_index) to it
+  // first (checked at MakeIterator).  shard_count 1 = fully resident.
+  int64_t global_count = 0, shard_count = 1, shard_index = 0;
 };
 using SourcePtr = std::shared_ptr<const SourceData>;
 
 // Synthetic inputs, generated on the device.
 SourcePtr SynthImages(int64_t count, int64_t h, int64_t w, uint64_t seed, int device = 0);
+// Only shard `index` of `num_shards` of a `global_count`-image dataset is
+// generated and held (pixels keyed by the global element id).
+SourcePtr SynthImagesSharded(int64_t global_count, int64_t h, int64_t w, uint64_t seed, int64_t num_shards,
+                             int64_t index, int device = 0);
 SourcePtr SynthTokens(int64_t count, uint32_t max_len, uint64_t len_seed, uint64_t tok_seed, int device = 0);
 // Uploads host data (copied); images: u8 [count, h, w, 3].
 SourcePtr ImagesFromHost(const uint8_t* data, int64_t count, int64_t h, int64_t w, int device = 0);

@@ -123,6 +123,19 @@ int dp_k_resize_normalize_batch(const uint8_t* images, int64_t num_images,
                                 const float stdv[3], int64_t* out_ids,
                                 float* out, void* stream);
 
+/* Sharded residency (one process per GPU holds shard `id_base` of
+ * `id_stride`): `images` row r is element id_base + r * id_stride; the
+ * gather order indexes rows, ids (Philox counter, out_ids) are global. */
+int dp_k_crop_flip_normalize_batch_ex(const uint8_t* images, int64_t num_images, int in_h, int in_w,
+                                      const int64_t* order, int64_t first, int64_t rows, int64_t id_base,
+                                      int64_t id_stride, uint64_t udf_seed, int crop_h, int crop_w, int do_flip,
+                                      const float mean[3], const float stdv[3], int64_t* out_ids, float* out,
+                                      void* stream);
+int dp_k_resize_normalize_batch_ex(const uint8_t* images, int64_t num_images, int in_h, int in_w,
+                                   const int64_t* order, int64_t first, int64_t rows, int64_t id_base,
+                                   int64_t id_stride, int out_h, int out_w, const float mean[3],
+                                   const float stdv[3], int64_t* out_ids, float* out, void* stream);
+
 /* ---------------------------------------------------------------------- */
 /* K5  filter(len <= max_keep) stream compaction + padded_batch.           */
 /*     FilterIterator (src/runtime.cpp:537-577) + BatchIterator on ragged  */
@@ -193,6 +206,9 @@ int dp_k_word_digest(const uint32_t* words, int64_t n, int64_t first,
 /* image_bytes + off)).                                                    */
 int dp_k_synth_images(uint8_t* images, uint64_t first_id, uint64_t count,
                       uint64_t image_bytes, uint64_t seed, void* stream);
+/* Row i holds image id first_id + i * id_stride (a Shard's residency). */
+int dp_k_synth_images_strided(uint8_t* images, uint64_t first_id, uint64_t id_stride, uint64_t count,
+                              uint64_t image_bytes, uint64_t seed, void* stream);
 /* tokens[offsets[i] + j] = SplitMix64Next(seed ^ (i << 20 | j)) & 0x7fffffff */
 int dp_k_synth_tokens(int32_t* tokens, const int64_t* offsets, int64_t n,
                       uint64_t seed, void* stream);

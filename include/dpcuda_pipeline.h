@@ -49,6 +49,10 @@ int dp_registry_contains(const dp_registry* reg, const char* name);
 
 /* ---- sources (new kinds) ---- */
 int dp_source_synthetic_images(int64_t count, int64_t h, int64_t w, uint64_t seed, int device, dp_source** out);
+/* Sharded residency: only elements p % num_shards == index of a global_count
+ * dataset are generated/held; graphs must start with shard(num_shards, index). */
+int dp_source_synthetic_images_sharded(int64_t global_count, int64_t h, int64_t w, uint64_t seed,
+                                       int64_t num_shards, int64_t index, int device, dp_source** out);
 int dp_source_images_from_host(const uint8_t* data, int64_t count, int64_t h, int64_t w, int device,
                                dp_source** out);
 /* pinned/registered host memory read by the kernels over PCIe (end-to-end runs; not copied) */

@@ -103,6 +103,11 @@ int dp_source_synthetic_images(int64_t count, int64_t h, int64_t w, uint64_t see
   DP_REQUIRE(out);
   return Guard([&] { *out = new dp_source{SynthImages(count, h, w, seed, device)}; });
 }
+int dp_source_synthetic_images_sharded(int64_t global_count, int64_t h, int64_t w, uint64_t seed,
+                                       int64_t num_shards, int64_t index, int device, dp_source** out) {
+  DP_REQUIRE(out);
+  return Guard([&] { *out = new dp_source{SynthImagesSharded(global_count, h, w, seed, num_shards, index, device)}; });
+}
 int dp_source_images_from_host(const uint8_t* data, int64_t count, int64_t h, int64_t w, int device,
                                dp_source** out) {
   DP_REQUIRE(data && out);

@@ -142,6 +142,29 @@ SourcePtr SynthImages(int64_t count, int64_t h, int64_t w, uint64_t seed, int de
   return s;
 }
 
+SourcePtr SynthImagesSharded(int64_t global_count, int64_t h, int64_t w, uint64_t seed, int64_t num_shards,
+                             int64_t index, int device) {
+  if (num_shards < 1 || index < 0 || index >= num_shards || global_count <= index)
+    throw PipelineError(ErrorCode::kInvalidAttr, "synth images: shard index must be in [0, num_shards) and < count");
+  if (h < 1 || w < 1) throw PipelineError(ErrorCode::kInvalidAttr, "synth images: bad shape");
+  auto s = std::make_shared<SourceData>();
+  s->kind = SourceData::Kind::kImages;
+  s->count = (global_count - index + num_shards - 1) / num_shards;
+  s->global_count = global_count;
+  s->shard_count = num_shards;
+  s->shard_index = index;
+  s->h = h;
+  s->w = w;
+  s->c = 3;
+  s->device = device;
+  s->values = DeviceAlloc(static_cast<size_t>(s->count) * h * w * 3, device);
+  DeviceGuard g(device);
+  KCheck(dp_k_synth_images_strided(P<uint8_t>(s->values), index, num_shards, s->count, h * w * 3, seed, nullptr),
+         "synth images");
+  CudaCheck(cudaDeviceSynchronize(), "synth images");
+  return s;
+}
+
 SourcePtr SynthTokens(int64_t count, uint32_t max_len, uint64_t len_seed, uint64_t tok_seed, int device) {
   if (count < 1 || max_len < 1) throw PipelineError(ErrorCode::kInvalidAttr, "synth tokens: bad shape");
   // lengths: Pcg32(len_seed).Bounded(max_len) + 1 drawn in order (random.hpp:41-63)
@@ -318,18 +341,17 @@ Lowered Lower(const DatasetGraph& g, const UdfRegistry& reg) {
   // ---- batch stage ----
   L.batch_node_path = path;
   L.node_paths.push_back(path);
-  if (n->kind() == NodeKind::kMapAndBatch) {
-    L.steps = reg.Get(n->GetString("udf")).map;
+  if (n->kind() == NodeKind::kMapAndBatch || n->kind() == NodeKind::kBatch) {
+    if (n->kind() == NodeKind::kMapAndBatch) L.steps = reg.Get(n->GetString("udf")).map;
     L.batch = n->GetInt("batch_size");
     L.drop = n->GetBoolOr("drop_remainder", false);
     descend();
-  } else if (n->kind() == NodeKind::kBatch) {
-    L.batch = n->GetInt("batch_size");
-    L.drop = n->GetBoolOr("drop_remainder", false);
-    descend();
-    if (n->kind() == NodeKind::kMap) {  // unfused map+batch: same result for total UDFs
+    // unfused map(f).map(g)...batch: the same result as the fused rewrite for
+    // total UDFs (optimizer.cpp map_map / map_batch fusion)
+    while (n->kind() == NodeKind::kMap) {
       if (n->HasAttr("fused_filter_udf")) Unsupported("map with a fused predicate under batch");
-      L.steps = reg.Get(n->GetString("udf")).map;
+      const auto& f = reg.Get(n->GetString("udf")).map;
+      L.steps.insert(L.steps.begin(), f.begin(), f.end());  // inner maps run first
       descend();
     }
   } else if (n->kind() == NodeKind::kPaddedBatch) {
@@ -391,7 +413,20 @@ Lowered Lower(const DatasetGraph& g, const UdfRegistry& reg) {
     default:
       Unsupported(std::string("unsupported node on the device path: ") + NodeKindName(n->kind()));
   }
+  if (L.source && L.source->shard_count > 1) {
+    // sharded residency: the graph's first transformation must be the shard
+    // this process holds; positions then index resident rows directly
+    const auto& s = *L.source;
+    if (L.chain.empty() || L.chain[0].kind != IndexOp::Kind::kShard || L.chain[0].a != s.shard_count ||
+        L.chain[0].b != s.shard_index)
+      Unsupported("source holds only shard " + std::to_string(s.shard_index) + " of " +
+                  std::to_string(s.shard_count) + ": apply shard(" + std::to_string(s.shard_count) + ", " +
+                  std::to_string(s.shard_index) + ") to it first");
+    L.chain.erase(L.chain.begin());
+    L.source_count = s.count;
+  }
   if (seen_interleave) {
+    if (L.records && L.records->shard_count > 1) Unsupported("interleave records must be fully resident");
     if (L.source && L.source->kind != SourceData::Kind::kInt64) Unsupported("interleave input must be int64 ordinals");
     if (L.source) Unsupported("interleave over from_memory ordinals: use range()");
     L.source = L.records;  // the batch stage reads the record source
@@ -973,15 +1008,16 @@ class DevicePipeline {
         const int oh = static_cast<int>(L_.kind == BatchKind::kCrop ? L_.crop.out_h : L_.resize.out_h);
         const int ow = static_cast<int>(L_.kind == BatchKind::kCrop ? L_.crop.out_w : L_.resize.out_w);
         if (L_.kind == BatchKind::kCrop)
-          KCheck(dp_k_crop_flip_normalize_batch(P<uint8_t>(src.values), src.count, static_cast<int>(src.h),
-                                                static_cast<int>(src.w), order, row0, rows_total, L_.crop.seed, oh, ow,
-                                                L_.crop.flip ? 1 : 0, mean, stdv, P<int64_t>(slot->a), P<float>(slot->b),
-                                                stream_),
+          KCheck(dp_k_crop_flip_normalize_batch_ex(P<uint8_t>(src.values), src.count, static_cast<int>(src.h),
+                                                   static_cast<int>(src.w), order, row0, rows_total, src.shard_index,
+                                                   src.shard_count, L_.crop.seed, oh, ow, L_.crop.flip ? 1 : 0, mean,
+                                                   stdv, P<int64_t>(slot->a), P<float>(slot->b), stream_),
                  "K3");
         else
-          KCheck(dp_k_resize_normalize_batch(P<uint8_t>(src.values), src.count, static_cast<int>(src.h),
-                                             static_cast<int>(src.w), order, row0, rows_total, oh, ow, mean, stdv,
-                                             P<int64_t>(slot->a), P<float>(slot->b), stream_),
+          KCheck(dp_k_resize_normalize_batch_ex(P<uint8_t>(src.values), src.count, static_cast<int>(src.h),
+                                                static_cast<int>(src.w), order, row0, rows_total, src.shard_index,
+                                                src.shard_count, oh, ow, mean, stdv, P<int64_t>(slot->a),
+                                                P<float>(slot->b), stream_),
                  "K4");
         launches_++;
         int64_t off = 0;

@@ -45,6 +45,7 @@ struct ImageArgs {
   int in_h, in_w, out_h, out_w;
   int bands;
   NormConsts nc;
+  int64_t id_base, id_stride;  // element id of row r = id_base + r * id_stride
 };
 
 // ---------------------------------------------------------------- K3 ----
@@ -54,8 +55,9 @@ crop_generic_kernel(ImageArgs a, uint64_t seed, int do_flip, int sstride) {
   extern __shared__ __align__(16) uint8_t stage[];
   const int band = blockIdx.x % a.bands;
   const int64_t j = blockIdx.x / a.bands;
-  const int64_t id = a.order ? a.order[a.first + j] : a.first + j;
-  if (id < 0 || id >= a.num_images) return;  // engine orders are in range by construction
+  const int64_t row = a.order ? a.order[a.first + j] : a.first + j;
+  if (row < 0 || row >= a.num_images) return;  // engine orders are in range by construction
+  const int64_t id = a.id_base + row * a.id_stride;  // element id (sharded residency)
   CropParams cp = crop_params(seed, id, a.in_h, a.in_w, a.out_h, a.out_w);
   if (!do_flip) cp.flip = 0;
   if (band == 0 && threadIdx.x == 0) a.out_ids[j] = id;
@@ -64,7 +66,7 @@ crop_generic_kernel(ImageArgs a, uint64_t seed, int do_flip, int sstride) {
   const int nrows = min(kCropBandRows, a.out_h - y_begin);
   const size_t row_bytes = static_cast<size_t>(a.in_w) * 3;
   const int seg = a.out_w * 3;  // bytes (= floats) per output row
-  const uint8_t* img = a.images + static_cast<size_t>(id) * a.in_h * row_bytes;
+  const uint8_t* img = a.images + static_cast<size_t>(row) * a.in_h * row_bytes;
   const uint8_t* src0 = img + static_cast<size_t>(cp.oy + y_begin) * row_bytes;
   const int start = cp.ox * 3;
 
@@ -143,9 +145,9 @@ resize_generic_kernel(ImageArgs a) {
   extern __shared__ __align__(16) uint8_t stage[];
   const int band = blockIdx.x % a.bands;
   const int64_t j = blockIdx.x / a.bands;
-  const int64_t id = a.order ? a.order[a.first + j] : a.first + j;
-  if (id < 0 || id >= a.num_images) return;  // engine orders are in range by construction
-  if (band == 0 && threadIdx.x == 0) a.out_ids[j] = id;
+  const int64_t row = a.order ? a.order[a.first + j] : a.first + j;
+  if (row < 0 || row >= a.num_images) return;  // engine orders are in range by construction
+  if (band == 0 && threadIdx.x == 0) a.out_ids[j] = a.id_base + row * a.id_stride;
 
   const int y_begin = band * kResizeBandRows;
   const int nrows = min(kResizeBandRows, a.out_h - y_begin);
@@ -155,7 +157,7 @@ resize_generic_kernel(ImageArgs a) {
   resize_coord(y_begin + nrows - 1, a.in_h, a.out_h, tmp, ys1, wtmp);
   const size_t row_bytes = static_cast<size_t>(a.in_w) * 3;
   const size_t span = static_cast<size_t>(ys1 - ys0 + 1) * row_bytes;  // contiguous source rows
-  const uint8_t* src = a.images + (static_cast<size_t>(id) * a.in_h + ys0) * row_bytes;
+  const uint8_t* src = a.images + (static_cast<size_t>(row) * a.in_h + ys0) * row_bytes;
   if (kAligned) {
     for (size_t t = threadIdx.x; t < span / 16; t += kThreads)
       *reinterpret_cast<uint4*>(stage + t * 16) = ld_nc_na_u4(src + t * 16);
@@ -260,7 +262,7 @@ struct StageMeta {
 // item, 32 items at a time, so the gather-index loads and Philox draws of a
 // whole group are in flight together instead of serialising per item.
 struct Plan {
-  int64_t id, j;
+  int64_t id, j, row;  // element id, batch row, source image row
   int band, nrows, src_row, col, shift, flip;
   uint32_t bytes_row;
 };
@@ -269,6 +271,7 @@ __device__ __forceinline__ Plan shfl_plan(const Plan& p, int src) {
   Plan o;
   o.id = __shfl_sync(0xffffffffu, p.id, src);
   o.j = __shfl_sync(0xffffffffu, p.j, src);
+  o.row = __shfl_sync(0xffffffffu, p.row, src);
   o.band = __shfl_sync(0xffffffffu, p.band, src);
   o.nrows = __shfl_sync(0xffffffffu, p.nrows, src);
   o.src_row = __shfl_sync(0xffffffffu, p.src_row, src);
@@ -291,6 +294,7 @@ struct FastArgs {
   uint64_t seed;
   int do_flip;
   NormConsts nc;
+  int64_t id_base, id_stride;  // element id of row r = id_base + r * id_stride
 };
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -323,12 +327,13 @@ struct CropOp {
     Plan p;
     p.j = item / a.bands;
     p.band = static_cast<int>(item - p.j * a.bands);
-    const int64_t id = a.order ? a.order[a.first + p.j] : a.first + p.j;
-    const bool valid = id >= 0 && id < a.num_images;
-    p.id = valid ? id : -1;
+    const int64_t row = a.order ? a.order[a.first + p.j] : a.first + p.j;
+    const bool valid = row >= 0 && row < a.num_images;
+    p.row = valid ? row : -1;
+    p.id = valid ? a.id_base + row * a.id_stride : -1;
     p.nrows = min(a.band_rows, a.out_h - p.band * a.band_rows);
     CropParams cp{0, 0, 0};
-    if (valid) cp = crop_params(a.seed, id, a.in_h, a.in_w, a.out_h, a.out_w);
+    if (valid) cp = crop_params(a.seed, p.id, a.in_h, a.in_w, a.out_h, a.out_w);
     const int start = cp.ox * 3;
     p.shift = start & 15;
     p.src_row = cp.oy + p.band * a.band_rows;  // first source row
@@ -349,7 +354,7 @@ struct CropOp {
     __syncwarp();
     if (valid) {
       const size_t row_bytes = static_cast<size_t>(a.in_w) * 3;
-      const uint8_t* src0 = a.images + (static_cast<size_t>(p.id) * a.in_h + p.src_row) * row_bytes + p.col;
+      const uint8_t* src0 = a.images + (static_cast<size_t>(p.row) * a.in_h + p.src_row) * row_bytes + p.col;
       for (int r = lane; r < p.nrows; r += 32)
         bulk_g2s(dst + r * a.stage_stride, src0 + r * row_bytes, p.bytes_row, full, pol);
     }
@@ -396,8 +401,10 @@ struct ResizeOp {
     Plan p;
     p.j = item / a.bands;
     p.band = static_cast<int>(item - p.j * a.bands);
-    const int64_t id = a.order ? a.order[a.first + p.j] : a.first + p.j;
-    p.id = (id >= 0 && id < a.num_images) ? id : -1;
+    const int64_t row = a.order ? a.order[a.first + p.j] : a.first + p.j;
+    const bool valid = row >= 0 && row < a.num_images;
+    p.row = valid ? row : -1;
+    p.id = valid ? a.id_base + row * a.id_stride : -1;
     const int y_begin = p.band * a.band_rows;
     p.nrows = min(a.band_rows, a.out_h - y_begin);
     p.src_row = taps[y_begin].y0;
@@ -416,7 +423,7 @@ struct ResizeOp {
       *meta = StageMeta{p.id, p.j, p.band, p.nrows, 0, 0, p.src_row, 0};
       mbar_arrive_expect_tx(full, valid ? p.bytes_row : 0u);
       if (valid)
-        bulk_g2s(dst, a.images + (static_cast<size_t>(p.id) * a.in_h + p.src_row) * static_cast<size_t>(a.in_w) * 3,
+        bulk_g2s(dst, a.images + (static_cast<size_t>(p.row) * a.in_h + p.src_row) * static_cast<size_t>(a.in_w) * 3,
                  p.bytes_row, full, pol);
     }
     __syncwarp();
@@ -624,10 +631,10 @@ FastArgs make_fast(const uint8_t* images, int64_t num_images, int in_h, int in_w
 
 using namespace dpk;
 
-extern "C" int dp_k_crop_flip_normalize_batch(const uint8_t* images, int64_t num_images, int in_h, int in_w,
-                                              const int64_t* order, int64_t first, int64_t rows, uint64_t udf_seed,
-                                              int crop_h, int crop_w, int do_flip, const float mean[3],
-                                              const float stdv[3], int64_t* out_ids, float* out, void* stream) {
+static int crop_impl(const uint8_t* images, int64_t num_images, int in_h, int in_w, const int64_t* order, int64_t first,
+                     int64_t rows, uint64_t udf_seed, int crop_h, int crop_w, int do_flip, const float mean[3],
+                     const float stdv[3], int64_t* out_ids, float* out, void* stream, int64_t id_base,
+                     int64_t id_stride) {
   int st = check_common(images, num_images, in_h, in_w, rows, crop_h, crop_w, out_ids, out, "crop_flip_normalize");
   if (st) return st;
   if (crop_h > in_h || crop_w > in_w)
@@ -637,6 +644,8 @@ extern "C" int dp_k_crop_flip_normalize_batch(const uint8_t* images, int64_t num
   if (fast_ok(images, in_w, crop_w, out)) {
     FastArgs f = make_fast(images, num_images, in_h, in_w, order, first, rows, crop_h, crop_w, mean, stdv, out_ids,
                            out, env_int("DP_DEV_CROP_BAND", kFastCropBandRows), kCropStages);
+    f.id_base = id_base;
+    f.id_stride = id_stride;
     f.seed = udf_seed;
     f.do_flip = do_flip;
     f.stage_stride = ((crop_w * 3 + 15 + 15) / 16) * 16;
@@ -647,7 +656,7 @@ extern "C" int dp_k_crop_flip_normalize_batch(const uint8_t* images, int64_t num
     if (smem <= kSmemBudget) return launch_persistent(pipeline_kernel<CropOp>, f, smem, s, "crop_flip_normalize");
   }
   ImageArgs a{images, order, first, out_ids, out, num_images, in_h, in_w, crop_h, crop_w,
-              (crop_h + kCropBandRows - 1) / kCropBandRows, make_norm(mean, stdv)};
+              (crop_h + kCropBandRows - 1) / kCropBandRows, make_norm(mean, stdv), id_base, id_stride};
   const size_t row_bytes = static_cast<size_t>(in_w) * 3;
   const bool aligned = (row_bytes % 16 == 0) && (reinterpret_cast<uintptr_t>(images) % 16 == 0) &&
                        (crop_w % 4 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
@@ -666,10 +675,9 @@ extern "C" int dp_k_crop_flip_normalize_batch(const uint8_t* images, int64_t num
   return launch_status("crop_flip_normalize");
 }
 
-extern "C" int dp_k_resize_normalize_batch(const uint8_t* images, int64_t num_images, int in_h, int in_w,
-                                           const int64_t* order, int64_t first, int64_t rows, int out_h, int out_w,
-                                           const float mean[3], const float stdv[3], int64_t* out_ids, float* out,
-                                           void* stream) {
+static int resize_impl(const uint8_t* images, int64_t num_images, int in_h, int in_w, const int64_t* order,
+                       int64_t first, int64_t rows, int out_h, int out_w, const float mean[3], const float stdv[3],
+                       int64_t* out_ids, float* out, void* stream, int64_t id_base, int64_t id_stride) {
   int st = check_common(images, num_images, in_h, in_w, rows, out_h, out_w, out_ids, out, "resize_normalize");
   if (st) return st;
   if (rows == 0) return DP_OK;
@@ -677,6 +685,8 @@ extern "C" int dp_k_resize_normalize_batch(const uint8_t* images, int64_t num_im
   if (fast_ok(images, in_w, out_w, out)) {
     FastArgs f = make_fast(images, num_images, in_h, in_w, order, first, rows, out_h, out_w, mean, stdv, out_ids, out,
                            env_int("DP_DEV_RESIZE_BAND", kFastResizeBandRows), kResizeStages);
+    f.id_base = id_base;
+    f.id_stride = id_stride;
     const double sc = static_cast<double>(in_h) / out_h;
     int src_rows = static_cast<int>(f.band_rows * sc) + 3;
     if (src_rows > in_h) src_rows = in_h;
@@ -689,7 +699,7 @@ extern "C" int dp_k_resize_normalize_batch(const uint8_t* images, int64_t num_im
       return launch_persistent(pipeline_kernel<ResizeOp>, f, smem, s, "resize_normalize");
   }
   ImageArgs a{images, order, first, out_ids, out, num_images, in_h, in_w, out_h, out_w,
-              (out_h + kResizeBandRows - 1) / kResizeBandRows, make_norm(mean, stdv)};
+              (out_h + kResizeBandRows - 1) / kResizeBandRows, make_norm(mean, stdv), id_base, id_stride};
   const size_t row_bytes = static_cast<size_t>(in_w) * 3;
   const bool aligned = (row_bytes % 16 == 0) && (reinterpret_cast<uintptr_t>(images) % 16 == 0) &&
                        (out_w % 4 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
@@ -709,4 +719,37 @@ extern "C" int dp_k_resize_normalize_batch(const uint8_t* images, int64_t num_im
     resize_generic_kernel<false><<<static_cast<int>(grid), kThreads, smem, s>>>(a);
   }
   return launch_status("resize_normalize");
+}
+
+extern "C" int dp_k_crop_flip_normalize_batch(const uint8_t* images, int64_t num_images, int in_h, int in_w,
+                                              const int64_t* order, int64_t first, int64_t rows, uint64_t udf_seed,
+                                              int crop_h, int crop_w, int do_flip, const float mean[3],
+                                              const float stdv[3], int64_t* out_ids, float* out, void* stream) {
+  return crop_impl(images, num_images, in_h, in_w, order, first, rows, udf_seed, crop_h, crop_w, do_flip, mean, stdv,
+                   out_ids, out, stream, 0, 1);
+}
+
+extern "C" int dp_k_crop_flip_normalize_batch_ex(const uint8_t* images, int64_t num_images, int in_h, int in_w,
+                                                 const int64_t* order, int64_t first, int64_t rows, int64_t id_base,
+                                                 int64_t id_stride, uint64_t udf_seed, int crop_h, int crop_w,
+                                                 int do_flip, const float mean[3], const float stdv[3],
+                                                 int64_t* out_ids, float* out, void* stream) {
+  return crop_impl(images, num_images, in_h, in_w, order, first, rows, udf_seed, crop_h, crop_w, do_flip, mean, stdv,
+                   out_ids, out, stream, id_base, id_stride);
+}
+
+extern "C" int dp_k_resize_normalize_batch(const uint8_t* images, int64_t num_images, int in_h, int in_w,
+                                           const int64_t* order, int64_t first, int64_t rows, int out_h, int out_w,
+                                           const float mean[3], const float stdv[3], int64_t* out_ids, float* out,
+                                           void* stream) {
+  return resize_impl(images, num_images, in_h, in_w, order, first, rows, out_h, out_w, mean, stdv, out_ids, out,
+                     stream, 0, 1);
+}
+
+extern "C" int dp_k_resize_normalize_batch_ex(const uint8_t* images, int64_t num_images, int in_h, int in_w,
+                                              const int64_t* order, int64_t first, int64_t rows, int64_t id_base,
+                                              int64_t id_stride, int out_h, int out_w, const float mean[3],
+                                              const float stdv[3], int64_t* out_ids, float* out, void* stream) {
+  return resize_impl(images, num_images, in_h, in_w, order, first, rows, out_h, out_w, mean, stdv, out_ids, out,
+                     stream, id_base, id_stride);
 }

@@ -223,6 +223,20 @@ extern "C" int dp_k_word_digest(const uint32_t* words, int64_t n, int64_t first,
   return launch_status("word_digest");
 }
 
+extern "C" int dp_k_synth_images_strided(uint8_t* images, uint64_t first_id, uint64_t id_stride, uint64_t count,
+                                         uint64_t image_bytes, uint64_t seed, void* stream) {
+  if (id_stride <= 1) return dp_k_synth_images(images, first_id, count, image_bytes, seed, stream);
+  if (reinterpret_cast<uintptr_t>(images) & 15)
+    return fail(DP_ERR_INVALID_ATTR, "synth_images: buffer must be 16-byte aligned");
+  // one launch per row (setup path, not timed): rows are contiguous id runs of length 1
+  for (uint64_t i = 0; i < count; ++i) {
+    synth_images_kernel<<<grid_for(static_cast<int64_t>((image_bytes + 15) / 16), 4), kThreads, 0,
+                          as_stream(stream)>>>(images + i * image_bytes, (first_id + i * id_stride) * image_bytes,
+                                               image_bytes, seed);
+  }
+  return launch_status("synth_images_strided");
+}
+
 extern "C" int dp_k_synth_images(uint8_t* images, uint64_t first_id, uint64_t count, uint64_t image_bytes,
                                  uint64_t seed, void* stream) {
   uint64_t total = count * image_bytes;

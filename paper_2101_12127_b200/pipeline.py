@@ -56,6 +56,7 @@ _SIGS = {
     "dp_registry_contains": [c_vp, ctypes.c_char_p],
     "dp_source_synthetic_images": [c_i64, c_i64, c_i64, c_u64, c_int, PP],
     "dp_source_images_from_host": [c_vp, c_i64, c_i64, c_i64, c_int, PP],
+    "dp_source_synthetic_images_sharded": [c_i64, c_i64, c_i64, c_u64, c_i64, c_i64, c_int, PP],
     "dp_source_images_pinned_host": [c_vp, c_i64, c_i64, c_i64, c_int, PP],
     "dp_source_synthetic_tokens": [c_i64, ctypes.c_uint32, c_u64, c_u64, c_int, PP],
     "dp_source_tokens_from_host": [c_vp, c_i64, c_vp, c_int, PP],
@@ -183,6 +184,15 @@ class Source:
     def synthetic_images(count, h, w, seed=0x5EED, device=0):
         out = c_vp()
         _check(L().dp_source_synthetic_images(count, h, w, seed, device, ctypes.byref(out)))
+        return Source(out)
+
+    @staticmethod
+    def synthetic_images_sharded(global_count, h, w, num_shards, index, seed=0x5EED, device=0):
+        """Holds only shard `index` of `num_shards` (one process per GPU);
+        graphs over it must start with .shard(num_shards, index)."""
+        out = c_vp()
+        _check(L().dp_source_synthetic_images_sharded(global_count, h, w, seed, num_shards, index, device,
+                                                      ctypes.byref(out)))
         return Source(out)
 
     @staticmethod

@@ -287,6 +287,33 @@ def test_cfg5_interleave_shuffle_map_and_batch(dp, orc):
         assert np.array_equal(pix[r], orc.crop_flip_normalize(orc.images(p, 1, 48, 48)[0], p, 32, 32))
 
 
+def test_sharded_residency_equals_shard_of_full_dataset(dp, orc):
+    """Per-GPU residency: a process holding only shard i of k
+    produces exactly shard(k, i) of the full dataset, ids and pixels."""
+    n, buf = 2000, 300
+    reg = image_registry(dp, 0, crop=(48, 48))
+    for k in (2, 8):
+        seen = []
+        for i in range(k):
+            src = dp.Source.synthetic_images_sharded(n, 64, 64, k, i)
+            g, _ = dp.Dataset.tensor_slices(reg, src).shard(k, i).shuffle(buf, 42).map("crop").map("norm") \
+                .batch(64).optimize()
+            batches = drain(dp.make_iterator(g, seed_override=1), comps=(0, 1))
+            ids = np.concatenate([b[0] for b in batches])
+            pos = orc.shard_positions(n, k, i)
+            want = pos[orc.shuffle_order(pos.size, buf, orc.shuffle_seed(1, 42))]
+            assert (ids == want).all(), (k, i)
+            p = int(batches[0][0][3])
+            assert np.array_equal(batches[0][1][3], orc.crop_flip_normalize(orc.images(p, 1, 64, 64)[0], p, 48, 48))
+            seen.append(ids)
+        assert sorted(np.concatenate(seen).tolist()) == list(range(n))
+    src = dp.Source.synthetic_images_sharded(n, 64, 64, 4, 1)
+    bad = dp.Dataset.tensor_slices(reg, src).map("crop").map("norm").batch(8)
+    with pytest.raises(Exception) as e:
+        dp.make_iterator(bad)
+    assert "apply shard(4, 1)" in str(e.value)
+
+
 def test_unsupported_graph_fails_loudly(dp):
     reg = dp.Registry()
     reg.register_affine("a", 1, 1)

@@ -46,7 +46,17 @@ CFG = {
                           "normalize fp32) -> Batch(256) -> Prefetch(AUTOTUNE)",
                  in_hw=(320, 320), out_hw=(224, 224), mode=1, batch=256, n=65536,
                  bytes_per_elem=320 * 320 * 3 + IMG_BYTES_WRITE, kernel="K4 resize_normalize_batch"),
+    "cfg1": dict(workload="Range(2^24) int64 -> Map(x*3+1) -> Batch(1024) (cfg1 shape at roofline size)",
+                 kind="range", batch=1024, n=1 << 24, bytes_per_elem=8, kernel="K1 range_affine_batch",
+                 unit="elements/s", dtype="int64"),
+    "cfg4": dict(workload="1M int32 token sequences, len U[1,1024] -> Filter(len<=512) -> PaddedBatch(128, pad 0)",
+                 kind="tokens", batch=128, n=1_000_000, max_keep=512, kernel="K5 padded_batches",
+                 unit="sequences/s", dtype="int32"),
 }
+for _c in CFG.values():
+    _c.setdefault("kind", "images")
+    _c.setdefault("unit", "images/s")
+    _c.setdefault("dtype", "u8->f32")
 
 
 def load_peaks():
@@ -159,11 +169,27 @@ def cpu_reference(cfg, threads, warmup_batches, steps):
                       f"{warmup_batches} warm-up, map_and_batch num_parallel_calls={threads}, prefetch(2)"}
 
 
+def cpu_reference_range(cfg):
+    """cfg1 on the compiled reference: Range(1M) -> Map -> Batch(1024), optimized."""
+    from tests.oracle_lib import Reference
+    ref = Reference.load()
+    if ref is None:
+        return None
+    n = 1_000_000
+    eps = ref.time_range_map_batch(n, cfg["batch"], 1, epochs=3)
+    return {"value": n / float(sorted(eps)[1]), "sample": f"Range({n}) -> Map(x*3+1, p=1) -> Batch(1024), "
+                                                          f"median of 3 epochs after 1 warm-up"}
+
+
 def run_reference(args, cfg):
     rank, world, _ = dist_env()
     if rank != 0:
         return
     threads = os.cpu_count() or 1
+    if cfg["kind"] != "images":
+        print(json.dumps({"impl": "reference", "unavailable": "the reference arm is timed on the image configs "
+                                                              "(cfg2 headline)"}), flush=True)
+        return
     r = cpu_reference(cfg, threads, args.warmup, args.steps)
     line = {"impl": "reference", "metric": "pipeline elements/sec", "value": round(r["value"], 2),
             "unit": "images/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -193,6 +219,38 @@ def build_graph(dp, cfg, src, repeat=True, shard=None):
     return g, report
 
 
+def build_other_graph(dp, cfg, local, rank, world):
+    reg = dp.Registry()
+    if cfg["kind"] == "range":  # cfg1
+        reg.register_affine("affine(3,1)", 3, 1)
+        g = dp.Dataset.range(reg, cfg["n"] * world)
+        if world > 1:
+            g = g.shard(world, rank)
+        g = g.map("affine(3,1)").batch(cfg["batch"]).repeat(-1).prefetch(-1)
+    else:  # cfg4 tokens
+        reg.register_length_filter("len<=512", cfg["max_keep"])
+        src = dp.Source.synthetic_tokens(cfg["n"], 1024, 4 + rank, 4 + rank, device=local)
+        g = dp.Dataset.token_sequences(reg, src).filter("len<=512").padded_batch(cfg["batch"]).repeat(-1) \
+            .prefetch(-1)
+    return g.optimize()
+
+
+def padded_bytes_per_batch(dp, g, local):
+    """cfg4 algorithmic bytes per batch of K5 padded_batches over one epoch:
+    reads = kept tokens + (order, length, offset) per row; writes = the
+    padded rows + lengths (padding is the output, so it counts)."""
+    it = dp.make_iterator(g, seed_override=1, device=local)
+    per_epoch = int(re.search(r"elements, (\d+) batches", it.describe()).group(1))
+    total = 0
+    for _ in range(per_epoch):
+        b = it.get_next()
+        lens = b.numpy(1)
+        rows, lmax = b.components[0][1]
+        total += 4 * int(lens.sum()) + rows * (8 + 4 + 8) + 4 * rows * lmax + 4 * rows
+        b.release()
+    return total / per_epoch
+
+
 def run_ours(args, cfg):
     import numpy as np
     import torch
@@ -207,7 +265,9 @@ def run_ours(args, cfg):
 
     # ---- device-resident workload (not timed) ----
     n = cfg["n"]
-    if world > 1:  # each rank holds and processes shard `rank` of a world * n dataset
+    if cfg["kind"] != "images":
+        g, report = build_other_graph(dp, cfg, local, rank, world)
+    elif world > 1:  # each rank holds and processes shard `rank` of a world * n dataset
         lay = shard_layout(world, rank, n)
         src = dp.Source.synthetic_images_sharded(lay["global_count"], *cfg["in_hw"], world, rank, seed=0x5EED,
                                                  device=local)
@@ -218,11 +278,13 @@ def run_ours(args, cfg):
     it = dp.make_iterator(g, seed_override=1, device=local)
     stream = torch.cuda.ExternalStream(it.stream, device=dev)
     per_launch = int(re.search(r"(\d+) batch\(es\) per launch", it.describe()).group(1))
+    if cfg["kind"] != "images":  # small batches: whole epochs (one launch each)
+        args.steps = max(args.steps, per_launch)
+        args.warmup = max(args.warmup, per_launch)
     # W and K whole launch groups, so the event window holds exactly K batches
     args.warmup = -(-args.warmup // per_launch) * per_launch
     args.steps = -(-args.steps // per_launch) * per_launch
-    for _ in range(args.warmup):
-        it.get_next().release()
+    it.skip(args.warmup)  # GetNext in C++, batches dropped (no-op consumer)
     torch.cuda.synchronize(dev)
     if world > 1:
         distr.barrier()
@@ -231,10 +293,10 @@ def run_ours(args, cfg):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
         e0.record(stream)
-        for _ in range(args.steps):
-            it.get_next().release()
+        got = it.skip(args.steps)
         e1.record(stream)
         e1.synchronize()
+    assert got == args.steps
     torch.cuda.synchronize(dev)
     ms = e0.elapsed_time(e1)
     launches = it.kernel_launches - launches0
@@ -249,11 +311,14 @@ def run_ours(args, cfg):
     kernel_s = (ns1 - ns0) / max(k1 - k0, 1) / 1e9  # per launch
     batches_per_launch = batches_in_window / max(k1 - k0, 1)
     peak, peak_src = load_peaks()
-    achieved = cfg["bytes_per_elem"] * cfg["batch"] * batches_per_launch / kernel_s / 1e9
+    bytes_per_batch = cfg["bytes_per_elem"] * cfg["batch"] if cfg.get("bytes_per_elem") else \
+        padded_bytes_per_batch(dp, g, local)
+    achieved = bytes_per_batch * batches_per_launch / kernel_s / 1e9
     del it
 
     # ---- end to end through the C ABI with host buffers ----
-    e2e = run_e2e(dp, cfg, local, args)
+    e2e = run_e2e(dp, cfg, local, args) if cfg["kind"] == "images" else {
+        "value": None, "note": "e2e is measured on the image configs (cfg2 headline)"}
 
     # ---- the final ordering check: K7 digest of each rank's
     # first 8 emitted batches of ids, gathered (8 bytes per rank over NCCL) ----
@@ -264,9 +329,11 @@ def run_ours(args, cfg):
     pos = 0
     for _ in range(8):
         b = vit.get_next()
-        _, shape, ptr, _ = b.components[0]
-        _capi.check(_capi.lib().dp_k_order_digest(ctypes.c_void_p(ptr), shape[0], pos,
-                                                  ctypes.c_void_p(digest.data_ptr()), ctypes.c_void_p(vit.stream)))
+        comp = 1 if cfg["kind"] == "tokens" else 0  # ids / values, or the row lengths of padded batches
+        dt, shape, ptr, _ = b.components[comp]
+        fn = _capi.lib().dp_k_order_digest if dt == np.int64 else _capi.lib().dp_k_word_digest
+        _capi.check(fn(ctypes.c_void_p(ptr), shape[0], pos, ctypes.c_void_p(digest.data_ptr()),
+                       ctypes.c_void_p(vit.stream)))
         pos += shape[0]
         b.release()
     torch.cuda.synchronize(dev)
@@ -279,7 +346,8 @@ def run_ours(args, cfg):
         return
     cpu = None
     try:
-        cpu = cpu_reference(cfg, os.cpu_count() or 1, 2, 8)
+        cpu = cpu_reference(cfg, os.cpu_count() or 1, 2, 8) if cfg["kind"] == "images" else \
+            cpu_reference_range(cfg) if cfg["kind"] == "range" else None
     except Exception as ex:  # reported, not fatal
         cpu = {"value": None, "sample": f"unavailable: {ex}"}
     traffic = None
@@ -290,20 +358,23 @@ def run_ours(args, cfg):
             traffic = None if t16 is None else int(t16 * batches_per_launch / 16)
         except Exception:
             traffic = None
+    l2 = (f"inputs {n * cfg['in_hw'][0] * cfg['in_hw'][1] * 3 / 1e9:.1f} GB/GPU and the rotating output slots "
+          f"exceed the 126 MB L2 (no flush needed)" if cfg["kind"] == "images" else
+          "one launch = one epoch of output (> 126 MB L2); no flush needed")
     line = {
-        "metric": "pipeline elements/sec", "value": round(value, 1), "unit": "images/s", "n_gpus": world,
+        "metric": "pipeline elements/sec", "value": round(value, 1), "unit": cfg["unit"], "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 5),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8->f32",
-        "data": "synthetic (device-generated images, SplitMix64 pixels)",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": cfg["dtype"],
+        "data": "synthetic (device-generated, SplitMix64 / PCG32 keyed)",
         "config": {"workload": cfg["workload"], "global_batch": cfg["batch"] * world,
-                   "images_per_gpu": n, "parallelism": f"dp{world} (Shard, no data-path collective)",
-                   "l2": f"inputs {n * cfg['in_hw'][0] * cfg['in_hw'][1] * 3 / 1e9:.1f} GB/GPU and the rotating "
-                         f"output slots exceed the 126 MB L2 (no flush needed)",
+                   "elements_per_gpu": n, "parallelism": f"dp{world} (Shard, no data-path collective)",
+                   "l2": l2,
                    "optimized": "map_and_batch" in report or "map_batch_fusion" in report},
         "roofline": {"bound": "hbm", "kernel": cfg["kernel"], "achieved": round(achieved, 1), "peak": peak,
                      "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                     "algorithmic_bytes_per_launch": int(cfg["bytes_per_elem"] * cfg["batch"] * batches_per_launch),
-                     "algorithmic_bytes_per_image": cfg["bytes_per_elem"], "batches_per_launch": batches_per_launch,
+                     "algorithmic_bytes_per_launch": int(bytes_per_batch * batches_per_launch),
+                     "algorithmic_bytes_per_element": round(bytes_per_batch / cfg["batch"], 1),
+                     "batches_per_launch": batches_per_launch,
                      "avg_launch_us": round(kernel_s * 1e6, 3), "launches_timed": k1 - k0, "traffic": traffic},
         "batches_in_window": batches_in_window, "steps_per_launch_group": per_launch,
         "order_check": {"digest": "K7 position-keyed digest of each rank's first 8 batches of ids",

@@ -135,6 +135,9 @@ int dp_iterator_get_next(dp_iterator* it, dp_batch* batch);
 /* Ends the lease.  The slot is rewritten only after the work queued on the
  * iterator's consumer_stream before this call. */
 int dp_batch_release(dp_batch* batch);
+/* GetNext `n` times, dropping every batch (a consumer that only advances the
+ * stream, like tf.data's skip); *produced = batches actually delivered. */
+int dp_iterator_skip(dp_iterator* it, int64_t n, int64_t* produced);
 /* Blocks the calling host thread until the batch is written (and, with
  * host_output, copied to its pinned host slot). */
 int dp_batch_wait(const dp_batch* batch);

@@ -277,6 +277,17 @@ int dp_batch_release(dp_batch* batch) {
   return DP_OK;
 }
 
+int dp_iterator_skip(dp_iterator* it, int64_t n, int64_t* produced) {
+  DP_REQUIRE(it && produced);
+  *produced = 0;
+  return Guard([&] {
+    for (int64_t i = 0; i < n; ++i) {
+      if (!it->it->GetNext()) break;
+      ++*produced;
+    }
+  });
+}
+
 int dp_batch_wait(const dp_batch* batch) {
   DP_REQUIRE(batch && batch->handle);
   return Guard([&] {

@@ -83,6 +83,7 @@ _SIGS = {
     "dp_iterator_get_next": [c_vp, ctypes.POINTER(dp_batch)],
     "dp_batch_release": [ctypes.POINTER(dp_batch)],
     "dp_batch_wait": [ctypes.POINTER(dp_batch)],
+    "dp_iterator_skip": [c_vp, c_i64, ctypes.POINTER(c_i64)],
     "dp_tensor_copy_to_host": [ctypes.POINTER(dp_batch), c_int, c_vp, c_size],
     "dp_iterator_stream": [c_vp], "dp_iterator_kernel_launches": [c_vp], "dp_iterator_prefetch_depth": [c_vp],
     "dp_iterator_batch_stage_timing": [c_vp, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64)],
@@ -384,6 +385,12 @@ class Iterator:
             return None
         _check(st)
         return Batch(b, self)
+
+    def skip(self, n):
+        """GetNext n times in C++ dropping the batches; returns how many were delivered."""
+        k = c_i64()
+        _check(L().dp_iterator_skip(self.h, n, ctypes.byref(k)))
+        return k.value
 
     def __iter__(self):
         while True:

@@ -286,6 +286,12 @@ class PipelineIterator {
   int64_t prefetch_depth() const;       // device slots in use (autotuned)
   int64_t kernel_launches() const;      // sm_100a kernels issued so far
   int64_t batches_launched() const;     // batches covered by issued batch-stage launches
+  // Checkpoint in the reference's DPC1 layout (checkpoint.hpp:36-49,
+  // formats.md:76-94).  Restore() seeks instead of replaying.
+  std::string Save() const;
+  // Repositions a fresh iterator at batch `batches` without computing the
+  // skipped ones (kCorruptBlob past the end).
+  void Seek(int64_t batches);
   // Device time (CUDA events around each launch, on the launching stream)
   // of the fused batch-stage launches issued so far: {total ns, launches}.
   std::pair<int64_t, int64_t> BatchStageTiming() const;
@@ -301,6 +307,13 @@ class PipelineIterator {
 
 std::unique_ptr<PipelineIterator> MakeIterator(const DatasetGraph& graph, const UdfRegistry& registry,
                                                IteratorOptions options = {});
+
+// Restore(graph, registry, blob) (checkpoint.cpp:50-105): validates magic
+// (kCorruptBlob), version (kVersionMismatch) and the seed-invariant graph
+// fingerprint (kFingerprintMismatch), then MakeIterator with the recorded
+// base seed and Seek to the saved position.
+std::unique_ptr<PipelineIterator> Restore(const DatasetGraph& graph, const UdfRegistry& registry,
+                                          const std::string& blob, IteratorOptions options = {});
 
 // PRNG contract helpers (random.hpp:24-34; runtime.cpp:713-718).
 uint64_t MixSeeds(uint64_t a, uint64_t b);

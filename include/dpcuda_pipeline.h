@@ -135,6 +135,15 @@ int dp_iterator_get_next(dp_iterator* it, dp_batch* batch);
 /* Ends the lease.  The slot is rewritten only after the work queued on the
  * iterator's consumer_stream before this call. */
 int dp_batch_release(dp_batch* batch);
+/* Checkpoint (include/datapipe/checkpoint.hpp:36-49, DPC1 layout of
+ * docs/formats.md:76-94).  dp_iterator_save writes the blob into buf (cap
+ * bytes) and its size into *len; with buf == NULL or cap too small it only
+ * reports *len and returns DP_ERR_INVALID_ATTR.  dp_iterator_restore validates
+ * magic / version / fingerprint (CorruptBlob, VersionMismatch,
+ * FingerprintMismatch) and seeks a fresh iterator to the saved position. */
+int dp_iterator_save(const dp_iterator* it, void* buf, size_t cap, size_t* len);
+int dp_iterator_restore(const dp_graph* g, const dp_registry* reg, const void* blob, size_t len,
+                        const dp_iterator_options* opt, dp_iterator** out);
 /* GetNext `n` times, dropping every batch (a consumer that only advances the
  * stream, like tf.data's skip); *produced = batches actually delivered. */
 int dp_iterator_skip(dp_iterator* it, int64_t n, int64_t* produced);

@@ -277,6 +277,34 @@ int dp_batch_release(dp_batch* batch) {
   return DP_OK;
 }
 
+int dp_iterator_save(const dp_iterator* it, void* buf, size_t cap, size_t* len) {
+  DP_REQUIRE(it && len);
+  std::string blob;
+  int st = Guard([&] { blob = it->it->Save(); });
+  if (st != DP_OK) return st;
+  *len = blob.size();
+  if (!buf || cap < blob.size()) return dpk::fail(DP_ERR_INVALID_ATTR, "checkpoint buffer too small");
+  std::memcpy(buf, blob.data(), blob.size());
+  return DP_OK;
+}
+
+int dp_iterator_restore(const dp_graph* g, const dp_registry* reg, const void* blob, size_t len,
+                        const dp_iterator_options* opt, dp_iterator** out) {
+  DP_REQUIRE(g && reg && out && (blob || len == 0));
+  return Guard([&] {
+    IteratorOptions o;
+    if (opt) {
+      o.device = opt->device;
+      o.consumer_stream = opt->consumer_stream;
+      o.host_output = opt->host_output != 0;
+      if (opt->slot_memory_budget) o.slot_memory_budget = opt->slot_memory_budget;
+      o.max_launch_bytes = opt->max_launch_bytes;
+    }
+    std::string b(static_cast<const char*>(blob), len);
+    *out = new dp_iterator{Restore(g->g, reg->reg, b, o)};
+  });
+}
+
 int dp_iterator_skip(dp_iterator* it, int64_t n, int64_t* produced) {
   DP_REQUIRE(it && produced);
   *produced = 0;

@@ -575,7 +575,7 @@ class DevicePipeline {
       done_ = true;
       return std::nullopt;
     }
-    const int64_t grp = i / group_;
+    const int64_t grp = GroupOf(i);
     const auto t0 = std::chrono::steady_clock::now();
     while (issued_groups_ <= grp) IssueGroup(issued_groups_);
     // keep `depth` groups in flight
@@ -584,6 +584,11 @@ class DevicePipeline {
     }
     const auto t1 = std::chrono::steady_clock::now();
     auto slot = group_slot_.at(grp);
+    {
+      // after a Seek into the middle of a group, the skipped batches count as handed out
+      std::lock_guard lk(shared_->mu);
+      if (slot->handed_out < i - slot->first_batch) slot->handed_out = i - slot->first_batch;
+    }
     next_batch_++;
     if (consumer_ != stream_ && !opt_.host_output) CudaCheck(cudaStreamWaitEvent(consumer_, slot->ready, 0), "wait");
     produced_++;
@@ -691,6 +696,30 @@ class DevicePipeline {
   // Batches of group g: [first, first + n).  Groups never straddle the
   // boundary of a non-spanning epoch, so every group is one contiguous range
   // of one epoch plan (plus the next epoch's head when spanning).
+  // Launch group holding batch i (inverse of GroupRange).
+  int64_t GroupOf(int64_t i) const {
+    if (span_epochs_) return i / group_;
+    const int64_t bpe = std::max<int64_t>(batches_per_epoch_, 1);
+    const int64_t gpe = (bpe + group_ - 1) / group_;
+    return (i / bpe) * gpe + (i % bpe) / group_;
+  }
+
+ public:
+  // O(1) repositioning of a fresh iterator at batch n (checkpoint restore):
+  // the skipped batches are never computed.
+  void Seek(int64_t n) {
+    if (produced_ != 0 || issued_groups_ != 0)
+      throw PipelineError(ErrorCode::kInternal, "Seek needs a fresh iterator");
+    if (n < 0 || (total_batches_ >= 0 && n > total_batches_))
+      throw PipelineError(ErrorCode::kCorruptBlob, "checkpoint claims " + std::to_string(n) +
+                                                       " delivered elements but the pipeline has " +
+                                                       std::to_string(total_batches_));
+    next_batch_ = n;
+    produced_ = n;
+    issued_groups_ = GroupOf(n);
+  }
+
+ private:
   std::pair<int64_t, int64_t> GroupRange(int64_t g) const {
     if (span_epochs_) {
       int64_t first = g * group_;
@@ -1297,6 +1326,10 @@ void* PipelineIterator::stream() const { return impl_->stream(); }
 int64_t PipelineIterator::prefetch_depth() const { return impl_->depth(); }
 int64_t PipelineIterator::kernel_launches() const { return impl_->launches(); }
 int64_t PipelineIterator::batches_launched() const { return impl_->batches_launched(); }
+void PipelineIterator::Seek(int64_t batches) {
+  std::lock_guard lock(mu_);
+  impl_->Seek(batches);
+}
 std::pair<int64_t, int64_t> PipelineIterator::BatchStageTiming() const {
   std::lock_guard lock(mu_);
   return impl_->BatchStageTiming();

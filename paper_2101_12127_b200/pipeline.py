@@ -84,6 +84,8 @@ _SIGS = {
     "dp_batch_release": [ctypes.POINTER(dp_batch)],
     "dp_batch_wait": [ctypes.POINTER(dp_batch)],
     "dp_iterator_skip": [c_vp, c_i64, ctypes.POINTER(c_i64)],
+    "dp_iterator_save": [c_vp, c_vp, c_size, ctypes.POINTER(c_size)],
+    "dp_iterator_restore": [c_vp, c_vp, ctypes.c_char_p, c_size, ctypes.POINTER(dp_iterator_options), PP],
     "dp_tensor_copy_to_host": [ctypes.POINTER(dp_batch), c_int, c_vp, c_size],
     "dp_iterator_stream": [c_vp], "dp_iterator_kernel_launches": [c_vp], "dp_iterator_prefetch_depth": [c_vp],
     "dp_iterator_batch_stage_timing": [c_vp, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64)],
@@ -386,6 +388,14 @@ class Iterator:
         _check(st)
         return Batch(b, self)
 
+    def save(self) -> bytes:
+        """Checkpoint blob (DPC1 layout)."""
+        n = c_size()
+        L().dp_iterator_save(self.h, None, 0, ctypes.byref(n))
+        buf = ctypes.create_string_buffer(n.value)
+        _check(L().dp_iterator_save(self.h, buf, n.value, ctypes.byref(n)))
+        return buf.raw[:n.value]
+
     def skip(self, n):
         """GetNext n times in C++ dropping the batches; returns how many were delivered."""
         k = c_i64()
@@ -433,6 +443,18 @@ class Iterator:
         buf = ctypes.create_string_buffer(4096)
         _check(L().dp_iterator_describe(self.h, buf, len(buf)))
         return buf.value.decode()
+
+
+def restore(ds: Dataset, blob: bytes, device=0, consumer_stream=None, host_output=False):
+    """Restore(graph, registry, blob) (checkpoint.hpp:44-49): seeks, never replays."""
+    o = dp_iterator_options()
+    L().dp_iterator_options_default(ctypes.byref(o))
+    o.device = device
+    o.consumer_stream = consumer_stream
+    o.host_output = int(host_output)
+    out = c_vp()
+    _check(L().dp_iterator_restore(ds.h, ds.reg.h, blob, len(blob), ctypes.byref(o), ctypes.byref(out)))
+    return Iterator(out, ds)
 
 
 def make_iterator(ds: Dataset, seed_override=None, device=0, consumer_stream=None, host_output=False,

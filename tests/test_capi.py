@@ -137,6 +137,28 @@ def test_no_cpu_fallback_without_gpu():
     assert e.value.code == dp.ERR["Cuda"] and "no CPU fallback" in str(e.value)
 
 
+def test_checkpoint_restore_validation_before_device():
+    """Restore checks magic / version / length / fingerprint first
+    (P/tests/test_checkpoint.cpp:104-139: corrupt, truncated, versioned)."""
+    import struct
+    reg = reg_cfg1()
+    g = dp.Dataset.range(reg, 100).map("affine(3,1)").batch(10)
+
+    def blob(magic=b"DPC1", version=1, fp=b"\0" * 32, entries=b"", extra=b""):
+        return magic + struct.pack("<H", version) + fp + struct.pack("<QBQI", 1, 1, 3, 0) + entries + extra
+
+    for bad, code in ((b"", "CorruptBlob"), (b"XXXX\x01\x00", "CorruptBlob"), (blob(version=2), "VersionMismatch"),
+                      (blob()[:20], "CorruptBlob"), (blob(extra=b"\0"), "CorruptBlob"),
+                      (blob(), "FingerprintMismatch")):
+        with pytest.raises(DpError) as e:
+            dp.restore(g, bad)
+        assert code in str(e.value), (bad, str(e.value))
+    codes = {"CorruptBlob": 12, "VersionMismatch": 11, "FingerprintMismatch": 10}
+    with pytest.raises(DpError) as e:
+        dp.restore(g, blob(version=7))
+    assert e.value.code == codes["VersionMismatch"]
+
+
 def test_kernel_entry_rejects_bad_args_without_launching():
     lib = _capi.lib()
     assert lib.dp_k_range_affine_batch(0, -1, 1, 0, None, None) == dp.ERR["InvalidAttr"]

@@ -314,6 +314,50 @@ def test_sharded_residency_equals_shard_of_full_dataset(dp, orc):
     assert "apply shard(4, 1)" in str(e.value)
 
 
+def _ids_all(dp, it, comp=0):
+    out = []
+    while (b := it.get_next()) is not None:
+        out.append(b.numpy(comp).reshape(-1))
+        b.release()
+    return np.concatenate(out) if out else np.zeros(0, np.int64)
+
+
+def test_checkpoint_restore_equals_uninterrupted(dp):
+    """Save at random cut points, Restore (O(1) seek, no replay) and continue:
+    the concatenation equals the uninterrupted sequence
+    (acceptance criterion #8, P/tests/acceptance/acceptance_main.cpp:361-398)."""
+    rng = np.random.default_rng(8)
+    reg = image_registry(dp, 0, crop=(32, 32))
+    reg.register_affine("aff", 5, -2)
+    reg.register_length_filter("short", 100)
+    imgs = dp.Source.synthetic_images(700, 48, 48)
+    toks = dp.Source.synthetic_tokens(900, 300, 3, 3)
+    graphs = [  # spanning epochs, per-epoch repeat with a ragged last batch, big groups, padded batches
+        dp.Dataset.tensor_slices(reg, imgs).shuffle(150, 9).repeat(3).map("crop").map("norm").batch(64),
+        dp.Dataset.tensor_slices(reg, imgs).shuffle(150, 9).map("crop").map("norm").batch(64).repeat(3),
+        dp.Dataset.range(reg, 100_000).shuffle(5000, 1).map("aff").batch(1000).repeat(2),
+        dp.Dataset.token_sequences(reg, toks).filter("short").padded_batch(32).repeat(2),
+    ]
+    for g in graphs:
+        g, _ = g.optimize()
+        full = _ids_all(dp, dp.make_iterator(g, seed_override=4))
+        total = dp.make_iterator(g, seed_override=4).skip(10 ** 9)
+        for cut in sorted(set(rng.integers(0, total + 1, 5).tolist()) | {0, total}):
+            it = dp.make_iterator(g, seed_override=4)
+            head = []
+            for _ in range(cut):
+                b = it.get_next()
+                head.append(b.numpy(0).reshape(-1))
+                b.release()
+            blob = it.save()
+            assert blob[:4] == b"DPC1"
+            rest = _ids_all(dp, dp.restore(g, blob))
+            got = np.concatenate(head + [rest]) if head else rest
+            assert np.array_equal(got, full), (str(g)[:60], cut, total)
+        with pytest.raises(Exception):
+            dp.restore(graphs[0] if g is not graphs[0] else graphs[1], blob)  # different pipeline
+
+
 def test_unsupported_graph_fails_loudly(dp):
     reg = dp.Registry()
     reg.register_affine("a", 1, 1)

@@ -1,0 +1,63 @@
+// A reference user's program, ported by changing the include and namespace:
+// builds the cfg1 graph with ops::*, optimizes it to map_and_batch, drains
+// it with GetNext and prints the SURVEY.md Appendix A known answers; then a
+// cfg2-shaped image pipeline, with a checkpoint Save/Restore in the middle.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <vector>
+
+#include "dpb200/datapipe.hpp"
+
+using namespace datapipe::b200;
+
+int main() {
+  UdfRegistry reg;
+  reg.RegisterAffine("affine(3,1)", 3, 1);
+  DatasetGraph g = ops::Batch(ops::Map(ops::Range(1000000, reg), "affine(3,1)", 1, reg), 1024, false, reg);
+  auto [opt, report] = Optimize(g, RuleSet::Default(), reg);
+  IteratorOptions o;
+  o.seed_override = 1;
+  auto it = MakeIterator(opt, reg, o);
+  uint64_t h = 0xcbf29ce484222325ULL;
+  int64_t sum = 0, batches = 0, last = 0;
+  std::vector<int64_t> host;
+  while (auto e = it->GetNext()) {
+    const Tensor& t = e->component(0).tensor();
+    host.resize(t.shape[0]);
+    cudaEventSynchronize(static_cast<cudaEvent_t>(t.ready));
+    cudaMemcpy(host.data(), t.data, t.nbytes(), cudaMemcpyDeviceToHost);
+    for (int64_t v : host) {
+      h = (h ^ static_cast<uint64_t>(v)) * 0x100000001b3ULL;
+      sum += v;
+    }
+    last = t.shape[0];
+    ++batches;
+  }
+  std::printf("cfg1 root=%s batches=%lld last=%lld sum=%lld fnv=%016llx\n", NodeKindName(opt.root()->kind()),
+              static_cast<long long>(batches), static_cast<long long>(last), static_cast<long long>(sum),
+              static_cast<unsigned long long>(h));
+
+  reg.RegisterRandomCropFlip("crop", 224, 224, 7, true);
+  reg.RegisterNormalize("norm", {123.675f, 116.28f, 103.53f}, {58.395f, 57.12f, 57.375f});
+  auto images = SynthImages(4096, 256, 256, 0x5EED);
+  DatasetGraph p = ops::TensorSlices(images, reg);
+  p = ops::Shuffle(p, 1000, 42, reg);
+  p = ops::Map(p, "crop", kAutotune, reg);
+  p = ops::Map(p, "norm", kAutotune, reg);
+  p = ops::Prefetch(ops::Batch(p, 256, false, reg), kAutotune, reg);
+  auto popt = Optimize(p, RuleSet::Default(), reg).first;
+  auto pit = MakeIterator(popt, reg, o);
+  for (int i = 0; i < 5; ++i) pit->GetNext();
+  std::string blob = pit->Save();
+  auto a = pit->GetNext();
+  auto restored = Restore(popt, reg, blob);
+  auto b = restored->GetNext();
+  std::vector<int64_t> ia(256), ib(256);
+  cudaDeviceSynchronize();
+  cudaMemcpy(ia.data(), a->component(0).tensor().data, 2048, cudaMemcpyDeviceToHost);
+  cudaMemcpy(ib.data(), b->component(0).tensor().data, 2048, cudaMemcpyDeviceToHost);
+  std::printf("cfg2 restore_matches=%d first_id=%lld plan:\n%s", ia == ib ? 1 : 0, static_cast<long long>(ia[0]),
+              pit->LoweringPlan().c_str());
+  return ia == ib ? 0 : 1;
+}

@@ -125,10 +125,17 @@ def shard_layout(world, rank, n_per_rank):
             "resident": (global_count - rank + world - 1) // world}
 
 
+def _coll_device(device):
+    """gloo collectives run on host tensors (CPU tests, or the one-GPU
+    multi-process rehearsal of the multi-rank path); nccl on the GPU."""
+    import torch.distributed as distr
+    return "cpu" if distr.is_initialized() and distr.get_backend() == "gloo" else device
+
+
 def max_over_ranks(ms, world, device):
     import torch
     import torch.distributed as distr
-    t = torch.tensor([ms], device=device, dtype=torch.float64)
+    t = torch.tensor([ms], device=_coll_device(device), dtype=torch.float64)
     if world > 1:
         distr.all_reduce(t, op=distr.ReduceOp.MAX)
         distr.barrier()
@@ -139,6 +146,7 @@ def gather_digests(digest, world):
     """The final ordering check: every rank's 8-byte order digest."""
     import torch
     import torch.distributed as distr
+    digest = digest.to(_coll_device(digest.device))
     digests = [digest]
     if world > 1:
         digests = [torch.zeros_like(digest) for _ in range(world)]
@@ -258,9 +266,18 @@ def run_ours(args, cfg):
     from paper_2101_12127_b200 import pipeline as dp
 
     rank, world, local = dist_env()
+    # DP_BENCH_ONE_GPU=1 rehearses the multi-rank path on a single GPU: every
+    # rank uses cuda:0 and the (tiny) collectives go over gloo.  The ranks'
+    # kernels never wait on one another (no data-path collective).
+    rehearsal = os.environ.get("DP_BENCH_ONE_GPU") == "1"
+    if rehearsal:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        distr.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if rehearsal:
+            distr.init_process_group("gloo")
+        else:
+            distr.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
 
     # ---- device-resident workload (not timed) ----
@@ -427,10 +444,13 @@ def main():
     ap.add_argument("--warmup", type=int, default=32)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CFG), default="cfg2")
+    ap.add_argument("--elements-per-gpu", type=int, default=0, help="override the per-GPU dataset size (tests)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
-    cfg = CFG[args.config]
+    cfg = dict(CFG[args.config])
+    if args.elements_per_gpu:
+        cfg["n"] = args.elements_per_gpu
     if args.impl == "reference":
         run_reference(args, cfg)
     else:

@@ -1,0 +1,37 @@
+"""The multi-rank bench path on the one GPU of the test box: two torchrun
+ranks (gloo for the 8-byte collectives, DP_BENCH_ONE_GPU=1) each run the
+cfg2 pipeline on its own shard(2, rank) with sharded residency.  The final
+ordering check's per-rank K7 digests must equal the oracle's digest of
+shard(2, rank) -> shuffle(10k, 42) for that rank.  The
+ranks' kernels never wait on one another (no data-path collective)."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_two_rank_bench_order_check_matches_oracle(orc):
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    n = 8192
+    env = dict(os.environ, DP_BENCH_ONE_GPU="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", "29533", os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "32",
+           "--warmup", "16", "--elements-per-gpu", str(n)]
+    out = subprocess.run(cmd, capture_output=True, text=True, env=env, cwd=ROOT, timeout=900)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
+    line = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["batches_in_window"] == 32
+    digests = line["order_check"]["per_rank"]
+    for r in range(2):
+        pos = orc.shard_positions(2 * n, 2, r)
+        # the bench graph repeats above the batch: epoch 0's shuffle is salted
+        # MixSeeds(base, 0) (RepeatIterator::MakeChild, runtime.cpp:1175-1177)
+        ids = pos[orc.shuffle_order(pos.size, 10000, orc.shuffle_seed(orc.mix_seeds(1, 0), 42))]
+        assert digests[r] == f"{orc.order_digest(ids[:8 * 256]):016x}", r

@@ -46,8 +46,9 @@ CFG = {
                           "normalize fp32) -> Batch(256) -> Prefetch(AUTOTUNE)",
                  in_hw=(320, 320), out_hw=(224, 224), mode=1, batch=256, n=65536,
                  bytes_per_elem=320 * 320 * 3 + IMG_BYTES_WRITE, kernel="K4 resize_normalize_batch"),
-    "cfg1": dict(workload="Range(2^24) int64 -> Map(x*3+1) -> Batch(1024) (cfg1 shape at roofline size)",
-                 kind="range", batch=1024, n=1 << 24, bytes_per_elem=8, kernel="K1 range_affine_batch",
+    "cfg1": dict(workload="Range(2^28) int64 -> Map(x*3+1) -> Batch(1024) (cfg1 shape at the roofline size "
+                          "SURVEY.md 8(d) names; Range(1M) is the parity case)",
+                 kind="range", batch=1024, n=1 << 28, bytes_per_elem=8, kernel="K1 range_affine_batch",
                  unit="elements/s", dtype="int64"),
     "cfg4": dict(workload="1M int32 token sequences, len U[1,1024] -> Filter(len<=512) -> PaddedBatch(128, pad 0)",
                  kind="tokens", batch=128, n=1_000_000, max_keep=512, kernel="K5 padded_batches",

@@ -465,7 +465,8 @@ Lowered Lower(const DatasetGraph& g, const UdfRegistry& reg) {
     }
     if (L.source->c != 3) Unsupported("images must have 3 channels");
   }
-  if (seen_interleave && !L.records) Unsupported("interleave needs a record source");
+  // (interleave without a record source emits the int64 record indices
+  // themselves: the batch stage gathers them like a range)
   return L;
 }
 

@@ -183,7 +183,16 @@ padded_batches_kernel(const int32_t* __restrict__ tokens, const int64_t* __restr
   const int32_t len = lengths[p];
   const int32_t* src = tokens + offsets[p];
   int32_t* dst = out + (boff[j] - boff[j0]) + (R - j * batch) * static_cast<int64_t>(lm);
-  for (int c = lane; c < lm; c += 32) __stcs(dst + c, c < len ? __ldcs(src + c) : pad);
+  // 4 independent loads in flight per lane before the stores
+  int c = lane;
+  for (; c + 96 < lm; c += 128) {
+    int32_t v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = c + 32 * u < len ? __ldcs(src + c + 32 * u) : pad;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) __stcs(dst + c + 32 * u, v[u]);
+  }
+  for (; c < lm; c += 32) __stcs(dst + c, c < len ? __ldcs(src + c) : pad);
   if (lane == 0) out_lengths[r] = len;
 }
 

@@ -358,6 +358,32 @@ def test_checkpoint_restore_equals_uninterrupted(dp):
             dp.restore(graphs[0] if g is not graphs[0] else graphs[1], blob)  # different pipeline
 
 
+def test_edge_cases(dp, orc):
+    reg = dp.Registry()
+    reg.register_affine("inc", 1, 1)
+    reg.register_length_filter("none", 0)
+    reg.register_record_reader("zero", 0)
+
+    def vals(g, **kw):
+        return [b[0].tolist() for b in drain(dp.make_iterator(g, seed_override=1, **kw))]
+
+    assert vals(dp.Dataset.range(reg, 0).map("inc").batch(4)) == []                       # empty source
+    assert vals(dp.Dataset.range(reg, 5).map("inc").batch(10)) == [[1, 2, 3, 4, 5]]       # batch > dataset
+    assert vals(dp.Dataset.range(reg, 5).map("inc").batch(10, drop_remainder=True)) == []
+    assert vals(dp.Dataset.range(reg, 1).shuffle(100, 3).batch(4)) == [[0]]               # n = 1
+    got = vals(dp.Dataset.range(reg, 50).shuffle(1000, 3).batch(64))[0]                     # buffer > n
+    assert got == orc.shuffle_order(50, 1000, orc.shuffle_seed(1, 3)).tolist()
+    assert vals(dp.Dataset.range(reg, 3).shard(8, 5).batch(2)) == []                        # shard past the end
+    assert vals(dp.Dataset.range(reg, 3).shard(8, 2).batch(2)) == [[2]]
+    assert vals(dp.Dataset.range(reg, 7).map("inc").batch(3).repeat(2)) == [[1, 2, 3], [4, 5, 6], [7]] * 2
+    src = dp.Source.synthetic_tokens(100, 50, 1, 1)
+    assert vals(dp.Dataset.token_sequences(reg, src).filter("none").padded_batch(8)) == []  # filter keeps none
+    assert vals(dp.Dataset.range(reg, 4).interleave("zero", 2, 1).batch(2)) == []          # empty readers
+    # infinite repeat keeps producing; sticky end never reached
+    it = dp.make_iterator(dp.Dataset.range(reg, 3).batch(2).repeat(-1), seed_override=1)
+    assert [it.get_next().numpy(0).tolist() for _ in range(5)] == [[0, 1], [2], [0, 1], [2], [0, 1]]
+
+
 def test_unsupported_graph_fails_loudly(dp):
     reg = dp.Registry()
     reg.register_affine("a", 1, 1)

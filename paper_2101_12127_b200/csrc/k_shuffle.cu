@@ -271,15 +271,17 @@ __global__ void __launch_bounds__(kPT) p2_scatter(const uint32_t* __restrict__ r
   }
 }
 
-__global__ void __launch_bounds__(kPT) scan_small_u32(const uint32_t* __restrict__ counts, uint32_t cap,
+constexpr int kScanT = 1024;
+
+__global__ void __launch_bounds__(kScanT) scan_small_u32(const uint32_t* __restrict__ counts, uint32_t cap,
                                                       uint32_t* __restrict__ start) {
-  // single CTA: start[s] = sum_{s' < s} counts[s'] (cap <= 2^31, totals < 2^32)
-  __shared__ uint32_t ws[kPT / 32];
+  // single 1024-thread CTA: start[s] = sum_{s' < s} counts[s'] (cap <= 2^31, totals < 2^32)
+  __shared__ uint32_t ws[kScanT / 32];
   __shared__ uint32_t carry;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
-  for (uint32_t base = 0; base < cap; base += kPT) {
+  for (uint32_t base = 0; base < cap; base += kScanT) {
     const uint32_t i = base + threadIdx.x;
     const uint32_t x0 = i < cap ? counts[i] : 0;
     uint32_t x = x0;
@@ -290,19 +292,19 @@ __global__ void __launch_bounds__(kPT) scan_small_u32(const uint32_t* __restrict
     if (lane == 31) ws[warp] = x;
     __syncthreads();
     if (warp == 0) {
-      const uint32_t w = lane < kPT / 32 ? ws[lane] : 0;
+      const uint32_t w = lane < kScanT / 32 ? ws[lane] : 0;
       uint32_t z = w;
       for (int o = 1; o < 32; o <<= 1) {
         const uint32_t y = __shfl_up_sync(kFull, z, o);
         if (lane >= o) z += y;
       }
-      if (lane < kPT / 32) ws[lane] = z - w;
+      if (lane < kScanT / 32) ws[lane] = z - w;
     }
     __syncthreads();
     const uint32_t ex = x - x0 + ws[warp] + carry;
     if (i < cap) start[i] = ex;
     __syncthreads();
-    if (threadIdx.x == kPT - 1) carry = ex + x0;
+    if (threadIdx.x == kScanT - 1) carry = ex + x0;
     __syncthreads();
   }
   if (threadIdx.x == 0) start[cap] = carry;
@@ -385,8 +387,12 @@ __device__ void block_scan_u32(uint32_t* v, uint32_t n, uint32_t* ws, uint32_t* 
 // cursor[cap] (then terminal ancestors) | bucket[cap] | par[cap].
 __global__ void __launch_bounds__(1024) p5_drain(uint64_t s0, const uint32_t* __restrict__ raws, uint64_t R,
                                                  const uint64_t* __restrict__ meta, uint64_t F, uint32_t cap,
-                                                 const uint32_t* __restrict__ B, uint32_t* __restrict__ dstate,
+                                                 const uint32_t* __restrict__ B, uint32_t* __restrict__ gstate,
                                                  const int64_t* __restrict__ in_map, int64_t* __restrict__ out) {
+  // work arrays in shared memory when they fit (every phase is a chain of
+  // dependent lookups: smem latency instead of L2 latency), else global
+  extern __shared__ uint32_t sstate[];
+  uint32_t* dstate = gstate ? gstate : sstate;
   uint32_t* ids = dstate;
   uint32_t* start = ids + cap;
   uint32_t* cursor = start + cap + 1;
@@ -550,14 +556,29 @@ extern "C" int dp_k_shuffle_plan(uint64_t n, uint64_t buffer_size, uint64_t engi
       scan_u64<<<1, 1024, 0, st>>>(tiles, l.tiles, meta + 1);
       p2_scatter<<<static_cast<unsigned>(l.tiles), kPT, 0, st>>>(raws, l.R, thr, cap, l.F, tiles, slot_of, counts,
                                                                    meta);
-      scan_small_u32<<<1, kPT, 0, st>>>(counts, cap, start);
+      scan_small_u32<<<1, kScanT, 0, st>>>(counts, cap, start);
       const int kgrid = static_cast<int>(std::min<uint64_t>((l.F + kPT - 1) / kPT, 148 * 16));
       p3_bucket<<<kgrid, kPT, 0, st>>>(slot_of, l.F, start, cursor, bucket);
       p4_resolve<<<kgrid, kPT, 0, st>>>(slot_of, l.F, cap, start, bucket, B, in_map, out);
     } else {
       // no fill: the drain starts at raw 0 (raws computed on demand)
     }
-    p5_drain<<<1, 1024, 0, st>>>(s0, raws, l.F > 0 ? l.R : 0, meta, l.F, cap, B, dstate, in_map, out);
+    const size_t dbytes = (5 * static_cast<size_t>(cap) + 1) * sizeof(uint32_t);
+    constexpr size_t kDrainSmem = 200 * 1024;
+    if (dbytes <= kDrainSmem) {
+      static int attr_dev = -1;
+      int dev = 0;
+      cudaGetDevice(&dev);
+      if (attr_dev != dev) {
+        cudaError_t e = cudaFuncSetAttribute(p5_drain, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(kDrainSmem));
+        if (e != cudaSuccess) return cuda_status(e, "shuffle_plan: smem attribute");
+        attr_dev = dev;
+      }
+      p5_drain<<<1, 1024, dbytes, st>>>(s0, raws, l.F > 0 ? l.R : 0, meta, l.F, cap, B, nullptr, in_map, out);
+    } else {
+      p5_drain<<<1, 1024, 0, st>>>(s0, raws, l.F > 0 ? l.R : 0, meta, l.F, cap, B, dstate, in_map, out);
+    }
     return launch_status("shuffle_plan");
   }
   const size_t bytes = static_cast<size_t>(cap) * sizeof(uint32_t);

@@ -36,6 +36,7 @@ constexpr int64_t kInfiniteRepeat = -1;  // graph.hpp:36
 enum class NodeKind : uint8_t {
   // reference kinds on the path (numbering of graph.hpp:38-56)
   kFromMemory = 0,
+  kFromFile = 1,
   kInterleave = 5,
   kBatch = 6,
   kPrefetch = 8,
@@ -56,7 +57,10 @@ const char* NodeKindName(NodeKind kind);
 
 // ---- source data (device resident, or pinned host for end-to-end runs) ----
 struct SourceData {
-  enum class Kind { kInt64, kImages, kTokens } kind;
+  // kRecords: length-prefixed record files (from_file); payloads packed
+  // back to back in `values` (record_len bytes each when uniform, else 0)
+  enum class Kind { kInt64, kImages, kTokens, kRecords } kind;
+  int64_t record_len = 0;
   int64_t count = 0;
   // kInt64: values[count] (device);  kImages: u8 [count, h, w, c]
   // kTokens: lengths i32[count], offsets i64[count+1], tokens i32[total]
@@ -87,6 +91,11 @@ SourcePtr ImagesFromHost(const uint8_t* data, int64_t count, int64_t h, int64_t 
 SourcePtr ImagesFromPinnedHost(const uint8_t* data, int64_t count, int64_t h, int64_t w, int device = 0);
 SourcePtr Int64FromHost(const int64_t* values, int64_t count, int device = 0);
 SourcePtr TokensFromHost(const int32_t* lengths, int64_t count, const int32_t* tokens, int device = 0);
+// Length-prefixed record files (formats.md:67-74) read in order; payloads
+// packed into device memory.
+SourcePtr RecordsFromFiles(const std::vector<std::string>& paths, int device = 0);
+// WriteRecordFile (runtime.hpp:102-107): [u32 LE length][payload] per record.
+void WriteRecordFile(const std::string& path, const std::vector<std::string>& payloads);
 
 // ---- graph IR ----
 using AttrValue = std::variant<int64_t, uint64_t, double, bool, std::string, std::vector<std::string>, SourcePtr>;
@@ -133,7 +142,9 @@ class DatasetGraph {
 // kernel at lowering time (K1 affine, K3 crop+flip+normalize, K4 resize +
 // normalize).
 struct MapStep {
-  enum class Op { kAffine, kRandomCropFlip, kResizeBilinear, kNormalize } op;
+  // kDecodeRaw: a from_file record (bytes) holding a raw uint8 HWC image of
+  // out_h x out_w x 3 -> (int64 record ordinal, tensor u8[out_h, out_w, 3])
+  enum class Op { kAffine, kRandomCropFlip, kResizeBilinear, kNormalize, kDecodeRaw } op;
   int64_t a = 1, b = 0;                 // affine
   int64_t out_h = 0, out_w = 0;         // crop / resize
   uint64_t seed = 0;                    // crop: Philox key
@@ -169,6 +180,7 @@ class UdfRegistry {
   void RegisterRandomCropFlip(const std::string& name, int64_t crop_h, int64_t crop_w, uint64_t seed, bool flip);
   void RegisterResizeBilinear(const std::string& name, int64_t out_h, int64_t out_w);
   void RegisterNormalize(const std::string& name, std::array<float, 3> mean, std::array<float, 3> stdv);
+  void RegisterDecodeRaw(const std::string& name, int64_t h, int64_t w);
   void RegisterLengthFilter(const std::string& name, int64_t max_len);
   void RegisterRecordReader(const std::string& name, int64_t records);
   bool Contains(const std::string& name) const;
@@ -189,6 +201,11 @@ DatasetGraph Range(int64_t n, const UdfRegistry& reg);
 DatasetGraph FromMemory(const std::vector<int64_t>& values, const UdfRegistry& reg, int device = 0);
 DatasetGraph TensorSlices(SourcePtr images, const UdfRegistry& reg);
 DatasetGraph TokenSequences(SourcePtr tokens, const UdfRegistry& reg);
+// ops::FromFile (graph.hpp:137; record format formats.md:67-74): the files'
+// length-prefixed records, in file order, become (bytes) elements.  Read and
+// validated here (kMissingFile, kMalformedInput); payloads are packed into
+// device memory once.
+DatasetGraph FromFile(const std::vector<std::string>& paths, const UdfRegistry& reg, int device = 0);
 DatasetGraph Map(const DatasetGraph& in, const std::string& udf, int64_t num_parallel_calls, const UdfRegistry& reg);
 DatasetGraph Filter(const DatasetGraph& in, const std::string& udf, const UdfRegistry& reg);
 DatasetGraph Interleave(const DatasetGraph& in, const std::string& udf, int64_t cycle_length,

@@ -45,6 +45,9 @@ int dp_registry_register_normalize(dp_registry* reg, const char* name, const flo
 int dp_registry_register_length_filter(dp_registry* reg, const char* name, int64_t max_len);
 /* interleave dataset UDF: element x opens records x*records .. x*records+records-1 */
 int dp_registry_register_record_reader(dp_registry* reg, const char* name, int64_t records);
+/* decode a from_file record holding a raw u8 HWC image of h x w x 3 ->
+ * (int64 ordinal, u8[h,w,3]); must be the first map after from_file */
+int dp_registry_register_decode_raw(dp_registry* reg, const char* name, int64_t h, int64_t w);
 int dp_registry_contains(const dp_registry* reg, const char* name);
 
 /* ---- sources (new kinds) ---- */
@@ -69,6 +72,15 @@ int dp_graph_range(const dp_registry* reg, int64_t n, dp_graph** out);          
 int dp_graph_from_memory_i64(const dp_registry* reg, const int64_t* values, int64_t n, int device,
                              dp_graph** out);                                           /* ops::FromMemory */
 int dp_graph_tensor_slices(const dp_registry* reg, const dp_source* images, dp_graph** out);
+/* ops::FromFile (graph.hpp:137): length-prefixed record files (formats.md:67-74)
+ * read in order into device memory.  kMissingFile / kMalformedInput as the
+ * reference's FromFileIterator (runtime.cpp:416-474), raised here, before any
+ * iteration. */
+int dp_graph_from_file(const dp_registry* reg, const char* const* paths, int64_t num_paths, int device,
+                       dp_graph** out);
+/* WriteRecordFile (runtime.hpp:102-107): [u32 LE length][payload] per record;
+ * payload i = data[offsets[i] .. offsets[i+1]) */
+int dp_write_record_file(const char* path, const uint8_t* data, const int64_t* offsets, int64_t count);
 int dp_graph_token_sequences(const dp_registry* reg, const dp_source* tokens, dp_graph** out);
 int dp_graph_map(const dp_graph* in, const char* udf, int64_t num_parallel_calls, const dp_registry* reg,
                  dp_graph** out);                                                       /* ops::Map */

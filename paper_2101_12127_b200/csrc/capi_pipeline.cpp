@@ -94,6 +94,10 @@ int dp_registry_register_record_reader(dp_registry* reg, const char* name, int64
   DP_REQUIRE(reg && name);
   return Guard([&] { reg->reg.RegisterRecordReader(name, records); });
 }
+int dp_registry_register_decode_raw(dp_registry* reg, const char* name, int64_t h, int64_t w) {
+  DP_REQUIRE(reg && name);
+  return Guard([&] { reg->reg.RegisterDecodeRaw(name, h, w); });
+}
 int dp_registry_contains(const dp_registry* reg, const char* name) {
   return reg && name && reg->reg.Contains(name) ? 1 : 0;
 }
@@ -142,6 +146,30 @@ int dp_graph_from_memory_i64(const dp_registry* reg, const int64_t* values, int6
 int dp_graph_tensor_slices(const dp_registry* reg, const dp_source* images, dp_graph** out) {
   DP_REQUIRE(reg && images && out);
   return Guard([&] { Emit(out, ops::TensorSlices(images->s, reg->reg)); });
+}
+int dp_graph_from_file(const dp_registry* reg, const char* const* paths, int64_t num_paths, int device,
+                       dp_graph** out) {
+  DP_REQUIRE(reg && out && (paths || num_paths == 0) && num_paths >= 0);
+  return Guard([&] {
+    std::vector<std::string> p;
+    for (int64_t i = 0; i < num_paths; ++i) {
+      if (!paths[i]) throw PipelineError(ErrorCode::kInvalidAttr, "from_file: null path");
+      p.emplace_back(paths[i]);
+    }
+    Emit(out, ops::FromFile(p, reg->reg, device));
+  });
+}
+int dp_write_record_file(const char* path, const uint8_t* data, const int64_t* offsets, int64_t count) {
+  DP_REQUIRE(path && offsets && count >= 0 && (data || count == 0));
+  return Guard([&] {
+    std::vector<std::string> payloads;
+    payloads.reserve(count);
+    for (int64_t i = 0; i < count; ++i) {
+      if (offsets[i + 1] < offsets[i]) throw PipelineError(ErrorCode::kInvalidAttr, "write_record_file: offsets");
+      payloads.emplace_back(reinterpret_cast<const char*>(data) + offsets[i], offsets[i + 1] - offsets[i]);
+    }
+    WriteRecordFile(path, payloads);
+  });
 }
 int dp_graph_token_sequences(const dp_registry* reg, const dp_source* tokens, dp_graph** out) {
   DP_REQUIRE(reg && tokens && out);

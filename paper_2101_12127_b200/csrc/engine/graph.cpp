@@ -16,6 +16,7 @@ namespace datapipe::b200 {
 const char* NodeKindName(NodeKind kind) {
   switch (kind) {
     case NodeKind::kFromMemory: return "from_memory";
+    case NodeKind::kFromFile: return "from_file";
     case NodeKind::kMap: return "map";
     case NodeKind::kFilter: return "filter";
     case NodeKind::kInterleave: return "interleave";
@@ -155,6 +156,16 @@ void UdfRegistry::RegisterNormalize(const std::string& name, std::array<float, 3
   Register(name, std::move(e));
 }
 
+void UdfRegistry::RegisterDecodeRaw(const std::string& name, int64_t h, int64_t w) {
+  if (h < 1 || w < 1) throw PipelineError(ErrorCode::kInvalidAttr, "decode_raw: shape must be >= 1");
+  Entry e;
+  MapStep s{MapStep::Op::kDecodeRaw};
+  s.out_h = h;
+  s.out_w = w;
+  e.map.push_back(s);
+  Register(name, std::move(e));
+}
+
 void UdfRegistry::RegisterLengthFilter(const std::string& name, int64_t max_len) {
   Entry e;
   e.predicate = LengthPredicate{max_len};
@@ -207,6 +218,11 @@ ElementSpec ApplyMapSteps(const std::vector<MapStep>& steps, const ElementSpec& 
         cur = ElementSpec({TypeSpec::Int64(), TypeSpec::OfTensor(DType::kFloat32, {s.out_h, s.out_w, 3})});
         break;
       }
+      case MapStep::Op::kDecodeRaw:
+        if (cur.arity() != 1 || cur.components()[0].kind() != Value::Kind::kBytes)
+          throw TypeMismatchError("decode_raw expects (bytes) records", cur);
+        cur = ElementSpec({TypeSpec::Int64(), TypeSpec::OfTensor(DType::kUInt8, {s.out_h, s.out_w, 3})});
+        break;
       case MapStep::Op::kNormalize: {
         const TypeSpec& t = image_spec("normalize expects (int64 id, tensor[h,w,3])");
         cur = ElementSpec({TypeSpec::Int64(), TypeSpec::OfTensor(DType::kFloat32, t.shape())});
@@ -275,6 +291,7 @@ ElementSpec SourceSpec(const SourceData& s) {
     case SourceData::Kind::kImages:
       return ElementSpec({TypeSpec::Int64(), TypeSpec::OfTensor(DType::kUInt8, {s.h, s.w, s.c})});
     case SourceData::Kind::kTokens: return ElementSpec({TypeSpec::OfTensor(DType::kInt32, {-1})});
+    case SourceData::Kind::kRecords: return ElementSpec({TypeSpec::Bytes()});
   }
   return ElementSpec();
 }
@@ -286,9 +303,18 @@ void ValidateAttrs(NodeKind kind, const Attrs& a) {
       if (RequireInt(kind, a, "count") < 0) BadAttr(kind, "count must be >= 0");
       break;
     case NodeKind::kFromMemory:
+    case NodeKind::kFromFile:
     case NodeKind::kTensorSlices:
     case NodeKind::kTokenSequences: {
-      CheckKeys(kind, a, {"source"}, {});
+      if (kind == NodeKind::kFromFile) {
+        CheckKeys(kind, a, {"source", "paths"}, {});
+        auto p = a.find("paths");
+        if (!std::holds_alternative<std::vector<std::string>>(p->second) ||
+            std::get<std::vector<std::string>>(p->second).empty())
+          BadAttr(kind, "'paths' must be a non-empty list of strings");
+      } else {
+        CheckKeys(kind, a, {"source"}, {});
+      }
       auto it = a.find("source");
       if (!std::holds_alternative<SourcePtr>(it->second) || !std::get<SourcePtr>(it->second))
         BadAttr(kind, "'source' must be a source");
@@ -361,6 +387,7 @@ int Arity(NodeKind kind) {
   switch (kind) {
     case NodeKind::kRange:
     case NodeKind::kFromMemory:
+    case NodeKind::kFromFile:
     case NodeKind::kTensorSlices:
     case NodeKind::kTokenSequences:
       return 0;
@@ -378,6 +405,7 @@ ElementSpec DeriveSpec(NodeKind kind, const std::vector<NodePtr>& in, const Attr
   switch (kind) {
     case NodeKind::kRange: return ElementSpec({TypeSpec::Int64()});
     case NodeKind::kFromMemory:
+    case NodeKind::kFromFile:
     case NodeKind::kTensorSlices:
     case NodeKind::kTokenSequences: return SourceSpec(*std::get<SourcePtr>(a.at("source")));
     case NodeKind::kMap: return reg.MapOutputSpec(std::get<std::string>(a.at("udf")), in[0]->output_spec());
@@ -435,6 +463,9 @@ DatasetGraph Range(int64_t n, const UdfRegistry& reg) {
 DatasetGraph FromMemory(const std::vector<int64_t>& values, const UdfRegistry& reg, int device) {
   return DatasetGraph(Build(NodeKind::kFromMemory, {},
                             {{"source", Int64FromHost(values.data(), static_cast<int64_t>(values.size()), device)}}, reg));
+}
+DatasetGraph FromFile(const std::vector<std::string>& paths, const UdfRegistry& reg, int device) {
+  return DatasetGraph(Build(NodeKind::kFromFile, {}, {{"source", RecordsFromFiles(paths, device)}, {"paths", paths}}, reg));
 }
 DatasetGraph TensorSlices(SourcePtr images, const UdfRegistry& reg) {
   if (!images || images->kind != SourceData::Kind::kImages)

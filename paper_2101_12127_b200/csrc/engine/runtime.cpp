@@ -247,6 +247,75 @@ SourcePtr ImagesFromPinnedHost(const uint8_t* data, int64_t count, int64_t h, in
   return s;
 }
 
+// FromFileIterator::Next (/root/reference/proj/src/runtime.cpp:416-474):
+// records are [u32 little-endian length][payload], files read in order; a
+// truncated length or payload is MalformedInput, a missing file MissingFile.
+SourcePtr RecordsFromFiles(const std::vector<std::string>& paths, int device) {
+  if (paths.empty()) throw PipelineError(ErrorCode::kInvalidAttr, "from_file: 'paths' must be non-empty");
+  std::vector<std::string> blobs;
+  std::vector<int64_t> offsets{0};
+  int64_t uniform = -1;
+  for (const auto& path : paths) {
+    FILE* f = std::fopen(path.c_str(), "rb");
+    if (!f) throw PipelineError(ErrorCode::kMissingFile, "no such file: " + path);
+    std::string data;
+    char chunk[1 << 16];
+    size_t got;
+    while ((got = std::fread(chunk, 1, sizeof(chunk), f)) > 0) data.append(chunk, got);
+    std::fclose(f);
+    size_t pos = 0;
+    while (pos < data.size()) {
+      if (pos + 4 > data.size())
+        throw PipelineError(ErrorCode::kMalformedInput, "at byte " + std::to_string(pos) +
+                                                            ": truncated record length in " + path);
+      uint32_t len = 0;
+      for (int i = 0; i < 4; ++i) len |= static_cast<uint32_t>(static_cast<uint8_t>(data[pos + i])) << (8 * i);
+      pos += 4;
+      if (pos + len > data.size())
+        throw PipelineError(ErrorCode::kMalformedInput, "at byte " + std::to_string(pos) +
+                                                            ": truncated record payload in " + path);
+      blobs.emplace_back(data, pos, len);
+      offsets.push_back(offsets.back() + len);
+      uniform = (uniform < 0 || uniform == static_cast<int64_t>(len)) ? len : -2;
+      pos += len;
+    }
+  }
+  auto s = std::make_shared<SourceData>();
+  s->kind = SourceData::Kind::kRecords;
+  s->count = static_cast<int64_t>(blobs.size());
+  s->record_len = uniform >= 0 ? uniform : 0;
+  s->device = device;
+  const size_t total = static_cast<size_t>(offsets.back());
+  s->values = DeviceAlloc(std::max<size_t>(total, 16), device);
+  s->offsets = DeviceAlloc(sizeof(int64_t) * offsets.size(), device);
+  // pack the payloads back to back in pinned memory, one H2D copy
+  auto staging = PinnedAlloc(std::max<size_t>(total, 16));
+  size_t at = 0;
+  for (const auto& b : blobs) {
+    std::memcpy(static_cast<char*>(staging.get()) + at, b.data(), b.size());
+    at += b.size();
+  }
+  DeviceGuard g(device);
+  CudaCheck(cudaMemcpy(s->values.get(), staging.get(), total, cudaMemcpyHostToDevice), "upload records");
+  CudaCheck(cudaMemcpy(s->offsets.get(), offsets.data(), sizeof(int64_t) * offsets.size(), cudaMemcpyHostToDevice),
+            "upload offsets");
+  return s;
+}
+
+// runtime.cpp:2251-2266
+void WriteRecordFile(const std::string& path, const std::vector<std::string>& payloads) {
+  FILE* f = std::fopen(path.c_str(), "wb");
+  if (!f) throw PipelineError(ErrorCode::kMissingFile, "cannot write: " + path);
+  for (const auto& p : payloads) {
+    const uint32_t len = static_cast<uint32_t>(p.size());
+    unsigned char lb[4] = {static_cast<unsigned char>(len), static_cast<unsigned char>(len >> 8),
+                           static_cast<unsigned char>(len >> 16), static_cast<unsigned char>(len >> 24)};
+    std::fwrite(lb, 1, 4, f);
+    std::fwrite(p.data(), 1, p.size(), f);
+  }
+  std::fclose(f);
+}
+
 SourcePtr Int64FromHost(const int64_t* values, int64_t count, int device) {
   auto s = std::make_shared<SourceData>();
   s->kind = SourceData::Kind::kInt64;
@@ -366,6 +435,7 @@ Lowered Lower(const DatasetGraph& g, const UdfRegistry& reg) {
   }
   // ---- index chain ----
   std::vector<IndexOp> top_down;
+  std::vector<MapStep> below;  // maps under the index ops (e.g. from_file.map(decode).shuffle)
   bool seen_interleave = false;
   for (;;) {
     const NodeKind k = n->kind();
@@ -389,6 +459,14 @@ Lowered Lower(const DatasetGraph& g, const UdfRegistry& reg) {
       if (!e.reader) Unsupported("interleave UDF is not a record reader");
       top_down.push_back({IndexOp::Kind::kInterleave, n->GetInt("cycle_length"), e.reader->records, {}, path});
       if (n->HasAttr("records")) L.records = n->GetSource("records");
+    } else if (k == NodeKind::kMap) {
+      // a map is a pure per-element function whose randomness is keyed by the
+      // element id (Philox counter), which travels with the element: it
+      // commutes with shard / shuffle / repeat and is run in the batch stage
+      if (n->HasAttr("fused_filter_udf")) Unsupported("map with a fused predicate under batch");
+      if (seen_interleave) Unsupported("map under interleave");
+      const auto& f = reg.Get(n->GetString("udf")).map;
+      below.insert(below.begin(), f.begin(), f.end());
     } else if (k == NodeKind::kPrefetch) {
       // prefetch inside the index chain only buffers indices: a no-op here
     } else {
@@ -399,12 +477,14 @@ Lowered Lower(const DatasetGraph& g, const UdfRegistry& reg) {
   }
   L.node_paths.push_back(path);
   L.chain.assign(top_down.rbegin(), top_down.rend());
+  L.steps.insert(L.steps.begin(), below.begin(), below.end());
   // ---- source ----
   switch (n->kind()) {
     case NodeKind::kRange:
       L.source_count = n->GetInt("count");
       break;
     case NodeKind::kFromMemory:
+    case NodeKind::kFromFile:
     case NodeKind::kTensorSlices:
     case NodeKind::kTokenSequences:
       L.source = n->GetSource("source");
@@ -433,6 +513,24 @@ Lowered Lower(const DatasetGraph& g, const UdfRegistry& reg) {
     for (const auto& op : L.chain)
       if (op.kind == IndexOp::Kind::kInterleave) break;
       else if (op.kind != IndexOp::Kind::kShard) Unsupported("only shard may precede interleave");
+  }
+  // ---- from_file records: decode_raw views the packed payloads as images ----
+  if (L.source && L.source->kind == SourceData::Kind::kRecords) {
+    if (L.steps.empty() || L.steps[0].op != MapStep::Op::kDecodeRaw)
+      Unsupported("from_file records must be decoded (decode_raw) before batching");
+    const MapStep dec = L.steps[0];
+    if (L.source->record_len != dec.out_h * dec.out_w * 3)
+      throw PipelineError(ErrorCode::kMalformedInput,
+                          "from_file: records are not all " + std::to_string(dec.out_h * dec.out_w * 3) +
+                              " bytes (decode_raw " + std::to_string(dec.out_h) + "x" + std::to_string(dec.out_w) +
+                              "x3)");
+    auto view = std::make_shared<SourceData>(*L.source);
+    view->kind = SourceData::Kind::kImages;
+    view->h = dec.out_h;
+    view->w = dec.out_w;
+    view->c = 3;
+    L.source = view;
+    L.steps.erase(L.steps.begin());
   }
   // ---- batch kind from source + UDF chain ----
   const SourceData::Kind sk = L.source ? L.source->kind : SourceData::Kind::kInt64;

@@ -12,6 +12,7 @@ Every call goes through libdpcuda.so; there is no Python or CPU compute path.
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 
@@ -21,8 +22,10 @@ c_i64, c_u64, c_int, c_vp, c_size = ctypes.c_int64, ctypes.c_uint64, ctypes.c_in
 PP = ctypes.POINTER(c_vp)
 
 ERR = {  # dp_status values (include/dpcuda.h)
-    "InvalidArity": 1, "InvalidAttr": 2, "TypeMismatch": 3, "ValidationFailed": 5, "DuplicateName": 6,
-    "UnknownUdf": 7, "RewriteDiverged": 14, "Internal": 19, "Cuda": 100, "EndOfSequence": 102,
+    "InvalidArity": 1, "InvalidAttr": 2, "TypeMismatch": 3, "MalformedInput": 4, "ValidationFailed": 5,
+    "DuplicateName": 6, "UnknownUdf": 7, "MissingFile": 8, "FingerprintMismatch": 10, "VersionMismatch": 11,
+    "CorruptBlob": 12, "RewriteDiverged": 14, "Internal": 19, "Cuda": 100, "OutOfMemory": 101,
+    "EndOfSequence": 102,
 }
 DTYPES = {0: np.uint8, 1: np.int32, 2: np.int64, 3: np.float32}
 MEAN = (123.675, 116.28, 103.53)
@@ -53,6 +56,7 @@ _SIGS = {
                                        ctypes.POINTER(ctypes.c_float)],
     "dp_registry_register_length_filter": [c_vp, ctypes.c_char_p, c_i64],
     "dp_registry_register_record_reader": [c_vp, ctypes.c_char_p, c_i64],
+    "dp_registry_register_decode_raw": [c_vp, ctypes.c_char_p, c_i64, c_i64],
     "dp_registry_contains": [c_vp, ctypes.c_char_p],
     "dp_source_synthetic_images": [c_i64, c_i64, c_i64, c_u64, c_int, PP],
     "dp_source_images_from_host": [c_vp, c_i64, c_i64, c_i64, c_int, PP],
@@ -64,6 +68,8 @@ _SIGS = {
     "dp_graph_range": [c_vp, c_i64, PP],
     "dp_graph_from_memory_i64": [c_vp, c_vp, c_i64, c_int, PP],
     "dp_graph_tensor_slices": [c_vp, c_vp, PP],
+    "dp_graph_from_file": [c_vp, ctypes.POINTER(ctypes.c_char_p), c_i64, c_int, PP],
+    "dp_write_record_file": [ctypes.c_char_p, c_vp, c_vp, c_i64],
     "dp_graph_token_sequences": [c_vp, c_vp, PP],
     "dp_graph_map": [c_vp, ctypes.c_char_p, c_i64, c_vp, PP],
     "dp_graph_filter": [c_vp, ctypes.c_char_p, c_vp, PP],
@@ -169,6 +175,10 @@ class Registry:
         _check(L().dp_registry_register_record_reader(self.h, _b(name), records))
         return name
 
+    def register_decode_raw(self, name, h, w):
+        _check(L().dp_registry_register_decode_raw(self.h, _b(name), h, w))
+        return name
+
     def contains(self, name):
         return bool(L().dp_registry_contains(self.h, _b(name)))
 
@@ -267,6 +277,16 @@ class Dataset:
         out = c_vp()
         _check(L().dp_graph_tensor_slices(reg.h, src.h, ctypes.byref(out)))
         return Dataset(out, reg, (src,))
+
+    @staticmethod
+    def from_file(reg, paths, device=0):
+        """ops::FromFile (graph.hpp:137): length-prefixed record files read in order."""
+        if isinstance(paths, (str, bytes, os.PathLike)):
+            paths = [paths]
+        arr = (ctypes.c_char_p * max(1, len(paths)))(*[os.fsencode(p) for p in paths])
+        out = c_vp()
+        _check(L().dp_graph_from_file(reg.h, arr, len(paths), device, ctypes.byref(out)))
+        return Dataset(out, reg)
 
     @staticmethod
     def token_sequences(reg, src: Source):
@@ -474,3 +494,12 @@ def make_iterator(ds: Dataset, seed_override=None, device=0, consumer_stream=Non
     out = c_vp()
     _check(L().dp_iterator_create(ds.h, ds.reg.h, ctypes.byref(o), ctypes.byref(out)))
     return Iterator(out, ds)
+
+
+def write_record_file(path, payloads):
+    """WriteRecordFile (runtime.hpp:102-107): [u32 LE length][payload] per record."""
+    bufs = [bytes(p) for p in payloads]
+    offs = np.zeros(len(bufs) + 1, np.int64)
+    offs[1:] = np.cumsum([len(b) for b in bufs]) if bufs else []
+    data = np.frombuffer(b"".join(bufs) or b"\0", np.uint8)
+    _check(L().dp_write_record_file(os.fsencode(path), data.ctypes.data, offs.ctypes.data, len(bufs)))

@@ -166,3 +166,32 @@ def test_kernel_entry_rejects_bad_args_without_launching():
     assert lib.dp_k_shard_index(10, 0, 0, None, None, None) == dp.ERR["InvalidAttr"]
     assert b"num_shards" in lib.dp_last_error()
     assert lib.dp_k_shard_interleave_count(64, 8, 3, 16) == 8 * 16
+
+
+def test_write_record_file_format(tmp_path):
+    """WriteRecordFile (runtime.hpp:102-107, formats.md:67-74): [u32 LE len][payload]."""
+    p = tmp_path / "r.rec"
+    dp.write_record_file(str(p), [b"ab", b"", b"xyz"])
+    assert p.read_bytes() == b"\x02\x00\x00\x00ab" + b"\x00\x00\x00\x00" + b"\x03\x00\x00\x00xyz"
+
+
+def test_from_file_errors_raised_before_device(tmp_path):
+    """FromFileIterator (runtime.cpp:416-474): a missing file is MissingFile, a
+    truncated length or payload MalformedInput -- raised while reading, before
+    any device memory is touched (so they hold without a GPU)."""
+    reg = dp.Registry()
+    with pytest.raises(DpError) as e:
+        dp.Dataset.from_file(reg, [str(tmp_path / "absent.rec")])
+    assert e.value.code == dp.ERR["MissingFile"]
+    good = tmp_path / "good.rec"
+    dp.write_record_file(str(good), [b"hello"])
+    for name, blob in (("len.rec", b"\x05\x00"), ("payload.rec", b"\x05\x00\x00\x00hel")):
+        bad = tmp_path / name
+        bad.write_bytes(blob)
+        with pytest.raises(DpError) as e:
+            dp.Dataset.from_file(reg, [str(good), str(bad)])
+        assert e.value.code == dp.ERR["MalformedInput"]
+        assert "truncated record" in str(e.value)
+    with pytest.raises(DpError) as e:
+        dp.Dataset.from_file(reg, [])
+    assert e.value.code == dp.ERR["InvalidAttr"]

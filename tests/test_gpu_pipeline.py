@@ -227,6 +227,44 @@ def test_pinned_host_source_equals_device_source(dp, orc):
         assert (a[0] == b[0]).all() and np.array_equal(a[1], b[1])
 
 
+def test_from_file_records_equal_tensor_slices(dp, orc, tmp_path):
+    """from_file (graph.hpp:137, FromFileIterator runtime.cpp:416-474) over
+    record files holding raw HWC images, decoded on the device by decode_raw:
+    the record ordinal is the element id, so the pipeline equals tensor_slices
+    over the same images bit for bit."""
+    imgs = orc.images(5, 90, 72, 64)
+    paths = [str(tmp_path / "a.rec"), str(tmp_path / "b.rec")]
+    dp.write_record_file(paths[0], [im.tobytes() for im in imgs[:37]])
+    dp.write_record_file(paths[1], [im.tobytes() for im in imgs[37:]])
+    out = []
+    for mode in (0, 1):
+        reg = image_registry(dp, mode, crop=(48, 40))
+        reg.register_decode_raw("decode", 72, 64)
+        a = dp.Dataset.from_file(reg, paths).map("decode")
+        b = dp.Dataset.tensor_slices(reg, dp.Source.images_from_host(imgs))
+        res = []
+        for d in (a, b):
+            op = "crop" if mode == 0 else "resize"
+            g, _ = d.shuffle(30, 4).map(op).map("norm").batch(16).optimize()
+            res.append(drain(dp.make_iterator(g, seed_override=6), comps=(0, 1)))
+        assert len(res[0]) == len(res[1]) == 6
+        for x, y in zip(*res):
+            assert np.array_equal(x[0], y[0]) and np.array_equal(x[1], y[1])
+        # a map under the shuffle commutes with it (randomness keyed by element id)
+        g, _ = a.map(op).shuffle(30, 4).map("norm").batch(16).optimize()
+        for x, y in zip(drain(dp.make_iterator(g, seed_override=6), comps=(0, 1)), res[1]):
+            assert np.array_equal(x[0], y[0]) and np.array_equal(x[1], y[1])
+        out.append(res[0])
+    # wrong decode shape / missing decode are rejected at MakeIterator
+    reg = image_registry(dp, 0, crop=(48, 40))
+    reg.register_decode_raw("decode_bad", 70, 64)
+    with pytest.raises(dp.DpError) as e:
+        dp.make_iterator(dp.Dataset.from_file(reg, paths).map("decode_bad").map("crop").map("norm").batch(8))
+    assert e.value.code == dp.ERR["MalformedInput"]
+    with pytest.raises(dp.DpError):
+        dp.make_iterator(dp.Dataset.from_file(reg, paths).batch(8))
+
+
 # ------------------------------------------------------------------ cfg4 ----
 def test_cfg4_filter_padded_batch(dp, orc):
     c = GOLDEN["cfg4_filter_batch"]

@@ -127,6 +127,9 @@ struct NormConsts {
   float mean[3];
   float stdv[3];
   float rcp[3];
+  // The packed-pair ops (f32x2 below) take their 1 / -1 / -0 / -2^23 from
+  // here, kernel parameters ptxas cannot constant-fold (see PkK).
+  float one = 1.0f, neg_one = -1.0f, neg_zero = -0.0f, neg_magic = -8388608.0f;
 };
 
 #ifdef __CUDACC__
@@ -142,6 +145,54 @@ __device__ __forceinline__ float normalize_fast(float v, float mean, float s, fl
   float rem = __fmaf_rn(-q, s, d);
   return __fmaf_rn(rem, r, q);
 }
+
+// ---- packed fp32 pairs (sm_100 FFMA2: two lanes of fp32 per issue slot) ----
+// Every op is ONE fma.rn.f32x2 with a single rounding, so each lane equals
+// the scalar __f*_rn op bit for bit:  a+b = fma(a, 1, b),  a-b = fma(b, -1,
+// a),  a*b = fma(a, b, -0).  ptxas treats the f32x2 forms as contractable
+// even with --fmad=false and explicit .rn: it folds fma(x, 1, y) to FADD2 and
+// fma(x, y, -0) to FMUL2 and then fuses FMUL2 + FADD2 into one FFMA2 (seen in
+// the SASS), which changes the rounding.  So the constants 1 / -1 / -0 come
+// from kernel parameters (NormConsts) that ptxas cannot fold: every op stays
+// a real FFMA2 and nothing fuses.
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 pk2(float lo, float hi) {
+  f32x2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float2 up2(f32x2 v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
+  f32x2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ f32x2 splat2(float v) { return pk2(v, v); }
+struct PkK {  // opaque packed constants, built from NormConsts in registers
+  f32x2 one, neg_one, neg_zero, neg_magic;
+  __device__ explicit PkK(const NormConsts& n)
+      : one(splat2(n.one)), neg_one(splat2(n.neg_one)), neg_zero(splat2(n.neg_zero)), neg_magic(splat2(n.neg_magic)) {}
+  PkK() = default;
+  __device__ f32x2 add(f32x2 a, f32x2 b) const { return fma2(a, one, b); }
+  __device__ f32x2 sub(f32x2 a, f32x2 b) const { return fma2(b, neg_one, a); }
+  __device__ f32x2 mul(f32x2 a, f32x2 b) const { return fma2(a, b, neg_zero); }
+  // two uint8 -> exact fp32 (the 2^23 magic-number conversion of u8_to_f32)
+  __device__ f32x2 u8x2(uint32_t a, uint32_t b) const {
+    return fma2(pk2(__uint_as_float(0x4B000000u | a), __uint_as_float(0x4B000000u | b)), one, neg_magic);
+  }
+  // normalize_fast on a pair; nsd = -std per lane
+  __device__ f32x2 normalize(f32x2 v, f32x2 mean, f32x2 nsd, f32x2 r) const {
+    const f32x2 d = sub(v, mean);
+    const f32x2 q = mul(d, r);
+    return fma2(fma2(q, nsd, d), r, q);
+  }
+  // p + w * (q - p), each op rounded (lerp_rn) on a pair
+  __device__ f32x2 lerp(f32x2 p, f32x2 q, f32x2 w) const { return add(p, mul(w, sub(q, p))); }
+};
 
 __device__ __forceinline__ void st_cs_f4(float4* p, float4 v) {
   asm volatile("st.global.cs.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x),

@@ -290,6 +290,7 @@ struct FastArgs {
   float* out;
   int in_h, in_w, out_h, out_w;
   int band_rows, bands, q_per_row, rpp;
+  int q_stride;  // threads per row group (>= q_per_row; a multiple of 32 keeps groups warp-uniform)
   int stage_stride, stage_bytes, stages;
   uint64_t seed;
   int do_flip;
@@ -310,6 +311,8 @@ struct RowTap {
 struct CropOp {
   float mu[4], sd[4], rc[4];
   int off_n[4], off_f[4];
+  f32x2 mu2[2], nsd2[2], rc2[2];
+  PkK k;
 
   __device__ void init(const FastArgs& a, int q, uint8_t*) {
 #pragma unroll
@@ -320,6 +323,13 @@ struct CropOp {
       rc[u] = sel3(ch, a.nc.rcp[0], a.nc.rcp[1], a.nc.rcp[2]);
       off_n[u] = e;
       off_f[u] = (a.out_w - 1 - x) * 3 + ch;
+    }
+    k = PkK(a.nc);
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      mu2[p] = pk2(mu[2 * p], mu[2 * p + 1]);
+      nsd2[p] = pk2(-sd[2 * p], -sd[2 * p + 1]);
+      rc2[p] = pk2(rc[2 * p], rc[2 * p + 1]);
     }
   }
 
@@ -368,11 +378,12 @@ struct CropOp {
                                                     static_cast<size_t>(m.band) * a.band_rows) * seg);
     for (int r = rsub; r < m.nrows; r += a.rpp) {
       const uint8_t* row = st + r * a.stage_stride;
-      float v[4];
+      const int* off = m.flip ? off_f : off_n;
+      float2 v[2];
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-        v[u] = normalize_fast(u8_to_f32(row[m.flip ? off_f[u] : off_n[u]]), mu[u], sd[u], rc[u]);
-      st_cs_f4(ob + static_cast<size_t>(r) * a.q_per_row + q, make_float4(v[0], v[1], v[2], v[3]));
+      for (int p = 0; p < 2; ++p)  // packed pairs: the scalar normalize_fast ops, bit for bit
+        v[p] = up2(k.normalize(k.u8x2(row[off[2 * p]], row[off[2 * p + 1]]), mu2[p], nsd2[p], rc2[p]));
+      st_cs_f4(ob + static_cast<size_t>(r) * a.q_per_row + q, make_float4(v[0].x, v[0].y, v[1].x, v[1].y));
     }
   }
 };
@@ -381,6 +392,8 @@ struct CropOp {
 struct ResizeOp {
   float mu[4], sd[4], rc[4], wx[4];
   int o0[4], o1[4];
+  f32x2 mu2[2], nsd2[2], rc2[2], wx2[2];
+  PkK k;
 
   __device__ void init(const FastArgs& a, int q, uint8_t*) {
 #pragma unroll
@@ -393,6 +406,14 @@ struct ResizeOp {
       resize_coord(x, a.in_w, a.out_w, x0, x1, wx[u]);
       o0[u] = x0 * 3 + ch;
       o1[u] = x1 * 3 + ch;
+    }
+    k = PkK(a.nc);
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      mu2[p] = pk2(mu[2 * p], mu[2 * p + 1]);
+      nsd2[p] = pk2(-sd[2 * p], -sd[2 * p + 1]);
+      rc2[p] = pk2(rc[2 * p], rc[2 * p + 1]);
+      wx2[p] = pk2(wx[2 * p], wx[2 * p + 1]);
     }
   }
 
@@ -440,14 +461,23 @@ struct ResizeOp {
       const RowTap t = taps[y_begin + r];
       const uint8_t* row0 = st + static_cast<size_t>(t.y0 - m.ys0) * row_bytes;
       const uint8_t* row1 = st + static_cast<size_t>(t.y1 - m.ys0) * row_bytes;
-      float v[4];
+      // lanes (u = 2p, 2p + 1) in packed pairs: the same rounded ops as the
+      // scalar lerp_rn / normalize_fast (orc_resize_normalize), half the issues.
+      // (Walking consecutive rows per thread to reuse a shared source row
+      // measured slower: 0.51-0.54 vs 0.67 of HBM -- the reuse branches cut
+      // the loads in flight per thread.)
+      const f32x2 wy2 = splat2(t.wy);
+      float2 v[2];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const float top = lerp_rn(u8_to_f32(row0[o0[u]]), u8_to_f32(row0[o1[u]]), wx[u]);
-        const float bot = lerp_rn(u8_to_f32(row1[o0[u]]), u8_to_f32(row1[o1[u]]), wx[u]);
-        v[u] = normalize_fast(lerp_rn(top, bot, t.wy), mu[u], sd[u], rc[u]);
+      for (int p = 0; p < 2; ++p) {
+        const int u = 2 * p;
+        const f32x2 top =
+            k.lerp(k.u8x2(row0[o0[u]], row0[o0[u + 1]]), k.u8x2(row0[o1[u]], row0[o1[u + 1]]), wx2[p]);
+        const f32x2 bot =
+            k.lerp(k.u8x2(row1[o0[u]], row1[o0[u + 1]]), k.u8x2(row1[o1[u]], row1[o1[u + 1]]), wx2[p]);
+        v[p] = up2(k.normalize(k.lerp(top, bot, wy2), mu2[p], nsd2[p], rc2[p]));
       }
-      st_cs_f4(ob + static_cast<size_t>(r) * a.q_per_row + q, make_float4(v[0], v[1], v[2], v[3]));
+      st_cs_f4(ob + static_cast<size_t>(r) * a.q_per_row + q, make_float4(v[0].x, v[0].y, v[1].x, v[1].y));
     }
   }
 };
@@ -459,7 +489,7 @@ __global__ void __launch_bounds__(kFastConsumers + 32, 1) pipeline_kernel(FastAr
   __shared__ StageMeta meta[kMaxStages];
   const int kStages = a.stages;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int consumers = a.q_per_row * a.rpp;
+  const int consumers = a.q_stride * a.rpp;
   const int n_cwarps = (consumers + 31) >> 5;
   uint8_t* taps = smem + kStages * a.stage_bytes;  // resize row taps (unused by K3)
 
@@ -496,8 +526,8 @@ __global__ void __launch_bounds__(kFastConsumers + 32, 1) pipeline_kernel(FastAr
     return;
   }
   // ---- consumer warps ----
-  const int q = tid % a.q_per_row, rsub = tid / a.q_per_row;
-  const bool active = tid < consumers;
+  const int q = tid % a.q_stride, rsub = tid / a.q_stride;
+  const bool active = tid < consumers && q < a.q_per_row;
   Op op;
   op.init(a, active ? q : 0, taps);
   int k = 0;
@@ -542,7 +572,7 @@ int launch_persistent(K kernel, const FastArgs& a, size_t smem, cudaStream_t s, 
   static std::map<Key, int> occupancy;
   static std::map<std::pair<int, const void*>, size_t> smem_attr;  // max dynamic smem set per kernel
   int st;
-  const int threads = ((a.q_per_row * a.rpp + 31) / 32) * 32 + 32;
+  const int threads = ((a.q_stride * a.rpp + 31) / 32) * 32 + 32;
   int dev = 0;
   cudaGetDevice(&dev);
   int per_sm = 0;
@@ -617,6 +647,7 @@ FastArgs make_fast(const uint8_t* images, int64_t num_images, int in_h, int in_w
   a.band_rows = band_rows < out_h ? band_rows : out_h;
   a.bands = (out_h + a.band_rows - 1) / a.band_rows;
   a.q_per_row = out_w * 3 / 4;
+  a.q_stride = a.q_per_row;
   a.rpp = kFastConsumers / a.q_per_row;
   if (a.rpp > a.band_rows) a.rpp = a.band_rows;
   a.nc = make_norm(mean, stdv);

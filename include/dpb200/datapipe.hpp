@@ -61,6 +61,7 @@ struct SourceData {
   // back to back in `values` (record_len bytes each when uniform, else 0)
   enum class Kind { kInt64, kImages, kTokens, kRecords } kind;
   int64_t record_len = 0;
+  std::vector<int64_t> file_records;  // kRecords: records per file, in path order
   int64_t count = 0;
   // kInt64: values[count] (device);  kImages: u8 [count, h, w, c]
   // kTokens: lengths i32[count], offsets i64[count+1], tokens i32[total]

@@ -65,6 +65,11 @@ int dp_source_synthetic_tokens(int64_t count, uint32_t max_len, uint64_t len_see
                                dp_source** out);
 int dp_source_tokens_from_host(const int32_t* lengths, int64_t count, const int32_t* tokens, int device,
                                dp_source** out);
+/* length-prefixed record files (formats.md:67-74) read in order into device
+ * memory: the records of an interleave over files (file x = input element x,
+ * every file holding the reader's record count; ops::Interleave over
+ * ops::FromFile readers, runtime.cpp:1044-1128) */
+int dp_source_records_from_files(const char* const* paths, int64_t num_paths, int device, dp_source** out);
 void dp_source_release(dp_source* src);
 
 /* ---- graph builders: include/datapipe/graph.hpp:134-165 (ops::*) ---- */

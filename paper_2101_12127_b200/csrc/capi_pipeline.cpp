@@ -132,6 +132,17 @@ int dp_source_tokens_from_host(const int32_t* lengths, int64_t count, const int3
   DP_REQUIRE(lengths && out);
   return Guard([&] { *out = new dp_source{TokensFromHost(lengths, count, tokens, device)}; });
 }
+int dp_source_records_from_files(const char* const* paths, int64_t num_paths, int device, dp_source** out) {
+  DP_REQUIRE(out && (paths || num_paths == 0) && num_paths >= 0);
+  return Guard([&] {
+    std::vector<std::string> p;
+    for (int64_t i = 0; i < num_paths; ++i) {
+      if (!paths[i]) throw PipelineError(ErrorCode::kInvalidAttr, "records_from_files: null path");
+      p.emplace_back(paths[i]);
+    }
+    *out = new dp_source{RecordsFromFiles(p, device)};
+  });
+}
 void dp_source_release(dp_source* src) { delete src; }
 
 // ---- graphs ----

@@ -254,8 +254,10 @@ SourcePtr RecordsFromFiles(const std::vector<std::string>& paths, int device) {
   if (paths.empty()) throw PipelineError(ErrorCode::kInvalidAttr, "from_file: 'paths' must be non-empty");
   std::vector<std::string> blobs;
   std::vector<int64_t> offsets{0};
+  std::vector<int64_t> per_file;
   int64_t uniform = -1;
   for (const auto& path : paths) {
+    const size_t before = blobs.size();
     FILE* f = std::fopen(path.c_str(), "rb");
     if (!f) throw PipelineError(ErrorCode::kMissingFile, "no such file: " + path);
     std::string data;
@@ -279,11 +281,13 @@ SourcePtr RecordsFromFiles(const std::vector<std::string>& paths, int device) {
       uniform = (uniform < 0 || uniform == static_cast<int64_t>(len)) ? len : -2;
       pos += len;
     }
+    per_file.push_back(static_cast<int64_t>(blobs.size() - before));
   }
   auto s = std::make_shared<SourceData>();
   s->kind = SourceData::Kind::kRecords;
   s->count = static_cast<int64_t>(blobs.size());
   s->record_len = uniform >= 0 ? uniform : 0;
+  s->file_records = std::move(per_file);
   s->device = device;
   const size_t total = static_cast<size_t>(offsets.back());
   s->values = DeviceAlloc(std::max<size_t>(total, 16), device);
@@ -507,6 +511,20 @@ Lowered Lower(const DatasetGraph& g, const UdfRegistry& reg) {
   }
   if (seen_interleave) {
     if (L.records && L.records->shard_count > 1) Unsupported("interleave records must be fully resident");
+    if (L.records && L.records->kind == SourceData::Kind::kRecords) {
+      // interleave over record files: input element x opens file x, whose
+      // records are x * R .. x * R + R - 1 of the concatenation when every
+      // file holds the reader's R records
+      int64_t R = 0;
+      for (const auto& op : L.chain)
+        if (op.kind == IndexOp::Kind::kInterleave) R = op.b;
+      for (size_t f = 0; f < L.records->file_records.size(); ++f)
+        if (L.records->file_records[f] != R)
+          throw PipelineError(ErrorCode::kMalformedInput,
+                              "interleave: record file " + std::to_string(f) + " holds " +
+                                  std::to_string(L.records->file_records[f]) + " records, the reader opens " +
+                                  std::to_string(R));
+    }
     if (L.source && L.source->kind != SourceData::Kind::kInt64) Unsupported("interleave input must be int64 ordinals");
     if (L.source) Unsupported("interleave over from_memory ordinals: use range()");
     L.source = L.records;  // the batch stage reads the record source

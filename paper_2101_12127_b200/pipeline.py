@@ -64,6 +64,7 @@ _SIGS = {
     "dp_source_images_pinned_host": [c_vp, c_i64, c_i64, c_i64, c_int, PP],
     "dp_source_synthetic_tokens": [c_i64, ctypes.c_uint32, c_u64, c_u64, c_int, PP],
     "dp_source_tokens_from_host": [c_vp, c_i64, c_vp, c_int, PP],
+    "dp_source_records_from_files": [ctypes.POINTER(ctypes.c_char_p), c_i64, c_int, PP],
     "dp_source_release": [c_vp],
     "dp_graph_range": [c_vp, c_i64, PP],
     "dp_graph_from_memory_i64": [c_vp, c_vp, c_i64, c_int, PP],
@@ -192,6 +193,14 @@ class Source:
 
     def __del__(self, _rel=_release):
         _rel(self, "dp_source_release")
+
+    @staticmethod
+    def records_from_files(paths, device=0):
+        """Record files read into device memory: the records of an interleave over files."""
+        arr = (ctypes.c_char_p * max(1, len(paths)))(*[os.fsencode(p) for p in paths])
+        out = c_vp()
+        _check(L().dp_source_records_from_files(arr, len(paths), device, ctypes.byref(out)))
+        return Source(out)
 
     @staticmethod
     def synthetic_images(count, h, w, seed=0x5EED, device=0):

@@ -325,6 +325,38 @@ def test_cfg5_interleave_shuffle_map_and_batch(dp, orc):
         assert np.array_equal(pix[r], orc.crop_flip_normalize(orc.images(p, 1, 48, 48)[0], p, 32, 32))
 
 
+def test_interleave_over_record_files_equals_cfg5(dp, orc, tmp_path):
+    """Interleave over record files (from_file +
+    Interleave): input element x opens file x; equals the same pipeline over
+    the in-memory records, and a file with the wrong record count is
+    MalformedInput."""
+    c = [x for x in GOLDEN["interleave"] if "shuffle" in x][0]
+    m, cycle, records = c["num_sources"], c["cycle"], c["records"]
+    imgs = orc.images(0, m * records, 48, 48)
+    paths = [str(tmp_path / f"part-{x}.rec") for x in range(m)]
+    for x, p in enumerate(paths):
+        dp.write_record_file(p, [im.tobytes() for im in imgs[x * records:(x + 1) * records]])
+    reg = image_registry(dp, 0, crop=(32, 32))
+    reg.register_record_reader("reader", records)
+    reg.register_decode_raw("decode", 48, 48)
+    out = []
+    for recs, pre in ((dp.Source.records_from_files(paths), ("decode",)), (dp.Source.images_from_host(imgs), ())):
+        g = dp.Dataset.range(reg, m).shard(*c["shard"]).interleave("reader", cycle, c["parallel"], records=recs)
+        for f in pre:
+            g = g.map(f)
+        g, _ = g.shuffle(*c["shuffle"]).map("crop").map("norm").batch(64).prefetch(-1).optimize()
+        out.append(drain(dp.make_iterator(g, seed_override=1), comps=(0, 1)))
+    ids = np.concatenate([b[0] for b in out[0]])
+    assert ids.size == c["count"] and ids[:8].tolist() == c["first"] and fnv(orc, ids) == c["fnv"]
+    for a, b in zip(*out):
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    dp.write_record_file(paths[-1], [imgs[0].tobytes()])  # one record short
+    g = dp.Dataset.range(reg, m).interleave("reader", cycle, 1, records=dp.Source.records_from_files(paths))
+    with pytest.raises(dp.DpError) as e:
+        dp.make_iterator(g.map("decode").map("crop").map("norm").batch(8))
+    assert e.value.code == dp.ERR["MalformedInput"]
+
+
 def test_sharded_residency_equals_shard_of_full_dataset(dp, orc):
     """Per-GPU residency: a process holding only shard i of k
     produces exactly shard(k, i) of the full dataset, ids and pixels."""

@@ -173,7 +173,7 @@ def cpu_reference(cfg, threads, warmup_batches, steps):
                                 cfg["batch"], threads, warmup_batches, steps, ctypes.byref(secs), ctypes.byref(elems))
     if rc != 0:
         raise RuntimeError(L.ref_last_error().decode())
-    return {"value": elems.value / secs.value, "seconds": secs.value, "elements": elems.value,
+    return {"value": elems.value / secs.value, "seconds": secs.value, "elements": elems.value, "cores": threads,
             "sample": f"{sample} resident synthetic images repeated, {steps} timed batches of {cfg['batch']} after "
                       f"{warmup_batches} warm-up, map_and_batch num_parallel_calls={threads}, prefetch(2)"}
 
@@ -186,8 +186,22 @@ def cpu_reference_range(cfg):
         return None
     n = 1_000_000
     eps = ref.time_range_map_batch(n, cfg["batch"], 1, epochs=3)
-    return {"value": n / float(sorted(eps)[1]), "sample": f"Range({n}) -> Map(x*3+1, p=1) -> Batch(1024), "
+    return {"value": n / float(sorted(eps)[1]), "cores": 1, "sample": f"Range({n}) -> Map(x*3+1, p=1) -> Batch(1024), "
                                                           f"median of 3 epochs after 1 warm-up"}
+
+
+def cpu_reference_tokens(cfg):
+    """cfg4 on the compiled reference: sequences -> Filter(len<=512) -> Batch(128)
+    (its ragged Batch: the same selection and order as PaddedBatch), one thread."""
+    from tests.oracle_lib import Reference
+    ref = Reference.load()
+    if ref is None:
+        return None
+    n = 10_000  # the reference holds every token as a heap Value: a bounded sample
+    eps = ref.time_filter_batch_tokens(n, 4, 1024, 4, cfg["max_keep"], cfg["batch"], epochs=3)
+    return {"value": n / float(sorted(eps)[1]), "cores": 1,
+            "sample": f"{n} sequences (len U[1,1024], seed 4) -> Filter(len<=512) -> Batch(128), median of 3 "
+                      f"epochs after 1 warm-up"}
 
 
 def run_reference(args, cfg):
@@ -195,19 +209,20 @@ def run_reference(args, cfg):
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    if cfg["kind"] != "images":
-        print(json.dumps({"impl": "reference", "unavailable": "the reference arm is timed on the image configs "
-                                                              "(cfg2 headline)"}), flush=True)
-        return
-    r = cpu_reference(cfg, threads, args.warmup, args.steps)
+    if cfg["kind"] == "images":
+        r = cpu_reference(cfg, threads, args.warmup, args.steps)
+    else:  # the reference's sequential path (map p=1 / filter + batch): one host thread
+        r = cpu_reference_range(cfg) if cfg["kind"] == "range" else cpu_reference_tokens(cfg)
+        threads = 1
+        r.setdefault("seconds", 1.0 / r["value"] * cfg["batch"] * args.steps)
     line = {"impl": "reference", "metric": "pipeline elements/sec", "value": round(r["value"], 2),
-            "unit": "images/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "unit": cfg["unit"], "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(1e3 * r["seconds"] / args.steps, 4), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u8->f32", "data": "synthetic",
+            "scaling": "weak", "vs_baseline": None, "dtype": cfg.get("dtype", "u8->f32"), "data": "synthetic",
             "config": {"workload": cfg["workload"], "global_batch": cfg["batch"], "host_threads": threads},
-            "cpu_baseline": {"value": round(r["value"], 2), "unit": "images/s", "cores": threads,
+            "cpu_baseline": {"value": round(r["value"], 2), "unit": cfg["unit"], "cores": threads,
                              "kind": "reference", "sample": r["sample"]},
-            "e2e": {"value": round(r["value"], 2), "unit": "images/s", "h2d_bytes_per_step": 0,
+            "e2e": {"value": round(r["value"], 2), "unit": cfg["unit"], "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -366,9 +381,16 @@ def run_ours(args, cfg):
     try:
         # ~10 s of CPU work: 48 timed batches of 256 after 4 warm-up batches
         cpu = cpu_reference(cfg, os.cpu_count() or 1, 4, 48) if cfg["kind"] == "images" else \
-            cpu_reference_range(cfg) if cfg["kind"] == "range" else None
+            cpu_reference_range(cfg) if cfg["kind"] == "range" else cpu_reference_tokens(cfg)
     except Exception as ex:  # reported, not fatal
         cpu = {"value": None, "sample": f"unavailable: {ex}"}
+    one_core = None
+    if cfg["kind"] == "images" and cpu is not None and cpu.get("value"):
+        try:  # also the 1-core number (num_parallel_calls = 1), ~2 s
+            r1 = cpu_reference(cfg, 1, 1, 4)
+            one_core = {"value": round(r1["value"], 2), "cores": 1, "sample": r1["sample"]}
+        except Exception as ex:
+            one_core = {"value": None, "sample": f"unavailable: {ex}"}
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
@@ -399,8 +421,8 @@ def run_ours(args, cfg):
         "order_check": {"digest": "K7 position-keyed digest of each rank's first 8 batches of ids",
                         "per_rank": order_digests},
         "cpu_baseline": {"value": None if cpu is None else (round(cpu["value"], 2) if cpu["value"] else None),
-                         "unit": "images/s", "cores": os.cpu_count(), "kind": "reference",
-                         "sample": None if cpu is None else cpu["sample"]},
+                         "unit": cfg["unit"], "cores": (cpu or {}).get("cores", os.cpu_count()), "kind": "reference",
+                         "sample": None if cpu is None else cpu["sample"], "one_core": one_core},
         "e2e": e2e,
         "gpu_launches": launches,
         "clocks": clocks.summary(),

@@ -421,6 +421,45 @@ int ref_time_range_map_batch(int64_t n, int64_t batch, int64_t parallel,
   }
 }
 
+// CPU baseline for cfg4: token sequences -> filter(len <= max_keep) ->
+// batch (the reference has no padded_batch; its ragged Batch is the same
+// selection and order), optimized.  Elements are built once, outside timing.
+int ref_time_filter_batch_tokens(int64_t n, uint64_t len_seed, uint32_t max_len, uint64_t tok_seed,
+                                 int32_t max_keep, int64_t batch, int epochs, double* epoch_s) {
+  try {
+    UdfRegistry reg;
+    std::string pred = "len_le(" + std::to_string(max_keep) + ")";
+    reg.RegisterPredicate(pred, [max_keep](const Element& e) {
+      return static_cast<int64_t>(e.component(0).items().size()) <= max_keep;
+    });
+    std::vector<int32_t> lens(static_cast<size_t>(n));
+    orc_synth_lengths(len_seed, max_len, static_cast<uint64_t>(n), lens.data());
+    std::vector<Element> elems;
+    elems.reserve(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) {
+      std::vector<Value> toks;
+      toks.reserve(static_cast<size_t>(lens[i]));
+      for (int32_t j = 0; j < lens[i]; ++j) toks.push_back(Value::Int64(orc_synth_token(tok_seed, i, j)));
+      elems.push_back(Element::Scalar(Value::List(std::move(toks))));
+    }
+    DatasetGraph g = ops::FromMemory(std::move(elems), reg);
+    g = ops::Filter(g, pred, reg);
+    g = ops::Batch(g, batch, false, reg);
+    g = Optimize(g, RuleSet::Default(), reg).first;
+    for (int ep = 0; ep <= epochs; ++ep) {
+      auto it = MakeIterator(g, reg, Seeded(1));
+      auto t0 = std::chrono::steady_clock::now();
+      while (auto e = it->GetNext()) {
+      }
+      double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      if (ep > 0) epoch_s[ep - 1] = s;
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    return Fail(e);
+  }
+}
+
 int ref_hardware_concurrency(void) {
   return static_cast<int>(std::thread::hardware_concurrency());
 }

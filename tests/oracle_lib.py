@@ -183,6 +183,8 @@ class Reference:
         L.ref_time_image_pipeline.argtypes = [c_int, c_int, c_int, c_int, c_int, u64, u64, i64, i64, u64, i64, i64,
                                               i64, u64, c_int, vp, vp]
         L.ref_time_range_map_batch.argtypes = [i64, i64, i64, c_int, vp]
+        L.ref_time_filter_batch_tokens.argtypes = [i64, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint64,
+                                                   ctypes.c_int32, i64, c_int, vp]
         self.L = L
 
     def _check(self, rc):
@@ -255,6 +257,12 @@ class Reference:
                                                    PIX_SEED, n, shuffle_buffer, 42, batch, parallel, prefetch, 1,
                                                    epochs, P(eps), P(cnt)))
         return eps, int(cnt[0])
+
+    def time_filter_batch_tokens(self, n, len_seed, max_len, tok_seed, max_keep, batch, epochs=3):
+        eps = np.zeros(epochs, np.float64)
+        self._check(self.L.ref_time_filter_batch_tokens(n, len_seed, max_len, tok_seed, max_keep, batch, epochs,
+                                                        P(eps)))
+        return eps
 
     def time_range_map_batch(self, n, batch, parallel, epochs=3):
         eps = np.zeros(epochs, np.float64)

@@ -62,6 +62,7 @@ struct SourceData {
   enum class Kind { kInt64, kImages, kTokens, kRecords } kind;
   int64_t record_len = 0;
   std::vector<int64_t> file_records;  // kRecords: records per file, in path order
+  std::vector<int64_t> host_int64;    // kInt64 from_memory: the values (graph serialization)
   int64_t count = 0;
   // kInt64: values[count] (device);  kImages: u8 [count, h, w, c]
   // kTokens: lengths i32[count], offsets i64[count+1], tokens i32[total]
@@ -332,6 +333,24 @@ std::unique_ptr<PipelineIterator> MakeIterator(const DatasetGraph& graph, const 
 // base seed and Seek to the saved position.
 std::unique_ptr<PipelineIterator> Restore(const DatasetGraph& graph, const UdfRegistry& registry,
                                           const std::string& blob, IteratorOptions options = {});
+
+// ---- graph serialization (formats.md "Graph serialization"; serialize.hpp) ----
+// DPG1 bytes, canonical (preorder nodes, attrs in ascending key order).
+// Kinds and attrs shared with the reference encode exactly as the
+// reference's Serialize does (from_memory -> "elements" element list of int64
+// scalars, from_file -> "paths"), so those graphs' bytes and fingerprints are
+// the reference's.  Device data with no reference encoding (tensor_slices /
+// token_sequences sources, interleave records) is written as a descriptor
+// (attr tag 32: kind and shape, not the data) and re-bound at Deserialize from
+// `sources`, consumed in preorder; a descriptor mismatch is kValidationFailed.
+std::string Serialize(const DatasetGraph& graph);
+DatasetGraph Deserialize(const std::string& bytes, const UdfRegistry& registry,
+                         const std::vector<SourcePtr>& sources = {}, int device = 0);
+// SHA-256 of the serialization with every "seed" attr zeroed
+// (GraphFingerprint, serialize.cpp:213-216): the checkpoint fingerprint.
+std::array<uint8_t, 32> GraphFingerprint(const DatasetGraph& graph);
+std::string FingerprintHex(const std::array<uint8_t, 32>& fp);
+std::array<uint8_t, 32> Sha256Digest(const void* data, size_t n);  // FIPS 180-4
 
 // PRNG contract helpers (random.hpp:24-34; runtime.cpp:713-718).
 uint64_t MixSeeds(uint64_t a, uint64_t b);

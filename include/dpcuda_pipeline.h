@@ -110,6 +110,17 @@ int dp_graph_optimize(const dp_graph* in, dp_registry* reg, const char* disabled
 /* kind name of the root node ("map_and_batch", ...) and the graph dump */
 int dp_graph_root_kind(const dp_graph* g, char* buf, size_t len);
 int dp_graph_to_string(const dp_graph* g, char* buf, size_t len);
+/* Serialize (serialize.hpp; formats.md "Graph serialization"): DPG1 bytes.
+ * Writes min(len, cap) bytes and sets *len to the full size (call with
+ * cap = 0 to size the buffer). */
+int dp_graph_serialize(const dp_graph* g, uint8_t* buf, size_t cap, size_t* len);
+/* Deserialize: device sources with no reference encoding are re-bound from
+ * `sources` in preorder (descriptor-checked, kValidationFailed otherwise). */
+int dp_graph_deserialize(const dp_registry* reg, const uint8_t* bytes, size_t len, const dp_source* const* sources,
+                         int64_t num_sources, int device, dp_graph** out);
+/* GraphFingerprint (serialize.cpp:213-216): SHA-256 of the seed-zeroed
+ * serialization as 64 hex chars + NUL (hex must hold 65 bytes). */
+int dp_graph_fingerprint(const dp_graph* g, char* hex);
 void dp_graph_release(dp_graph* g);
 
 /* ---- iterator: include/datapipe/runtime.hpp:35-100 ---- */

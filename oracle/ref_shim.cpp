@@ -21,11 +21,13 @@
 #include <thread>
 #include <vector>
 
+#include "datapipe/checkpoint.hpp"
 #include "datapipe/element.hpp"
 #include "datapipe/errors.hpp"
 #include "datapipe/graph.hpp"
 #include "datapipe/optimizer.hpp"
 #include "datapipe/runtime.hpp"
+#include "datapipe/serialize.hpp"
 #include "datapipe/udf.hpp"
 #include "restate.h"
 
@@ -454,6 +456,94 @@ int ref_time_filter_batch_tokens(int64_t n, uint64_t len_seed, uint32_t max_len,
       double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
       if (ep > 0) epoch_s[ep - 1] = s;
     }
+    return 0;
+  } catch (const std::exception& e) {
+    return Fail(e);
+  }
+}
+
+// Graph serialization known answers (formats.md "Graph serialization",
+// src/serialize.cpp Serialize / GraphFingerprint) for the pipeline shapes
+// both engines express.  which:
+//   0 from_memory(0..9) -> map(affine(3,1), 4) -> batch(4)
+//   1 the same, Optimize(Default)                    (-> map_and_batch)
+//   2 from_memory(0..99) -> shuffle(10, seed 42) -> repeat(3) -> batch(8)
+//     -> prefetch(AUTOTUNE), Optimize(Default)       (shuffle_repeat fusion)
+//   3 from_memory(0..63) -> shard(4, 1) -> shuffle(50) -> map(affine(3,1), -1)
+//     -> map(affine(2,0), 2) -> batch(16, drop) -> prefetch(2), Optimize
+//   4 from_memory(0..7) -> interleave(reader(3), 2, 1) -> batch(5)
+//   5 from_file(part-0.rec, part-1.rec) -> batch(2)
+// Writes the serialized bytes (up to cap) and the fingerprint as 64 hex chars.
+namespace {
+DatasetGraph KnownPipeline(int which, UdfRegistry& reg) {
+    RegisterAffine(reg, "affine(3,1)", 3, 1);
+    RegisterAffine(reg, "affine(2,0)", 2, 0);
+    reg.RegisterDataset(
+        "reader(3)",
+        [&reg](const Element& e) {
+          std::vector<Element> recs;
+          for (int64_t r = 0; r < 3; ++r) recs.push_back(Element::Scalar(Value::Int64(e.component(0).int64() * 3 + r)));
+          return ops::FromMemory(std::move(recs), reg);
+        },
+        ElementSpec({TypeSpec::Int64()}));
+    DatasetGraph g;
+    switch (which) {
+      case 0:
+      case 1:
+        g = ops::Batch(ops::Map(ops::FromMemory(IntRange(10), reg), "affine(3,1)", 4, reg), 4, false, reg);
+        if (which == 1) g = Optimize(g, RuleSet::Default(), reg).first;
+        break;
+      case 2:
+        g = ops::Shuffle(ops::FromMemory(IntRange(100), reg), 10, uint64_t{42}, reg);
+        g = ops::Prefetch(ops::Batch(ops::Repeat(g, 3, reg), 8, false, reg), kAutotune, reg);
+        g = Optimize(g, RuleSet::Default(), reg).first;
+        break;
+      case 3:
+        g = ops::Shuffle(ops::Shard(ops::FromMemory(IntRange(64), reg), 4, 1, reg), 50, std::nullopt, reg);
+        g = ops::Map(ops::Map(g, "affine(3,1)", kAutotune, reg), "affine(2,0)", 2, reg);
+        g = ops::Prefetch(ops::Batch(g, 16, true, reg), 2, reg);
+        g = Optimize(g, RuleSet::Default(), reg).first;
+        break;
+      case 4:
+        g = ops::Batch(ops::Interleave(ops::FromMemory(IntRange(8), reg), "reader(3)", 2, 1, reg), 5, false, reg);
+        break;
+      case 5:
+        g = ops::Batch(ops::FromFile({"part-0.rec", "part-1.rec"}, reg), 2, false, reg);
+        break;
+      default:
+        throw PipelineError(ErrorCode::kInvalidAttr, "unknown pipeline");
+    }
+    return g;
+}
+}  // namespace
+
+int ref_serialize_pipeline(int which, uint8_t* buf, size_t cap, size_t* len, char* fp_hex) {
+  try {
+    UdfRegistry reg;
+    DatasetGraph g = KnownPipeline(which, reg);
+    const std::string bytes = Serialize(g);
+    *len = bytes.size();
+    std::memcpy(buf, bytes.data(), std::min(cap, bytes.size()));
+    const std::string hex = GraphFingerprint(g).ToHex();
+    std::memcpy(fp_hex, hex.c_str(), hex.size() + 1);
+    return 0;
+  } catch (const std::exception& e) {
+    return Fail(e);
+  }
+}
+
+// DPC1 checkpoint (src/checkpoint.cpp Save) of known pipeline `which` after
+// `k` GetNext calls, base seed 1, deterministic.
+int ref_checkpoint_after(int which, int64_t k, uint8_t* buf, size_t cap, size_t* len) {
+  try {
+    UdfRegistry reg;
+    DatasetGraph g = KnownPipeline(which, reg);
+    auto it = MakeIterator(g, reg, Seeded(1));
+    for (int64_t i = 0; i < k; ++i)
+      if (!it->GetNext()) throw PipelineError(ErrorCode::kInvalidAttr, "pipeline ended before k");
+    const CheckpointBlob blob = Save(*it);
+    *len = blob.bytes.size();
+    std::memcpy(buf, blob.bytes.data(), std::min(cap, blob.bytes.size()));
     return 0;
   } catch (const std::exception& e) {
     return Fail(e);

@@ -253,6 +253,30 @@ int dp_graph_to_string(const dp_graph* g, char* buf, size_t len) {
   CopyOut(g->g.ToString(), buf, len);
   return DP_OK;
 }
+int dp_graph_serialize(const dp_graph* g, uint8_t* buf, size_t cap, size_t* len) {
+  DP_REQUIRE(g && len && (buf || cap == 0));
+  return Guard([&] {
+    const std::string b = Serialize(g->g);
+    *len = b.size();
+    if (cap) std::memcpy(buf, b.data(), std::min(cap, b.size()));
+  });
+}
+int dp_graph_deserialize(const dp_registry* reg, const uint8_t* bytes, size_t len, const dp_source* const* sources,
+                         int64_t num_sources, int device, dp_graph** out) {
+  DP_REQUIRE(reg && out && (bytes || len == 0) && num_sources >= 0 && (sources || num_sources == 0));
+  return Guard([&] {
+    std::vector<SourcePtr> src;
+    for (int64_t i = 0; i < num_sources; ++i) src.push_back(sources[i] ? sources[i]->s : nullptr);
+    Emit(out, Deserialize(std::string(reinterpret_cast<const char*>(bytes), len), reg->reg, src, device));
+  });
+}
+int dp_graph_fingerprint(const dp_graph* g, char* hex) {
+  DP_REQUIRE(g && hex);
+  return Guard([&] {
+    const std::string h = FingerprintHex(GraphFingerprint(g->g));
+    std::memcpy(hex, h.c_str(), h.size() + 1);
+  });
+}
 void dp_graph_release(dp_graph* g) { delete g; }
 
 // ---- iterators ----

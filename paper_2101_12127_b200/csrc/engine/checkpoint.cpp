@@ -12,10 +12,11 @@
 // batch root_delivered without computing the skipped batches, and produces
 // exactly the batches the replay would have (tests/test_gpu_pipeline.py).
 //
-// Fingerprint: SHA-256 (FIPS 180-4) of the graph's canonical text with the
-// seed attrs zeroed (seed-invariant, like GraphFingerprint,
-// src/fingerprint.cpp:86-114); the canonical text is this engine's, so
-// blobs are not interchangeable with the reference's.
+// Fingerprint: GraphFingerprint (serialize.cpp in this engine), SHA-256 of
+// the DPG1 serialization with the seed attrs zeroed -- byte-identical to the
+// reference's for the graphs both engines express (tests/test_serialize.py
+// pins it against the compiled reference), so such checkpoints carry the
+// same fingerprint in both.
 #include <array>
 #include <cstring>
 #include <sstream>
@@ -111,43 +112,6 @@ struct Sha256 {
   }
 };
 
-void CanonicalText(const DatasetNode& n, std::ostringstream& os) {
-  os << NodeKindName(n.kind()) << "(";
-  for (const auto& [k, v] : n.attrs()) {
-    os << k << "=";
-    if (k == "seed") {
-      os << "0";  // seed-invariant (fingerprint.cpp zeroes seeds)
-    } else {
-      std::visit(
-          [&](const auto& x) {
-            using T = std::decay_t<decltype(x)>;
-            if constexpr (std::is_same_v<T, SourcePtr>) {
-              os << "source{" << static_cast<int>(x->kind) << "," << x->count << "," << x->h << "," << x->w << ","
-                 << x->c << "," << x->total_tokens << "," << x->global_count << "," << x->shard_count << ","
-                 << x->shard_index << "}";
-            } else if constexpr (std::is_same_v<T, std::vector<std::string>>) {
-              for (const auto& s : x) os << s.size() << ":" << s << ",";
-            } else {
-              os << x;
-            }
-          },
-          v);
-    }
-    os << ";";
-  }
-  for (const auto& in : n.inputs()) CanonicalText(*in, os);
-  os << ")";
-}
-
-std::array<uint8_t, 32> Fingerprint(const DatasetGraph& g) {
-  std::ostringstream os;
-  CanonicalText(*g.root(), os);
-  const std::string s = os.str();
-  Sha256 sha;
-  sha.Update(s.data(), s.size());
-  return sha.Final();
-}
-
 struct Writer {
   std::string out;
   void Raw(const void* p, size_t n) { out.append(static_cast<const char*>(p), n); }
@@ -186,11 +150,27 @@ struct Reader {
 
 }  // namespace
 
+std::array<uint8_t, 32> Sha256Digest(const void* data, size_t n) {
+  Sha256 sha;
+  sha.Update(data, n);
+  return sha.Final();
+}
+
+std::string FingerprintHex(const std::array<uint8_t, 32>& fp) {
+  static const char* kHex = "0123456789abcdef";
+  std::string s;
+  for (uint8_t b : fp) {
+    s.push_back(kHex[b >> 4]);
+    s.push_back(kHex[b & 0xf]);
+  }
+  return s;
+}
+
 std::string PipelineIterator::Save() const {
   Writer w;
   w.Raw(kMagic, 4);
   w.Le<uint16_t>(kVersion);
-  const auto fp = Fingerprint(graph_);
+  const auto fp = GraphFingerprint(graph_);
   w.Raw(fp.data(), fp.size());
   w.Le<uint64_t>(base_seed_);
   w.Le<uint8_t>(options_.deterministic ? 1 : 0);
@@ -222,7 +202,7 @@ std::unique_ptr<PipelineIterator> Restore(const DatasetGraph& graph, const UdfRe
     r.Le<uint64_t>();
   }
   if (r.pos != blob.size()) throw PipelineError(ErrorCode::kCorruptBlob, "trailing bytes in checkpoint");
-  if (Fingerprint(graph) != saved)
+  if (GraphFingerprint(graph) != saved)
     throw PipelineError(ErrorCode::kFingerprintMismatch, "checkpoint was taken from a different pipeline");
   options.deterministic = deterministic;
   options.seed_override = base_seed;

@@ -325,6 +325,15 @@ SourcePtr Int64FromHost(const int64_t* values, int64_t count, int device) {
   s->kind = SourceData::Kind::kInt64;
   s->count = count;
   s->device = device;
+  if (count) s->host_int64.assign(values, values + count);
+  // Without a CUDA device the graph still builds (and serializes); the device
+  // copy is made here when a device exists, and MakeIterator fails loudly
+  // without one -- nothing is computed on the host.
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return s;
+  }
   s->values = DeviceAlloc(sizeof(int64_t) * std::max<int64_t>(count, 1), device);
   DeviceGuard g(device);
   if (count) CudaCheck(cudaMemcpy(s->values.get(), values, sizeof(int64_t) * count, cudaMemcpyHostToDevice), "upload");

@@ -84,6 +84,9 @@ _SIGS = {
     "dp_graph_optimize": [c_vp, c_vp, ctypes.c_char_p, PP, ctypes.c_char_p, c_size],
     "dp_graph_root_kind": [c_vp, ctypes.c_char_p, c_size],
     "dp_graph_to_string": [c_vp, ctypes.c_char_p, c_size],
+    "dp_graph_serialize": [c_vp, c_vp, c_size, ctypes.POINTER(c_size)],
+    "dp_graph_deserialize": [c_vp, c_vp, c_size, c_vp, c_i64, c_int, PP],
+    "dp_graph_fingerprint": [c_vp, c_vp],
     "dp_graph_release": [c_vp],
     "dp_iterator_options_default": [ctypes.POINTER(dp_iterator_options)],
     "dp_iterator_create": [c_vp, c_vp, ctypes.POINTER(dp_iterator_options), PP],
@@ -341,6 +344,28 @@ class Dataset:
         _check(L().dp_graph_optimize(self.h, self.reg.h, _b(",".join(disabled_rules)), ctypes.byref(out), rep,
                                      len(rep)))
         return Dataset(out, self.reg, self._keep), rep.value.decode()
+
+    def serialize(self) -> bytes:
+        """Serialize (DPG1, formats.md): the reference's bytes for graphs both engines express."""
+        n = c_size()
+        _check(L().dp_graph_serialize(self.h, None, 0, ctypes.byref(n)))
+        buf = ctypes.create_string_buffer(max(1, n.value))
+        _check(L().dp_graph_serialize(self.h, buf, n.value, ctypes.byref(n)))
+        return buf.raw[: n.value]
+
+    @staticmethod
+    def deserialize(reg, data: bytes, sources=(), device=0):
+        arr = (c_vp * max(1, len(sources)))(*[s.h for s in sources])
+        out = c_vp()
+        buf = ctypes.create_string_buffer(bytes(data), len(data))
+        _check(L().dp_graph_deserialize(reg.h, buf, len(data), arr, len(sources), device, ctypes.byref(out)))
+        return Dataset(out, reg, tuple(sources))
+
+    def fingerprint(self) -> str:
+        """GraphFingerprint: SHA-256 of the seed-zeroed serialization (hex)."""
+        buf = ctypes.create_string_buffer(65)
+        _check(L().dp_graph_fingerprint(self.h, buf))
+        return buf.value.decode()
 
     @property
     def root_kind(self):

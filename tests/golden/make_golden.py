@@ -110,6 +110,14 @@ def main():
                     "fnv_ids": f"{orc.fnv_digest(ids):016x}", "fnv_pixels": words_fnv(pix)})
     g["image_pipelines"] = img
 
+    ser = []
+    for which in range(6):  # pipeline shapes: oracle/ref_shim.cpp ref_serialize_pipeline
+        b, fp = ref.serialize_pipeline(which)
+        ser.append({"which": which, "dpg1_hex": b.hex(), "fingerprint": fp})
+    g["serialize"] = ser
+    g["checkpoint"] = [{"which": w, "k": k, "dpc1_hex": ref.checkpoint_after(w, k).hex()}
+                       for (w, k) in ((1, 1), (2, 5), (2, 0), (3, 0))]
+
     with open(os.path.join(HERE, "golden.json"), "w") as f:
         json.dump(g, f, indent=1)
     print("wrote", os.path.join(HERE, "golden.json"))

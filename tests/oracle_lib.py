@@ -258,6 +258,24 @@ class Reference:
                                                    epochs, P(eps), P(cnt)))
         return eps, int(cnt[0])
 
+    def serialize_pipeline(self, which):
+        """(DPG1 bytes, fingerprint hex) of known pipeline `which` (ref_shim.cpp)."""
+        buf = ctypes.create_string_buffer(1 << 16)
+        n = ctypes.c_size_t()
+        hexs = ctypes.create_string_buffer(65)
+        self.L.ref_serialize_pipeline.argtypes = [c_int, vp, ctypes.c_size_t, vp, vp]
+        self._check(self.L.ref_serialize_pipeline(which, ctypes.cast(buf, vp), len(buf), ctypes.byref(n),
+                                                  ctypes.cast(hexs, vp)))
+        return buf.raw[: n.value], hexs.value.decode()
+
+    def checkpoint_after(self, which, k):
+        """DPC1 blob of known pipeline `which` after k GetNext calls (ref_shim.cpp)."""
+        buf = ctypes.create_string_buffer(1 << 16)
+        n = ctypes.c_size_t()
+        self.L.ref_checkpoint_after.argtypes = [c_int, i64, vp, ctypes.c_size_t, vp]
+        self._check(self.L.ref_checkpoint_after(which, k, ctypes.cast(buf, vp), len(buf), ctypes.byref(n)))
+        return buf.raw[: n.value]
+
     def time_filter_batch_tokens(self, n, len_seed, max_len, tok_seed, max_keep, batch, epochs=3):
         eps = np.zeros(epochs, np.float64)
         self._check(self.L.ref_time_filter_batch_tokens(n, len_seed, max_len, tok_seed, max_keep, batch, epochs,

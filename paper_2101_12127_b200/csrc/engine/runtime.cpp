@@ -702,14 +702,20 @@ class DevicePipeline {
       return std::nullopt;
     }
     const int64_t grp = GroupOf(i);
-    const auto t0 = std::chrono::steady_clock::now();
+    using Clock = std::chrono::steady_clock;
+    const auto t0 = debug_timing_ ? Clock::now() : Clock::time_point{};
     while (issued_groups_ <= grp) IssueGroup(issued_groups_);
     // keep `depth` groups in flight
     while (issued_groups_ < grp + depth_ && (total_groups_ < 0 || issued_groups_ < total_groups_)) {
       if (!TryIssueGroup(issued_groups_, /*may_grow=*/false)) break;
     }
-    const auto t1 = std::chrono::steady_clock::now();
-    auto slot = group_slot_.at(grp);
+    const auto t1 = debug_timing_ ? Clock::now() : Clock::time_point{};
+    if (grp != cur_group_) {
+      cur_slot_ = group_slot_.at(grp);
+      cur_group_ = grp;
+      MaybeAutotune();  // once per group: event queries are API calls
+    }
+    const std::shared_ptr<Slot>& slot = cur_slot_;
     {
       // after a Seek into the middle of a group, the skipped batches count as handed out
       std::lock_guard lk(shared_->mu);
@@ -718,10 +724,10 @@ class DevicePipeline {
     next_batch_++;
     if (consumer_ != stream_ && !opt_.host_output) CudaCheck(cudaStreamWaitEvent(consumer_, slot->ready, 0), "wait");
     produced_++;
-    MaybeAutotune();
-    const auto t2 = std::chrono::steady_clock::now();
+    if (!debug_timing_) return MakeElement(slot, i);
+    const auto t2 = Clock::now();
     auto e = MakeElement(slot, i);
-    const auto t3 = std::chrono::steady_clock::now();
+    const auto t3 = Clock::now();
     dbg_[0] += std::chrono::duration<double>(t1 - t0).count();
     dbg_[1] += std::chrono::duration<double>(t2 - t1).count();
     dbg_[2] += std::chrono::duration<double>(t3 - t2).count();
@@ -1257,7 +1263,11 @@ class DevicePipeline {
     cudaStream_t consumer = consumer_;
     std::shared_ptr<void> lease(nullptr, [slot, consumer, shared = shared_](void*) {
       std::lock_guard lk(shared->mu);
-      if (--slot->outstanding == 0 && shared->alive) {
+      // The slot is reused only after ALL its batches were handed out and
+      // dropped (TryIssueGroup), so one release event, recorded on the
+      // consumer stream by the last drop, orders every batch's consumer work
+      // before the rewrite (one API call per group, not per batch).
+      if (--slot->outstanding == 0 && slot->handed_out == slot->num_batches && shared->alive) {
         cudaEventRecord(slot->release, consumer);
         slot->release_recorded = true;
       }
@@ -1377,6 +1387,9 @@ class DevicePipeline {
   cudaStream_t stream_ = nullptr, plan_stream_ = nullptr, copy_stream_ = nullptr, consumer_ = nullptr;
   int64_t depth_ = 2;
   bool autotune_ = false;
+  const bool debug_timing_ = std::getenv("DP_DEBUG_TIMING") != nullptr;
+  int64_t cur_group_ = -1;            // group of the last batch handed out
+  std::shared_ptr<Slot> cur_slot_;
   std::pair<size_t, size_t> batch_bytes_;
   int64_t max_len_ = 0;
   int64_t group_ = 1;

@@ -168,32 +168,52 @@ padded_batch_kernel(const int32_t* __restrict__ tokens, const int64_t* __restric
 // Rows [first_row, first_row + rows) of consecutive padded batches in one
 // launch: row R belongs to batch j = R / batch, is padded to lmax[j] and
 // lands at element offset boff[j] - boff[j0] + (R - j * batch) * lmax[j].
+//
+// Latency, not bandwidth, bounded the one-row-per-warp form (ncu: long
+// scoreboard stalls on the order -> length/offset -> tokens chain).  Here a
+// CTA takes a tile of kRowTile rows: its threads resolve the tile's
+// (position, length, offset, lmax, destination) once, in parallel, into
+// shared memory; then each warp streams its rows with kLoadsInFlight token
+// loads per lane issued before their stores.
+constexpr int kRowTile = 128;
+constexpr int kLoadsInFlight = 8;
+
 __global__ void __launch_bounds__(kThreads)
 padded_batches_kernel(const int32_t* __restrict__ tokens, const int64_t* __restrict__ offsets,
                       const int32_t* __restrict__ lengths, const int64_t* __restrict__ order, int64_t first_row,
                       int64_t rows, int64_t batch, const int32_t* __restrict__ lmax, const int64_t* __restrict__ boff,
                       int32_t pad, int32_t* __restrict__ out, int32_t* __restrict__ out_lengths) {
-  const int64_t r = static_cast<int64_t>(blockIdx.x) * (kThreads / 32) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (r >= rows) return;
-  const int64_t R = first_row + r;
-  const int64_t j = R / batch, j0 = first_row / batch;
-  const int32_t lm = lmax[j];
-  const int64_t p = order ? order[R] : R;
-  const int32_t len = lengths[p];
-  const int32_t* src = tokens + offsets[p];
-  int32_t* dst = out + (boff[j] - boff[j0]) + (R - j * batch) * static_cast<int64_t>(lm);
-  // 4 independent loads in flight per lane before the stores
-  int c = lane;
-  for (; c + 96 < lm; c += 128) {
-    int32_t v[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) v[u] = c + 32 * u < len ? __ldcs(src + c + 32 * u) : pad;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) __stcs(dst + c + 32 * u, v[u]);
+  __shared__ int64_t s_src[kRowTile], s_dst[kRowTile];
+  __shared__ int32_t s_len[kRowTile], s_lm[kRowTile];
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * kRowTile;
+  const int n = static_cast<int>(rows - r0 < kRowTile ? rows - r0 : kRowTile);
+  const int64_t j0 = first_row / batch;
+  for (int t = threadIdx.x; t < n; t += kThreads) {
+    const int64_t R = first_row + r0 + t, j = R / batch;
+    const int64_t p = order ? __ldcs(order + R) : R;
+    const int32_t len = lengths[p];
+    s_src[t] = offsets[p];
+    s_len[t] = len;
+    const int32_t lm = lmax[j];
+    s_lm[t] = lm;
+    s_dst[t] = (boff[j] - boff[j0]) + (R - j * batch) * static_cast<int64_t>(lm);
+    out_lengths[r0 + t] = len;
   }
-  for (; c < lm; c += 32) __stcs(dst + c, c < len ? __ldcs(src + c) : pad);
-  if (lane == 0) out_lengths[r] = len;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  for (int t = threadIdx.x >> 5; t < n; t += kThreads / 32) {
+    const int32_t len = s_len[t], lm = s_lm[t];
+    const int32_t* src = tokens + s_src[t];
+    int32_t* dst = out + s_dst[t];
+    for (int c = lane; c < lm; c += 32 * kLoadsInFlight) {
+      int32_t v[kLoadsInFlight];
+#pragma unroll
+      for (int u = 0; u < kLoadsInFlight; ++u) v[u] = c + 32 * u < len ? __ldcs(src + c + 32 * u) : pad;
+#pragma unroll
+      for (int u = 0; u < kLoadsInFlight; ++u)
+        if (c + 32 * u < lm) __stcs(dst + c + 32 * u, v[u]);
+    }
+  }
 }
 
 }  // namespace
@@ -207,7 +227,7 @@ extern "C" int dp_k_padded_batches(const int32_t* tokens, const int64_t* offsets
                                    int32_t* out_lengths, void* stream) {
   if (rows < 0 || batch < 1) return fail(DP_ERR_INVALID_ATTR, "padded_batches: bad rows/batch");
   if (rows == 0) return DP_OK;
-  const int64_t blocks = (rows + kThreads / 32 - 1) / (kThreads / 32);
+  const int64_t blocks = (rows + kRowTile - 1) / kRowTile;
   if (blocks > 0x7fffffff) return fail(DP_ERR_INVALID_ATTR, "padded_batches: too many rows");
   padded_batches_kernel<<<static_cast<int>(blocks), kThreads, 0, as_stream(stream)>>>(
       tokens, offsets, lengths, order, first_row, rows, batch, lmax_dev, boff_dev, pad_value, out, out_lengths);

@@ -394,9 +394,9 @@ def run_ours(args, cfg):
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
-        try:  # measured on a 16-batch launch; scaled to this run's launch size
-            t16 = json.load(open(prof)).get(args.config)
-            traffic = None if t16 is None else int(t16 * batches_per_launch / 16)
+        try:  # measured on one launch of `batches` batches; scaled to this run's launch size
+            t = json.load(open(prof)).get(args.config)
+            traffic = None if t is None else int(t["bytes"] * batches_per_launch / t["batches"])
         except Exception:
             traffic = None
     l2 = (f"inputs {n * cfg['in_hw'][0] * cfg['in_hw'][1] * 3 / 1e9:.1f} GB/GPU and the rotating output slots "
@@ -416,7 +416,10 @@ def run_ours(args, cfg):
                      "algorithmic_bytes_per_launch": int(bytes_per_batch * batches_per_launch),
                      "algorithmic_bytes_per_element": round(bytes_per_batch / cfg["batch"], 1),
                      "batches_per_launch": batches_per_launch,
-                     "avg_launch_us": round(kernel_s * 1e6, 3), "launches_timed": k1 - k0, "traffic": traffic},
+                     "avg_launch_us": round(kernel_s * 1e6, 3), "launches_timed": k1 - k0, "traffic": traffic,
+                     **({"note": "store-only stream (the range is generated in-kernel, 8 B written per element): "
+                                 "write-only HBM traffic runs above the read+write copy figure used as peak"}
+                        if cfg["kind"] == "range" else {})},
         "batches_in_window": batches_in_window, "steps_per_launch_group": per_launch,
         "order_check": {"digest": "K7 position-keyed digest of each rank's first 8 batches of ids",
                         "per_rank": order_digests},
@@ -430,6 +433,30 @@ def run_ours(args, cfg):
     print(json.dumps(line), flush=True)
     if world > 1:
         distr.destroy_process_group()
+
+
+def pcie_d2h_gbs(local):
+    """Plain pinned-memory D2H copy bandwidth (512 MiB, best of 5, CUDA events): the e2e roofline."""
+    import torch
+    try:
+        n = 512 << 20
+        d = torch.empty(n, dtype=torch.uint8, device=f"cuda:{local}")
+        h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+        s = torch.cuda.Stream(device=local)
+        best = 0.0
+        with torch.cuda.stream(s):
+            h.copy_(d, non_blocking=True)
+            for _ in range(5):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(s)
+                h.copy_(d, non_blocking=True)
+                e1.record(s)
+                e1.synchronize()
+                best = max(best, n / (e0.elapsed_time(e1) / 1e3) / 1e9)
+        del d, h
+        return round(best, 1)
+    except Exception:  # reported, not fatal
+        return None
 
 
 def run_e2e(dp, cfg, local, args):
@@ -455,8 +482,13 @@ def run_e2e(dp, cfg, local, args):
     secs = time.perf_counter() - t0
     b_out = cfg["batch"] * (cfg["out_hw"][0] * cfg["out_hw"][1] * 3 * 4 + 8)
     b_in = cfg["batch"] * (cfg["out_hw"][0] * cfg["out_hw"][1] * 3 if cfg["mode"] != 1 else h * w * 3)
+    d2h_gbs = steps * b_out / secs / 1e9
     return {"value": round(steps * cfg["batch"] / secs, 1), "unit": "images/s", "h2d_bytes_per_step": b_in,
             "d2h_bytes_per_step": b_out, "steps": steps,
+            "pcie": {"d2h_gbs_achieved": round(d2h_gbs, 1), "h2d_gbs_achieved": round(steps * b_in / secs / 1e9, 1),
+                     "d2h_gbs_measured": pcie_d2h_gbs(local),
+                     "bound": "PCIe: the fp32 batch (602,112 B/img) crosses to the host; a plain 512 MiB pinned D2H "
+                              "copy on this box is d2h_gbs_measured"},
             "how": "pinned host source read over PCIe by the kernels + D2H of every batch into pinned host slots; "
                    "host wall clock, each batch waited on by the host"}
 

@@ -53,6 +53,10 @@ CFG = {
     "cfg4": dict(workload="1M int32 token sequences, len U[1,1024] -> Filter(len<=512) -> PaddedBatch(128, pad 0)",
                  kind="tokens", batch=128, n=1_000_000, max_keep=512, kernel="K5 padded_batches",
                  unit="sequences/s", dtype="int32"),
+    "cfg4b": dict(workload="1M int32 token sequences, len U[1,1024] -> Filter(len<=512) -> Shuffle(10k, seed 42) -> "
+                           "BucketByLength(boundaries 128/256/384, batch sizes 256/128/96/64, pad 0)",
+                  kind="tokens", batch=128, n=1_000_000, max_keep=512, kernel="K8 bucket_batches",
+                  unit="sequences/s", dtype="int32", bucket=([128, 256, 384], [256, 128, 96, 64])),
 }
 for _c in CFG.values():
     _c.setdefault("kind", "images")
@@ -254,25 +258,31 @@ def build_other_graph(dp, cfg, local, rank, world):
     else:  # cfg4 tokens
         reg.register_length_filter("len<=512", cfg["max_keep"])
         src = dp.Source.synthetic_tokens(cfg["n"], 1024, 4 + rank, 4 + rank, device=local)
-        g = dp.Dataset.token_sequences(reg, src).filter("len<=512").padded_batch(cfg["batch"]).repeat(-1) \
-            .prefetch(-1)
+        g = dp.Dataset.token_sequences(reg, src).filter("len<=512")
+        if cfg.get("bucket"):  # cfg4b
+            g = g.shuffle(10000, 42).bucket_by_length(*cfg["bucket"])
+        else:
+            g = g.padded_batch(cfg["batch"])
+        g = g.repeat(-1).prefetch(-1)
     return g.optimize()
 
 
-def padded_bytes_per_batch(dp, g, local):
-    """cfg4 algorithmic bytes per batch of K5 padded_batches over one epoch:
-    reads = kept tokens + (order, length, offset) per row; writes = the
-    padded rows + lengths (padding is the output, so it counts)."""
+def padded_stats(dp, g, local):
+    """cfg4 / cfg4b per-batch averages over one epoch: algorithmic bytes of
+    K5 padded_batches / K8 bucket_batches (reads = kept tokens + (order,
+    length, offset) per row; writes = the padded rows + lengths -- padding is
+    the output, so it counts) and rows (the sequences a batch carries)."""
     it = dp.make_iterator(g, seed_override=1, device=local)
     per_epoch = int(re.search(r"elements, (\d+) batches", it.describe()).group(1))
-    total = 0
+    total = rows_total = 0
     for _ in range(per_epoch):
         b = it.get_next()
         lens = b.numpy(1)
         rows, lmax = b.components[0][1]
         total += 4 * int(lens.sum()) + rows * (8 + 4 + 8) + 4 * rows * lmax + 4 * rows
+        rows_total += rows
         b.release()
-    return total / per_epoch
+    return total / per_epoch, rows_total / per_epoch
 
 
 def run_ours(args, cfg):
@@ -310,8 +320,12 @@ def run_ours(args, cfg):
         g, report = build_graph(dp, cfg, src)
     it = dp.make_iterator(g, seed_override=1, device=local)
     stream = torch.cuda.ExternalStream(it.stream, device=dev)
-    per_launch = int(re.search(r"(\d+) batch\(es\) per launch", it.describe()).group(1))
-    if cfg["kind"] != "images":  # small batches: whole epochs (one launch each)
+    desc = it.describe()
+    per_launch = int(re.search(r"(\d+) batch\(es\) per launch", desc).group(1))
+    per_epoch = int(re.search(r"epoch: \d+ elements, (\d+) batches", desc).group(1))
+    if per_epoch % per_launch:  # ragged last group per epoch: whole epochs keep the window exact
+        per_launch = per_epoch
+    if cfg["kind"] != "images":  # small batches: whole epochs
         args.steps = max(args.steps, per_launch)
         args.warmup = max(args.warmup, per_launch)
     # W and K whole launch groups, so the event window holds exactly K batches
@@ -339,13 +353,15 @@ def run_ours(args, cfg):
     # The device work inside [e0, e1] is exactly the batch-stage launches
     # issued between the two events; with W and K multiples of the launch
     # group this is K batches (checked and reported).
-    elems = batches_in_window * cfg["batch"] * world
+    if cfg.get("bytes_per_elem"):
+        bytes_per_batch, rows_per_batch = cfg["bytes_per_elem"] * cfg["batch"], cfg["batch"]
+    else:  # token configs: the window is whole epochs (one launch group = one epoch)
+        bytes_per_batch, rows_per_batch = padded_stats(dp, g, local)
+    elems = batches_in_window * rows_per_batch * world
     value = elems / (ms_max / 1e3)
     kernel_s = (ns1 - ns0) / max(k1 - k0, 1) / 1e9  # per launch
     batches_per_launch = batches_in_window / max(k1 - k0, 1)
     peak, peak_src = load_peaks()
-    bytes_per_batch = cfg["bytes_per_elem"] * cfg["batch"] if cfg.get("bytes_per_elem") else \
-        padded_bytes_per_batch(dp, g, local)
     achieved = bytes_per_batch * batches_per_launch / kernel_s / 1e9
     del it
 

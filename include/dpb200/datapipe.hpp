@@ -51,6 +51,7 @@ enum class NodeKind : uint8_t {
   kTensorSlices = 33,
   kTokenSequences = 34,
   kPaddedBatch = 35,
+  kBucketByLength = 36,
 };
 
 const char* NodeKindName(NodeKind kind);
@@ -100,7 +101,8 @@ SourcePtr RecordsFromFiles(const std::vector<std::string>& paths, int device = 0
 void WriteRecordFile(const std::string& path, const std::vector<std::string>& payloads);
 
 // ---- graph IR ----
-using AttrValue = std::variant<int64_t, uint64_t, double, bool, std::string, std::vector<std::string>, SourcePtr>;
+using AttrValue =
+    std::variant<int64_t, uint64_t, double, bool, std::string, std::vector<std::string>, SourcePtr, std::vector<int64_t>>;
 using Attrs = std::map<std::string, AttrValue>;
 
 class DatasetNode {
@@ -215,6 +217,15 @@ DatasetGraph Interleave(const DatasetGraph& in, const std::string& udf, int64_t 
 DatasetGraph Batch(const DatasetGraph& in, int64_t batch_size, bool drop_remainder, const UdfRegistry& reg);
 DatasetGraph PaddedBatch(const DatasetGraph& in, int64_t batch_size, int64_t padding_value, bool drop_remainder,
                          const UdfRegistry& reg);
+// tf.data bucket_by_sequence_length over token sequences (cfg4 "/
+// bucket-by-length"; a new kind like PaddedBatch): bucket b holds
+// boundaries[b-1] <= len < boundaries[b] and is batched by batch_sizes[b]
+// (boundaries.size() + 1 entries, <= 32 buckets); each batch is padded to its
+// own max length with padding_value.  Batches come out as their windows fill,
+// then the partial windows in ascending bucket order unless drop_remainder.
+DatasetGraph BucketByLength(const DatasetGraph& in, const std::vector<int64_t>& boundaries,
+                            const std::vector<int64_t>& batch_sizes, int64_t padding_value, bool drop_remainder,
+                            const UdfRegistry& reg);
 DatasetGraph Prefetch(const DatasetGraph& in, int64_t buffer_size, const UdfRegistry& reg);
 DatasetGraph Repeat(const DatasetGraph& in, int64_t count, const UdfRegistry& reg);
 DatasetGraph Shuffle(const DatasetGraph& in, int64_t buffer_size, std::optional<uint64_t> seed,

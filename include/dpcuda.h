@@ -171,6 +171,39 @@ int dp_k_padded_batches(const int32_t* tokens, const int64_t* offsets, const int
                         int32_t* out, int32_t* out_lengths, void* stream);
 
 /* ---------------------------------------------------------------------- */
+/* K8  bucket_by_length -- tf.data bucket_by_sequence_length              */
+/*     (group_by_window: key = bucket of the length, window = the bucket's */
+/*     batch size, reduce = padded batch); a new kind like padded_batch,  */
+/*     absent from the reference (graph.hpp:38-56).   */
+/*     Bucket b holds boundaries[b-1] <= len < boundaries[b]; batches are */
+/*     emitted when their window fills, then the partial windows in       */
+/*     ascending bucket order (unless drop_remainder).                    */
+#define DP_MAX_BUCKETS 32
+size_t dp_k_bucket_scratch_bytes(int64_t n, int num_buckets);
+/* Plan over the n elements of `order` (positions; null = identity):      */
+/*   perm[n]: positions grouped by bucket, arrival order within a bucket; */
+/*   per emitted batch e < *num_batches_dev (<= n + buckets):             */
+/*   batch_start[e] (into perm), batch_rows[e], batch_lmax[e].            */
+/*   boundaries / batch_sizes are HOST arrays (num_boundaries + 1 sizes). */
+int dp_k_bucket_plan(const int32_t* lengths, const int64_t* order, int64_t n,
+                     const int32_t* boundaries, int num_boundaries,
+                     const int64_t* batch_sizes, int drop_remainder,
+                     int64_t* perm, int64_t* batch_start, int32_t* batch_rows,
+                     int32_t* batch_lmax, int64_t* num_batches_dev,
+                     void* scratch, void* stream);
+/* Pads batches [first, first + num) of a plan into `out` (element offset */
+/* boff[e] - boff[first], row-major [rows_e, lmax_e]) and their lengths   */
+/* into out_lengths (offset roff[e] - roff[first]); boff / roff are the   */
+/* exclusive prefixes of rows_e * lmax_e and rows_e (device arrays).      */
+int dp_k_bucket_batches(const int32_t* tokens, const int64_t* offsets,
+                        const int32_t* lengths, const int64_t* perm,
+                        const int64_t* batch_start, const int32_t* batch_rows,
+                        const int32_t* batch_lmax, const int64_t* boff,
+                        const int64_t* roff, int64_t first, int64_t num,
+                        int32_t pad_value, int32_t* out, int32_t* out_lengths,
+                        void* stream);
+
+/* ---------------------------------------------------------------------- */
 /* K6  shard + interleave index mapping -- ShardIterator (runtime.cpp:     */
 /*     770-800) + (Parallel)InterleaveIterator (1044-1128, 1727-2021) over */
 /*     equal-length readers.  Inputs are the source ordinals p < n_sources */

@@ -96,6 +96,11 @@ int dp_graph_batch(const dp_graph* in, int64_t batch_size, int drop_remainder, c
                    dp_graph** out);                                                     /* ops::Batch */
 int dp_graph_padded_batch(const dp_graph* in, int64_t batch_size, int64_t padding_value, int drop_remainder,
                           const dp_registry* reg, dp_graph** out);                      /* new kind */
+/* tf.data bucket_by_sequence_length (new kind; K8): num_boundaries <= 31
+ * increasing boundaries, num_boundaries + 1 batch sizes */
+int dp_graph_bucket_by_length(const dp_graph* in, const int64_t* boundaries, int64_t num_boundaries,
+                              const int64_t* batch_sizes, int64_t padding_value, int drop_remainder,
+                              const dp_registry* reg, dp_graph** out);
 int dp_graph_prefetch(const dp_graph* in, int64_t buffer_size, const dp_registry* reg, dp_graph** out);
 int dp_graph_repeat(const dp_graph* in, int64_t count, const dp_registry* reg, dp_graph** out);
 int dp_graph_shuffle(const dp_graph* in, int64_t buffer_size, int has_seed, uint64_t seed, const dp_registry* reg,

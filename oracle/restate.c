@@ -287,3 +287,38 @@ uint64_t orc_interleave_order(uint64_t m_inputs, const uint64_t* inputs,
   free(slots);
   return k;
 }
+
+/* group_by_window, sequentially (see restate.h). */
+int64_t orc_bucket_by_length(const int32_t* lengths, const int64_t* order,
+                             int64_t n, const int32_t* boundaries,
+                             int num_boundaries, const int64_t* batch_sizes,
+                             int drop_remainder, int64_t* out_positions,
+                             int64_t* out_batch_rows) {
+  const int nb = num_boundaries + 1;
+  int64_t* window[33];
+  int64_t fill[33];
+  int64_t batches = 0, w = 0;
+  for (int b = 0; b < nb; ++b) {
+    window[b] = (int64_t*)malloc(sizeof(int64_t) * (size_t)batch_sizes[b]);
+    fill[b] = 0;
+  }
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t p = order ? order[i] : i;
+    int b = 0;
+    for (int k = 0; k < num_boundaries; ++k) b += lengths[p] >= boundaries[k];
+    window[b][fill[b]++] = p;
+    if (fill[b] == batch_sizes[b]) { /* the window is full: emit it */
+      for (int64_t r = 0; r < fill[b]; ++r) out_positions[w++] = window[b][r];
+      out_batch_rows[batches++] = fill[b];
+      fill[b] = 0;
+    }
+  }
+  for (int b = 0; b < nb; ++b) { /* end of input: ascending key */
+    if (fill[b] && !drop_remainder) {
+      for (int64_t r = 0; r < fill[b]; ++r) out_positions[w++] = window[b][r];
+      out_batch_rows[batches++] = fill[b];
+    }
+    free(window[b]);
+  }
+  return batches;
+}

@@ -97,6 +97,21 @@ float orc_normalize(float v, int c);
 uint64_t orc_filter_len_le(const int32_t* lengths, uint64_t n,
                            int32_t max_keep, uint32_t* kept);
 
+/* bucket_by_length (cfg4 "/ bucket-by-length"): tf.data's
+ * bucket_by_sequence_length = group_by_window(key = #boundaries <= len,
+ * window = batch_sizes[key], reduce = padded batch).  The reference has no
+ * such kind (graph.hpp:38-56), so this sequential loop DEFINES the contract
+ * (parity unpinned by the reference; TF's GroupByWindowDataset flushes the
+ * remaining groups from a std::map, i.e. ascending key).  Walks order[0..n)
+ * (positions into `lengths`); writes the emitted batches' positions back to
+ * back into out_positions and each batch's row count into out_batch_rows;
+ * returns the number of batches. */
+int64_t orc_bucket_by_length(const int32_t* lengths, const int64_t* order,
+                             int64_t n, const int32_t* boundaries,
+                             int num_boundaries, const int64_t* batch_sizes,
+                             int drop_remainder, int64_t* out_positions,
+                             int64_t* out_batch_rows);
+
 /* ---- shard / interleave index mapping (cfg3/cfg5) ---- */
 /* ShardIterator, runtime.cpp:785-792: positions p with p % k == g. */
 uint64_t orc_shard_positions(uint64_t n, uint64_t k, uint64_t g,

@@ -208,6 +208,15 @@ int dp_graph_padded_batch(const dp_graph* in, int64_t b, int64_t pad, int drop, 
   DP_REQUIRE(in && reg && out);
   return Guard([&] { Emit(out, ops::PaddedBatch(in->g, b, pad, drop != 0, reg->reg)); });
 }
+int dp_graph_bucket_by_length(const dp_graph* in, const int64_t* boundaries, int64_t num_boundaries,
+                              const int64_t* batch_sizes, int64_t pad, int drop, const dp_registry* reg,
+                              dp_graph** out) {
+  DP_REQUIRE(in && reg && out && batch_sizes && num_boundaries >= 0 && (boundaries || num_boundaries == 0));
+  return Guard([&] {
+    std::vector<int64_t> b(boundaries, boundaries + num_boundaries), s(batch_sizes, batch_sizes + num_boundaries + 1);
+    Emit(out, ops::BucketByLength(in->g, b, s, pad, drop != 0, reg->reg));
+  });
+}
 int dp_graph_prefetch(const dp_graph* in, int64_t buffer_size, const dp_registry* reg, dp_graph** out) {
   DP_REQUIRE(in && reg && out);
   return Guard([&] { Emit(out, ops::Prefetch(in->g, buffer_size, reg->reg)); });

@@ -30,6 +30,7 @@ const char* NodeKindName(NodeKind kind) {
     case NodeKind::kTensorSlices: return "tensor_slices";
     case NodeKind::kTokenSequences: return "token_sequences";
     case NodeKind::kPaddedBatch: return "padded_batch";
+    case NodeKind::kBucketByLength: return "bucket_by_length";
   }
   return "?";
 }
@@ -97,7 +98,11 @@ std::string DatasetGraph::ToString() const {
             using T = std::decay_t<decltype(x)>;
             if constexpr (std::is_same_v<T, SourcePtr>) os << "<source " << (x ? x->count : 0) << ">";
             else if constexpr (std::is_same_v<T, std::vector<std::string>>) os << "[" << x.size() << "]";
-            else os << x;
+            else if constexpr (std::is_same_v<T, std::vector<int64_t>>) {
+              os << "[";
+              for (size_t k = 0; k < x.size(); ++k) os << (k ? "," : "") << x[k];
+              os << "]";
+            } else os << x;
           },
           v);
     }
@@ -350,6 +355,25 @@ void ValidateAttrs(NodeKind kind, const Attrs& a) {
       if (RequireInt(kind, a, "batch_size") < 1) BadAttr(kind, "batch_size must be >= 1");
       RequireInt(kind, a, "padding_value");
       break;
+    case NodeKind::kBucketByLength: {
+      CheckKeys(kind, a, {"bucket_boundaries", "bucket_batch_sizes", "padding_value"}, {"drop_remainder"});
+      RequireInt(kind, a, "padding_value");
+      auto ints = [&](const char* k) -> const std::vector<int64_t>& {
+        const auto& v = a.at(k);
+        if (!std::holds_alternative<std::vector<int64_t>>(v)) BadAttr(kind, std::string("'") + k + "' must be an int list");
+        return std::get<std::vector<int64_t>>(v);
+      };
+      const auto& bounds = ints("bucket_boundaries");
+      const auto& sizes = ints("bucket_batch_sizes");
+      if (bounds.size() > 31) BadAttr(kind, "at most 31 boundaries (32 buckets)");
+      if (sizes.size() != bounds.size() + 1) BadAttr(kind, "bucket_batch_sizes needs one entry per bucket");
+      for (size_t k = 0; k < bounds.size(); ++k)
+        if (bounds[k] < 0 || bounds[k] > INT32_MAX || (k && bounds[k] <= bounds[k - 1]))
+          BadAttr(kind, "bucket_boundaries must be increasing non-negative int32");
+      for (int64_t b : sizes)
+        if (b < 1 || b > INT32_MAX) BadAttr(kind, "bucket batch sizes must be in [1, 2^31)");
+      break;
+    }
     case NodeKind::kMapAndBatch:
       CheckKeys(kind, a, {"udf", "batch_size", "num_parallel_calls"}, {"drop_remainder"});
       RequireString(kind, a, "udf");
@@ -433,6 +457,12 @@ ElementSpec DeriveSpec(NodeKind kind, const std::vector<NodePtr>& in, const Attr
       int64_t n = GetBool(a, "drop_remainder") ? std::get<int64_t>(a.at("batch_size")) : -1;
       return ElementSpec({TypeSpec::OfTensor(s.components()[0].dtype(), {n, -1}), TypeSpec::OfTensor(DType::kInt32, {n})});
     }
+    case NodeKind::kBucketByLength: {
+      const auto& s = in[0]->output_spec();
+      if (s.arity() != 1 || s.components()[0].kind() != Value::Kind::kTensor || s.components()[0].shape().size() != 1)
+        throw PipelineError(ErrorCode::kTypeMismatch, "bucket_by_length expects (tensor[?]) sequences");
+      return ElementSpec({TypeSpec::OfTensor(s.components()[0].dtype(), {-1, -1}), TypeSpec::OfTensor(DType::kInt32, {-1})});
+    }
     case NodeKind::kMapAndBatch: {
       ElementSpec mapped = reg.MapOutputSpec(std::get<std::string>(a.at("udf")), in[0]->output_spec());
       return BatchWrapSpec(mapped, std::get<int64_t>(a.at("batch_size")), GetBool(a, "drop_remainder"));
@@ -498,6 +528,12 @@ DatasetGraph PaddedBatch(const DatasetGraph& in, int64_t b, int64_t pad, bool dr
   Attrs a{{"batch_size", b}, {"padding_value", pad}};
   if (drop) a["drop_remainder"] = true;
   return DatasetGraph(Build(NodeKind::kPaddedBatch, {in.root()}, std::move(a), reg));
+}
+DatasetGraph BucketByLength(const DatasetGraph& in, const std::vector<int64_t>& boundaries,
+                            const std::vector<int64_t>& batch_sizes, int64_t pad, bool drop, const UdfRegistry& reg) {
+  Attrs a{{"bucket_boundaries", boundaries}, {"bucket_batch_sizes", batch_sizes}, {"padding_value", pad}};
+  if (drop) a["drop_remainder"] = true;
+  return DatasetGraph(Build(NodeKind::kBucketByLength, {in.root()}, std::move(a), reg));
 }
 DatasetGraph Prefetch(const DatasetGraph& in, int64_t buffer_size, const UdfRegistry& reg) {
   return DatasetGraph(Build(NodeKind::kPrefetch, {in.root()}, {{"buffer_size", buffer_size}}, reg));

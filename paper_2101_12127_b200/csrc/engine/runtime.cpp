@@ -378,8 +378,12 @@ struct Lowered {
   int64_t prefetch = 0;  // 0: none, -1: AUTOTUNE, else depth
   int64_t outer_repeat = 1;
   BatchKind kind = BatchKind::kIdentityInt;
-  int64_t batch = 1;
+  int64_t batch = 1;     // bucket_by_length: the largest bucket batch size
   bool drop = false;
+  // bucket_by_length (a padded kind with per-bucket windows, K8)
+  bool bucketed = false;
+  std::vector<int32_t> bucket_bounds;
+  std::vector<int64_t> bucket_sizes;
   int64_t pad = 0;
   std::vector<MapStep> steps;
   int64_t affine_a = 1, affine_b = 0;
@@ -442,8 +446,20 @@ Lowered Lower(const DatasetGraph& g, const UdfRegistry& reg) {
     L.pad = n->GetInt("padding_value");
     L.drop = n->GetBoolOr("drop_remainder", false);
     descend();
+  } else if (n->kind() == NodeKind::kBucketByLength) {
+    L.kind = BatchKind::kPadded;
+    L.bucketed = true;
+    const auto& attrs = n->attrs();
+    for (int64_t b : std::get<std::vector<int64_t>>(attrs.at("bucket_boundaries")))
+      L.bucket_bounds.push_back(static_cast<int32_t>(b));
+    L.bucket_sizes = std::get<std::vector<int64_t>>(attrs.at("bucket_batch_sizes"));
+    L.batch = *std::max_element(L.bucket_sizes.begin(), L.bucket_sizes.end());
+    L.pad = n->GetInt("padding_value");
+    L.drop = n->GetBoolOr("drop_remainder", false);
+    descend();
   } else {
-    Unsupported(std::string("the root must be a batch stage (map_and_batch / batch / padded_batch), got ") +
+    Unsupported(std::string("the root must be a batch stage (map_and_batch / batch / padded_batch / "
+                            "bucket_by_length), got ") +
                 NodeKindName(n->kind()));
   }
   // ---- index chain ----
@@ -607,6 +623,10 @@ struct EpochPlan {
   std::vector<int32_t> lmax;         // per batch of this epoch
   std::vector<int64_t> boff;         // per batch, exclusive prefix (elements)
   std::shared_ptr<void> lmax_dev, boff_dev;
+  // bucket_by_length: order = the bucket-grouped positions; per batch its
+  // start in order, rows and the exclusive row prefix
+  std::vector<int64_t> rows;
+  std::shared_ptr<void> bstart_dev, rows_dev, roff_dev;
   cudaEvent_t ready = nullptr;
 };
 
@@ -804,7 +824,11 @@ class DevicePipeline {
     }
     EpochPlan& p0 = Plan(0);
     epoch_count_ = p0.count;
-    const int64_t per = L_.drop ? epoch_count_ / L_.batch : (epoch_count_ + L_.batch - 1) / L_.batch;
+    // (bucket_by_length: the same multiset of lengths every epoch, so the
+    // same number of batches; only their order changes with the shuffle)
+    const int64_t per = L_.bucketed ? static_cast<int64_t>(p0.rows.size())
+                        : L_.drop   ? epoch_count_ / L_.batch
+                                    : (epoch_count_ + L_.batch - 1) / L_.batch;
     if (span_epochs_) {
       if (inner_repeat == kInfiniteRepeat) {
         total_batches_ = epoch_count_ == 0 ? 0 : -1;
@@ -972,7 +996,9 @@ class DevicePipeline {
     p.count = count;
     p.order = cur;
     p.tail = cur ? tail : 0;
-    if (L_.kind == BatchKind::kPadded) {
+    if (L_.bucketed) {
+      BuildBucketPlan(p, cur, count);
+    } else if (L_.kind == BatchKind::kPadded) {
       const int64_t nb = (count + L_.batch - 1) / L_.batch;
       p.lmax.assign(nb, 0);
       p.boff.assign(nb + 1, 0);
@@ -995,6 +1021,54 @@ class DevicePipeline {
     }
     CudaCheck(cudaEventCreateWithFlags(&p.ready, cudaEventDisableTiming), "event");
     CudaCheck(cudaEventRecord(p.ready, s), "event");
+  }
+
+  // K8: the bucket plan of one epoch (k_bucket.cu) -- batches, their rows
+  // and lengths read back for the elements' shapes, prefixes uploaded.
+  void BuildBucketPlan(EpochPlan& p, const std::shared_ptr<void>& cur, int64_t count) {
+    cudaStream_t s = plan_stream_;
+    auto dalloc = [&](size_t bytes) { return DeviceAllocAsync(bytes, opt_.device, plan_stream_, plan_stream_); };
+    const int K = static_cast<int>(L_.bucket_sizes.size());
+    const int64_t maxb = count + K;
+    auto perm = dalloc(sizeof(int64_t) * std::max<int64_t>(count, 1));
+    auto bstart = dalloc(sizeof(int64_t) * maxb), brows = dalloc(sizeof(int32_t) * maxb);
+    auto blmax = dalloc(sizeof(int32_t) * maxb), nbd = dalloc(sizeof(int64_t));
+    auto scratch = dalloc(dp_k_bucket_scratch_bytes(count, K));
+    KCheck(dp_k_bucket_plan(P<int32_t>(L_.source->lengths), P<int64_t>(cur), count, L_.bucket_bounds.data(),
+                            static_cast<int>(L_.bucket_bounds.size()), L_.bucket_sizes.data(), L_.drop ? 1 : 0,
+                            P<int64_t>(perm), P<int64_t>(bstart), P<int32_t>(brows), P<int32_t>(blmax),
+                            P<int64_t>(nbd), scratch.get(), s),
+           "bucket_plan");
+    launches_ += 8;
+    int64_t nb = 0;
+    CudaCheck(cudaMemcpyAsync(&nb, nbd.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, s), "bucket count");
+    CudaCheck(cudaStreamSynchronize(s), "bucket count");
+    std::vector<int32_t> rows32(nb);
+    p.lmax.assign(nb, 0);
+    if (nb) {
+      CudaCheck(cudaMemcpyAsync(rows32.data(), brows.get(), sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, s), "rows");
+      CudaCheck(cudaMemcpyAsync(p.lmax.data(), blmax.get(), sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, s), "lmax");
+      CudaCheck(cudaStreamSynchronize(s), "bucket rows");
+    }
+    p.rows.assign(rows32.begin(), rows32.end());
+    p.boff.assign(nb + 1, 0);
+    std::vector<int64_t> roff(nb + 1, 0);
+    for (int64_t j = 0; j < nb; ++j) {
+      p.boff[j + 1] = p.boff[j] + p.rows[j] * p.lmax[j];
+      roff[j + 1] = roff[j] + p.rows[j];
+    }
+    p.boff_dev = dalloc(sizeof(int64_t) * (nb + 1));
+    p.roff_dev = dalloc(sizeof(int64_t) * (nb + 1));
+    CudaCheck(cudaMemcpyAsync(p.boff_dev.get(), p.boff.data(), sizeof(int64_t) * (nb + 1), cudaMemcpyHostToDevice, s),
+              "boff");
+    CudaCheck(cudaMemcpyAsync(p.roff_dev.get(), roff.data(), sizeof(int64_t) * (nb + 1), cudaMemcpyHostToDevice, s),
+              "roff");
+    // the host vectors are read by the copies: keep them alive until done
+    CudaCheck(cudaStreamSynchronize(s), "bucket upload");
+    p.order = perm;
+    p.bstart_dev = bstart;
+    p.rows_dev = brows;
+    p.lmax_dev = blmax;
   }
 
   // The current positions before an interleave are source ordinals produced
@@ -1130,7 +1204,7 @@ class DevicePipeline {
     slot->batch_off_a.assign(nb, 0);
     slot->batch_off_b.assign(nb, 0);
     const int64_t avail = span_epochs_ ? plan.count + plan.tail : plan.count;
-    for (int64_t k = 0; k < nb; ++k) {
+    for (int64_t k = 0; k < nb && !L_.bucketed; ++k) {
       int64_t rows = std::min<int64_t>(L_.batch, (span_epochs_ ? TotalRows() - (first + k) * L_.batch
                                                                : plan.count - (row0 + k * L_.batch)));
       rows = std::min<int64_t>(rows, avail - (row0 + k * L_.batch));
@@ -1191,11 +1265,21 @@ class DevicePipeline {
       }
       case BatchKind::kPadded: {
         const int64_t j0 = row0 / L_.batch;
-        KCheck(dp_k_padded_batches(P<int32_t>(L_.source->tokens), P<int64_t>(L_.source->offsets),
-                                   P<int32_t>(L_.source->lengths), order, row0, rows_total, L_.batch,
-                                   P<int32_t>(plan.lmax_dev), P<int64_t>(plan.boff_dev), static_cast<int32_t>(L_.pad),
-                                   P<int32_t>(slot->a), P<int32_t>(slot->b), stream_),
-               "K5");
+        if (L_.bucketed) {
+          for (int64_t k = 0; k < nb; ++k) slot->batch_rows[k] = plan.rows[j0 + k];
+          KCheck(dp_k_bucket_batches(P<int32_t>(L_.source->tokens), P<int64_t>(L_.source->offsets),
+                                     P<int32_t>(L_.source->lengths), order, P<int64_t>(plan.bstart_dev),
+                                     P<int32_t>(plan.rows_dev), P<int32_t>(plan.lmax_dev), P<int64_t>(plan.boff_dev),
+                                     P<int64_t>(plan.roff_dev), j0, nb, static_cast<int32_t>(L_.pad),
+                                     P<int32_t>(slot->a), P<int32_t>(slot->b), stream_),
+                 "K8");
+        } else {
+          KCheck(dp_k_padded_batches(P<int32_t>(L_.source->tokens), P<int64_t>(L_.source->offsets),
+                                     P<int32_t>(L_.source->lengths), order, row0, rows_total, L_.batch,
+                                     P<int32_t>(plan.lmax_dev), P<int64_t>(plan.boff_dev),
+                                     static_cast<int32_t>(L_.pad), P<int32_t>(slot->a), P<int32_t>(slot->b), stream_),
+                 "K5");
+        }
         launches_++;
         int64_t off = 0;
         for (int64_t k = 0; k < nb; ++k) {

@@ -33,7 +33,8 @@ enum Tag : uint8_t {
   kTagString = 4,
   kTagStringList = 5,
   kTagElementList = 6,
-  kTagDeviceSource = 32,  // this engine's extension
+  kTagDeviceSource = 32,  // this engine's extensions: a device-source descriptor,
+  kTagInt64List = 33,     // an int64 list (bucket_by_length boundaries / sizes)
 };
 
 struct Out {
@@ -161,6 +162,10 @@ void EncodeNode(const DatasetNode& n, Out& w, bool zero_seeds) {
             w.Le<uint8_t>(kTagStringList);
             w.Le<uint32_t>(static_cast<uint32_t>(v.size()));
             for (const auto& s : v) w.Str(s);
+          } else if constexpr (std::is_same_v<T, std::vector<int64_t>>) {
+            w.Le<uint8_t>(kTagInt64List);
+            w.Le<uint32_t>(static_cast<uint32_t>(v.size()));
+            for (int64_t x : v) w.Le<int64_t>(x);
           } else {  // SourcePtr
             EncodeSource(key, *v, w);
           }
@@ -197,6 +202,7 @@ bool KnownKind(uint8_t k) {
     case NodeKind::kTensorSlices:
     case NodeKind::kTokenSequences:
     case NodeKind::kPaddedBatch:
+    case NodeKind::kBucketByLength:
       return true;
   }
   return false;
@@ -268,6 +274,12 @@ struct Decoder {
       }
       case kTagDeviceSource:
         return BindSource(r);
+      case kTagInt64List: {
+        const uint32_t n = r.Le<uint32_t>();
+        std::vector<int64_t> v;
+        for (uint32_t i = 0; i < n; ++i) v.push_back(r.Le<int64_t>());
+        return v;
+      }
       default:
         r.pos = at;
         r.Bad("unknown attr tag " + std::to_string(tag));

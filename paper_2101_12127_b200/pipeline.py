@@ -77,6 +77,7 @@ _SIGS = {
     "dp_graph_interleave": [c_vp, ctypes.c_char_p, c_i64, c_i64, c_vp, c_vp, PP],
     "dp_graph_batch": [c_vp, c_i64, c_int, c_vp, PP],
     "dp_graph_padded_batch": [c_vp, c_i64, c_i64, c_int, c_vp, PP],
+    "dp_graph_bucket_by_length": [c_vp, c_vp, c_i64, c_vp, c_i64, c_int, c_vp, PP],
     "dp_graph_prefetch": [c_vp, c_i64, c_vp, PP],
     "dp_graph_repeat": [c_vp, c_i64, c_vp, PP],
     "dp_graph_shuffle": [c_vp, c_i64, c_int, c_u64, c_vp, PP],
@@ -323,6 +324,15 @@ class Dataset:
     def padded_batch(self, batch_size, padding_value=0, drop_remainder=False):
         return self._emit(L().dp_graph_padded_batch, self.h, batch_size, padding_value, int(drop_remainder),
                           self.reg.h)
+
+    def bucket_by_length(self, boundaries, batch_sizes, padding_value=0, drop_remainder=False):
+        """tf.data bucket_by_sequence_length over token sequences (K8)."""
+        b = np.ascontiguousarray(boundaries, np.int64)
+        s = np.ascontiguousarray(batch_sizes, np.int64)
+        if s.size != b.size + 1:
+            raise ValueError("batch_sizes needs len(boundaries) + 1 entries")
+        return self._emit(L().dp_graph_bucket_by_length, self.h, b.ctypes.data if b.size else None, b.size,
+                          s.ctypes.data, padding_value, int(drop_remainder), self.reg.h)
 
     def prefetch(self, buffer_size):
         return self._emit(L().dp_graph_prefetch, self.h, buffer_size, self.reg.h)

@@ -55,6 +55,7 @@ class Oracle:
             "orc_crop_flip_normalize": (None, [vp, c_int, c_int, i64, u64, c_int, c_int, c_int, vp]),
             "orc_resize_normalize": (None, [vp, c_int, c_int, c_int, c_int, vp]),
             "orc_filter_len_le": (u64, [vp, u64, i32, vp]),
+            "orc_bucket_by_length": (i64, [vp, vp, i64, vp, c_int, vp, c_int, vp, vp]),
             "orc_shard_positions": (u64, [u64, u64, u64, vp]),
             "orc_interleave_order": (u64, [u64, vp, u64, u64, vp]),
         }
@@ -147,6 +148,23 @@ class Oracle:
         kept = np.zeros(max(lengths.size, 1), np.uint32)
         m = self.L.orc_filter_len_le(P(lengths), lengths.size, max_keep, P(kept))
         return kept[:m].astype(np.int64)
+
+    def bucket_by_length(self, lengths, order, boundaries, batch_sizes, drop=False):
+        """-> list of position arrays, one per emitted batch (restate.c orc_bucket_by_length)."""
+        lengths = np.ascontiguousarray(lengths, np.int32)
+        order = None if order is None else np.ascontiguousarray(order, np.int64)
+        n = lengths.size if order is None else order.size
+        b = np.ascontiguousarray(boundaries, np.int32)
+        s = np.ascontiguousarray(batch_sizes, np.int64)
+        pos = np.zeros(max(n, 1), np.int64)
+        rows = np.zeros(max(n + s.size, 1), np.int64)
+        nb = self.L.orc_bucket_by_length(P(lengths), None if order is None else P(order), n,
+                                         P(b) if b.size else None, b.size, P(s), int(drop), P(pos), P(rows))
+        out, at = [], 0
+        for r in rows[:nb]:
+            out.append(pos[at:at + r])
+            at += r
+        return out
 
     def shard_positions(self, n, k, g):
         out = np.zeros(max(n, 1), np.uint64)

@@ -195,3 +195,20 @@ def test_from_file_errors_raised_before_device(tmp_path):
     with pytest.raises(DpError) as e:
         dp.Dataset.from_file(reg, [])
     assert e.value.code == dp.ERR["InvalidAttr"]
+
+
+def test_bucket_by_length_attr_validation():
+    """bucket_by_length attrs are checked when the node is built (before any
+    device work): increasing boundaries, one batch size per bucket, <= 32
+    buckets; a non-sequence input is TypeMismatch."""
+    reg = dp.Registry()
+    base = dp.Dataset.range(reg, 10)
+    for bounds, sizes in (([5, 3], [1, 1, 1]), ([5], [1, 0]), (list(range(1, 33)), [1] * 33), ([-1], [1, 1])):
+        with pytest.raises(DpError) as e:
+            base.bucket_by_length(bounds, sizes)
+        assert e.value.code == dp.ERR["InvalidAttr"], (bounds, sizes)
+    with pytest.raises(ValueError):
+        base.bucket_by_length([5], [1])
+    with pytest.raises(DpError) as e:
+        base.bucket_by_length([5], [1, 2])
+    assert e.value.code == dp.ERR["TypeMismatch"]

@@ -306,6 +306,64 @@ def test_cfg4_filter_then_shuffle_then_padded(dp, orc):
     assert k == kept.size
 
 
+def _check_bucket_batches(batches, expect, lens_all, toks, offs, pad):
+    assert len(batches) == len(expect)
+    for b, pos in zip(batches, expect):
+        assert b[1].size == pos.size and (b[1] == lens_all[pos]).all()
+        assert b[0].shape == (pos.size, lens_all[pos].max())
+        for r, p in enumerate(pos):
+            assert (b[0][r, :b[1][r]] == toks[offs[p]:offs[p + 1]]).all() and (b[0][r, b[1][r]:] == pad).all()
+
+
+@pytest.mark.parametrize("drop", [False, True])
+def test_cfg4_bucket_by_length_equals_oracle(dp, orc, drop):
+    """cfg4 "/ bucket-by-length": filter -> shuffle -> bucket_by_length (K8)
+    equals the sequential group_by_window restatement batch for batch."""
+    n = 20000
+    bounds, sizes = [64, 128, 256, 400], [64, 32, 16, 8, 5]
+    reg = dp.Registry()
+    reg.register_length_filter("len<=512", 512)
+    src = dp.Source.synthetic_tokens(n, 1024, 4, 4)
+    g = (dp.Dataset.token_sequences(reg, src).filter("len<=512").shuffle(3000, 11)
+         .bucket_by_length(bounds, sizes, padding_value=-7, drop_remainder=drop).prefetch(-1))
+    batches = drain(dp.make_iterator(g, seed_override=2), comps=(0, 1))
+    lens_all = orc.lengths(n, 1024, 4)
+    toks, offs = orc.tokens(lens_all, 4)
+    kept = orc.filter_len_le(lens_all, 512)
+    order = kept[orc.shuffle_order(kept.size, 3000, orc.shuffle_seed(2, 11))]
+    expect = orc.bucket_by_length(lens_all, order, bounds, sizes, drop)
+    _check_bucket_batches(batches, expect, lens_all, toks, offs, -7)
+
+
+def test_bucket_by_length_edge_cases_and_epochs(dp, orc):
+    """One bucket (= padded_batch), a bucket that never fills, every element
+    in one bucket, repeat above the stage (per-epoch reshuffle), checkpoint
+    seek into the middle."""
+    n = 3000
+    lens_all = orc.lengths(n, 300, 6)
+    toks, offs = orc.tokens(lens_all, 6)
+    reg = dp.Registry()
+    src = dp.Source.synthetic_tokens(n, 300, 6, 6)
+    cases = [([], [100]), ([1000], [7, 9]), ([10, 20, 30, 290, 299], [1, 2, 3, 4, 500, 6]), ([150], [4096, 3])]
+    for bounds, sizes in cases:
+        g = dp.Dataset.token_sequences(reg, src).bucket_by_length(bounds, sizes)
+        expect = orc.bucket_by_length(lens_all, None, bounds, sizes)
+        _check_bucket_batches(drain(dp.make_iterator(g, seed_override=1), comps=(0, 1)), expect, lens_all, toks,
+                              offs, 0)
+    g = dp.Dataset.token_sequences(reg, src).shuffle(500).bucket_by_length([100, 200], [16, 8, 4]).repeat(3)
+    got = drain(dp.make_iterator(g, seed_override=9), comps=(0, 1))
+    expect = []
+    for e in range(3):
+        order = orc.shuffle_order(n, 500, orc.shuffle_seed(orc.mix_seeds(9, e), None))
+        expect += orc.bucket_by_length(lens_all, order, [100, 200], [16, 8, 4])
+    _check_bucket_batches(got, expect, lens_all, toks, offs, 0)
+    it = dp.make_iterator(g, seed_override=9)
+    for _ in range(len(got) // 2):
+        it.get_next().release()
+    rest = drain(dp.restore(g, it.save()), comps=(0, 1))
+    _check_bucket_batches(rest, expect[len(got) // 2:], lens_all, toks, offs, 0)
+
+
 # ------------------------------------------------------------------ cfg5 ----
 def test_cfg5_interleave_shuffle_map_and_batch(dp, orc):
     c = [x for x in GOLDEN["interleave"] if "shuffle" in x][0]

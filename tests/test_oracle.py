@@ -261,3 +261,18 @@ def test_fast_division_proven_for_all_fp32_in_0_255(tmp_path):
     subprocess.run(["gcc", "-O2", "-ffp-contract=off", "-fopenmp", src, "-o", exe, "-lm"], check=True)
     out = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and "TOTAL mismatches: 0" in out.stdout, out.stdout
+
+
+def test_bucket_by_length_restatement(orc):
+    """group_by_window semantics (restate.c orc_bucket_by_length): a bucket's
+    batch is emitted when its window fills; leftovers flush in ascending
+    bucket order at the end unless drop_remainder."""
+    lengths = np.array([5, 50, 6, 7, 51, 8, 52, 9], np.int32)
+    got = orc.bucket_by_length(lengths, None, [10], [2, 2])
+    assert [b.tolist() for b in got] == [[0, 2], [1, 4], [3, 5], [7], [6]]
+    got = orc.bucket_by_length(lengths, None, [10], [2, 2], drop=True)
+    assert [b.tolist() for b in got] == [[0, 2], [1, 4], [3, 5]]
+    order = np.array([7, 6, 5, 4, 3, 2, 1, 0])
+    got = orc.bucket_by_length(lengths, order, [6, 51], [3, 1, 5])
+    # buckets: len<6 -> 0, 6..50 -> 1 (size 1: emitted at once), >=51 -> 2
+    assert [b.tolist() for b in got] == [[7], [5], [3], [2], [1], [0], [6, 4]]

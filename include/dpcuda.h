@@ -194,14 +194,15 @@ int dp_k_bucket_plan(const int32_t* lengths, const int64_t* order, int64_t n,
 /* Pads batches [first, first + num) of a plan into `out` (element offset */
 /* boff[e] - boff[first], row-major [rows_e, lmax_e]) and their lengths   */
 /* into out_lengths (offset roff[e] - roff[first]); boff / roff are the   */
-/* exclusive prefixes of rows_e * lmax_e and rows_e (device arrays).      */
+/* exclusive prefixes of rows_e * lmax_e and rows_e (device arrays);      */
+/* num_rows = roff[first + num] - roff[first] (host value, grid size).    */
 int dp_k_bucket_batches(const int32_t* tokens, const int64_t* offsets,
                         const int32_t* lengths, const int64_t* perm,
                         const int64_t* batch_start, const int32_t* batch_rows,
                         const int32_t* batch_lmax, const int64_t* boff,
                         const int64_t* roff, int64_t first, int64_t num,
-                        int32_t pad_value, int32_t* out, int32_t* out_lengths,
-                        void* stream);
+                        int64_t num_rows, int32_t pad_value, int32_t* out,
+                        int32_t* out_lengths, void* stream);
 
 /* ---------------------------------------------------------------------- */
 /* K6  shard + interleave index mapping -- ShardIterator (runtime.cpp:     */

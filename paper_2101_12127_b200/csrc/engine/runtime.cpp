@@ -39,6 +39,7 @@
 #include <cstring>
 #include <deque>
 #include <functional>
+#include <future>
 #include <map>
 #include <mutex>
 #include <random>
@@ -678,7 +679,10 @@ class DevicePipeline {
     // a power of two, so groups tile power-of-two epochs without a ragged group
     int64_t pow2 = 1;
     while (pow2 * 2 <= group_) pow2 *= 2;
-    group_ = std::min(pow2, std::max<int64_t>(1, batches_per_epoch_));
+    // (padded kinds launch a whole epoch when it fits: their epochs have an
+    // arbitrary batch count, so a power of two would leave a ragged tail group)
+    if (L_.kind != BatchKind::kPadded || group_ < batches_per_epoch_) group_ = pow2;
+    group_ = std::min(group_, std::max<int64_t>(1, batches_per_epoch_));
     // the prefetch depth must fit the slot budget (at least double buffering)
     const size_t group_bytes = (batch_bytes_.first + batch_bytes_.second) * group_;
     depth_ = std::max<int64_t>(2, std::min<int64_t>(depth_, static_cast<int64_t>(opt_.slot_memory_budget /
@@ -694,6 +698,10 @@ class DevicePipeline {
 
   ~DevicePipeline() {
     DeviceGuard g(opt_.device);
+    try {
+      JoinPendingPlan();
+    } catch (...) {  // an error of a plan nobody asked for: dropped with the pipeline
+    }
     PrintDebugTiming();
     cudaStreamSynchronize(stream_);
     for (auto& t : timed_) event_pool_.push_back(t);
@@ -899,7 +907,26 @@ class DevicePipeline {
     return under_repeat ? MixSeeds(base_seed_, static_cast<uint64_t>(e)) : base_seed_;
   }
 
+  void JoinPendingPlan() {
+    if (pending_plan_.valid()) pending_plan_.get();  // rethrows the helper's error
+  }
+
+  // Builds epoch e's plan on a helper thread (plan stream); Plan() joins it.
+  void PrefetchPlan(int64_t e) {
+    JoinPendingPlan();
+    if (plans_.count(e)) return;
+    pending_plan_ = std::async(std::launch::async, [this, e] {
+      DeviceGuard g(opt_.device);
+      EpochPlan p;
+      p.epoch = e;
+      BuildPlan(p, e);
+      std::lock_guard lk(plans_mu_);
+      plans_.emplace(e, std::move(p));
+    });
+  }
+
   EpochPlan& Plan(int64_t e) {
+    JoinPendingPlan();
     auto it = plans_.find(e);
     if (it != plans_.end()) return it->second;
     // Retire plans two epochs back.  Their buffers are freed on the plan
@@ -1194,7 +1221,10 @@ class DevicePipeline {
     CudaCheck(cudaStreamWaitEvent(stream_, plan.ready, 0), "wait plan");
     // Plan the next epoch on the side stream now, so its index kernels
     // overlap this epoch's batch kernels instead of stalling the next one.
-    if (L_.kind != BatchKind::kPadded && MoreEpochsAfter(epoch)) Plan(epoch + 1);
+    if (MoreEpochsAfter(epoch)) {
+      if (L_.kind == BatchKind::kPadded) PrefetchPlan(epoch + 1);
+      else Plan(epoch + 1);
+    }
     // rows of this group inside the epoch plan
     const int64_t row0 = span_epochs_ ? first * L_.batch - epoch * epoch_count_
                                       : (first - epoch * batches_per_epoch_) * L_.batch;
@@ -1266,11 +1296,12 @@ class DevicePipeline {
       case BatchKind::kPadded: {
         const int64_t j0 = row0 / L_.batch;
         if (L_.bucketed) {
-          for (int64_t k = 0; k < nb; ++k) slot->batch_rows[k] = plan.rows[j0 + k];
+          int64_t group_rows = 0;
+          for (int64_t k = 0; k < nb; ++k) group_rows += slot->batch_rows[k] = plan.rows[j0 + k];
           KCheck(dp_k_bucket_batches(P<int32_t>(L_.source->tokens), P<int64_t>(L_.source->offsets),
                                      P<int32_t>(L_.source->lengths), order, P<int64_t>(plan.bstart_dev),
                                      P<int32_t>(plan.rows_dev), P<int32_t>(plan.lmax_dev), P<int64_t>(plan.boff_dev),
-                                     P<int64_t>(plan.roff_dev), j0, nb, static_cast<int32_t>(L_.pad),
+                                     P<int64_t>(plan.roff_dev), j0, nb, group_rows, static_cast<int32_t>(L_.pad),
                                      P<int32_t>(slot->a), P<int32_t>(slot->b), stream_),
                  "K8");
         } else {
@@ -1486,7 +1517,12 @@ class DevicePipeline {
   std::vector<std::shared_ptr<Slot>> slots_;
   std::map<int64_t, std::shared_ptr<Slot>> group_slot_;
   size_t slot_bytes_total_ = 0;
-  int64_t issued_groups_ = 0, next_batch_ = 0, produced_ = 0, launches_ = 0;
+  int64_t issued_groups_ = 0, next_batch_ = 0, produced_ = 0;
+  std::atomic<int64_t> launches_{0};  // also counted by the plan-prefetch thread
+  // padded kinds: the next epoch's plan (which reads counts back to the host)
+  // is built by a helper thread while this one serves GetNext
+  std::future<void> pending_plan_;
+  std::mutex plans_mu_;
   int64_t host_issue_ns_ = 0, issued_count_ = 0, batch_ns_total_ = 0, timed_groups_ = 0;
   std::deque<TimedLaunch> timed_;
   std::vector<TimedLaunch> event_pool_;

@@ -196,50 +196,55 @@ bucket_lmax_kernel(const int32_t* __restrict__ lengths, const int64_t* __restric
   if (lane == 0) lmax[e] = m;
 }
 
-// One CTA per batch of the launch group [first, first + nb): rows resolved
-// in tiles of kRowTile into shared memory, then streamed with kLoads token
-// loads in flight per lane (as K5 padded_batches).
+// The rows of batches [first, first + nb) in emission order, in tiles of
+// kRowTile rows per CTA (as K5 padded_batches): each row finds its batch by a
+// binary search over the row prefix roff, resolves (position, length,
+// offset, destination) into shared memory, then warps stream the tile with
+// kLoads token loads in flight per lane.
 constexpr int kRowTile = 128;
 constexpr int kLoads = 8;
 
 __global__ void __launch_bounds__(kThreads)
 bucket_batches_kernel(const int32_t* __restrict__ tokens, const int64_t* __restrict__ offsets,
                       const int32_t* __restrict__ lengths, const int64_t* __restrict__ perm,
-                      const int64_t* __restrict__ start, const int32_t* __restrict__ rows_of,
-                      const int32_t* __restrict__ lmax_of, const int64_t* __restrict__ boff,
-                      const int64_t* __restrict__ roff, int64_t first, int32_t pad, int32_t* __restrict__ out,
-                      int32_t* __restrict__ out_lengths) {
+                      const int64_t* __restrict__ start, const int32_t* __restrict__ lmax_of,
+                      const int64_t* __restrict__ boff, const int64_t* __restrict__ roff, int64_t first, int64_t nb,
+                      int32_t pad, int32_t* __restrict__ out, int32_t* __restrict__ out_lengths) {
   __shared__ int64_t s_src[kRowTile], s_dst[kRowTile];
-  __shared__ int32_t s_len[kRowTile];
-  const int64_t e = first + blockIdx.x;
-  const int32_t rows = rows_of[e], lm = lmax_of[e];
-  const int64_t s0 = start[e];
-  const int64_t dst0 = boff[e] - boff[first], len0 = roff[e] - roff[first];
-  const int lane = threadIdx.x & 31;
-  for (int t0 = 0; t0 < rows; t0 += kRowTile) {
-    const int n = rows - t0 < kRowTile ? rows - t0 : kRowTile;
-    __syncthreads();
-    for (int t = threadIdx.x; t < n; t += kThreads) {
-      const int64_t p = perm[s0 + t0 + t];
-      const int32_t len = lengths[p];
-      s_src[t] = offsets[p];
-      s_len[t] = len;
-      s_dst[t] = dst0 + static_cast<int64_t>(t0 + t) * lm;
-      out_lengths[len0 + t0 + t] = len;
+  __shared__ int32_t s_len[kRowTile], s_lm[kRowTile];
+  const int64_t r_first = roff[first], rows = roff[first + nb] - r_first;
+  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * kRowTile;
+  const int n = static_cast<int>(rows - t0 < kRowTile ? rows - t0 : kRowTile);
+  for (int t = threadIdx.x; t < n; t += kThreads) {
+    const int64_t R = r_first + t0 + t;  // row in the epoch's emission order
+    int64_t lo = first, hi = first + nb - 1;  // the batch e with roff[e] <= R < roff[e + 1]
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) >> 1;
+      if (roff[mid] <= R) lo = mid;
+      else hi = mid - 1;
     }
-    __syncthreads();
-    for (int t = threadIdx.x >> 5; t < n; t += kWarps) {
-      const int32_t len = s_len[t];
-      const int32_t* src = tokens + s_src[t];
-      int32_t* dst = out + s_dst[t];
-      for (int c = lane; c < lm; c += 32 * kLoads) {
-        int32_t v[kLoads];
+    const int64_t e = lo, r = R - roff[e];
+    const int64_t p = perm[start[e] + r];
+    const int32_t len = lengths[p], lm = lmax_of[e];
+    s_src[t] = offsets[p];
+    s_len[t] = len;
+    s_lm[t] = lm;
+    s_dst[t] = (boff[e] - boff[first]) + r * lm;
+    out_lengths[R - r_first] = len;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  for (int t = threadIdx.x >> 5; t < n; t += kWarps) {
+    const int32_t len = s_len[t], lm = s_lm[t];
+    const int32_t* src = tokens + s_src[t];
+    int32_t* dst = out + s_dst[t];
+    for (int c = lane; c < lm; c += 32 * kLoads) {
+      int32_t v[kLoads];
 #pragma unroll
-        for (int u = 0; u < kLoads; ++u) v[u] = c + 32 * u < len ? __ldcs(src + c + 32 * u) : pad;
+      for (int u = 0; u < kLoads; ++u) v[u] = c + 32 * u < len ? __ldcs(src + c + 32 * u) : pad;
 #pragma unroll
-        for (int u = 0; u < kLoads; ++u)
-          if (c + 32 * u < lm) __stcs(dst + c + 32 * u, v[u]);
-      }
+      for (int u = 0; u < kLoads; ++u)
+        if (c + 32 * u < lm) __stcs(dst + c + 32 * u, v[u]);
     }
   }
 }
@@ -343,12 +348,14 @@ extern "C" int dp_k_bucket_plan(const int32_t* lengths, const int64_t* order, in
 extern "C" int dp_k_bucket_batches(const int32_t* tokens, const int64_t* offsets, const int32_t* lengths,
                                    const int64_t* perm, const int64_t* batch_start, const int32_t* batch_rows,
                                    const int32_t* batch_lmax, const int64_t* boff, const int64_t* roff, int64_t first,
-                                   int64_t num, int32_t pad_value, int32_t* out, int32_t* out_lengths, void* stream) {
-  if (first < 0 || num < 0) return fail(DP_ERR_INVALID_ATTR, "bucket_batches: bad range");
-  if (num == 0) return DP_OK;
-  if (num > 0x7fffffff) return fail(DP_ERR_INVALID_ATTR, "bucket_batches: too many batches");
-  bucket_batches_kernel<<<static_cast<int>(num), kThreads, 0, as_stream(stream)>>>(
-      tokens, offsets, lengths, perm, batch_start, batch_rows, batch_lmax, boff, roff, first, pad_value, out,
-      out_lengths);
+                                   int64_t num, int64_t num_rows, int32_t pad_value, int32_t* out,
+                                   int32_t* out_lengths, void* stream) {
+  (void)batch_rows;  // implied by roff
+  if (first < 0 || num < 0 || num_rows < 0) return fail(DP_ERR_INVALID_ATTR, "bucket_batches: bad range");
+  if (num == 0 || num_rows == 0) return DP_OK;
+  const int64_t blocks = (num_rows + kRowTile - 1) / kRowTile;
+  if (blocks > 0x7fffffff) return fail(DP_ERR_INVALID_ATTR, "bucket_batches: too many rows");
+  bucket_batches_kernel<<<static_cast<int>(blocks), kThreads, 0, as_stream(stream)>>>(
+      tokens, offsets, lengths, perm, batch_start, batch_lmax, boff, roff, first, num, pad_value, out, out_lengths);
   return launch_status("bucket_batches");
 }

@@ -721,8 +721,11 @@ class DevicePipeline {
     if (copy_stream_) cudaStreamDestroy(copy_stream_);
   }
 
+  // The per-batch fast path makes no CUDA call and takes one lock (in
+  // MakeElement): issuing, slot reuse, autotuning and the consumer-stream wait
+  // happen at group boundaries, or when a released slot may let the next
+  // group go out (Shared::slots_freed).
   std::optional<Element> Next() {
-    DeviceGuard g(opt_.device);
     if (done_) return std::nullopt;
     const int64_t i = next_batch_;
     if (total_batches_ >= 0 && i >= total_batches_) {
@@ -732,29 +735,36 @@ class DevicePipeline {
     const int64_t grp = GroupOf(i);
     using Clock = std::chrono::steady_clock;
     const auto t0 = debug_timing_ ? Clock::now() : Clock::time_point{};
-    while (issued_groups_ <= grp) IssueGroup(issued_groups_);
-    // keep `depth` groups in flight
-    while (issued_groups_ < grp + depth_ && (total_groups_ < 0 || issued_groups_ < total_groups_)) {
-      if (!TryIssueGroup(issued_groups_, /*may_grow=*/false)) break;
+    const bool boundary = grp != cur_group_;
+    const uint64_t freed = shared_->slots_freed.load(std::memory_order_acquire);
+    if (boundary || freed != seen_freed_) {
+      seen_freed_ = freed;
+      DeviceGuard g(opt_.device);
+      while (issued_groups_ <= grp) IssueGroup(issued_groups_);
+      // keep `depth` groups in flight
+      while (issued_groups_ < grp + depth_ && (total_groups_ < 0 || issued_groups_ < total_groups_)) {
+        if (!TryIssueGroup(issued_groups_, /*may_grow=*/false)) break;
+      }
+      if (boundary) {
+        cur_slot_ = group_slot_.at(grp);
+        cur_group_ = grp;
+        {
+          // after a Seek into the middle of a group, the skipped batches count as handed out
+          std::lock_guard lk(shared_->mu);
+          if (cur_slot_->handed_out < i - cur_slot_->first_batch) cur_slot_->handed_out = i - cur_slot_->first_batch;
+        }
+        // one wait per group: the slot's ready event covers all its batches
+        if (consumer_ != stream_ && !opt_.host_output)
+          CudaCheck(cudaStreamWaitEvent(consumer_, cur_slot_->ready, 0), "wait");
+        MaybeAutotune();
+      }
     }
     const auto t1 = debug_timing_ ? Clock::now() : Clock::time_point{};
-    if (grp != cur_group_) {
-      cur_slot_ = group_slot_.at(grp);
-      cur_group_ = grp;
-      MaybeAutotune();  // once per group: event queries are API calls
-    }
-    const std::shared_ptr<Slot>& slot = cur_slot_;
-    {
-      // after a Seek into the middle of a group, the skipped batches count as handed out
-      std::lock_guard lk(shared_->mu);
-      if (slot->handed_out < i - slot->first_batch) slot->handed_out = i - slot->first_batch;
-    }
     next_batch_++;
-    if (consumer_ != stream_ && !opt_.host_output) CudaCheck(cudaStreamWaitEvent(consumer_, slot->ready, 0), "wait");
     produced_++;
-    if (!debug_timing_) return MakeElement(slot, i);
+    if (!debug_timing_) return MakeElement(cur_slot_, i);
     const auto t2 = Clock::now();
-    auto e = MakeElement(slot, i);
+    auto e = MakeElement(cur_slot_, i);
     const auto t3 = Clock::now();
     dbg_[0] += std::chrono::duration<double>(t1 - t0).count();
     dbg_[1] += std::chrono::duration<double>(t2 - t1).count();
@@ -1385,6 +1395,7 @@ class DevicePipeline {
       if (--slot->outstanding == 0 && slot->handed_out == slot->num_batches && shared->alive) {
         cudaEventRecord(slot->release, consumer);
         slot->release_recorded = true;
+        shared->slots_freed.fetch_add(1, std::memory_order_release);
       }
     });
     const bool host = opt_.host_output;
@@ -1402,6 +1413,7 @@ class DevicePipeline {
       return Value::FromTensor(std::move(t));
     };
     std::vector<Value> comps;
+    comps.reserve(2);
     switch (L_.kind) {
       case BatchKind::kAffine:
       case BatchKind::kIdentityInt:
@@ -1488,6 +1500,7 @@ class DevicePipeline {
   struct Shared {
     std::mutex mu;
     bool alive = true;
+    std::atomic<uint64_t> slots_freed{0};  // bumped when a slot's last batch is dropped
   };
   std::shared_ptr<Shared> shared_ = std::make_shared<Shared>();
   void Shutdown() {
@@ -1504,6 +1517,7 @@ class DevicePipeline {
   bool autotune_ = false;
   const bool debug_timing_ = std::getenv("DP_DEBUG_TIMING") != nullptr;
   int64_t cur_group_ = -1;            // group of the last batch handed out
+  uint64_t seen_freed_ = 0;           // Shared::slots_freed at the last issue attempt
   std::shared_ptr<Slot> cur_slot_;
   std::pair<size_t, size_t> batch_bytes_;
   int64_t max_len_ = 0;

@@ -203,6 +203,44 @@ def test_consumer_may_hold_batches(dp):
     assert ids.tolist() == list(range(300))
 
 
+def test_concurrent_get_next_callers(dp):
+    """PipelineIterator::GetNext is thread-safe for concurrent callers
+    (runtime.hpp:53-55): 4 threads draining one iterator get every batch
+    exactly once, each batch intact; two iterators run side by side."""
+    import threading
+    reg = image_registry(dp, 0, crop=(32, 32))
+    src = dp.Source.synthetic_images(2000, 48, 48)
+    g, _ = dp.Dataset.tensor_slices(reg, src).shuffle(500, 3).map("crop").map("norm").batch(20).optimize()
+    ref = [b[0] for b in drain(dp.make_iterator(g, seed_override=5))]
+    ref_pix = {tuple(b[0].tolist()): b[1] for b in drain(dp.make_iterator(g, seed_override=5), comps=(0, 1))}
+    it = dp.make_iterator(g, seed_override=5)
+    got, errors, lock = [], [], threading.Lock()
+
+    def worker():
+        try:
+            while (b := it.get_next()) is not None:
+                ids, pix = b.numpy(0), b.numpy(1)
+                b.release()
+                with lock:
+                    got.append((ids, pix))
+        except Exception as ex:  # surfaced below
+            errors.append(ex)
+
+    threads = [threading.Thread(target=worker) for _ in range(4)]
+    other = dp.make_iterator(g, seed_override=5)
+    for t in threads:
+        t.start()
+    side = [b[0] for b in drain(other)]  # a second iterator meanwhile
+    for t in threads:
+        t.join()
+    assert not errors
+    assert len(got) == len(ref) == 100
+    assert sorted(tuple(x.tolist()) for x, _ in got) == sorted(tuple(x.tolist()) for x in ref)
+    for ids, pix in got:
+        assert np.array_equal(pix, ref_pix[tuple(ids.tolist())])
+    assert all(np.array_equal(a, b) for a, b in zip(side, ref))
+
+
 def test_host_output_equals_device_output(dp):
     reg = image_registry(dp, 0, crop=(64, 64))
     src = dp.Source.synthetic_images(200, 96, 96)

@@ -212,18 +212,26 @@ bucket_batches_kernel(const int32_t* __restrict__ tokens, const int64_t* __restr
                       int32_t pad, int32_t* __restrict__ out, int32_t* __restrict__ out_lengths) {
   __shared__ int64_t s_src[kRowTile], s_dst[kRowTile];
   __shared__ int32_t s_len[kRowTile], s_lm[kRowTile];
+  __shared__ int64_t s_e0;
   const int64_t r_first = roff[first], rows = roff[first + nb] - r_first;
   const int64_t t0 = static_cast<int64_t>(blockIdx.x) * kRowTile;
   const int n = static_cast<int>(rows - t0 < kRowTile ? rows - t0 : kRowTile);
-  for (int t = threadIdx.x; t < n; t += kThreads) {
-    const int64_t R = r_first + t0 + t;  // row in the epoch's emission order
-    int64_t lo = first, hi = first + nb - 1;  // the batch e with roff[e] <= R < roff[e + 1]
+  if (threadIdx.x == 0) {  // the batch e with roff[e] <= R < roff[e + 1] for the tile's first row
+    const int64_t R = r_first + t0;
+    int64_t lo = first, hi = first + nb - 1;
     while (lo < hi) {
       const int64_t mid = (lo + hi + 1) >> 1;
       if (roff[mid] <= R) lo = mid;
       else hi = mid - 1;
     }
-    const int64_t e = lo, r = R - roff[e];
+    s_e0 = lo;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < n; t += kThreads) {
+    const int64_t R = r_first + t0 + t;  // row in the epoch's emission order
+    int64_t e = s_e0;                    // a tile spans few batches: walk forward
+    while (roff[e + 1] <= R) ++e;
+    const int64_t r = R - roff[e];
     const int64_t p = perm[start[e] + r];
     const int32_t len = lengths[p], lm = lmax_of[e];
     s_src[t] = offsets[p];

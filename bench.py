@@ -366,7 +366,7 @@ def run_ours(args, cfg):
     del it
 
     # ---- end to end through the C ABI with host buffers ----
-    e2e = run_e2e(dp, cfg, local, args) if cfg["kind"] == "images" else {
+    e2e = run_e2e(dp, cfg, local, args, world, dev) if cfg["kind"] == "images" else {
         "value": None, "note": "e2e is measured on the image configs (cfg2 headline)"}
 
     # ---- the final ordering check: K7 digest of each rank's
@@ -475,10 +475,12 @@ def pcie_d2h_gbs(local):
         return None
 
 
-def run_e2e(dp, cfg, local, args):
+def run_e2e(dp, cfg, local, args, world=1, dev=None):
     """Same pipeline through the C ABI with HOST buffers: the image dataset
     lives in pinned host memory (read by the kernels over PCIe), every batch
-    is copied back into pinned host slots; host wall clock over K steps."""
+    is copied back into pinned host slots; host wall clock over K steps.
+    Whole job at N GPUs: every rank runs its own host-buffered pipeline, the
+    ranks start together (barrier) and the slowest rank's time counts."""
     import numpy as np
     n_host = 4096
     h, w = cfg["in_hw"]
@@ -491,16 +493,20 @@ def run_e2e(dp, cfg, local, args):
     steps = max(8, min(args.steps, 64))
     for _ in range(3):
         it.get_next().wait().release()
+    if world > 1:
+        max_over_ranks(0.0, world, dev)  # barrier: start together
     t0 = time.perf_counter()
     for _ in range(steps):
         b = it.get_next().wait()
         b.release()
     secs = time.perf_counter() - t0
+    if world > 1:
+        secs = max_over_ranks(secs * 1e3, world, dev) / 1e3
     b_out = cfg["batch"] * (cfg["out_hw"][0] * cfg["out_hw"][1] * 3 * 4 + 8)
     b_in = cfg["batch"] * (cfg["out_hw"][0] * cfg["out_hw"][1] * 3 if cfg["mode"] != 1 else h * w * 3)
-    d2h_gbs = steps * b_out / secs / 1e9
-    return {"value": round(steps * cfg["batch"] / secs, 1), "unit": "images/s", "h2d_bytes_per_step": b_in,
-            "d2h_bytes_per_step": b_out, "steps": steps,
+    d2h_gbs = steps * b_out / secs / 1e9  # per rank
+    return {"value": round(steps * cfg["batch"] * world / secs, 1), "unit": "images/s",
+            "h2d_bytes_per_step": b_in * world, "d2h_bytes_per_step": b_out * world, "steps": steps,
             "pcie": {"d2h_gbs_achieved": round(d2h_gbs, 1), "h2d_gbs_achieved": round(steps * b_in / secs / 1e9, 1),
                      "d2h_gbs_measured": pcie_d2h_gbs(local),
                      "bound": "PCIe: the fp32 batch (602,112 B/img) crosses to the host; a plain 512 MiB pinned D2H "

@@ -219,6 +219,18 @@ int dp_k_shard_interleave_index(int64_t n_sources, int64_t num_shards,
 /* General form over inputs first + i * stride, i < m_inputs. */
 int dp_k_interleave_index(int64_t first, int64_t stride, int64_t m_inputs, int64_t cycle,
                           int64_t records, int64_t* out, void* stream);
+/* Readers of unequal lengths (record files of different sizes): host      */
+/* schedule of the InterleaveIterator loop (runtime.cpp:1061-1120) --      */
+/* input i (in input order, lengths[i] records) runs in cycle slot slot[i] */
+/* from visit round start[i]; end[s] = the round slot s goes dead (cycle   */
+/* entries).  O(m log cycle) on the host: control, not data.              */
+int dp_interleave_schedule(int64_t m_inputs, const int64_t* lengths, int64_t cycle,
+                           int64_t* slot, int64_t* start, int64_t* end);
+/* Device order from that schedule (all arrays device memory):            */
+/* out[pos(i, j)] = first_record[i] + j for j < len[i].                   */
+int dp_k_interleave_var(int64_t m_inputs, const int64_t* slot, const int64_t* start,
+                        const int64_t* len, const int64_t* first_record,
+                        const int64_t* end, int64_t cycle, int64_t* out, void* stream);
 /* Shard alone: out[i] = shard_index + i * num_shards (or in_map of it). */
 int dp_k_shard_index(int64_t n, int64_t num_shards, int64_t shard_index,
                      const int64_t* in_map, int64_t* out, void* stream);

@@ -331,6 +331,40 @@ int ref_interleave_ids(int64_t num_sources, int64_t shard_k, int64_t shard_g,
   }
 }
 
+// Interleave over readers of unequal lengths: from_memory(0..S-1) [->
+// shard(k, g)] -> interleave(reader: input s opens lengths[s] records valued
+// start_s + r, start_s = sum of earlier lengths; cycle, parallel).
+int ref_interleave_var_ids(int64_t num_sources, const int64_t* lengths, int64_t shard_k, int64_t shard_g,
+                           int64_t cycle, int64_t parallel, uint64_t base_seed, int64_t* out, int64_t* count) {
+  try {
+    UdfRegistry reg;
+    std::vector<int64_t> len(lengths, lengths + num_sources), start(num_sources + 1, 0);
+    for (int64_t s = 0; s < num_sources; ++s) start[s + 1] = start[s] + len[s];
+    reg.RegisterDataset(
+        "reader_var",
+        [&reg, len, start](const Element& e) {
+          const int64_t s = e.component(0).int64();
+          std::vector<Element> recs;
+          for (int64_t r = 0; r < len[s]; ++r) recs.push_back(Element::Scalar(Value::Int64(start[s] + r)));
+          if (recs.empty())  // an empty reader: one element filtered out (from_memory must be non-empty)
+            return ops::Filter(ops::FromMemory({Element::Scalar(Value::Int64(0))}, reg), "none", reg);
+          return ops::FromMemory(std::move(recs), reg);
+        },
+        ElementSpec({TypeSpec::Int64()}));
+    reg.RegisterPredicate("none", [](const Element&) { return false; });
+    DatasetGraph g = ops::FromMemory(IntRange(num_sources), reg);
+    if (shard_k > 0) g = ops::Shard(g, shard_k, shard_g, reg);
+    g = ops::Interleave(g, "reader_var", cycle, parallel, reg);
+    auto it = MakeIterator(g, reg, Seeded(base_seed));
+    int64_t k = 0;
+    while (auto e = it->GetNext()) out[k++] = e->component(0).int64();
+    *count = k;
+    return 0;
+  } catch (const std::exception& e) {
+    return Fail(e);
+  }
+}
+
 // CPU baseline timing (bench::Run methodology, src/bench.cpp:192-249): the
 // image pipeline over `n` resident synthetic images with map parallelism
 // `parallel`, optimized to map_and_batch, prefetch(prefetch).  One warm-up

@@ -288,6 +288,49 @@ uint64_t orc_interleave_order(uint64_t m_inputs, const uint64_t* inputs,
   return k;
 }
 
+/* InterleaveIterator::Next / OpenNext (src/runtime.cpp:1061-1120) with
+ * per-input lengths: an exhausted slot opens the next input in the same
+ * visit (no turn is lost; empty inputs are skipped in place); a slot finding
+ * no input left is dead. */
+uint64_t orc_interleave_var(uint64_t m_inputs, const uint64_t* inputs,
+                            uint64_t cycle, const uint64_t* lengths,
+                            const uint64_t* starts, uint64_t* out) {
+  typedef struct { int open, dead; uint64_t input, pos; } slot_t;
+  slot_t* slots = (slot_t*)calloc(cycle, sizeof(slot_t));
+  uint64_t cursor = 0, next_input = 0, k = 0;
+  for (;;) {
+    uint64_t dead_streak = 0;
+    int produced = 0;
+    while (dead_streak < cycle) {
+      slot_t* s = &slots[cursor];
+      if (!s->open && !s->dead) {
+        if (next_input >= m_inputs) {
+          s->dead = 1;
+        } else {
+          s->open = 1;
+          s->input = inputs[next_input++];
+          s->pos = 0;
+        }
+      }
+      if (s->dead) {
+        cursor = (cursor + 1) % cycle;
+        dead_streak++;
+        continue;
+      }
+      if (s->pos < lengths[s->input]) {
+        out[k++] = starts[s->input] + s->pos++;
+        cursor = (cursor + 1) % cycle;
+        produced = 1;
+        break;
+      }
+      s->open = 0; /* exhausted: same cycle position opens the next input */
+    }
+    if (!produced) break;
+  }
+  free(slots);
+  return k;
+}
+
 /* group_by_window, sequentially (see restate.h). */
 int64_t orc_bucket_by_length(const int32_t* lengths, const int64_t* order,
                              int64_t n, const int32_t* boundaries,

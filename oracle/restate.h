@@ -121,6 +121,11 @@ uint64_t orc_shard_positions(uint64_t n, uint64_t k, uint64_t g,
 uint64_t orc_interleave_order(uint64_t m_inputs, const uint64_t* inputs,
                               uint64_t cycle, uint64_t records,
                               uint64_t* out);
+/* The same loop for readers of different lengths: input ordinal m opens
+ * lengths[m] records valued starts[m] + r (record files of unequal sizes). */
+uint64_t orc_interleave_var(uint64_t m_inputs, const uint64_t* inputs,
+                            uint64_t cycle, const uint64_t* lengths,
+                            const uint64_t* starts, uint64_t* out);
 
 #ifdef __cplusplus
 }

@@ -371,6 +371,7 @@ struct IndexOp {
   int64_t a = 0, b = 0;  // shard(k, i) | shuffle(buffer) | filter(max_len) | interleave(cycle, records) | repeat(count)
   std::optional<uint64_t> seed;
   std::string path;
+  int64_t parallel = 1;  // interleave num_parallel_calls
 };
 
 enum class BatchKind { kAffine, kCrop, kResize, kPadded, kIdentityInt };
@@ -487,7 +488,8 @@ Lowered Lower(const DatasetGraph& g, const UdfRegistry& reg) {
       seen_interleave = true;
       const auto& e = reg.Get(n->GetString("udf"));
       if (!e.reader) Unsupported("interleave UDF is not a record reader");
-      top_down.push_back({IndexOp::Kind::kInterleave, n->GetInt("cycle_length"), e.reader->records, {}, path});
+      top_down.push_back({IndexOp::Kind::kInterleave, n->GetInt("cycle_length"), e.reader->records, {}, path,
+                          n->GetInt("num_parallel_calls")});
       if (n->HasAttr("records")) L.records = n->GetSource("records");
     } else if (k == NodeKind::kMap) {
       // a map is a pure per-element function whose randomness is keyed by the
@@ -538,18 +540,30 @@ Lowered Lower(const DatasetGraph& g, const UdfRegistry& reg) {
   if (seen_interleave) {
     if (L.records && L.records->shard_count > 1) Unsupported("interleave records must be fully resident");
     if (L.records && L.records->kind == SourceData::Kind::kRecords) {
-      // interleave over record files: input element x opens file x, whose
-      // records are x * R .. x * R + R - 1 of the concatenation when every
-      // file holds the reader's R records
-      int64_t R = 0;
+      // interleave over record files: input element x opens file x.  A
+      // reader of R > 0 records requires every file to hold R (records
+      // x * R .. x * R + R - 1 of the concatenation, the closed form); a
+      // reader of 0 takes each file's own count (unequal files, scheduled).
+      int64_t R = 0, p = 1;
       for (const auto& op : L.chain)
-        if (op.kind == IndexOp::Kind::kInterleave) R = op.b;
-      for (size_t f = 0; f < L.records->file_records.size(); ++f)
-        if (L.records->file_records[f] != R)
+        if (op.kind == IndexOp::Kind::kInterleave) {
+          R = op.b;
+          p = op.parallel;
+        }
+      bool any_empty = false;
+      for (size_t f = 0; f < L.records->file_records.size(); ++f) {
+        if (R > 0 && L.records->file_records[f] != R)
           throw PipelineError(ErrorCode::kMalformedInput,
                               "interleave: record file " + std::to_string(f) + " holds " +
                                   std::to_string(L.records->file_records[f]) + " records, the reader opens " +
-                                  std::to_string(R));
+                                  std::to_string(R) + " (register the reader with 0 records for unequal files)");
+        any_empty = any_empty || L.records->file_records[f] == 0;
+      }
+      // The reference's ParallelInterleaveIterator orders elements around an
+      // EMPTY sub-dataset differently from the sequential loop (measured on the
+      // compiled reference); only the sequential order is reproduced there.
+      if (R == 0 && any_empty && p != 1)
+        Unsupported("parallel interleave over record files with an empty file: use num_parallel_calls=1");
     }
     if (L.source && L.source->kind != SourceData::Kind::kInt64) Unsupported("interleave input must be int64 ordinals");
     if (L.source) Unsupported("interleave over from_memory ordinals: use range()");
@@ -986,6 +1000,10 @@ class DevicePipeline {
           // arithmetic sequence here (identity or shards of it)
           int64_t first = 0, stride = 1;
           ArithmeticOf(count, first, stride);
+          if (op.b == 0 && L_.records && L_.records->kind == SourceData::Kind::kRecords) {
+            BuildVarInterleave(first, stride, op.a, cur, count);
+            break;
+          }
           const int64_t m = count * op.b;
           auto out = alloc(m);
           KCheck(dp_k_interleave_index(first, stride, count, op.a, op.b, P<int64_t>(out), s), "interleave");
@@ -1058,6 +1076,47 @@ class DevicePipeline {
     }
     CudaCheck(cudaEventCreateWithFlags(&p.ready, cudaEventDisableTiming), "event");
     CudaCheck(cudaEventRecord(p.ready, s), "event");
+  }
+
+  // Interleave over record files of unequal sizes: the host schedules the
+  // inputs over the cycle slots (O(inputs log cycle), dp_interleave_schedule),
+  // the device writes every record's position (K6 interleave_var).
+  void BuildVarInterleave(int64_t first, int64_t stride, int64_t cycle, std::shared_ptr<void>& cur, int64_t& count) {
+    cudaStream_t s = plan_stream_;
+    const auto& fr = L_.records->file_records;
+    std::vector<int64_t> file_start(fr.size() + 1, 0);
+    for (size_t f = 0; f < fr.size(); ++f) file_start[f + 1] = file_start[f] + fr[f];
+    const int64_t m = count;
+    std::vector<int64_t> host(5 * std::max<int64_t>(m, 1) + cycle, 0);  // slot | start | len | first_record | end
+    int64_t* slot = host.data();
+    int64_t* start = slot + m;
+    int64_t* len = start + m;
+    int64_t* rec = len + m;
+    int64_t* end = rec + m;
+    int64_t total = 0;
+    for (int64_t i = 0; i < m; ++i) {
+      const int64_t x = first + i * stride;
+      if (x < 0 || x >= static_cast<int64_t>(fr.size()))
+        throw PipelineError(ErrorCode::kMalformedInput, "interleave: input " + std::to_string(x) + " has no record file (" +
+                                                            std::to_string(fr.size()) + " files)");
+      len[i] = fr[x];
+      rec[i] = file_start[x];
+      total += len[i];
+    }
+    KCheck(dp_interleave_schedule(m, len, cycle, slot, start, end), "interleave schedule");
+    auto dalloc = [&](size_t bytes) { return DeviceAllocAsync(bytes, opt_.device, plan_stream_, plan_stream_); };
+    auto meta = dalloc(sizeof(int64_t) * host.size());
+    CudaCheck(cudaMemcpyAsync(meta.get(), host.data(), sizeof(int64_t) * host.size(), cudaMemcpyHostToDevice, s),
+              "interleave schedule");
+    const int64_t tail = std::max<int64_t>(L_.batch * group_, 1);
+    auto out = dalloc(sizeof(int64_t) * (total + tail));
+    const int64_t* d = P<int64_t>(meta);
+    KCheck(dp_k_interleave_var(m, d, d + m, d + 2 * m, d + 3 * m, d + 4 * m, cycle, P<int64_t>(out), s),
+           "interleave_var");
+    launches_++;
+    CudaCheck(cudaStreamSynchronize(s), "interleave schedule");  // `host` is read by the copy
+    cur = out;
+    count = total;
   }
 
   // K8: the bucket plan of one epoch (k_bucket.cu) -- batches, their rows

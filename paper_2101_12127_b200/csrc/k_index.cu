@@ -1,6 +1,8 @@
 // k_index.cu -- K1 range_affine_batch, K6 shard / interleave index mapping,
 // K7 order digest, synthetic input generators.  All HBM-bound integer work.
 #include <cstdint>
+#include <queue>
+#include <vector>
 
 #include "common.cuh"
 #include "status.hpp"
@@ -174,6 +176,73 @@ extern "C" int dp_k_interleave_index(int64_t first, int64_t stride, int64_t m_in
   shard_interleave_kernel<<<grid_for(count, 1), kThreads, 0, as_stream(stream)>>>(m_inputs, stride, first, cycle,
                                                                                     records, count, out);
   return launch_status("interleave_index");
+}
+
+namespace dpk {
+namespace {
+// K6 over readers of unequal lengths.  The host schedules the inputs
+// (dp_interleave_schedule): input i runs in cycle slot slot[i] during visits
+// ("rounds") [start[i], start[i] + len[i]), each slot's inputs back to back;
+// end[s] = the round slot s goes dead.  Element j of input i is emitted at
+// round r = start[i] + j and its position is
+//   sum_s' min(end[s'], r) + #{s' < slot[i] : end[s'] > r}
+// (every slot emits once per round until it is dead).  One CTA per input.
+__global__ void __launch_bounds__(kThreads)
+interleave_var_kernel(const int64_t* __restrict__ slot, const int64_t* __restrict__ start,
+                      const int64_t* __restrict__ len, const int64_t* __restrict__ first_record,
+                      const int64_t* __restrict__ end, int cycle, int64_t* __restrict__ out) {
+  extern __shared__ int64_t s_end[];
+  for (int s = threadIdx.x; s < cycle; s += blockDim.x) s_end[s] = end[s];
+  __syncthreads();
+  const int64_t i = blockIdx.x, sl = slot[i], st = start[i], rec = first_record[i];
+  for (int64_t j = threadIdx.x; j < len[i]; j += blockDim.x) {
+    const int64_t r = st + j;
+    int64_t pos = 0;
+    for (int s = 0; s < cycle; ++s) {
+      const int64_t e = s_end[s];
+      pos += e < r ? e : r;
+      pos += (s < sl && e > r) ? 1 : 0;
+    }
+    out[pos] = rec + j;
+  }
+}
+}  // namespace
+}  // namespace dpk
+
+extern "C" int dp_interleave_schedule(int64_t m_inputs, const int64_t* lengths, int64_t cycle, int64_t* slot,
+                                      int64_t* start, int64_t* end) {
+  if (m_inputs < 0 || cycle < 1 || (m_inputs && (!lengths || !slot || !start)) || !end)
+    return fail(DP_ERR_INVALID_ATTR, "interleave_schedule: bad arguments");
+  // (round, slot) of the visits that need a new input, smallest first: the
+  // InterleaveIterator loop (runtime.cpp:1061-1120) opens inputs in visit
+  // order, and an exhausted slot opens the next one in the same visit
+  using Visit = std::pair<int64_t, int64_t>;
+  std::priority_queue<Visit, std::vector<Visit>, std::greater<Visit>> need;
+  for (int64_t s = 0; s < cycle; ++s) {
+    need.push({0, s});
+    end[s] = 0;
+  }
+  for (int64_t i = 0; i < m_inputs; ++i) {
+    if (lengths[i] < 0) return fail(DP_ERR_INVALID_ATTR, "interleave_schedule: negative length");
+    const Visit v = need.top();
+    need.pop();
+    slot[i] = v.second;
+    start[i] = v.first;
+    end[v.second] = v.first + lengths[i];
+    need.push({end[v.second], v.second});
+  }
+  return DP_OK;
+}
+
+extern "C" int dp_k_interleave_var(int64_t m_inputs, const int64_t* slot, const int64_t* start, const int64_t* len,
+                                   const int64_t* first_record, const int64_t* end, int64_t cycle, int64_t* out,
+                                   void* stream) {
+  if (m_inputs < 0 || cycle < 1 || cycle > 4096) return fail(DP_ERR_INVALID_ATTR, "interleave_var: bad sizes");
+  if (m_inputs == 0) return DP_OK;
+  if (m_inputs > 0x7fffffff) return fail(DP_ERR_INVALID_ATTR, "interleave_var: too many inputs");
+  interleave_var_kernel<<<static_cast<int>(m_inputs), kThreads, sizeof(int64_t) * cycle, as_stream(stream)>>>(
+      slot, start, len, first_record, end, static_cast<int>(cycle), out);
+  return launch_status("interleave_var");
 }
 
 extern "C" int64_t dp_k_shard_interleave_count(int64_t n_sources, int64_t num_shards, int64_t shard_index,

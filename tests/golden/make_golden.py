@@ -110,6 +110,21 @@ def main():
                     "fnv_ids": f"{orc.fnv_digest(ids):016x}", "fnv_pixels": words_fnv(pix)})
     g["image_pipelines"] = img
 
+    # interleave over readers of unequal lengths (record files of different
+    # sizes): the sequential order, and the parallel one where it agrees (no
+    # empty reader -- see DESIGN.md 6d)
+    rng = np.random.default_rng(21)
+    ivar = []
+    for case in range(24):
+        m, c = int(rng.integers(1, 14)), int(rng.integers(1, 6))
+        lens = rng.integers(0 if case % 3 == 0 else 1, 9, m)
+        shard = [int(x) for x in rng.choice([[0, 0], [2, 1], [3, 0]])]
+        p = 1 if case % 3 == 0 else c
+        ids = ref.interleave_var_ids(lens, c, p, tuple(shard) if shard[0] else None)
+        ivar.append({"lengths": lens.tolist(), "cycle": c, "parallel": p, "shard": shard,
+                     "order": ids.tolist()})
+    g["interleave_var"] = ivar
+
     ser = []
     for which in range(6):  # pipeline shapes: oracle/ref_shim.cpp ref_serialize_pipeline
         b, fp = ref.serialize_pipeline(which)

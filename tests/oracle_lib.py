@@ -171,6 +171,18 @@ class Oracle:
         m = self.L.orc_shard_positions(n, k, g, P(out))
         return out[:m].astype(np.int64)
 
+    def interleave_var(self, inputs, cycle, lengths):
+        """Interleave over readers of unequal lengths (restate.c orc_interleave_var)."""
+        inputs = np.ascontiguousarray(inputs, np.uint64)
+        lengths = np.ascontiguousarray(lengths, np.uint64)
+        starts = np.zeros(lengths.size, np.uint64)
+        starts[1:] = np.cumsum(lengths)[:-1]
+        out = np.zeros(max(int(lengths.sum()), 1), np.uint64)
+        self.L.orc_interleave_var.restype = ctypes.c_uint64
+        self.L.orc_interleave_var.argtypes = [ctypes.c_uint64, vp, ctypes.c_uint64, vp, vp, vp]
+        m = self.L.orc_interleave_var(inputs.size, P(inputs), cycle, P(lengths), P(starts), P(out))
+        return out[:m].astype(np.int64)
+
     def interleave_order(self, inputs, cycle, records):
         inputs = np.ascontiguousarray(inputs, np.uint64)
         out = np.zeros(max(inputs.size * records, 1), np.uint64)
@@ -265,6 +277,16 @@ class Reference:
         cnt = np.zeros(1, np.int64)
         self._check(self.L.ref_interleave_ids(num_sources, k, g, cycle, parallel, records, shuffle_buffer,
                                               shuffle_seed, base_seed, P(out), P(cnt)))
+        return out[: cnt[0]]
+
+    def interleave_var_ids(self, lengths, cycle, parallel=1, shard=None, base_seed=1):
+        lengths = np.ascontiguousarray(lengths, np.int64)
+        k, g = shard if shard else (0, 0)
+        out = np.zeros(max(int(lengths.sum()), 1), np.int64)
+        cnt = np.zeros(1, np.int64)
+        self.L.ref_interleave_var_ids.argtypes = [i64, vp, i64, i64, i64, i64, ctypes.c_uint64, vp, vp]
+        self._check(self.L.ref_interleave_var_ids(lengths.size, P(lengths), k, g, cycle, parallel, base_seed,
+                                                  P(out), P(cnt)))
         return out[: cnt[0]]
 
     def time_image_pipeline(self, mode, n, in_hw, out_hw, parallel, epochs=3, shuffle_buffer=10000, batch=256,

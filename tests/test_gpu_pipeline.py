@@ -453,6 +453,52 @@ def test_interleave_over_record_files_equals_cfg5(dp, orc, tmp_path):
     assert e.value.code == dp.ERR["MalformedInput"]
 
 
+def test_interleave_over_unequal_record_files(dp, orc, tmp_path):
+    """Record files of different sizes (reader registered with 0 records =
+    each file's own count): the host schedule + K6 interleave_var give the
+    reference's order (sequential loop; parallel too when no file is empty),
+    then shuffle + crop; an empty file under a parallel interleave is
+    rejected (the reference's parallel order differs there)."""
+    lens = [7, 3, 0, 9, 1, 5, 4, 6, 2, 8, 5]
+    starts = np.concatenate([[0], np.cumsum(lens)[:-1]])
+    imgs = orc.images(0, int(sum(lens)), 40, 40)
+    paths = [str(tmp_path / f"f{i}.rec") for i in range(len(lens))]
+    for i, p in enumerate(paths):
+        dp.write_record_file(p, [imgs[starts[i] + r].tobytes() for r in range(lens[i])])
+    reg = image_registry(dp, 0, crop=(32, 32))
+    reg.register_record_reader("files", 0)
+    reg.register_decode_raw("decode", 40, 40)
+    recs = dp.Source.records_from_files(paths)
+    for cycle, par, shard in ((3, 1, None), (4, 1, (2, 1)), (2, 1, (3, 0))):
+        g = dp.Dataset.range(reg, len(lens))
+        if shard:
+            g = g.shard(*shard)
+        g = g.interleave("files", cycle, par, records=recs).map("decode").map("crop").map("norm").batch(6)
+        got = drain(dp.make_iterator(g, seed_override=1), comps=(0, 1))
+        inputs = np.arange(shard[1], len(lens), shard[0]) if shard else np.arange(len(lens))
+        want = orc.interleave_var(inputs, cycle, lens)
+        ids = np.concatenate([b[0] for b in got])
+        assert ids.tolist() == want.tolist()
+        p = int(ids[-1])
+        assert np.array_equal(got[-1][1][-1], orc.crop_flip_normalize(imgs[p], p, 32, 32))
+    # parallel is reproduced without empty files
+    lens2 = [x + 1 for x in lens]
+    starts2 = np.concatenate([[0], np.cumsum(lens2)[:-1]])
+    imgs2 = orc.images(0, int(sum(lens2)), 40, 40)
+    paths2 = [str(tmp_path / f"g{i}.rec") for i in range(len(lens2))]
+    for i, p in enumerate(paths2):
+        dp.write_record_file(p, [imgs2[starts2[i] + r].tobytes() for r in range(lens2[i])])
+    g = (dp.Dataset.range(reg, len(lens2)).interleave("files", 4, 4, records=dp.Source.records_from_files(paths2))
+         .shuffle(20, 3).map("decode").map("crop").map("norm").batch(8))
+    ids = np.concatenate([b[0] for b in drain(dp.make_iterator(g, seed_override=2))])
+    order = orc.interleave_var(np.arange(len(lens2)), 4, lens2)
+    assert ids.tolist() == order[orc.shuffle_order(order.size, 20, orc.shuffle_seed(2, 3))].tolist()
+    with pytest.raises(dp.DpError) as e:
+        dp.make_iterator(dp.Dataset.range(reg, len(lens)).interleave("files", 4, 4, records=recs)
+                         .map("decode").map("crop").map("norm").batch(8))
+    assert e.value.code == dp.ERR["InvalidAttr"]
+
+
 def test_sharded_residency_equals_shard_of_full_dataset(dp, orc):
     """Per-GPU residency: a process holding only shard i of k
     produces exactly shard(k, i) of the full dataset, ids and pixels."""

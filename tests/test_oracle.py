@@ -276,3 +276,40 @@ def test_bucket_by_length_restatement(orc):
     got = orc.bucket_by_length(lengths, order, [6, 51], [3, 1, 5])
     # buckets: len<6 -> 0, 6..50 -> 1 (size 1: emitted at once), >=51 -> 2
     assert [b.tolist() for b in got] == [[7], [5], [3], [2], [1], [0], [6, 4]]
+
+
+def test_interleave_var_restatement_vs_reference_golden(orc):
+    """Readers of unequal lengths (record files of different sizes): the
+    restatement equals the compiled reference's order (golden
+    interleave_var, sequential and parallel-without-empty-readers)."""
+    for c in GOLDEN["interleave_var"]:
+        lens = np.array(c["lengths"], np.int64)
+        k, g = c["shard"]
+        inputs = np.arange(g, lens.size, k) if k else np.arange(lens.size)
+        assert orc.interleave_var(inputs, c["cycle"], lens).tolist() == c["order"], c
+
+
+def test_interleave_schedule_closed_form(orc):
+    """dp_interleave_schedule (host, C ABI) + the position formula of the
+    interleave_var kernel reproduce the sequential loop on random cases --
+    the device kernel is this formula, one thread per record."""
+    import ctypes
+    from paper_2101_12127_b200 import _capi
+    L = _capi.lib()
+    P = lambda a: a.ctypes.data_as(ctypes.c_void_p)
+    rng = np.random.default_rng(5)
+    for _ in range(300):
+        m, c = int(rng.integers(0, 20)), int(rng.integers(1, 7))
+        lens = rng.integers(0, 9, m).astype(np.int64)
+        slot, start = np.zeros(max(m, 1), np.int64), np.zeros(max(m, 1), np.int64)
+        end = np.zeros(c, np.int64)
+        assert L.dp_interleave_schedule(ctypes.c_int64(m), P(lens), ctypes.c_int64(c), P(slot), P(start),
+                                        P(end)) == 0
+        first = np.concatenate([[0], np.cumsum(lens)[:-1]]) if m else np.zeros(0, np.int64)
+        out = np.full(int(lens.sum()), -1, np.int64)
+        for i in range(m):
+            for j in range(lens[i]):
+                r = start[i] + j
+                pos = int(np.minimum(end, r).sum()) + int(((np.arange(c) < slot[i]) & (end > r)).sum())
+                out[pos] = first[i] + j
+        assert out.tolist() == orc.interleave_var(np.arange(m), c, lens).tolist(), (lens.tolist(), c)

@@ -179,7 +179,7 @@ def cpu_reference(cfg, threads, warmup_batches, steps):
         raise RuntimeError(L.ref_last_error().decode())
     return {"value": elems.value / secs.value, "seconds": secs.value, "elements": elems.value, "cores": threads,
             "sample": f"{sample} resident synthetic images repeated, {steps} timed batches of {cfg['batch']} after "
-                      f"{warmup_batches} warm-up, map_and_batch num_parallel_calls={threads}, prefetch(2)"}
+                      f"{warmup_batches} warm-up, map_and_batch num_parallel_calls={threads}, prefetch(AUTOTUNE)"}
 
 
 def cpu_reference_range(cfg):

@@ -415,7 +415,7 @@ int ref_time_image_steps(int mode, int in_h, int in_w, int out_h, int out_w, uin
     g = ops::Repeat(g, kInfiniteRepeat, reg);
     g = ops::Map(g, ImageUdfName(p), parallel, reg);
     g = ops::Batch(g, batch, false, reg);
-    g = ops::Prefetch(g, 2, reg);
+    g = ops::Prefetch(g, kAutotune, reg);  // prefetch(AUTOTUNE)
     g = Optimize(g, RuleSet::Default(), reg).first;
     auto it = MakeIterator(g, reg, Seeded(1));
     for (int64_t i = 0; i < warmup; ++i) it->GetNext();

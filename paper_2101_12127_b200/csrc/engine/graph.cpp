@@ -100,7 +100,7 @@ std::string DatasetGraph::ToString() const {
             else if constexpr (std::is_same_v<T, std::vector<std::string>>) os << "[" << x.size() << "]";
             else if constexpr (std::is_same_v<T, std::vector<int64_t>>) {
               os << "[";
-              for (size_t k = 0; k < x.size(); ++k) os << (k ? "," : "") << x[k];
+              for (size_t i = 0; i < x.size(); ++i) os << (i ? "," : "") << x[i];
               os << "]";
             } else os << x;
           },

@@ -229,7 +229,6 @@ __global__ void __launch_bounds__(kPT) p2_scatter(const uint32_t* __restrict__ r
                                                   uint32_t* __restrict__ slot_of, uint32_t* __restrict__ counts,
                                                   uint64_t* __restrict__ meta) {
   __shared__ int ws[kPT / 32];
-  __shared__ int tot;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kTileK + threadIdx.x * 16ull;
   uint32_t mask = 0;
@@ -253,7 +252,6 @@ __global__ void __launch_bounds__(kPT) p2_scatter(const uint32_t* __restrict__ r
       if (lane >= o) z += y;
     }
     if (lane < kPT / 32) ws[lane] = z - w;
-    if (lane == kPT / 32 - 1) tot = z;
   }
   __syncthreads();
   uint64_t k = tiles[blockIdx.x] + (x - c) + ws[warp];

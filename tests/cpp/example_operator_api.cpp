@@ -1,10 +1,12 @@
 // A reference user's program, ported by changing the include and namespace:
 // builds the cfg1 graph with ops::*, optimizes it to map_and_batch, drains
 // it with GetNext and prints the SURVEY.md Appendix A known answers; then a
-// cfg2-shaped image pipeline, with a checkpoint Save/Restore in the middle.
+// cfg2-shaped image pipeline, with a checkpoint Save/Restore in the middle;
+// the reference's graph serialization / fingerprint; bucket_by_length.
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <numeric>
 #include <vector>
 
 #include "dpb200/datapipe.hpp"
@@ -59,5 +61,24 @@ int main() {
   cudaMemcpy(ib.data(), b->component(0).tensor().data, 2048, cudaMemcpyDeviceToHost);
   std::printf("cfg2 restore_matches=%d first_id=%lld plan:\n%s", ia == ib ? 1 : 0, static_cast<long long>(ia[0]),
               pit->LoweringPlan().c_str());
+
+  // DPG1 bytes + fingerprint: from_memory(0..9) -> map(affine(3,1), 4) -> batch(4)
+  std::vector<int64_t> ten(10);
+  std::iota(ten.begin(), ten.end(), 0);
+  DatasetGraph s = ops::Batch(ops::Map(ops::FromMemory(ten, reg), "affine(3,1)", 4, reg), 4, false, reg);
+  const std::string bytes = Serialize(s);
+  std::printf("fingerprint=%s roundtrip=%d\n", FingerprintHex(GraphFingerprint(s)).c_str(),
+              Serialize(Deserialize(bytes, reg)) == bytes ? 1 : 0);
+
+  // bucket_by_length over 5,000 token sequences
+  auto tokens = SynthTokens(5000, 300, 6, 6);
+  DatasetGraph bk = ops::BucketByLength(ops::TokenSequences(tokens, reg), {100, 200}, {16, 8, 4}, 0, false, reg);
+  auto bit = MakeIterator(bk, reg, o);
+  int64_t rows = 0, nb = 0;
+  while (auto e = bit->GetNext()) {
+    rows += e->component(1).tensor().shape[0];
+    ++nb;
+  }
+  std::printf("bucket rows=%lld batches=%lld\n", static_cast<long long>(rows), static_cast<long long>(nb));
   return ia == ib ? 0 : 1;
 }

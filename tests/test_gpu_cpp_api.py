@@ -23,3 +23,8 @@ def test_cpp_example_known_answers(tmp_path):
     # SURVEY.md Appendix A, via the C++ API
     assert "cfg1 root=map_and_batch batches=977 last=576 sum=1499999500000 fnv=8bc444c576bd14a5" in out.stdout
     assert "cfg2 restore_matches=1" in out.stdout
+    # the reference's fingerprint of the same graph (golden, from the compiled reference)
+    import json
+    golden = json.load(open(os.path.join(ROOT, "tests", "golden", "golden.json")))["serialize"][0]
+    assert f"fingerprint={golden['fingerprint']} roundtrip=1" in out.stdout
+    assert "bucket rows=5000" in out.stdout

@@ -253,53 +253,73 @@ SourcePtr ImagesFromPinnedHost(const uint8_t* data, int64_t count, int64_t h, in
 // truncated length or payload is MalformedInput, a missing file MissingFile.
 SourcePtr RecordsFromFiles(const std::vector<std::string>& paths, int device) {
   if (paths.empty()) throw PipelineError(ErrorCode::kInvalidAttr, "from_file: 'paths' must be non-empty");
-  std::vector<std::string> blobs;
+  // Pass 1: walk the length headers (seeking over payloads) -- validates the
+  // framing and sizes everything.  Pass 2 reads the payloads straight into
+  // one pinned staging buffer (one host copy of the data), then one H2D copy.
+  struct Rec {
+    size_t file;
+    long pos;
+    uint32_t len;
+  };
+  std::vector<Rec> recs;
   std::vector<int64_t> offsets{0};
   std::vector<int64_t> per_file;
   int64_t uniform = -1;
-  for (const auto& path : paths) {
-    const size_t before = blobs.size();
+  for (size_t fi = 0; fi < paths.size(); ++fi) {
+    const std::string& path = paths[fi];
     FILE* f = std::fopen(path.c_str(), "rb");
     if (!f) throw PipelineError(ErrorCode::kMissingFile, "no such file: " + path);
-    std::string data;
-    char chunk[1 << 16];
-    size_t got;
-    while ((got = std::fread(chunk, 1, sizeof(chunk), f)) > 0) data.append(chunk, got);
-    std::fclose(f);
-    size_t pos = 0;
-    while (pos < data.size()) {
-      if (pos + 4 > data.size())
-        throw PipelineError(ErrorCode::kMalformedInput, "at byte " + std::to_string(pos) +
-                                                            ": truncated record length in " + path);
-      uint32_t len = 0;
-      for (int i = 0; i < 4; ++i) len |= static_cast<uint32_t>(static_cast<uint8_t>(data[pos + i])) << (8 * i);
+    std::fseek(f, 0, SEEK_END);
+    const long size = std::ftell(f);
+    std::fseek(f, 0, SEEK_SET);
+    const size_t before = recs.size();
+    long pos = 0;
+    while (pos < size) {
+      unsigned char lb[4];
+      if (pos + 4 > size || std::fread(lb, 1, 4, f) != 4) {
+        std::fclose(f);
+        throw PipelineError(ErrorCode::kMalformedInput,
+                            "at byte " + std::to_string(pos) + ": truncated record length in " + path);
+      }
+      const uint32_t len = lb[0] | (lb[1] << 8) | (lb[2] << 16) | (static_cast<uint32_t>(lb[3]) << 24);
       pos += 4;
-      if (pos + len > data.size())
-        throw PipelineError(ErrorCode::kMalformedInput, "at byte " + std::to_string(pos) +
-                                                            ": truncated record payload in " + path);
-      blobs.emplace_back(data, pos, len);
+      if (pos + static_cast<long>(len) > size) {
+        std::fclose(f);
+        throw PipelineError(ErrorCode::kMalformedInput,
+                            "at byte " + std::to_string(pos) + ": truncated record payload in " + path);
+      }
+      recs.push_back({fi, pos, len});
       offsets.push_back(offsets.back() + len);
       uniform = (uniform < 0 || uniform == static_cast<int64_t>(len)) ? len : -2;
       pos += len;
+      std::fseek(f, pos, SEEK_SET);
     }
-    per_file.push_back(static_cast<int64_t>(blobs.size() - before));
+    std::fclose(f);
+    per_file.push_back(static_cast<int64_t>(recs.size() - before));
   }
   auto s = std::make_shared<SourceData>();
   s->kind = SourceData::Kind::kRecords;
-  s->count = static_cast<int64_t>(blobs.size());
+  s->count = static_cast<int64_t>(recs.size());
   s->record_len = uniform >= 0 ? uniform : 0;
   s->file_records = std::move(per_file);
   s->device = device;
   const size_t total = static_cast<size_t>(offsets.back());
+  auto staging = PinnedAlloc(std::max<size_t>(total, 16));
+  char* dst = static_cast<char*>(staging.get());
+  for (size_t fi = 0, r = 0; fi < paths.size(); ++fi) {
+    FILE* f = std::fopen(paths[fi].c_str(), "rb");
+    if (!f) throw PipelineError(ErrorCode::kMissingFile, "no such file: " + paths[fi]);
+    for (; r < recs.size() && recs[r].file == fi; ++r) {
+      std::fseek(f, recs[r].pos, SEEK_SET);
+      if (std::fread(dst + offsets[r], 1, recs[r].len, f) != recs[r].len) {
+        std::fclose(f);
+        throw PipelineError(ErrorCode::kMalformedInput, "file changed while reading: " + paths[fi]);
+      }
+    }
+    std::fclose(f);
+  }
   s->values = DeviceAlloc(std::max<size_t>(total, 16), device);
   s->offsets = DeviceAlloc(sizeof(int64_t) * offsets.size(), device);
-  // pack the payloads back to back in pinned memory, one H2D copy
-  auto staging = PinnedAlloc(std::max<size_t>(total, 16));
-  size_t at = 0;
-  for (const auto& b : blobs) {
-    std::memcpy(static_cast<char*>(staging.get()) + at, b.data(), b.size());
-    at += b.size();
-  }
   DeviceGuard g(device);
   CudaCheck(cudaMemcpy(s->values.get(), staging.get(), total, cudaMemcpyHostToDevice), "upload records");
   CudaCheck(cudaMemcpy(s->offsets.get(), offsets.data(), sizeof(int64_t) * offsets.size(), cudaMemcpyHostToDevice),

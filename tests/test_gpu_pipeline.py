@@ -591,6 +591,10 @@ def test_edge_cases(dp, orc):
     src = dp.Source.synthetic_tokens(100, 50, 1, 1)
     assert vals(dp.Dataset.token_sequences(reg, src).filter("none").padded_batch(8)) == []  # filter keeps none
     assert vals(dp.Dataset.range(reg, 4).interleave("zero", 2, 1).batch(2)) == []          # empty readers
+    assert vals(dp.Dataset.token_sequences(reg, src).filter("none").bucket_by_length([10], [4, 4])) == []
+    # EOF is sticky (runtime.cpp:147-156)
+    it = dp.make_iterator(dp.Dataset.range(reg, 3).batch(2), seed_override=1)
+    assert [it.get_next() is None for _ in range(5)] == [False, False, True, True, True]
     # infinite repeat keeps producing; sticky end never reached
     it = dp.make_iterator(dp.Dataset.range(reg, 3).batch(2).repeat(-1), seed_override=1)
     assert [it.get_next().numpy(0).tolist() for _ in range(5)] == [[0, 1], [2], [0, 1], [2], [0, 1]]

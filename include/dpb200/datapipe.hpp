@@ -156,9 +156,19 @@ struct MapStep {
   std::array<float, 3> mean{}, stdv{};  // normalize
 };
 
-// Predicate on a token sequence's length (the cfg4 filter).
-struct LengthPredicate {
-  int64_t max_len = 0;  // keep iff len <= max_len
+// Device predicate for Filter: a conjunction of terms on one quantity of
+// the element -- a token sequence's LENGTH (the cfg4 filter), or an int64
+// element's VALUE (after the affine maps beneath the filter; the reference's
+// keep_even / keep_odd, pipeline_spec.cpp:234-243).  % is C++'s truncated
+// remainder, as in those UDFs.
+struct PredicateTerm {
+  enum class Op { kLE, kGE, kLT, kModEq, kModNe } op;
+  int64_t a = 0, b = 0;  // v <= a | v >= a | v < a | v % a == b | v % a != b
+};
+struct DevicePredicate {
+  enum class On { kLength, kValue } on = On::kLength;
+  std::vector<PredicateTerm> terms;  // conjunction, at most 8
+  int64_t MaxLen() const;            // kLength: the tightest v <= a bound (INT64_MAX if none)
 };
 
 // Interleave reader: input element x opens a dataset of `records` records
@@ -171,7 +181,7 @@ class UdfRegistry {
  public:
   struct Entry {
     std::vector<MapStep> map;              // map / map_and_batch
-    std::optional<LengthPredicate> predicate;
+    std::optional<DevicePredicate> predicate;
     std::optional<RecordReader> reader;    // interleave
     std::optional<int64_t> cost_hint_ns;
   };
@@ -185,7 +195,11 @@ class UdfRegistry {
   void RegisterResizeBilinear(const std::string& name, int64_t out_h, int64_t out_w);
   void RegisterNormalize(const std::string& name, std::array<float, 3> mean, std::array<float, 3> stdv);
   void RegisterDecodeRaw(const std::string& name, int64_t h, int64_t w);
-  void RegisterLengthFilter(const std::string& name, int64_t max_len);
+  void RegisterLengthFilter(const std::string& name, int64_t max_len);  // keep len <= max_len
+  void RegisterValueFilter(const std::string& name, std::vector<PredicateTerm> terms);
+  // keep_even / keep_odd / keep_all on int64 elements (the reference's
+  // EnsurePredicates, pipeline_spec.cpp:234-243)
+  void RegisterStandardPredicates();
   void RegisterRecordReader(const std::string& name, int64_t records);
   bool Contains(const std::string& name) const;
   const Entry& Get(const std::string& name) const;  // kUnknownUdf

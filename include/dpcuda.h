@@ -144,6 +144,25 @@ int dp_k_resize_normalize_batch_ex(const uint8_t* images, int64_t num_images, in
 /*     kept: int64 [n] out (stable order), *num_kept written to device     */
 /*     memory `num_kept_dev` (int64).  scratch: dp_k_filter_scratch_bytes. */
 size_t dp_k_filter_scratch_bytes(int64_t n);
+/* General device predicate (FilterIterator runtime.cpp:556-571 with the     */
+/* predicate UDF as a descriptor): keep element i iff every term holds on   */
+/* v = mul * q + add (wrap-around int64), q = lengths[p] if lengths, else    */
+/* values[p] if values, else the position p itself (range); p = in_map[i].  */
+/* % is C's truncated remainder (the reference's keep_even/keep_odd,        */
+/* pipeline_spec.cpp:234-243).  terms: host array, 1..8.                   */
+#define DP_PRED_LE 0     /* v <= a      */
+#define DP_PRED_GE 1     /* v >= a      */
+#define DP_PRED_LT 2     /* v < a       */
+#define DP_PRED_MOD_EQ 3 /* v % a == b  */
+#define DP_PRED_MOD_NE 4 /* v % a != b  */
+typedef struct dp_predicate_term {
+  int op;
+  int64_t a, b;
+} dp_predicate_term;
+int dp_k_filter(const int32_t* lengths, const int64_t* values, int64_t n,
+                int64_t mul, int64_t add, const dp_predicate_term* terms,
+                int num_terms, const int64_t* in_map, int64_t* kept,
+                int64_t* num_kept_dev, void* scratch, void* stream);
 int dp_k_filter_len_le(const int32_t* lengths, int64_t n, int32_t max_keep,
                        const int64_t* in_map, int64_t* kept,
                        int64_t* num_kept_dev, void* scratch, void* stream);

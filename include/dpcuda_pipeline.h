@@ -43,6 +43,12 @@ int dp_registry_register_resize_bilinear(dp_registry* reg, const char* name, int
 int dp_registry_register_normalize(dp_registry* reg, const char* name, const float mean[3], const float stdv[3]);
 /* predicate: keep sequences with length <= max_len */
 int dp_registry_register_length_filter(dp_registry* reg, const char* name, int64_t max_len);
+/* predicate on int64 element values (after the maps beneath the filter):
+ * a conjunction of 1..8 terms (dp_predicate_term, include/dpcuda.h) */
+int dp_registry_register_value_filter(dp_registry* reg, const char* name, const dp_predicate_term* terms,
+                                      int num_terms);
+/* keep_even / keep_odd / keep_all (pipeline_spec.cpp:234-243 EnsurePredicates) */
+int dp_registry_register_standard_predicates(dp_registry* reg);
 /* interleave dataset UDF: element x opens records x*records .. x*records+records-1 */
 int dp_registry_register_record_reader(dp_registry* reg, const char* name, int64_t records);
 /* decode a from_file record holding a raw u8 HWC image of h x w x 3 ->

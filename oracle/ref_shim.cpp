@@ -15,6 +15,7 @@
 // UdfRegistry::RegisterMap (include/datapipe/udf.hpp:61-63).
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
 #include <cstring>
 #include <exception>
 #include <string>
@@ -324,6 +325,38 @@ int ref_interleave_ids(int64_t num_sources, int64_t shard_k, int64_t shard_g,
     auto it = MakeIterator(g, reg, Seeded(base_seed));
     int64_t k = 0;
     while (auto e = it->GetNext()) out[k++] = e->component(0).int64();
+    *count = k;
+    return 0;
+  } catch (const std::exception& e) {
+    return Fail(e);
+  }
+}
+
+// Value filters (the reference's keep_even / keep_odd, pipeline_spec.cpp:
+// 234-243): from_memory(IntRange(n)) -> map(x * a + b) -> filter(keep_*)
+// [-> shuffle(buffer, 42)] -> batch(64) [-> Optimize: map_filter_fusion,
+// map_batch_fusion].  Emits the values.
+int ref_filter_values(int64_t n, int64_t a, int64_t b, int odd, int64_t shuffle_buffer, int optimize,
+                      int64_t* out, int64_t* count, char* root_kind, size_t root_len) {
+  try {
+    UdfRegistry reg;
+    const std::string f = "affine(" + std::to_string(a) + "," + std::to_string(b) + ")";
+    RegisterAffine(reg, f, a, b);
+    reg.RegisterPredicate("keep_even", [](const Element& e) { return e.component(0).int64() % 2 == 0; });
+    reg.RegisterPredicate("keep_odd", [](const Element& e) { return e.component(0).int64() % 2 != 0; });
+    DatasetGraph g = ops::Map(ops::FromMemory(IntRange(n), reg), f, 1, reg);
+    g = ops::Filter(g, odd ? "keep_odd" : "keep_even", reg);
+    if (shuffle_buffer > 0) g = ops::Shuffle(g, shuffle_buffer, uint64_t{42}, reg);
+    g = ops::Batch(g, 64, false, reg);
+    if (optimize) g = Optimize(g, RuleSet::Default(), reg).first;
+    std::string chain;  // root first: kind<-kind<-...
+    for (const DatasetNode* nd = g.root().get(); nd; nd = nd->inputs().empty() ? nullptr : nd->inputs()[0].get())
+      chain += std::string(chain.empty() ? "" : "<-") + NodeKindName(nd->kind());
+    std::snprintf(root_kind, root_len, "%s", chain.c_str());
+    auto it = MakeIterator(g, reg, Seeded(1));
+    int64_t k = 0;
+    while (auto e = it->GetNext())
+      for (const auto& v : e->component(0).items()) out[k++] = v.int64();
     *count = k;
     return 0;
   } catch (const std::exception& e) {

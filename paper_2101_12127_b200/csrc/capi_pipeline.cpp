@@ -90,6 +90,23 @@ int dp_registry_register_length_filter(dp_registry* reg, const char* name, int64
   DP_REQUIRE(reg && name);
   return Guard([&] { reg->reg.RegisterLengthFilter(name, max_len); });
 }
+int dp_registry_register_value_filter(dp_registry* reg, const char* name, const dp_predicate_term* terms,
+                                      int num_terms) {
+  DP_REQUIRE(reg && name && (terms || num_terms == 0));
+  return Guard([&] {
+    std::vector<PredicateTerm> t;
+    for (int i = 0; i < num_terms; ++i) {
+      if (terms[i].op < DP_PRED_LE || terms[i].op > DP_PRED_MOD_NE)
+        throw PipelineError(ErrorCode::kInvalidAttr, "value filter: unknown predicate op");
+      t.push_back({static_cast<PredicateTerm::Op>(terms[i].op), terms[i].a, terms[i].b});
+    }
+    reg->reg.RegisterValueFilter(name, std::move(t));
+  });
+}
+int dp_registry_register_standard_predicates(dp_registry* reg) {
+  DP_REQUIRE(reg);
+  return Guard([&] { reg->reg.RegisterStandardPredicates(); });
+}
 int dp_registry_register_record_reader(dp_registry* reg, const char* name, int64_t records) {
   DP_REQUIRE(reg && name);
   return Guard([&] { reg->reg.RegisterRecordReader(name, records); });

@@ -171,10 +171,35 @@ void UdfRegistry::RegisterDecodeRaw(const std::string& name, int64_t h, int64_t 
   Register(name, std::move(e));
 }
 
+int64_t DevicePredicate::MaxLen() const {
+  int64_t m = INT64_MAX;
+  for (const auto& t : terms)
+    if (t.op == PredicateTerm::Op::kLE) m = std::min(m, t.a);
+  return m;
+}
+
 void UdfRegistry::RegisterLengthFilter(const std::string& name, int64_t max_len) {
   Entry e;
-  e.predicate = LengthPredicate{max_len};
+  e.predicate = DevicePredicate{DevicePredicate::On::kLength, {{PredicateTerm::Op::kLE, max_len, 0}}};
   Register(name, std::move(e));
+}
+
+void UdfRegistry::RegisterValueFilter(const std::string& name, std::vector<PredicateTerm> terms) {
+  if (terms.empty() || terms.size() > 8)
+    throw PipelineError(ErrorCode::kInvalidAttr, "value filter: 1..8 terms");
+  for (const auto& t : terms)
+    if ((t.op == PredicateTerm::Op::kModEq || t.op == PredicateTerm::Op::kModNe) && t.a == 0)
+      throw PipelineError(ErrorCode::kInvalidAttr, "value filter: modulus must be non-zero");
+  Entry e;
+  e.predicate = DevicePredicate{DevicePredicate::On::kValue, std::move(terms)};
+  Register(name, std::move(e));
+}
+
+void UdfRegistry::RegisterStandardPredicates() {
+  if (Contains("keep_even")) return;
+  RegisterValueFilter("keep_even", {{PredicateTerm::Op::kModEq, 2, 0}});
+  RegisterValueFilter("keep_odd", {{PredicateTerm::Op::kModNe, 2, 0}});
+  RegisterValueFilter("keep_all", {{PredicateTerm::Op::kGE, INT64_MIN, 0}});
 }
 
 void UdfRegistry::RegisterRecordReader(const std::string& name, int64_t records) {

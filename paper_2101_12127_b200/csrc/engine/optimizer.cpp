@@ -50,7 +50,10 @@ struct Engine {
     std::string name = "(" + p + ")&&(" + q + ")";
     if (!reg.Contains(name)) {
       UdfRegistry::Entry e;
-      e.predicate = LengthPredicate{std::min(reg.Get(p).predicate->max_len, reg.Get(q).predicate->max_len)};
+      DevicePredicate c = *reg.Get(p).predicate;
+      const auto& tq = reg.Get(q).predicate->terms;
+      c.terms.insert(c.terms.end(), tq.begin(), tq.end());
+      e.predicate = std::move(c);
       reg.Register(name, std::move(e));
     }
     return name;
@@ -86,6 +89,9 @@ struct Engine {
     if (in->kind() != NodeKind::kFilter) return nullptr;
     const std::string &p = in->GetString("udf"), &q = n->GetString("udf");
     if (!IsPred(p) || !IsPred(q)) return nullptr;
+    // device conjunctions hold at most 8 terms on one quantity
+    const auto &pp = *reg.Get(p).predicate, &pq = *reg.Get(q).predicate;
+    if (pp.on != pq.on || pp.terms.size() + pq.terms.size() > 8) return nullptr;
     return Apply(kFilterFilterFusion, path, [&] {
       return Build(NodeKind::kFilter, {in->inputs()[0]}, {{"udf", Conjunction(p, q)}}, reg);
     });

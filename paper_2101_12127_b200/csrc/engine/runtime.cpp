@@ -392,6 +392,10 @@ struct IndexOp {
   std::optional<uint64_t> seed;
   std::string path;
   int64_t parallel = 1;  // interleave num_parallel_calls
+  // filter: the predicate, and the affine maps beneath it (v -> v * mul + add)
+  DevicePredicate pred;
+  int64_t mul = 1, add = 0;
+  bool opaque = false;  // a non-affine map lies beneath the filter
 };
 
 enum class BatchKind { kAffine, kCrop, kResize, kPadded, kIdentityInt };
@@ -446,6 +450,22 @@ Lowered Lower(const DatasetGraph& g, const UdfRegistry& reg) {
       descend();
     }
   }
+  // top-down record of maps and index ops, to give every filter the affine
+  // maps beneath it (a value predicate sees mapped values)
+  std::vector<IndexOp> top_down;
+  struct SeqItem {
+    int op;                           // index into top_down, or -1
+    const std::vector<MapStep>* map;  // a map's steps
+  };
+  std::vector<SeqItem> seq;
+  auto push_filter = [&](const std::string& udf) {
+    const auto& e = reg.Get(udf);
+    if (!e.predicate) Unsupported("filter UDF '" + udf + "' is not a device predicate");
+    IndexOp op{IndexOp::Kind::kFilter, 0, 0, {}, path};
+    op.pred = *e.predicate;
+    top_down.push_back(op);
+    seq.push_back({static_cast<int>(top_down.size()) - 1, nullptr});
+  };
   // ---- batch stage ----
   L.batch_node_path = path;
   L.node_paths.push_back(path);
@@ -457,9 +477,10 @@ Lowered Lower(const DatasetGraph& g, const UdfRegistry& reg) {
     // unfused map(f).map(g)...batch: the same result as the fused rewrite for
     // total UDFs (optimizer.cpp map_map / map_batch fusion)
     while (n->kind() == NodeKind::kMap) {
-      if (n->HasAttr("fused_filter_udf")) Unsupported("map with a fused predicate under batch");
+      if (n->HasAttr("fused_filter_udf")) break;  // map(f) + filter: lowered with the index chain
       const auto& f = reg.Get(n->GetString("udf")).map;
       L.steps.insert(L.steps.begin(), f.begin(), f.end());  // inner maps run first
+      seq.push_back({-1, &f});
       descend();
     }
   } else if (n->kind() == NodeKind::kPaddedBatch) {
@@ -485,7 +506,6 @@ Lowered Lower(const DatasetGraph& g, const UdfRegistry& reg) {
                 NodeKindName(n->kind()));
   }
   // ---- index chain ----
-  std::vector<IndexOp> top_down;
   std::vector<MapStep> below;  // maps under the index ops (e.g. from_file.map(decode).shuffle)
   bool seen_interleave = false;
   for (;;) {
@@ -497,9 +517,7 @@ Lowered Lower(const DatasetGraph& g, const UdfRegistry& reg) {
       if (n->HasAttr("seed")) op.seed = n->GetUint("seed");
       top_down.push_back(op);
     } else if (k == NodeKind::kFilter) {
-      const auto& e = reg.Get(n->GetString("udf"));
-      if (!e.predicate) Unsupported("filter UDF '" + n->GetString("udf") + "' is not a device length predicate");
-      top_down.push_back({IndexOp::Kind::kFilter, e.predicate->max_len, 0, {}, path});
+      push_filter(n->GetString("udf"));
     } else if (k == NodeKind::kRepeat) {
       if (!top_down.empty()) Unsupported("repeat must sit directly under the batch stage");
       top_down.push_back({IndexOp::Kind::kRepeat, n->GetInt("count"), 0, {}, path});
@@ -515,10 +533,12 @@ Lowered Lower(const DatasetGraph& g, const UdfRegistry& reg) {
       // a map is a pure per-element function whose randomness is keyed by the
       // element id (Philox counter), which travels with the element: it
       // commutes with shard / shuffle / repeat and is run in the batch stage
-      if (n->HasAttr("fused_filter_udf")) Unsupported("map with a fused predicate under batch");
+      // map(f) with a fused predicate (map_filter_fusion) = filter(p) above map(f)
+      if (n->HasAttr("fused_filter_udf")) push_filter(n->GetString("fused_filter_udf"));
       if (seen_interleave) Unsupported("map under interleave");
       const auto& f = reg.Get(n->GetString("udf")).map;
       below.insert(below.begin(), f.begin(), f.end());
+      seq.push_back({-1, &f});
     } else if (k == NodeKind::kPrefetch) {
       // prefetch inside the index chain only buffers indices: a no-op here
     } else {
@@ -528,6 +548,28 @@ Lowered Lower(const DatasetGraph& g, const UdfRegistry& reg) {
     descend();
   }
   L.node_paths.push_back(path);
+  {  // bottom-up: the affine maps beneath each filter
+    int64_t mul = 1, add = 0;  // wrap-around int64, as K1
+    bool opaque = false;
+    for (auto it = seq.rbegin(); it != seq.rend(); ++it) {
+      if (it->map) {
+        for (const auto& st : *it->map) {
+          if (st.op == MapStep::Op::kAffine) {
+            mul = static_cast<int64_t>(static_cast<uint64_t>(mul) * static_cast<uint64_t>(st.a));
+            add = static_cast<int64_t>(static_cast<uint64_t>(add) * static_cast<uint64_t>(st.a) +
+                                       static_cast<uint64_t>(st.b));
+          } else {
+            opaque = true;
+          }
+        }
+      } else {
+        IndexOp& op = top_down[it->op];
+        op.mul = mul;
+        op.add = add;
+        op.opaque = opaque;
+      }
+    }
+  }
   L.chain.assign(top_down.rbegin(), top_down.rend());
   L.steps.insert(L.steps.begin(), below.begin(), below.end());
   // ---- source ----
@@ -612,6 +654,13 @@ Lowered Lower(const DatasetGraph& g, const UdfRegistry& reg) {
   }
   // ---- batch kind from source + UDF chain ----
   const SourceData::Kind sk = L.source ? L.source->kind : SourceData::Kind::kInt64;
+  for (const auto& op : L.chain) {
+    if (op.kind != IndexOp::Kind::kFilter) continue;
+    if (op.pred.on == DevicePredicate::On::kLength && sk != SourceData::Kind::kTokens)
+      Unsupported("a length predicate needs token sequences");
+    if (op.pred.on == DevicePredicate::On::kValue && (sk != SourceData::Kind::kInt64 || op.opaque))
+      Unsupported("a value predicate needs int64 elements (after affine maps only)");
+  }
   if (L.kind == BatchKind::kPadded) {
     if (sk != SourceData::Kind::kTokens) Unsupported("padded_batch needs token sequences");
     for (const auto& op : L.chain)
@@ -872,7 +921,8 @@ class DevicePipeline {
                 "lengths");
       max_len_ = lens.empty() ? 0 : *std::max_element(lens.begin(), lens.end());
       for (const auto& op : L_.chain)
-        if (op.kind == IndexOp::Kind::kFilter) max_len_ = std::min<int64_t>(max_len_, std::max<int64_t>(op.a, 0));
+        if (op.kind == IndexOp::Kind::kFilter && op.pred.on == DevicePredicate::On::kLength)
+          max_len_ = std::min<int64_t>(max_len_, std::max<int64_t>(op.pred.MaxLen(), 0));
     }
     EpochPlan& p0 = Plan(0);
     epoch_count_ = p0.count;
@@ -1036,8 +1086,17 @@ class DevicePipeline {
           auto out = alloc(count);
           auto nk = dalloc(sizeof(int64_t));
           auto scratch = dalloc(dp_k_filter_scratch_bytes(count));
-          KCheck(dp_k_filter_len_le(P<int32_t>(L_.source->lengths), count, static_cast<int32_t>(op.a), P<int64_t>(cur),
-                                    P<int64_t>(out), P<int64_t>(nk), scratch.get(), s),
+          std::vector<dp_predicate_term> terms;
+          for (const auto& t : op.pred.terms) terms.push_back({static_cast<int>(t.op), t.a, t.b});
+          const bool on_len = op.pred.on == DevicePredicate::On::kLength;
+          // value predicates: from_memory values, else the position (range /
+          // interleaved record indices)
+          const int64_t* vals =
+              !on_len && L_.source && L_.source->kind == SourceData::Kind::kInt64 ? P<int64_t>(L_.source->values)
+                                                                                  : nullptr;
+          KCheck(dp_k_filter(on_len ? P<int32_t>(L_.source->lengths) : nullptr, vals, count, op.mul, op.add,
+                             terms.data(), static_cast<int>(terms.size()), P<int64_t>(cur), P<int64_t>(out),
+                             P<int64_t>(nk), scratch.get(), s),
                  "filter");
           launches_ += 3;
           int64_t m = 0;

@@ -13,6 +13,7 @@
 #include <cstdint>
 
 #include "common.cuh"
+#include "dpcuda.h"
 #include "status.hpp"
 
 namespace dpk {
@@ -48,23 +49,51 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int* warp_sums, int* 
   return x - v + warp_sums[warp];
 }
 
+// The predicate of one Filter: a conjunction of up to 8 terms on a quantity
+// of the element at position p -- its token-sequence length, its int64
+// value, or the position itself (range) -- after the affine maps beneath the
+// filter (wrap-around int64, as K1).  % is C++'s truncated remainder.
+struct FilterSpec {
+  const int32_t* lengths;
+  const int64_t* values;
+  int64_t mul, add;
+  int nterms;
+  int op[8];
+  int64_t a[8], b[8];
+
+  __device__ __forceinline__ bool keep(int64_t p) const {
+    int64_t v = lengths ? static_cast<int64_t>(lengths[p]) : values ? values[p] : p;
+    v = static_cast<int64_t>(static_cast<uint64_t>(v) * static_cast<uint64_t>(mul) + static_cast<uint64_t>(add));
+    bool k = true;
+    for (int t = 0; t < nterms; ++t) {
+      switch (op[t]) {
+        case DP_PRED_LE: k = k && v <= a[t]; break;
+        case DP_PRED_GE: k = k && v >= a[t]; break;
+        case DP_PRED_LT: k = k && v < a[t]; break;
+        case DP_PRED_MOD_EQ: k = k && v % a[t] == b[t]; break;
+        default: k = k && v % a[t] != b[t]; break;
+      }
+    }
+    return k;
+  }
+};
+
 // Element i of the filtered sequence is source position in_map[i] (or i).
-__device__ __forceinline__ int thread_keep_mask(const int32_t* __restrict__ lengths, const int64_t* __restrict__ in_map,
-                                                int64_t n, int64_t base, int32_t max_keep) {
+__device__ __forceinline__ int thread_keep_mask(const FilterSpec& f, const int64_t* __restrict__ in_map, int64_t n,
+                                                int64_t base) {
   int mask = 0;
 #pragma unroll
   for (int u = 0; u < kItems; ++u) {
     const int64_t i = base + u;
-    if (i < n && lengths[in_map ? in_map[i] : i] <= max_keep) mask |= 1 << u;
+    if (i < n && f.keep(in_map ? in_map[i] : i)) mask |= 1 << u;
   }
   return mask;
 }
 
 __global__ void __launch_bounds__(kThreads)
-filter_count_kernel(const int32_t* __restrict__ lengths, const int64_t* __restrict__ in_map, int64_t n, int32_t max_keep,
-                    int64_t* __restrict__ tile_counts) {
+filter_count_kernel(FilterSpec f, const int64_t* __restrict__ in_map, int64_t n, int64_t* __restrict__ tile_counts) {
   const int64_t base = static_cast<int64_t>(blockIdx.x) * kTile + static_cast<int64_t>(threadIdx.x) * kItems;
-  int c = __popc(thread_keep_mask(lengths, in_map, n, base, max_keep));
+  int c = __popc(thread_keep_mask(f, in_map, n, base));
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
   __shared__ int warp_counts[kThreads / 32];
@@ -115,13 +144,12 @@ filter_scan_kernel(int64_t* __restrict__ tile_counts, int64_t tiles, int64_t* __
 }
 
 __global__ void __launch_bounds__(kThreads)
-filter_scatter_kernel(const int32_t* __restrict__ lengths, int64_t n, int32_t max_keep,
-                      const int64_t* __restrict__ tile_offsets, const int64_t* __restrict__ in_map,
-                      int64_t* __restrict__ kept) {
+filter_scatter_kernel(FilterSpec f, int64_t n, const int64_t* __restrict__ tile_offsets,
+                      const int64_t* __restrict__ in_map, int64_t* __restrict__ kept) {
   __shared__ int warp_sums[kThreads / 32];
   __shared__ int total;
   const int64_t base = static_cast<int64_t>(blockIdx.x) * kTile + static_cast<int64_t>(threadIdx.x) * kItems;
-  const int mask = thread_keep_mask(lengths, in_map, n, base, max_keep);
+  const int mask = thread_keep_mask(f, in_map, n, base);
   int off = block_exclusive_scan(__popc(mask), warp_sums, &total);
   int64_t dst = tile_offsets[blockIdx.x] + off;
 #pragma unroll
@@ -239,8 +267,8 @@ extern "C" size_t dp_k_filter_scratch_bytes(int64_t n) {
   return static_cast<size_t>(tiles < 1 ? 1 : tiles) * sizeof(int64_t);
 }
 
-extern "C" int dp_k_filter_len_le(const int32_t* lengths, int64_t n, int32_t max_keep, const int64_t* in_map,
-                                  int64_t* kept, int64_t* num_kept_dev, void* scratch, void* stream) {
+static int filter_impl(const FilterSpec& f, int64_t n, const int64_t* in_map, int64_t* kept, int64_t* num_kept_dev,
+                       void* scratch, void* stream) {
   if (n < 0) return fail(DP_ERR_INVALID_ATTR, "filter: n must be >= 0");
   if (!num_kept_dev || !scratch) return fail(DP_ERR_INVALID_ATTR, "filter: null num_kept/scratch");
   cudaStream_t s = as_stream(stream);
@@ -248,10 +276,44 @@ extern "C" int dp_k_filter_len_le(const int32_t* lengths, int64_t n, int32_t max
   const int64_t tiles = (n + kTile - 1) / kTile;
   if (tiles > 0x7fffffff) return fail(DP_ERR_INVALID_ATTR, "filter: n too large");
   int64_t* tile = static_cast<int64_t*>(scratch);
-  filter_count_kernel<<<static_cast<int>(tiles), kThreads, 0, s>>>(lengths, in_map, n, max_keep, tile);
+  filter_count_kernel<<<static_cast<int>(tiles), kThreads, 0, s>>>(f, in_map, n, tile);
   filter_scan_kernel<<<1, 1024, 0, s>>>(tile, tiles, num_kept_dev);
-  filter_scatter_kernel<<<static_cast<int>(tiles), kThreads, 0, s>>>(lengths, n, max_keep, tile, in_map, kept);
-  return launch_status("filter_len_le");
+  filter_scatter_kernel<<<static_cast<int>(tiles), kThreads, 0, s>>>(f, n, tile, in_map, kept);
+  return launch_status("filter");
+}
+
+extern "C" int dp_k_filter_len_le(const int32_t* lengths, int64_t n, int32_t max_keep, const int64_t* in_map,
+                                  int64_t* kept, int64_t* num_kept_dev, void* scratch, void* stream) {
+  if (!lengths && n > 0) return fail(DP_ERR_INVALID_ATTR, "filter: null lengths");
+  FilterSpec f{};
+  f.lengths = lengths;
+  f.mul = 1;
+  f.nterms = 1;
+  f.op[0] = DP_PRED_LE;
+  f.a[0] = max_keep;
+  return filter_impl(f, n, in_map, kept, num_kept_dev, scratch, stream);
+}
+
+extern "C" int dp_k_filter(const int32_t* lengths, const int64_t* values, int64_t n, int64_t mul, int64_t add,
+                           const dp_predicate_term* terms, int num_terms, const int64_t* in_map, int64_t* kept,
+                           int64_t* num_kept_dev, void* scratch, void* stream) {
+  if (num_terms < 1 || num_terms > 8 || !terms) return fail(DP_ERR_INVALID_ATTR, "filter: 1..8 predicate terms");
+  FilterSpec f{};
+  f.lengths = lengths;
+  f.values = lengths ? nullptr : values;
+  f.mul = mul;
+  f.add = add;
+  f.nterms = num_terms;
+  for (int t = 0; t < num_terms; ++t) {
+    if (terms[t].op < DP_PRED_LE || terms[t].op > DP_PRED_MOD_NE)
+      return fail(DP_ERR_INVALID_ATTR, "filter: unknown predicate op");
+    if ((terms[t].op == DP_PRED_MOD_EQ || terms[t].op == DP_PRED_MOD_NE) && terms[t].a == 0)
+      return fail(DP_ERR_INVALID_ATTR, "filter: modulus must be non-zero");
+    f.op[t] = terms[t].op;
+    f.a[t] = terms[t].a;
+    f.b[t] = terms[t].b;
+  }
+  return filter_impl(f, n, in_map, kept, num_kept_dev, scratch, stream);
 }
 
 extern "C" int dp_k_batch_max_len(const int32_t* lengths, const int64_t* kept, int64_t num_kept, int64_t batch,

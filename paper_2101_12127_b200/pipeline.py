@@ -56,6 +56,8 @@ _SIGS = {
                                        ctypes.POINTER(ctypes.c_float)],
     "dp_registry_register_length_filter": [c_vp, ctypes.c_char_p, c_i64],
     "dp_registry_register_record_reader": [c_vp, ctypes.c_char_p, c_i64],
+    "dp_registry_register_value_filter": [c_vp, ctypes.c_char_p, c_vp, c_int],
+    "dp_registry_register_standard_predicates": [c_vp],
     "dp_registry_register_decode_raw": [c_vp, ctypes.c_char_p, c_i64, c_i64],
     "dp_registry_contains": [c_vp, ctypes.c_char_p],
     "dp_source_synthetic_images": [c_i64, c_i64, c_i64, c_u64, c_int, PP],
@@ -175,6 +177,20 @@ class Registry:
     def register_length_filter(self, name, max_len):
         _check(L().dp_registry_register_length_filter(self.h, _b(name), max_len))
         return name
+
+    PRED = {"le": 0, "ge": 1, "lt": 2, "mod_eq": 3, "mod_ne": 4}
+
+    def register_value_filter(self, name, terms):
+        """Predicate on int64 element values: [("mod_eq", 2, 0), ("lt", 100), ...], all must hold."""
+        class Term(ctypes.Structure):
+            _fields_ = [("op", c_int), ("a", c_i64), ("b", c_i64)]
+        arr = (Term * max(1, len(terms)))(*[Term(self.PRED[t[0]], t[1], t[2] if len(t) > 2 else 0) for t in terms])
+        _check(L().dp_registry_register_value_filter(self.h, _b(name), ctypes.cast(arr, c_vp), len(terms)))
+        return name
+
+    def register_standard_predicates(self):
+        """keep_even / keep_odd / keep_all, as the reference's pipeline_spec registers them."""
+        _check(L().dp_registry_register_standard_predicates(self.h))
 
     def register_record_reader(self, name, records):
         _check(L().dp_registry_register_record_reader(self.h, _b(name), records))

@@ -125,6 +125,17 @@ def main():
                      "order": ids.tolist()})
     g["interleave_var"] = ivar
 
+    # value filters (keep_even / keep_odd after an affine map), unoptimized and
+    # optimized (map_filter_fusion), with and without a shuffle after them
+    vf = []
+    for (n, a, b, odd, buf) in ((1000, 3, 1, 0, 0), (1000, 3, 1, 1, 0), (5000, -7, 2, 0, 300), (777, 1, 0, 1, 50)):
+        for opt in (0, 1):
+            vals, graph = ref.filter_values(n, a, b, odd, buf, opt)
+            vf.append({"n": n, "a": a, "b": b, "odd": odd, "shuffle": buf, "optimize": opt,
+                       "count": int(vals.size), "first": vals[:6].tolist(), "fnv": f"{orc.fnv_digest(vals):016x}",
+                       "graph": graph})
+    g["value_filters"] = vf
+
     ser = []
     for which in range(6):  # pipeline shapes: oracle/ref_shim.cpp ref_serialize_pipeline
         b, fp = ref.serialize_pipeline(which)

@@ -279,6 +279,15 @@ class Reference:
                                               shuffle_seed, base_seed, P(out), P(cnt)))
         return out[: cnt[0]]
 
+    def filter_values(self, n, a, b, odd, shuffle_buffer=0, optimize=True):
+        out = np.zeros(max(n, 1), np.int64)
+        cnt = np.zeros(1, np.int64)
+        txt = ctypes.create_string_buffer(4096)
+        self.L.ref_filter_values.argtypes = [i64, i64, i64, c_int, i64, c_int, vp, vp, vp, ctypes.c_size_t]
+        self._check(self.L.ref_filter_values(n, a, b, int(odd), shuffle_buffer, int(optimize), P(out), P(cnt),
+                                             ctypes.cast(txt, vp), len(txt)))
+        return out[: cnt[0]], txt.value.decode()
+
     def interleave_var_ids(self, lengths, cycle, parallel=1, shard=None, base_seed=1):
         lengths = np.ascontiguousarray(lengths, np.int64)
         k, g = shard if shard else (0, 0)

@@ -212,3 +212,34 @@ def test_bucket_by_length_attr_validation():
     with pytest.raises(DpError) as e:
         base.bucket_by_length([5], [1, 2])
     assert e.value.code == dp.ERR["TypeMismatch"]
+
+
+def test_value_filter_optimizes_like_the_reference():
+    """from_memory -> map(affine) -> filter(keep_even/odd) [-> shuffle] ->
+    batch: Optimize rewrites it to the same node chain as the compiled
+    reference (golden value_filters: map_filter_fusion, then no map_batch
+    fusion because of the fused predicate)."""
+    import json, os
+    golden = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "golden.json")))["value_filters"]
+    for c in golden:
+        reg = dp.Registry()
+        reg.register_standard_predicates()
+        f = reg.register_affine(f"affine({c['a']},{c['b']})", c["a"], c["b"])
+        g = dp.Dataset.from_memory(reg, range(c["n"])).map(f).filter("keep_odd" if c["odd"] else "keep_even")
+        if c["shuffle"]:
+            g = g.shuffle(c["shuffle"], 42)
+        g = g.batch(64)
+        if c["optimize"]:
+            g = g.optimize()[0]
+        chain = "<-".join(line.split()[0] for line in str(g).splitlines())
+        assert chain == c["graph"], (chain, c)
+
+
+def test_value_filter_validation():
+    reg = dp.Registry()
+    with pytest.raises(DpError) as e:
+        reg.register_value_filter("bad", [("mod_eq", 0, 0)])
+    assert e.value.code == dp.ERR["InvalidAttr"]
+    with pytest.raises(DpError) as e:
+        reg.register_value_filter("many", [("lt", 5)] * 9)
+    assert e.value.code == dp.ERR["InvalidAttr"]

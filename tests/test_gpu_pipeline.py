@@ -103,6 +103,39 @@ def shuffle_ids(dp, n, buffer, seed, base_seed, shard=None, repeat=None, optimiz
     return np.concatenate([b[0] for b in drain(dp.make_iterator(g, seed_override=base_seed))])
 
 
+def test_value_filters_equal_the_reference(dp, orc):
+    """keep_even / keep_odd after an affine map, unoptimized and optimized
+    (map_filter_fusion), with a shuffle after the filter: the emitted values
+    equal the compiled reference's (golden value_filters)."""
+    for c in GOLDEN["value_filters"]:
+        reg = dp.Registry()
+        reg.register_standard_predicates()
+        f = reg.register_affine(f"affine({c['a']},{c['b']})", c["a"], c["b"])
+        g = dp.Dataset.from_memory(reg, range(c["n"])).map(f).filter("keep_odd" if c["odd"] else "keep_even")
+        if c["shuffle"]:
+            g = g.shuffle(c["shuffle"], 42)
+        g = g.batch(64)
+        if c["optimize"]:
+            g = g.optimize()[0]
+        vals = np.concatenate([b[0] for b in drain(dp.make_iterator(g, seed_override=1))])
+        assert vals.size == c["count"] and vals[:6].tolist() == c["first"] and fnv(orc, vals) == c["fnv"], c
+    # range source, a conjunction of terms, a filter between two maps
+    reg = dp.Registry()
+    reg.register_affine("x2", 2, 0)
+    reg.register_affine("p5", 1, 5)
+    reg.register_value_filter("window", [("ge", 100), ("lt", 900), ("mod_ne", 3, 1)])
+    g = dp.Dataset.range(reg, 1000).map("x2").filter("window").map("p5").batch(50)
+    got = np.concatenate([b[0] for b in drain(dp.make_iterator(g, seed_override=1))])
+    x = np.arange(1000) * 2
+    want = x[(x >= 100) & (x < 900) & (np.fmod(x, 3) != 1)] + 5
+    assert got.tolist() == want.tolist()
+    with pytest.raises(dp.DpError):  # a value predicate on images
+        reg2 = image_registry(dp, 0, crop=(32, 32))
+        reg2.register_standard_predicates()
+        src = dp.Source.synthetic_images(10, 48, 48)
+        dp.make_iterator(dp.Dataset.tensor_slices(reg2, src).filter("keep_even").map("crop").map("norm").batch(4))
+
+
 def test_shuffle_order_matches_reference(dp, orc):
     for c in GOLDEN["shuffle"]:
         got = shuffle_ids(dp, c["n"], c["buffer"], c["seed"], c["base_seed"])

@@ -102,6 +102,7 @@ class Value {
 
   Kind kind() const { return static_cast<Kind>(v_.index()); }
   int64_t int64() const { return std::get<int64_t>(v_); }
+  const int64_t* int64_ptr() const { return &std::get<int64_t>(v_); }  // stable while the Value lives
   double float64() const { return std::get<double>(v_); }
   const std::string& bytes() const { return std::get<BytesBox>(v_).data; }
   bool boolean() const { return std::get<BoolBox>(v_).data; }

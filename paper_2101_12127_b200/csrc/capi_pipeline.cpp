@@ -344,8 +344,16 @@ int dp_iterator_get_next(dp_iterator* it, dp_batch* batch) {
     batch->num_components = static_cast<int>(std::min<size_t>(held->arity(), 4));
     batch->index = it->it->root_delivered() - 1;
     for (int c = 0; c < batch->num_components; ++c) {
-      const Tensor& t = held->component(c).tensor();
       dp_tensor& d = batch->components[c];
+      const Value& v = held->component(c);
+      if (v.kind() == Value::Kind::kInt64) {  // unbatched int64 value: a 0-d host tensor
+        d.dtype = static_cast<int>(DType::kInt64);
+        d.ndim = 0;
+        d.data = const_cast<int64_t*>(v.int64_ptr());
+        d.on_host = 1;
+        continue;
+      }
+      const Tensor& t = v.tensor();
       d.dtype = static_cast<int>(t.dtype);
       d.ndim = static_cast<int>(std::min<size_t>(t.shape.size(), 6));
       for (int k = 0; k < d.ndim; ++k) d.shape[k] = t.shape[k];
@@ -421,6 +429,11 @@ int dp_tensor_copy_to_host(const dp_batch* batch, int component, void* dst, size
     const auto* e = static_cast<const Element*>(batch->handle);
     if (component < 0 || component >= static_cast<int>(e->arity()))
       throw PipelineError(ErrorCode::kInvalidAttr, "component out of range");
+    if (e->component(component).kind() == Value::Kind::kInt64) {
+      if (bytes < sizeof(int64_t)) throw PipelineError(ErrorCode::kInvalidAttr, "destination too small");
+      std::memcpy(dst, e->component(component).int64_ptr(), sizeof(int64_t));
+      return;
+    }
     const Tensor& t = e->component(component).tensor();
     if (bytes < t.nbytes()) throw PipelineError(ErrorCode::kInvalidAttr, "destination too small");
     if (t.ready) {

@@ -406,6 +406,10 @@ struct Lowered {
   BatchKind kind = BatchKind::kIdentityInt;
   int64_t batch = 1;     // bucket_by_length: the largest bucket batch size
   bool drop = false;
+  // no batch stage: GetNext delivers single elements (MapIterator and the
+  // index ops as roots, runtime.cpp:480-535); the device still works in
+  // internal batches of `batch` elements, served one by one
+  bool unbatched = false;
   // bucket_by_length (a padded kind with per-bucket windows, K8)
   bool bucketed = false;
   std::vector<int32_t> bucket_bounds;
@@ -501,9 +505,17 @@ Lowered Lower(const DatasetGraph& g, const UdfRegistry& reg) {
     L.drop = n->GetBoolOr("drop_remainder", false);
     descend();
   } else {
-    Unsupported(std::string("the root must be a batch stage (map_and_batch / batch / padded_batch / "
-                            "bucket_by_length), got ") +
-                NodeKindName(n->kind()));
+    // no batch stage: single elements (the maps under the root run in the
+    // internal batch kernels, as under a batch)
+    L.unbatched = true;
+    L.batch_node_path.clear();
+    while (n->kind() == NodeKind::kMap) {
+      if (n->HasAttr("fused_filter_udf")) break;
+      const auto& f = reg.Get(n->GetString("udf")).map;
+      L.steps.insert(L.steps.begin(), f.begin(), f.end());
+      seq.push_back({-1, &f});
+      descend();
+    }
   }
   // ---- index chain ----
   std::vector<MapStep> below;  // maps under the index ops (e.g. from_file.map(decode).shuffle)
@@ -692,6 +704,11 @@ Lowered Lower(const DatasetGraph& g, const UdfRegistry& reg) {
   }
   // (interleave without a record source emits the int64 record indices
   // themselves: the batch stage gathers them like a range)
+  if (L.unbatched) {
+    if (sk == SourceData::Kind::kTokens) Unsupported("unbatched token sequences: use padded_batch / bucket_by_length");
+    L.batch = L.kind == BatchKind::kAffine || L.kind == BatchKind::kIdentityInt ? 4096 : 64;  // internal unit
+    L.drop = false;
+  }
   return L;
 }
 
@@ -722,6 +739,7 @@ struct Slot {
   bool release_recorded = false;
   // group bookkeeping
   int64_t first_batch = 0, num_batches = 0, handed_out = 0;
+  int64_t units = 0;  // what GetNext hands out from this slot: batches, or elements when unbatched
   std::atomic<int64_t> outstanding{0};
   bool busy = false;
   std::vector<int64_t> batch_off_a, batch_off_b, batch_rows, batch_cols;
@@ -810,11 +828,14 @@ class DevicePipeline {
   // group go out (Shared::slots_freed).
   std::optional<Element> Next() {
     if (done_) return std::nullopt;
-    const int64_t i = next_batch_;
-    if (total_batches_ >= 0 && i >= total_batches_) {
+    const int64_t u = next_batch_;  // the unit GetNext hands out: a batch, or an element when unbatched
+    const int64_t total = L_.unbatched ? total_units_ : total_batches_;
+    if (total >= 0 && u >= total) {
       done_ = true;
       return std::nullopt;
     }
+    int64_t row = 0;
+    const int64_t i = L_.unbatched ? BatchOfElement(u, row) : u;  // internal batch
     const int64_t grp = GroupOf(i);
     using Clock = std::chrono::steady_clock;
     const auto t0 = debug_timing_ ? Clock::now() : Clock::time_point{};
@@ -832,22 +853,26 @@ class DevicePipeline {
         cur_slot_ = group_slot_.at(grp);
         cur_group_ = grp;
         {
-          // after a Seek into the middle of a group, the skipped batches count as handed out
+          // after a Seek into the middle of a group, the skipped units count as handed out
           std::lock_guard lk(shared_->mu);
-          if (cur_slot_->handed_out < i - cur_slot_->first_batch) cur_slot_->handed_out = i - cur_slot_->first_batch;
+          const int64_t before = UnitsBefore(*cur_slot_, i, row);
+          if (cur_slot_->handed_out < before) cur_slot_->handed_out = before;
         }
         // one wait per group: the slot's ready event covers all its batches
         if (consumer_ != stream_ && !opt_.host_output)
           CudaCheck(cudaStreamWaitEvent(consumer_, cur_slot_->ready, 0), "wait");
+        // unbatched: element values are read on the host (the reference
+        // returns int64 values, not device tensors)
+        if (L_.unbatched) CudaCheck(cudaEventSynchronize(cur_slot_->ready), "unbatched values");
         MaybeAutotune();
       }
     }
     const auto t1 = debug_timing_ ? Clock::now() : Clock::time_point{};
     next_batch_++;
     produced_++;
-    if (!debug_timing_) return MakeElement(cur_slot_, i);
+    if (!debug_timing_) return L_.unbatched ? MakeUnitElement(cur_slot_, i, row) : MakeElement(cur_slot_, i);
     const auto t2 = Clock::now();
-    auto e = MakeElement(cur_slot_, i);
+    auto e = L_.unbatched ? MakeUnitElement(cur_slot_, i, row) : MakeElement(cur_slot_, i);
     const auto t3 = Clock::now();
     dbg_[0] += std::chrono::duration<double>(t1 - t0).count();
     dbg_[1] += std::chrono::duration<double>(t2 - t1).count();
@@ -949,12 +974,40 @@ class DevicePipeline {
       (void)gpe;
     }
     total_groups_ = -1;  // computed lazily via GroupRange
+    if (L_.unbatched) {
+      if (span_epochs_) {
+        const int64_t rows = TotalRows();
+        total_units_ = rows == INT64_MAX ? (epoch_count_ == 0 ? 0 : -1) : rows;
+      } else {
+        total_units_ = L_.outer_repeat == kInfiniteRepeat ? (epoch_count_ == 0 ? 0 : -1)
+                                                          : epoch_count_ * L_.outer_repeat;
+      }
+    }
   }
 
   // Batches of group g: [first, first + n).  Groups never straddle the
   // boundary of a non-spanning epoch, so every group is one contiguous range
   // of one epoch plan (plus the next epoch's head when spanning).
   // Launch group holding batch i (inverse of GroupRange).
+  // unbatched: element u -> internal batch and row (batches never straddle a
+  // non-spanning epoch)
+  int64_t BatchOfElement(int64_t u, int64_t& row) const {
+    if (span_epochs_ || epoch_count_ == 0) {
+      row = u % L_.batch;
+      return u / L_.batch;
+    }
+    const int64_t e = u / epoch_count_, off = u - e * epoch_count_;
+    row = off % L_.batch;
+    return e * batches_per_epoch_ + off / L_.batch;
+  }
+  // units of `s` handed out before (batch i, row)
+  int64_t UnitsBefore(const Slot& s, int64_t i, int64_t row) const {
+    if (!L_.unbatched) return i - s.first_batch;
+    int64_t n = row;
+    for (int64_t b = s.first_batch; b < i; ++b) n += s.batch_rows[b - s.first_batch];
+    return n;
+  }
+
   int64_t GroupOf(int64_t i) const {
     if (span_epochs_) return i / group_;
     const int64_t bpe = std::max<int64_t>(batches_per_epoch_, 1);
@@ -968,13 +1021,15 @@ class DevicePipeline {
   void Seek(int64_t n) {
     if (produced_ != 0 || issued_groups_ != 0)
       throw PipelineError(ErrorCode::kInternal, "Seek needs a fresh iterator");
-    if (n < 0 || (total_batches_ >= 0 && n > total_batches_))
+    const int64_t total = L_.unbatched ? total_units_ : total_batches_;
+    if (n < 0 || (total >= 0 && n > total))
       throw PipelineError(ErrorCode::kCorruptBlob, "checkpoint claims " + std::to_string(n) +
                                                        " delivered elements but the pipeline has " +
-                                                       std::to_string(total_batches_));
+                                                       std::to_string(total));
     next_batch_ = n;
     produced_ = n;
-    issued_groups_ = GroupOf(n);
+    int64_t row = 0;
+    issued_groups_ = GroupOf(L_.unbatched ? BatchOfElement(n, row) : n);
   }
 
  private:
@@ -1312,6 +1367,8 @@ class DevicePipeline {
     if (opt_.host_output) {
       slot->ha = PinnedAlloc(slot->a_bytes);
       if (slot->b_bytes) slot->hb = PinnedAlloc(slot->b_bytes);
+    } else if (L_.unbatched) {
+      slot->ha = PinnedAlloc(slot->a_bytes);  // host copy of the values / ids
     }
     CudaCheck(cudaEventCreateWithFlags(&slot->ready, cudaEventDisableTiming), "event");
     CudaCheck(cudaEventCreateWithFlags(&slot->release, cudaEventDisableTiming), "event");
@@ -1324,7 +1381,7 @@ class DevicePipeline {
   std::shared_ptr<Slot> FindFreeSlot(bool may_grow) {
     for (auto& s : slots_) {
       std::lock_guard lk(shared_->mu);
-      if (!s->busy || (s->handed_out == s->num_batches && s->outstanding.load() == 0)) return s;
+      if (!s->busy || (s->handed_out == s->units && s->outstanding.load() == 0)) return s;
     }
     const size_t need = (batch_bytes_.first + batch_bytes_.second) * group_;
     if (static_cast<int64_t>(slots_.size()) < depth_ || may_grow) {
@@ -1357,6 +1414,7 @@ class DevicePipeline {
       slot->release_recorded = false;
       slot->first_batch = first;
       slot->num_batches = nb;
+      slot->units = nb;  // unbatched: set to the element count below
       slot->handed_out = 0;
       slot->outstanding = 0;
     }
@@ -1483,8 +1541,19 @@ class DevicePipeline {
       if (b_used) CudaCheck(cudaMemcpyAsync(slot->hb.get(), slot->b.get(), b_used, cudaMemcpyDeviceToHost, copy_stream_), "d2h");
       CudaCheck(cudaEventRecord(slot->ready, copy_stream_), "event");
       d2h_bytes_ += a_used + b_used;
+    } else if (L_.unbatched) {
+      // element values / ids are served as host int64 values
+      CudaCheck(cudaMemcpyAsync(slot->ha.get(), slot->a.get(), UsedBytesA(*slot), cudaMemcpyDeviceToHost, stream_),
+                "d2h values");
+      CudaCheck(cudaEventRecord(slot->ready, stream_), "event");
     } else {
       CudaCheck(cudaEventRecord(slot->ready, stream_), "event");
+    }
+    if (L_.unbatched) {
+      std::lock_guard lk(shared_->mu);
+      int64_t units = 0;
+      for (auto r : slot->batch_rows) units += r;
+      slot->units = units;
     }
     group_slot_[g] = slot;
     for (auto it = group_slot_.begin(); it != group_slot_.end() && it->first < g - 2 * depth_ - 4;)
@@ -1530,7 +1599,7 @@ class DevicePipeline {
       // dropped (TryIssueGroup), so one release event, recorded on the
       // consumer stream by the last drop, orders every batch's consumer work
       // before the rewrite (one API call per group, not per batch).
-      if (--slot->outstanding == 0 && slot->handed_out == slot->num_batches && shared->alive) {
+      if (--slot->outstanding == 0 && slot->handed_out == slot->units && shared->alive) {
         cudaEventRecord(slot->release, consumer);
         slot->release_recorded = true;
         shared->slots_freed.fetch_add(1, std::memory_order_release);
@@ -1571,6 +1640,50 @@ class DevicePipeline {
         break;
     }
     return Element(std::move(comps));
+  }
+
+  // unbatched: element `row` of internal batch i -- (int64 value) or (int64
+  // id, tensor [h, w, 3] view into the slot), as MapIterator delivers them
+  Element MakeUnitElement(const std::shared_ptr<Slot>& slot, int64_t i, int64_t row) {
+    const int64_t k = i - slot->first_batch;
+    {
+      std::lock_guard lk(shared_->mu);
+      slot->handed_out++;
+      slot->outstanding++;
+    }
+    cudaStream_t consumer = consumer_;
+    std::shared_ptr<void> lease(nullptr, [slot, consumer, shared = shared_](void*) {
+      std::lock_guard lk(shared->mu);
+      if (--slot->outstanding == 0 && slot->handed_out == slot->units && shared->alive) {
+        cudaEventRecord(slot->release, consumer);
+        slot->release_recorded = true;
+        shared->slots_freed.fetch_add(1, std::memory_order_release);
+      }
+    });
+    const int64_t idx = slot->batch_off_a[k] / static_cast<int64_t>(sizeof(int64_t)) + row;
+    const int64_t value = static_cast<const int64_t*>(slot->ha.get())[idx];
+    std::vector<Value> comps;
+    comps.reserve(2);
+    comps.push_back(Value::Int64(value));
+    if (L_.kind == BatchKind::kCrop || L_.kind == BatchKind::kResize) {
+      const int64_t oh = L_.kind == BatchKind::kCrop ? L_.crop.out_h : L_.resize.out_h;
+      const int64_t ow = L_.kind == BatchKind::kCrop ? L_.crop.out_w : L_.resize.out_w;
+      Tensor t;
+      t.dtype = DType::kFloat32;
+      t.shape = {oh, ow, 3};
+      t.data = static_cast<uint8_t*>(slot->b.get()) + slot->batch_off_b[k] + row * oh * ow * 3 * sizeof(float);
+      t.residency = Residency::kDevice;
+      t.device = opt_.device;
+      t.owner = lease;
+      t.ready = slot->ready;
+      comps.push_back(Value::FromTensor(std::move(t)));
+    } else {
+      // the value was copied out: the slot can go as soon as this returns
+      comps.reserve(1);
+    }
+    Element e(std::move(comps));
+    if (L_.kind != BatchKind::kCrop && L_.kind != BatchKind::kResize) lease.reset();
+    return e;
   }
 
   // AUTOTUNE prefetch: depth = ceil(host issue time / device time per group)
@@ -1662,6 +1775,7 @@ class DevicePipeline {
   int64_t group_ = 1;
   bool span_epochs_ = false;
   int64_t epoch_count_ = 0, batches_per_epoch_ = 0, total_batches_ = 0, total_groups_ = -1;
+  int64_t total_units_ = 0;  // unbatched: elements (-1 = infinite)
   std::map<int64_t, EpochPlan> plans_;
   cudaEvent_t retire_ev_ = nullptr;
   int64_t batches_launched_ = 0;

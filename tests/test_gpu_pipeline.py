@@ -136,6 +136,53 @@ def test_value_filters_equal_the_reference(dp, orc):
         dp.make_iterator(dp.Dataset.tensor_slices(reg2, src).filter("keep_even").map("crop").map("norm").batch(4))
 
 
+def test_unbatched_pipelines(dp, orc):
+    """No batch stage: GetNext delivers single elements, as MapIterator /
+    ShuffleIterator roots do (int64 values on the host; images as (id,
+    device tensor[h, w, 3]))."""
+    reg = image_registry(dp, 0, crop=(32, 32))
+    reg.register_affine("aff", 3, 1)
+    reg.register_standard_predicates()
+
+    def elems(g, comps=(0,), **kw):
+        it = dp.make_iterator(g, seed_override=1, **kw)
+        out = []
+        while (b := it.get_next()) is not None:
+            out.append([b.numpy(c) for c in comps])
+            b.release()
+        return out
+
+    got = [int(e[0]) for e in elems(dp.Dataset.range(reg, 10000).map("aff"))]
+    assert got == (np.arange(10000) * 3 + 1).tolist()
+    got = [int(e[0]) for e in elems(dp.Dataset.from_memory(reg, np.arange(5000) * 7).shuffle(300, 42).map("aff"))]
+    order = orc.shuffle_order(5000, 300, orc.shuffle_seed(1, 42))
+    assert got == (order * 7 * 3 + 1).tolist()
+    got = [int(e[0]) for e in elems(dp.Dataset.range(reg, 3000).map("aff").filter("keep_even").repeat(2))]
+    x = np.arange(3000) * 3 + 1
+    assert got == x[x % 2 == 0].tolist() * 2
+    # images: single (id, image) elements equal the rows of the batched pipeline
+    src = dp.Source.synthetic_images(300, 48, 48)
+    base = dp.Dataset.tensor_slices(reg, src).shuffle(100, 5).map("crop").map("norm")
+    single = elems(base, comps=(0, 1))
+    batched = drain(dp.make_iterator(base.batch(64), seed_override=1), comps=(0, 1))
+    ids = np.concatenate([b[0] for b in batched])
+    pix = np.concatenate([b[1] for b in batched])
+    assert [int(e[0]) for e in single] == ids.tolist()
+    assert all(np.array_equal(e[1], pix[r]) for r, e in enumerate(single))
+    # checkpoint in the middle of an unbatched, repeated pipeline
+    g = dp.Dataset.range(reg, 5000).shuffle(700, 2).map("aff").repeat(3)
+    full = [int(e[0]) for e in elems(g)]
+    it = dp.make_iterator(g, seed_override=1)
+    for _ in range(7777):
+        it.get_next().release()
+    rest = []
+    r_it = dp.restore(g, it.save())
+    while (b := r_it.get_next()) is not None:
+        rest.append(int(b.numpy(0)))
+        b.release()
+    assert rest == full[7777:]
+
+
 def test_shuffle_order_matches_reference(dp, orc):
     for c in GOLDEN["shuffle"]:
         got = shuffle_ids(dp, c["n"], c["buffer"], c["seed"], c["base_seed"])
@@ -635,8 +682,8 @@ def test_edge_cases(dp, orc):
 
 def test_unsupported_graph_fails_loudly(dp):
     reg = dp.Registry()
-    reg.register_affine("a", 1, 1)
-    g = dp.Dataset.range(reg, 10).map("a")  # no batch: no device lowering
+    src = dp.Source.synthetic_tokens(10, 20, 1, 1)
+    g = dp.Dataset.token_sequences(reg, src)  # ragged sequences without a padded batch
     with pytest.raises(Exception) as e:
         dp.make_iterator(g)
     assert "device lowering" in str(e.value)

@@ -53,6 +53,10 @@ CFG = {
     "cfg4": dict(workload="1M int32 token sequences, len U[1,1024] -> Filter(len<=512) -> PaddedBatch(128, pad 0)",
                  kind="tokens", batch=128, n=1_000_000, max_keep=512, kernel="K5 padded_batches",
                  unit="sequences/s", dtype="int32"),
+    "cfg4r": dict(workload="1M int32 token sequences, len U[1,1024] -> Filter(len<=512) -> Batch(128) (the "
+                           "reference's own cfg4 graph: ragged batches, values + int64 row splits)",
+                  kind="tokens", batch=128, n=1_000_000, max_keep=512, kernel="K5 ragged_batches",
+                  unit="sequences/s", dtype="int32", ragged=True),
     "cfg4b": dict(workload="1M int32 token sequences, len U[1,1024] -> Filter(len<=512) -> Shuffle(10k, seed 42) -> "
                            "BucketByLength(boundaries 128/256/384, batch sizes 256/128/96/64, pad 0)",
                   kind="tokens", batch=128, n=1_000_000, max_keep=512, kernel="K8 bucket_batches",
@@ -261,6 +265,8 @@ def build_other_graph(dp, cfg, local, rank, world):
         g = dp.Dataset.token_sequences(reg, src).filter("len<=512")
         if cfg.get("bucket"):  # cfg4b
             g = g.shuffle(10000, 42).bucket_by_length(*cfg["bucket"])
+        elif cfg.get("ragged"):  # cfg4r: the reference graph, Batch of sequences
+            g = g.batch(cfg["batch"])
         else:
             g = g.padded_batch(cfg["batch"])
         g = g.repeat(-1).prefetch(-1)
@@ -277,9 +283,14 @@ def padded_stats(dp, g, local):
     total = rows_total = 0
     for _ in range(per_epoch):
         b = it.get_next()
-        lens = b.numpy(1)
-        rows, lmax = b.components[0][1]
-        total += 4 * int(lens.sum()) + rows * (8 + 4 + 8) + 4 * rows * lmax + 4 * rows
+        if len(b.components[0][1]) == 1:  # ragged: (values, row splits)
+            splits = b.numpy(1)
+            rows, toks = splits.size - 1, int(splits[-1])
+            total += 4 * toks + rows * (8 + 4 + 8) + 4 * toks + 8 * (rows + 1)
+        else:
+            lens = b.numpy(1)
+            rows, lmax = b.components[0][1]
+            total += 4 * int(lens.sum()) + rows * (8 + 4 + 8) + 4 * rows * lmax + 4 * rows
         rows_total += rows
         b.release()
     return total / per_epoch, rows_total / per_epoch

@@ -189,6 +189,21 @@ int dp_k_padded_batches(const int32_t* tokens, const int64_t* offsets, const int
                         const int32_t* lmax_dev, const int64_t* boff_dev, int32_t pad_value,
                         int32_t* out, int32_t* out_lengths, void* stream);
 
+/* Ragged Batch of token sequences (the reference's Filter -> Batch lists, */
+/* runtime.cpp:579-637): prefix[i] = sum of lengths[order[j]], j < i, and  */
+/* prefix[n] = the total (int64 [n + 1]; order null = identity).          */
+size_t dp_k_len_prefix_scratch_bytes(int64_t n);
+int dp_k_len_prefix(const int32_t* lengths, const int64_t* order, int64_t n,
+                    int64_t* prefix, void* scratch, void* stream);
+/* Rows [first_row, first_row + rows) of an epoch of n_rows kept rows in   */
+/* batches of `batch`: tokens packed into values (offset prefix[R] -       */
+/* prefix[first_row]); each batch's rows_j + 1 row splits (int64, relative */
+/* to the batch) one after another in `splits`.                           */
+int dp_k_ragged_batches(const int32_t* tokens, const int64_t* offsets, const int32_t* lengths,
+                        const int64_t* order, int64_t first_row, int64_t rows, int64_t batch,
+                        int64_t n_rows, const int64_t* prefix, int32_t* values, int64_t* splits,
+                        void* stream);
+
 /* ---------------------------------------------------------------------- */
 /* K8  bucket_by_length -- tf.data bucket_by_sequence_length              */
 /*     (group_by_window: key = bucket of the length, window = the bucket's */

@@ -309,9 +309,19 @@ TypeSpec BatchWrap(const TypeSpec& c, std::optional<int64_t> len) {
   return TypeSpec::List(c, len ? std::optional<uint64_t>(*len) : std::nullopt);
 }
 
+// A batch of variable-length 1-D tensors (token sequences) is ragged: the
+// reference's list of lists (runtime.cpp:579-637) becomes two components,
+// the rows' values back to back and int64 row splits (rows + 1).
 ElementSpec BatchWrapSpec(const ElementSpec& in, int64_t b, bool drop) {
   std::vector<TypeSpec> out;
-  for (const auto& c : in.components()) out.push_back(BatchWrap(c, drop ? std::optional<int64_t>(b) : std::nullopt));
+  for (const auto& c : in.components()) {
+    if (c.kind() == Value::Kind::kTensor && c.shape().size() == 1 && c.shape()[0] < 0) {
+      out.push_back(TypeSpec::OfTensor(c.dtype(), {-1}));
+      out.push_back(TypeSpec::OfTensor(DType::kInt64, {drop ? b + 1 : -1}));
+      continue;
+    }
+    out.push_back(BatchWrap(c, drop ? std::optional<int64_t>(b) : std::nullopt));
+  }
   return ElementSpec(std::move(out));
 }
 

@@ -412,6 +412,9 @@ struct Lowered {
   bool unbatched = false;
   // bucket_by_length (a padded kind with per-bucket windows, K8)
   bool bucketed = false;
+  // Batch of token sequences: ragged (values + row splits), a padded kind
+  // without padding
+  bool ragged = false;
   std::vector<int32_t> bucket_bounds;
   std::vector<int64_t> bucket_sizes;
   int64_t pad = 0;
@@ -673,13 +676,16 @@ Lowered Lower(const DatasetGraph& g, const UdfRegistry& reg) {
     if (op.pred.on == DevicePredicate::On::kValue && (sk != SourceData::Kind::kInt64 || op.opaque))
       Unsupported("a value predicate needs int64 elements (after affine maps only)");
   }
+  if (sk == SourceData::Kind::kTokens && L.kind != BatchKind::kPadded && !L.unbatched) {
+    if (!L.steps.empty()) Unsupported("map on token sequences");
+    L.kind = BatchKind::kPadded;  // Batch of token sequences: ragged
+    L.ragged = true;
+  }
   if (L.kind == BatchKind::kPadded) {
     if (sk != SourceData::Kind::kTokens) Unsupported("padded_batch needs token sequences");
     for (const auto& op : L.chain)
       if (op.kind == IndexOp::Kind::kRepeat) Unsupported("repeat under padded_batch: put repeat above it");
     if (!L.steps.empty()) Unsupported("map before padded_batch");
-  } else if (sk == SourceData::Kind::kTokens) {
-    Unsupported("batch of ragged token sequences: use padded_batch");
   } else if (sk == SourceData::Kind::kInt64) {
     L.kind = BatchKind::kAffine;
     for (const auto& s : L.steps) {
@@ -924,7 +930,9 @@ class DevicePipeline {
       case BatchKind::kIdentityInt: return {sizeof(int64_t) * b, 0};
       case BatchKind::kCrop: return {sizeof(int64_t) * b, sizeof(float) * b * L_.crop.out_h * L_.crop.out_w * 3};
       case BatchKind::kResize: return {sizeof(int64_t) * b, sizeof(float) * b * L_.resize.out_h * L_.resize.out_w * 3};
-      case BatchKind::kPadded: return {sizeof(int32_t) * b * std::max<int64_t>(max_len_, 1), sizeof(int32_t) * b};
+      case BatchKind::kPadded:
+        if (L_.ragged) return {sizeof(int32_t) * b * std::max<int64_t>(max_len_, 1), sizeof(int64_t) * (b + 1)};
+        return {sizeof(int32_t) * b * std::max<int64_t>(max_len_, 1), sizeof(int32_t) * b};
     }
     return {0, 0};
   }
@@ -1187,6 +1195,8 @@ class DevicePipeline {
     p.tail = cur ? tail : 0;
     if (L_.bucketed) {
       BuildBucketPlan(p, cur, count);
+    } else if (L_.ragged) {
+      BuildRaggedPlan(p, cur, count);
     } else if (L_.kind == BatchKind::kPadded) {
       const int64_t nb = (count + L_.batch - 1) / L_.batch;
       p.lmax.assign(nb, 0);
@@ -1251,6 +1261,33 @@ class DevicePipeline {
     CudaCheck(cudaStreamSynchronize(s), "interleave schedule");  // `host` is read by the copy
     cur = out;
     count = total;
+  }
+
+  // Ragged batches: the epoch's length prefix over its kept rows; the batch
+  // boundaries' prefixes are read back for the elements' shapes.
+  void BuildRaggedPlan(EpochPlan& p, const std::shared_ptr<void>& cur, int64_t count) {
+    cudaStream_t s = plan_stream_;
+    auto dalloc = [&](size_t bytes) { return DeviceAllocAsync(bytes, opt_.device, plan_stream_, plan_stream_); };
+    auto prefix = dalloc(sizeof(int64_t) * (count + 1));
+    auto scratch = dalloc(dp_k_len_prefix_scratch_bytes(count));
+    KCheck(dp_k_len_prefix(P<int32_t>(L_.source->lengths), P<int64_t>(cur), count, P<int64_t>(prefix), scratch.get(),
+                           s),
+           "len_prefix");
+    launches_ += 3;
+    const int64_t B = L_.batch, nb = L_.drop ? count / B : (count + B - 1) / B;
+    p.boff.assign(nb + 1, 0);
+    if (nb) {  // prefix[j * B] for j < nb, then the end of the last batch
+      CudaCheck(cudaMemcpy2DAsync(p.boff.data(), sizeof(int64_t), prefix.get(), sizeof(int64_t) * B, sizeof(int64_t),
+                                  nb, cudaMemcpyDeviceToHost, s),
+                "batch starts");
+      CudaCheck(cudaMemcpyAsync(&p.boff[nb], P<int64_t>(prefix) + std::min(nb * B, count), sizeof(int64_t),
+                                cudaMemcpyDeviceToHost, s),
+                "batch end");
+      CudaCheck(cudaStreamSynchronize(s), "batch starts");
+    }
+    p.lmax.assign(nb, 0);
+    for (int64_t j = 0; j < nb; ++j) p.lmax[j] = static_cast<int32_t>(p.boff[j + 1] - p.boff[j]);  // tokens
+    p.roff_dev = prefix;
   }
 
   // K8: the bucket plan of one epoch (k_bucket.cu) -- batches, their rows
@@ -1510,6 +1547,11 @@ class DevicePipeline {
                                      P<int64_t>(plan.roff_dev), j0, nb, group_rows, static_cast<int32_t>(L_.pad),
                                      P<int32_t>(slot->a), P<int32_t>(slot->b), stream_),
                  "K8");
+        } else if (L_.ragged) {
+          KCheck(dp_k_ragged_batches(P<int32_t>(L_.source->tokens), P<int64_t>(L_.source->offsets),
+                                     P<int32_t>(L_.source->lengths), order, row0, rows_total, L_.batch, plan.count,
+                                     P<int64_t>(plan.roff_dev), P<int32_t>(slot->a), P<int64_t>(slot->b), stream_),
+                 "K5 ragged");
         } else {
           KCheck(dp_k_padded_batches(P<int32_t>(L_.source->tokens), P<int64_t>(L_.source->offsets),
                                      P<int32_t>(L_.source->lengths), order, row0, rows_total, L_.batch,
@@ -1522,7 +1564,7 @@ class DevicePipeline {
         for (int64_t k = 0; k < nb; ++k) {
           slot->batch_cols[k] = plan.lmax[j0 + k];
           slot->batch_off_a[k] = (plan.boff[j0 + k] - plan.boff[j0]) * sizeof(int32_t);
-          slot->batch_off_b[k] = off * sizeof(int32_t);
+          slot->batch_off_b[k] = L_.ragged ? (off + k) * sizeof(int64_t) : off * sizeof(int32_t);
           off += slot->batch_rows[k];
         }
         break;
@@ -1566,6 +1608,11 @@ class DevicePipeline {
   }
 
   size_t UsedBytesA(const Slot& s) const {
+    if (L_.ragged) {
+      size_t t = 0;
+      for (auto c : s.batch_cols) t += c * sizeof(int32_t);
+      return t;
+    }
     if (L_.kind == BatchKind::kPadded) {
       size_t t = 0;
       for (size_t k = 0; k < s.batch_rows.size(); ++k) t += s.batch_rows[k] * s.batch_cols[k] * sizeof(int32_t);
@@ -1578,6 +1625,7 @@ class DevicePipeline {
   size_t UsedBytesB(const Slot& s) const {
     int64_t rows = 0;
     for (auto r : s.batch_rows) rows += r;
+    if (L_.ragged) return (rows + static_cast<int64_t>(s.batch_rows.size())) * sizeof(int64_t);
     if (L_.kind == BatchKind::kPadded) return rows * sizeof(int32_t);
     if (L_.kind == BatchKind::kCrop) return rows * sizeof(float) * L_.crop.out_h * L_.crop.out_w * 3;
     if (L_.kind == BatchKind::kResize) return rows * sizeof(float) * L_.resize.out_h * L_.resize.out_w * 3;
@@ -1635,6 +1683,11 @@ class DevicePipeline {
         comps.push_back(mk(DType::kFloat32, {rows, L_.resize.out_h, L_.resize.out_w, 3}, base_b));
         break;
       case BatchKind::kPadded:
+        if (L_.ragged) {  // (values, row splits)
+          comps.push_back(mk(DType::kInt32, {slot->batch_cols[k]}, base_a));
+          comps.push_back(mk(DType::kInt64, {rows + 1}, base_b));
+          break;
+        }
         comps.push_back(mk(DType::kInt32, {rows, slot->batch_cols[k]}, base_a));
         comps.push_back(mk(DType::kInt32, {rows}, base_b));
         break;

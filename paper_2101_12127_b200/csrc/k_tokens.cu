@@ -244,6 +244,110 @@ padded_batches_kernel(const int32_t* __restrict__ tokens, const int64_t* __restr
   }
 }
 
+// ---- ragged Batch of token sequences (the reference's Filter -> Batch,
+// runtime.cpp:579-637: a batch of variable-length lists) ----
+// prefix[i] = sum of lengths[order[j]] for j < i (int64), by tile sums, the
+// one-CTA tile scan above and a per-tile apply.
+__device__ __forceinline__ int64_t block_exclusive_scan64(int64_t v, int64_t* warp_sums) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int64_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(kFull, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_sums[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    const int64_t w = lane < kThreads / 32 ? warp_sums[lane] : 0;
+    int64_t z = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(kFull, z, o);
+      if (lane >= o) z += y;
+    }
+    if (lane < kThreads / 32) warp_sums[lane] = z - w;
+  }
+  __syncthreads();
+  return x - v + warp_sums[warp];
+}
+
+__global__ void __launch_bounds__(kThreads)
+len_tile_sum_kernel(const int32_t* __restrict__ lengths, const int64_t* __restrict__ order, int64_t n,
+                    int64_t* __restrict__ tiles) {
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kTile + static_cast<int64_t>(threadIdx.x) * kItems;
+  int64_t v = 0;
+#pragma unroll
+  for (int u = 0; u < kItems; ++u)
+    if (base + u < n) v += lengths[order ? order[base + u] : base + u];
+  __shared__ int64_t ws[kThreads / 32];
+  const int64_t excl = block_exclusive_scan64(v, ws);
+  if (threadIdx.x == kThreads - 1) tiles[blockIdx.x] = excl + v;
+}
+
+__global__ void __launch_bounds__(kThreads)
+len_prefix_apply_kernel(const int32_t* __restrict__ lengths, const int64_t* __restrict__ order, int64_t n,
+                        const int64_t* __restrict__ tile_base, int64_t* __restrict__ prefix) {
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kTile + static_cast<int64_t>(threadIdx.x) * kItems;
+  int64_t len[kItems], v = 0;
+#pragma unroll
+  for (int u = 0; u < kItems; ++u) {
+    len[u] = base + u < n ? lengths[order ? order[base + u] : base + u] : 0;
+    v += len[u];
+  }
+  __shared__ int64_t ws[kThreads / 32];
+  int64_t at = tile_base[blockIdx.x] + block_exclusive_scan64(v, ws);
+#pragma unroll
+  for (int u = 0; u < kItems; ++u) {
+    if (base + u < n) prefix[base + u] = at;
+    at += len[u];
+  }
+}
+
+// Rows [first_row, first_row + rows) of an epoch's consecutive ragged
+// batches of `batch` rows (the last one may be short: n_rows in the epoch):
+// row R's tokens go to values[prefix[R] - prefix[first_row]]; batch j's
+// row splits (rows_j + 1 int64, relative to the batch) follow the splits of
+// the batches before it in the launch group.  Row tiles as padded_batches.
+__global__ void __launch_bounds__(kThreads)
+ragged_batches_kernel(const int32_t* __restrict__ tokens, const int64_t* __restrict__ offsets,
+                      const int32_t* __restrict__ lengths, const int64_t* __restrict__ order, int64_t first_row,
+                      int64_t rows, int64_t batch, int64_t n_rows, const int64_t* __restrict__ prefix,
+                      int32_t* __restrict__ values, int64_t* __restrict__ splits) {
+  __shared__ int64_t s_src[kRowTile], s_dst[kRowTile];
+  __shared__ int32_t s_len[kRowTile];
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * kRowTile;
+  const int n = static_cast<int>(rows - r0 < kRowTile ? rows - r0 : kRowTile);
+  const int64_t j0 = first_row / batch, base = prefix[first_row];
+  for (int t = threadIdx.x; t < n; t += kThreads) {
+    const int64_t R = first_row + r0 + t, j = R / batch, r = R - j * batch;
+    const int64_t p = order ? __ldcs(order + R) : R;
+    const int32_t len = lengths[p];
+    s_src[t] = offsets[p];
+    s_len[t] = len;
+    s_dst[t] = prefix[R] - base;
+    const int64_t slot = (R - first_row) + (j - j0), batch_start = prefix[j * batch];
+    splits[slot] = prefix[R] - batch_start;
+    const int64_t rows_j = n_rows - j * batch < batch ? n_rows - j * batch : batch;
+    if (r == rows_j - 1) splits[slot + 1] = prefix[R] + len - batch_start;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  for (int t = threadIdx.x >> 5; t < n; t += kThreads / 32) {
+    const int32_t len = s_len[t];
+    const int32_t* src = tokens + s_src[t];
+    int32_t* dst = values + s_dst[t];
+    for (int c = lane; c < len; c += 32 * kLoadsInFlight) {
+      int32_t v[kLoadsInFlight];
+#pragma unroll
+      for (int u = 0; u < kLoadsInFlight; ++u) v[u] = c + 32 * u < len ? __ldcs(src + c + 32 * u) : 0;
+#pragma unroll
+      for (int u = 0; u < kLoadsInFlight; ++u)
+        if (c + 32 * u < len) __stcs(dst + c + 32 * u, v[u]);
+    }
+  }
+}
+
 }  // namespace
 }  // namespace dpk
 
@@ -336,4 +440,34 @@ extern "C" int dp_k_padded_batch(const int32_t* tokens, const int64_t* offsets, 
   padded_batch_kernel<<<static_cast<int>(blocks), kThreads, 0, as_stream(stream)>>>(
       tokens, offsets, lengths, kept, first, rows, lmax, pad_value, out, out_lengths);
   return launch_status("padded_batch");
+}
+
+extern "C" size_t dp_k_len_prefix_scratch_bytes(int64_t n) { return dp_k_filter_scratch_bytes(n); }
+
+extern "C" int dp_k_len_prefix(const int32_t* lengths, const int64_t* order, int64_t n, int64_t* prefix,
+                               void* scratch, void* stream) {
+  if (n < 0 || !lengths || !prefix || !scratch) return fail(DP_ERR_INVALID_ATTR, "len_prefix: bad arguments");
+  cudaStream_t s = as_stream(stream);
+  if (n == 0) return cuda_status(cudaMemsetAsync(prefix, 0, sizeof(int64_t), s), "len_prefix: memset");
+  const int64_t tiles = (n + kTile - 1) / kTile;
+  if (tiles > 0x7fffffff) return fail(DP_ERR_INVALID_ATTR, "len_prefix: n too large");
+  int64_t* tile = static_cast<int64_t*>(scratch);
+  len_tile_sum_kernel<<<static_cast<int>(tiles), kThreads, 0, s>>>(lengths, order, n, tile);
+  filter_scan_kernel<<<1, 1024, 0, s>>>(tile, tiles, prefix + n);  // exclusive tile bases; prefix[n] = total
+  len_prefix_apply_kernel<<<static_cast<int>(tiles), kThreads, 0, s>>>(lengths, order, n, tile, prefix);
+  return launch_status("len_prefix");
+}
+
+extern "C" int dp_k_ragged_batches(const int32_t* tokens, const int64_t* offsets, const int32_t* lengths,
+                                   const int64_t* order, int64_t first_row, int64_t rows, int64_t batch,
+                                   int64_t n_rows, const int64_t* prefix, int32_t* values, int64_t* splits,
+                                   void* stream) {
+  if (rows < 0 || batch < 1 || first_row < 0 || first_row + rows > n_rows)
+    return fail(DP_ERR_INVALID_ATTR, "ragged_batches: bad rows/batch");
+  if (rows == 0) return DP_OK;
+  const int64_t blocks = (rows + kRowTile - 1) / kRowTile;
+  if (blocks > 0x7fffffff) return fail(DP_ERR_INVALID_ATTR, "ragged_batches: too many rows");
+  ragged_batches_kernel<<<static_cast<int>(blocks), kThreads, 0, as_stream(stream)>>>(
+      tokens, offsets, lengths, order, first_row, rows, batch, n_rows, prefix, values, splits);
+  return launch_status("ragged_batches");
 }

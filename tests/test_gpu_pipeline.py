@@ -403,6 +403,37 @@ def test_cfg4_filter_padded_batch(dp, orc):
     assert fnv(orc, sizes) == c["fnv_batch_sizes"]
 
 
+def test_cfg4_reference_graph_filter_then_ragged_batch(dp, orc):
+    """The reference's own cfg4 graph, Filter(len <= 512) -> Batch(128), as
+    is: a batch of variable-length sequences comes out ragged (values back
+    to back + int64 row splits) and equals the compiled reference's lists
+    (golden cfg4_filter_batch: row lengths, tokens, batch sizes)."""
+    c = GOLDEN["cfg4_filter_batch"]
+    reg = dp.Registry()
+    reg.register_length_filter("len<=512", c["max_keep"])
+    src = dp.Source.synthetic_tokens(c["n"], c["max_len"], c["len_seed"], c["tok_seed"])
+    g = dp.Dataset.token_sequences(reg, src).filter("len<=512").batch(c["batch"]).prefetch(-1)
+    batches = drain(dp.make_iterator(g, seed_override=1), comps=(0, 1))
+    sizes = [b[1].size - 1 for b in batches]
+    lens = np.concatenate([np.diff(b[1]) for b in batches])
+    toks = np.concatenate([b[0] for b in batches])
+    assert all(b[1][0] == 0 and b[1][-1] == b[0].size for b in batches)
+    assert len(sizes) == c["num_batches"] and sizes[-1] == c["last_batch"]
+    assert fnv(orc, lens) == c["fnv_row_lengths"] and fnv(orc, toks) == c["fnv_tokens"]
+    assert fnv(orc, sizes) == c["fnv_batch_sizes"]
+    # drop_remainder, shuffle, repeat above, checkpoint
+    g = dp.Dataset.token_sequences(reg, src).filter("len<=512").shuffle(999, 4).batch(100, drop_remainder=True)
+    g = g.repeat(2)
+    full = drain(dp.make_iterator(g, seed_override=3), comps=(0, 1))
+    assert all(b[1].size == 101 for b in full)
+    it = dp.make_iterator(g, seed_override=3)
+    for _ in range(7):
+        it.get_next().release()
+    rest = drain(dp.restore(g, it.save()), comps=(0, 1))
+    assert len(rest) == len(full) - 7
+    assert all(np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) for a, b in zip(rest, full[7:]))
+
+
 def test_cfg4_filter_then_shuffle_then_padded(dp, orc):
     n = 5000
     reg = dp.Registry()

@@ -359,6 +359,25 @@ std::unique_ptr<PipelineIterator> MakeIterator(const DatasetGraph& graph, const 
 std::unique_ptr<PipelineIterator> Restore(const DatasetGraph& graph, const UdfRegistry& registry,
                                           const std::string& blob, IteratorOptions options = {});
 
+// ---- pipeline description text (formats.md "Pipeline description text
+// format"; pipeline_spec.hpp ParsePipelineSpec) for device pipelines: the
+// reference's stanza grammar with the device UDF library (see
+// engine/pipeline_spec.cpp for the stanzas).  Errors: kParseError with
+// "line L, col C: ...".
+struct ParsedPipeline {
+  DatasetGraph graph;
+  IteratorOptions options;
+  int epochs = 5;
+  std::vector<std::string> disabled_rules;
+  struct TunableRef {
+    std::string name;  // "map@0.parallel", "prefetch@1.buffer"
+    std::string attr;  // "num_parallel_calls" | "buffer_size"
+  };
+  std::vector<TunableRef> tunables;
+};
+ParsedPipeline ParsePipelineSpec(const std::string& text, UdfRegistry& registry, int device = 0);
+ParsedPipeline ParsePipelineSpecFile(const std::string& path, UdfRegistry& registry, int device = 0);
+
 // ---- graph serialization (formats.md "Graph serialization"; serialize.hpp) ----
 // DPG1 bytes, canonical (preorder nodes, attrs in ascending key order).
 // Kinds and attrs shared with the reference encode exactly as the

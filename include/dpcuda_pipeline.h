@@ -132,6 +132,12 @@ int dp_graph_deserialize(const dp_registry* reg, const uint8_t* bytes, size_t le
 /* GraphFingerprint (serialize.cpp:213-216): SHA-256 of the seed-zeroed
  * serialization as 64 hex chars + NUL (hex must hold 65 bytes). */
 int dp_graph_fingerprint(const dp_graph* g, char* hex);
+/* ParsePipelineSpec (pipeline_spec.hpp; formats.md "Pipeline description
+ * text format") over the device UDF library.  Out: the graph, the `epochs`
+ * trailer, the `options` trailer (has_seed / seed / deterministic) and the
+ * `disable rule=` names comma-separated into `disabled` (len bytes). */
+int dp_graph_from_spec(dp_registry* reg, const char* text, int device, dp_graph** out, int* epochs, int* has_seed,
+                       uint64_t* seed, int* deterministic, char* disabled, size_t len);
 void dp_graph_release(dp_graph* g);
 
 /* ---- iterator: include/datapipe/runtime.hpp:35-100 ---- */

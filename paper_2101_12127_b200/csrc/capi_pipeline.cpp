@@ -296,6 +296,21 @@ int dp_graph_deserialize(const dp_registry* reg, const uint8_t* bytes, size_t le
     Emit(out, Deserialize(std::string(reinterpret_cast<const char*>(bytes), len), reg->reg, src, device));
   });
 }
+int dp_graph_from_spec(dp_registry* reg, const char* text, int device, dp_graph** out, int* epochs, int* has_seed,
+                       uint64_t* seed, int* deterministic, char* disabled, size_t len) {
+  DP_REQUIRE(reg && text && out);
+  return Guard([&] {
+    ParsedPipeline p = ParsePipelineSpec(text, reg->reg, device);
+    if (epochs) *epochs = p.epochs;
+    if (has_seed) *has_seed = p.options.seed_override.has_value() ? 1 : 0;
+    if (seed) *seed = p.options.seed_override.value_or(0);
+    if (deterministic) *deterministic = p.options.deterministic ? 1 : 0;
+    std::string d;
+    for (const auto& r : p.disabled_rules) d += (d.empty() ? "" : ",") + r;
+    if (disabled) CopyOut(d, disabled, len);
+    Emit(out, std::move(p.graph));
+  });
+}
 int dp_graph_fingerprint(const dp_graph* g, char* hex) {
   DP_REQUIRE(g && hex);
   return Guard([&] {

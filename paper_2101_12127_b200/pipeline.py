@@ -22,7 +22,7 @@ c_i64, c_u64, c_int, c_vp, c_size = ctypes.c_int64, ctypes.c_uint64, ctypes.c_in
 PP = ctypes.POINTER(c_vp)
 
 ERR = {  # dp_status values (include/dpcuda.h)
-    "InvalidArity": 1, "InvalidAttr": 2, "TypeMismatch": 3, "MalformedInput": 4, "ValidationFailed": 5,
+    "ParseError": 18, "InvalidArity": 1, "InvalidAttr": 2, "TypeMismatch": 3, "MalformedInput": 4, "ValidationFailed": 5,
     "DuplicateName": 6, "UnknownUdf": 7, "MissingFile": 8, "FingerprintMismatch": 10, "VersionMismatch": 11,
     "CorruptBlob": 12, "RewriteDiverged": 14, "Internal": 19, "Cuda": 100, "OutOfMemory": 101,
     "EndOfSequence": 102,
@@ -90,6 +90,8 @@ _SIGS = {
     "dp_graph_serialize": [c_vp, c_vp, c_size, ctypes.POINTER(c_size)],
     "dp_graph_deserialize": [c_vp, c_vp, c_size, c_vp, c_i64, c_int, PP],
     "dp_graph_fingerprint": [c_vp, c_vp],
+    "dp_graph_from_spec": [c_vp, ctypes.c_char_p, c_int, PP, ctypes.POINTER(c_int), ctypes.POINTER(c_int),
+                           ctypes.POINTER(c_u64), ctypes.POINTER(c_int), ctypes.c_char_p, c_size],
     "dp_graph_release": [c_vp],
     "dp_iterator_options_default": [ctypes.POINTER(dp_iterator_options)],
     "dp_iterator_create": [c_vp, c_vp, ctypes.POINTER(dp_iterator_options), PP],
@@ -386,6 +388,19 @@ class Dataset:
         buf = ctypes.create_string_buffer(bytes(data), len(data))
         _check(L().dp_graph_deserialize(reg.h, buf, len(data), arr, len(sources), device, ctypes.byref(out)))
         return Dataset(out, reg, tuple(sources))
+
+    @staticmethod
+    def from_spec(reg, text, device=0):
+        """ParsePipelineSpec: (Dataset, {"epochs", "seed", "deterministic", "disabled_rules"})."""
+        out = c_vp()
+        ep, hs, det = c_int(), c_int(), c_int()
+        seed = c_u64()
+        buf = ctypes.create_string_buffer(4096)
+        _check(L().dp_graph_from_spec(reg.h, _b(text), device, ctypes.byref(out), ctypes.byref(ep), ctypes.byref(hs),
+                                      ctypes.byref(seed), ctypes.byref(det), buf, len(buf)))
+        rules = [r for r in buf.value.decode().split(",") if r]
+        return Dataset(out, reg), {"epochs": ep.value, "seed": seed.value if hs.value else None,
+                                   "deterministic": bool(det.value), "disabled_rules": rules}
 
     def fingerprint(self) -> str:
         """GraphFingerprint: SHA-256 of the seed-zeroed serialization (hex)."""

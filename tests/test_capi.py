@@ -243,3 +243,44 @@ def test_value_filter_validation():
     with pytest.raises(DpError) as e:
         reg.register_value_filter("many", [("lt", 5)] * 9)
     assert e.value.code == dp.ERR["InvalidAttr"]
+
+
+def test_pipeline_spec_parses_like_the_builders():
+    """ParsePipelineSpec (the reference's stanza grammar over the device UDF
+    library) builds the same graph as the ops:: builders, with the trailers."""
+    reg = dp.Registry()
+    g, info = dp.Dataset.from_spec(reg, """
+        # cfg1 as text
+        source range count=1000000
+        map affine a=3 b=1 parallel=AUTO
+        filter keep=even
+        shuffle buffer=100 seed=42
+        batch size=1024 drop_remainder=true
+        prefetch buffer=AUTO
+        options seed=7 deterministic=false
+        epochs 3
+        disable rule=map_batch_fusion
+    """)
+    reg2 = dp.Registry()
+    reg2.register_affine("affine(3,1)", 3, 1)
+    reg2.register_standard_predicates()
+    want = (dp.Dataset.range(reg2, 1000000).map("affine(3,1)", -1).filter("keep_even").shuffle(100, 42)
+            .batch(1024, drop_remainder=True).prefetch(-1))
+    assert str(g) == str(want) and g.fingerprint() == want.fingerprint()
+    assert info == {"epochs": 3, "seed": 7, "deterministic": False, "disabled_rules": ["map_batch_fusion"]}
+
+
+def test_pipeline_spec_errors_carry_line_and_column():
+    reg = dp.Registry()
+    cases = [("map affine a=1", "line 1, col 1: 'map' before a source stanza"),
+             ("source range count=5\nfrob x=1", "line 2, col 1: unknown stanza 'frob'"),
+             ("source range count=5\nbatch size=x", "line 2, col 7: 'size' must be an integer"),
+             ("source range count=5\nbatch size=4 speed=9", "line 2, col 14: batch: unknown argument 'speed'"),
+             ("source range count=5\nsource range count=6", "line 2, col 1: multiple source stanzas"),
+             ("source range count=5\nbatch size=0", "line 2, col 1: "),
+             ("epochs 3", "no source stanza")]
+    for text, msg in cases:
+        with pytest.raises(DpError) as e:
+            dp.Dataset.from_spec(reg, text)
+        assert e.value.code == dp.ERR["ParseError"], (text, str(e.value))
+        assert msg in str(e.value), (text, str(e.value))

@@ -183,6 +183,38 @@ def test_unbatched_pipelines(dp, orc):
     assert rest == full[7777:]
 
 
+def test_pipeline_spec_runs_like_the_builders(dp, tmp_path):
+    """A pipeline description (the reference's text format with device UDFs)
+    iterates exactly like the ops:: graph; tools/dpbench.py runs it."""
+    spec = """
+        source images count=600 h=64 w=64 seed=0x5EED
+        shuffle buffer=200 seed=42
+        map crop h=48 w=48 seed=7 flip=true
+        map normalize
+        batch size=50
+        prefetch buffer=AUTO
+        epochs 2
+    """
+    reg = dp.Registry()
+    g, info = dp.Dataset.from_spec(reg, spec)
+    reg2 = image_registry(dp, 0, crop=(48, 48))
+    want = dp.Dataset.tensor_slices(reg2, dp.Source.synthetic_images(600, 64, 64)).shuffle(200, 42).map("crop") \
+        .map("norm").batch(50).prefetch(-1)
+    a = drain(dp.make_iterator(g.optimize()[0], seed_override=3), comps=(0, 1))
+    b = drain(dp.make_iterator(want.optimize()[0], seed_override=3), comps=(0, 1))
+    assert len(a) == len(b) == 12
+    assert all(np.array_equal(x[0], y[0]) and np.array_equal(x[1], y[1]) for x, y in zip(a, b))
+    import subprocess
+    import sys
+    path = tmp_path / "p.txt"
+    path.write_text(spec)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "tools", "dpbench.py"), str(path)],
+                         capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert "epoch 2: 600 elements" in out.stdout and "median epoch" in out.stdout
+
+
 def test_shuffle_order_matches_reference(dp, orc):
     for c in GOLDEN["shuffle"]:
         got = shuffle_ids(dp, c["n"], c["buffer"], c["seed"], c["base_seed"])

@@ -676,9 +676,9 @@ Lowered Lower(const DatasetGraph& g, const UdfRegistry& reg) {
     if (op.pred.on == DevicePredicate::On::kValue && (sk != SourceData::Kind::kInt64 || op.opaque))
       Unsupported("a value predicate needs int64 elements (after affine maps only)");
   }
-  if (sk == SourceData::Kind::kTokens && L.kind != BatchKind::kPadded && !L.unbatched) {
+  if (sk == SourceData::Kind::kTokens && L.kind != BatchKind::kPadded) {
     if (!L.steps.empty()) Unsupported("map on token sequences");
-    L.kind = BatchKind::kPadded;  // Batch of token sequences: ragged
+    L.kind = BatchKind::kPadded;  // Batch of token sequences (or single ones, internally): ragged
     L.ragged = true;
   }
   if (L.kind == BatchKind::kPadded) {
@@ -711,8 +711,9 @@ Lowered Lower(const DatasetGraph& g, const UdfRegistry& reg) {
   // (interleave without a record source emits the int64 record indices
   // themselves: the batch stage gathers them like a range)
   if (L.unbatched) {
-    if (sk == SourceData::Kind::kTokens) Unsupported("unbatched token sequences: use padded_batch / bucket_by_length");
-    L.batch = L.kind == BatchKind::kAffine || L.kind == BatchKind::kIdentityInt ? 4096 : 64;  // internal unit
+    L.batch = L.kind == BatchKind::kAffine || L.kind == BatchKind::kIdentityInt ? 4096
+              : L.ragged                                                         ? 1024
+                                                                                 : 64;  // internal unit
     L.drop = false;
   }
   return L;
@@ -1404,6 +1405,8 @@ class DevicePipeline {
     if (opt_.host_output) {
       slot->ha = PinnedAlloc(slot->a_bytes);
       if (slot->b_bytes) slot->hb = PinnedAlloc(slot->b_bytes);
+    } else if (L_.unbatched && L_.ragged) {
+      slot->hb = PinnedAlloc(slot->b_bytes);  // host copy of the row splits
     } else if (L_.unbatched) {
       slot->ha = PinnedAlloc(slot->a_bytes);  // host copy of the values / ids
     }
@@ -1583,6 +1586,11 @@ class DevicePipeline {
       if (b_used) CudaCheck(cudaMemcpyAsync(slot->hb.get(), slot->b.get(), b_used, cudaMemcpyDeviceToHost, copy_stream_), "d2h");
       CudaCheck(cudaEventRecord(slot->ready, copy_stream_), "event");
       d2h_bytes_ += a_used + b_used;
+    } else if (L_.unbatched && L_.ragged) {
+      // single token sequences: the row splits locate them in the values
+      CudaCheck(cudaMemcpyAsync(slot->hb.get(), slot->b.get(), UsedBytesB(*slot), cudaMemcpyDeviceToHost, stream_),
+                "d2h splits");
+      CudaCheck(cudaEventRecord(slot->ready, stream_), "event");
     } else if (L_.unbatched) {
       // element values / ids are served as host int64 values
       CudaCheck(cudaMemcpyAsync(slot->ha.get(), slot->a.get(), UsedBytesA(*slot), cudaMemcpyDeviceToHost, stream_),
@@ -1713,6 +1721,21 @@ class DevicePipeline {
         shared->slots_freed.fetch_add(1, std::memory_order_release);
       }
     });
+    if (L_.ragged) {  // one token sequence: a device view into the batch's values
+      const int64_t* splits = reinterpret_cast<const int64_t*>(static_cast<const uint8_t*>(slot->hb.get()) +
+                                                               slot->batch_off_b[k]);
+      Tensor t;
+      t.dtype = DType::kInt32;
+      t.shape = {splits[row + 1] - splits[row]};
+      t.data = static_cast<uint8_t*>(slot->a.get()) + slot->batch_off_a[k] + splits[row] * sizeof(int32_t);
+      t.residency = Residency::kDevice;
+      t.device = opt_.device;
+      t.owner = lease;
+      t.ready = slot->ready;
+      std::vector<Value> one;
+      one.push_back(Value::FromTensor(std::move(t)));
+      return Element(std::move(one));
+    }
     const int64_t idx = slot->batch_off_a[k] / static_cast<int64_t>(sizeof(int64_t)) + row;
     const int64_t value = static_cast<const int64_t*>(slot->ha.get())[idx];
     std::vector<Value> comps;

@@ -169,6 +169,16 @@ def test_unbatched_pipelines(dp, orc):
     pix = np.concatenate([b[1] for b in batched])
     assert [int(e[0]) for e in single] == ids.tolist()
     assert all(np.array_equal(e[1], pix[r]) for r, e in enumerate(single))
+    # single token sequences (device views into internal ragged batches)
+    reg.register_length_filter("short", 40)
+    tsrc = dp.Source.synthetic_tokens(2000, 80, 5, 5)
+    seqs = elems(dp.Dataset.token_sequences(reg, tsrc).filter("short").shuffle(300, 9))
+    lens_all = orc.lengths(2000, 80, 5)
+    toks, offs = orc.tokens(lens_all, 5)
+    kept = orc.filter_len_le(lens_all, 40)
+    order = kept[orc.shuffle_order(kept.size, 300, orc.shuffle_seed(1, 9))]
+    assert len(seqs) == order.size
+    assert all(np.array_equal(e[0], toks[offs[p]:offs[p + 1]]) for e, p in zip(seqs, order))
     # checkpoint in the middle of an unbatched, repeated pipeline
     g = dp.Dataset.range(reg, 5000).shuffle(700, 2).map("aff").repeat(3)
     full = [int(e[0]) for e in elems(g)]
@@ -745,8 +755,9 @@ def test_edge_cases(dp, orc):
 
 def test_unsupported_graph_fails_loudly(dp):
     reg = dp.Registry()
-    src = dp.Source.synthetic_tokens(10, 20, 1, 1)
-    g = dp.Dataset.token_sequences(reg, src)  # ragged sequences without a padded batch
+    reg.register_normalize("norm")
+    src = dp.Source.synthetic_images(10, 32, 32)
+    g = dp.Dataset.tensor_slices(reg, src).map("norm").batch(4)  # normalize alone: no device kernel
     with pytest.raises(Exception) as e:
         dp.make_iterator(g)
     assert "device lowering" in str(e.value)

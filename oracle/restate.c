@@ -197,6 +197,28 @@ static void resize_coord(int d, int in, int out, int* i0, int* i1, float* w) {
   *w = s - (float)a;
 }
 
+void orc_resize(const uint8_t* img, int in_h, int in_w, int out_h, int out_w, float* out) {
+  for (int y = 0; y < out_h; ++y) {
+    int y0, y1;
+    float wy;
+    resize_coord(y, in_h, out_h, &y0, &y1, &wy);
+    for (int x = 0; x < out_w; ++x) {
+      int x0, x1;
+      float wx;
+      resize_coord(x, in_w, out_w, &x0, &x1, &wx);
+      for (int c = 0; c < 3; ++c) {
+        float p00 = (float)img[((size_t)y0 * in_w + x0) * 3 + c];
+        float p01 = (float)img[((size_t)y0 * in_w + x1) * 3 + c];
+        float p10 = (float)img[((size_t)y1 * in_w + x0) * 3 + c];
+        float p11 = (float)img[((size_t)y1 * in_w + x1) * 3 + c];
+        float top = p00 + wx * (p01 - p00);
+        float bot = p10 + wx * (p11 - p10);
+        out[((size_t)y * out_w + x) * 3 + c] = top + wy * (bot - top);
+      }
+    }
+  }
+}
+
 void orc_resize_normalize(const uint8_t* img, int in_h, int in_w, int out_h,
                           int out_w, float* out) {
   for (int y = 0; y < out_h; ++y) {

@@ -86,6 +86,8 @@ extern const float ORC_STD[3];
 void orc_crop_flip_normalize(const uint8_t* img, int in_h, int in_w,
                              int64_t id, uint64_t seed, int crop_h, int crop_w,
                              int do_flip, float* out);
+/* bilinear resize alone (fp32 out), the same rounded ops. */
+void orc_resize(const uint8_t* img, int in_h, int in_w, int out_h, int out_w, float* out);
 /* bilinear resize (half-pixel centres, edge clamp) + normalize. */
 void orc_resize_normalize(const uint8_t* img, int in_h, int in_w, int out_h,
                           int out_w, float* out);

@@ -703,8 +703,23 @@ Lowered Lower(const DatasetGraph& g, const UdfRegistry& reg) {
       L.kind = BatchKind::kResize;
       L.resize = st[0];
       L.norm = st[1];
+    } else if (st.size() == 1 && st[0].op == MapStep::Op::kResizeBilinear) {
+      // resize alone (fp32 out): K4 with the identity normalize, (v - 0) / 1 == v exactly
+      L.kind = BatchKind::kResize;
+      L.resize = st[0];
+      L.norm = MapStep{MapStep::Op::kNormalize};
+      L.norm.mean = {0.f, 0.f, 0.f};
+      L.norm.stdv = {1.f, 1.f, 1.f};
+    } else if (st.size() == 1 && st[0].op == MapStep::Op::kNormalize) {
+      // normalize alone: K3 with the whole image as the window (offsets 0, no flip)
+      L.kind = BatchKind::kCrop;
+      L.crop = MapStep{MapStep::Op::kRandomCropFlip};
+      L.crop.out_h = L.source->h;
+      L.crop.out_w = L.source->w;
+      L.crop.flip = false;
+      L.norm = st[0];
     } else {
-      Unsupported("image UDF chain must be random_crop_flip>>normalize or resize_bilinear>>normalize");
+      Unsupported("image UDF chain must be random_crop_flip>>normalize, resize_bilinear[>>normalize] or normalize");
     }
     if (L.source->c != 3) Unsupported("images must have 3 channels");
   }

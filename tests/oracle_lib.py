@@ -136,6 +136,12 @@ class Oracle:
                                        1 if do_flip else 0, P(out))
         return out
 
+    def resize(self, img, out_h, out_w):
+        img = np.ascontiguousarray(img, np.uint8)
+        out = np.zeros((out_h, out_w, 3), np.float32)
+        self.L.orc_resize(P(img), img.shape[0], img.shape[1], out_h, out_w, P(out))
+        return out
+
     def resize_normalize(self, img, out_h=224, out_w=224):
         img = np.ascontiguousarray(img, np.uint8)
         out = np.zeros((out_h, out_w, 3), np.float32)

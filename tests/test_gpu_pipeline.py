@@ -363,6 +363,28 @@ def test_concurrent_get_next_callers(dp):
     assert all(np.array_equal(a, b) for a, b in zip(side, ref))
 
 
+def test_resize_alone_and_normalize_alone(dp, orc):
+    """resize without normalize (fp32) and normalize without a crop: the
+    restatement's rounded ops, bit for bit."""
+    imgs = orc.images(0, 40, 50, 70)
+    src = dp.Source.images_from_host(imgs)
+    reg = dp.Registry()
+    reg.register_resize_bilinear("rs", 33, 41)
+    reg.register_normalize("norm")
+    out = drain(dp.make_iterator(dp.Dataset.tensor_slices(reg, src).shuffle(16, 1).map("rs").batch(8),
+                                 seed_override=2), comps=(0, 1))
+    for b in out:
+        for r, i in enumerate(b[0]):
+            assert np.array_equal(b[1][r].view(np.uint32), orc.resize(imgs[i], 33, 41).view(np.uint32))
+    out = drain(dp.make_iterator(dp.Dataset.tensor_slices(reg, src).map("norm").batch(16), seed_override=2),
+                comps=(0, 1))
+    mean = np.array([123.675, 116.28, 103.53], np.float32)
+    std = np.array([58.395, 57.12, 57.375], np.float32)
+    want = (imgs.astype(np.float32) - mean) / std  # IEEE fp32 subtract + divide
+    got = np.concatenate([b[1] for b in out])
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
 def test_host_output_equals_device_output(dp):
     reg = image_registry(dp, 0, crop=(64, 64))
     src = dp.Source.synthetic_images(200, 96, 96)
@@ -755,9 +777,9 @@ def test_edge_cases(dp, orc):
 
 def test_unsupported_graph_fails_loudly(dp):
     reg = dp.Registry()
-    reg.register_normalize("norm")
+    reg.register_random_crop_flip("crop", 16, 16)
     src = dp.Source.synthetic_images(10, 32, 32)
-    g = dp.Dataset.tensor_slices(reg, src).map("norm").batch(4)  # normalize alone: no device kernel
+    g = dp.Dataset.tensor_slices(reg, src).map("crop").batch(4)  # a u8 crop alone: no device kernel
     with pytest.raises(Exception) as e:
         dp.make_iterator(g)
     assert "device lowering" in str(e.value)

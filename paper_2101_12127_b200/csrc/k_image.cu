@@ -404,8 +404,16 @@ struct ResizeOp {
       rc[u] = sel3(ch, a.nc.rcp[0], a.nc.rcp[1], a.nc.rcp[2]);
       int x0, x1;
       resize_coord(x, a.in_w, a.out_w, x0, x1, wx[u]);
+      // Right-edge clamp (x1 == x0 == in_w - 1): blending (x0 - 1, x0) with
+      // weight 1 gives p(x0) exactly (integer-valued fp32), as the oracle's
+      // p00 + wx * (p00 - p00) does; so the right tap is always o0 + 3 and its
+      // load takes an immediate offset (in_w >= 16 on this path).
+      if (x1 == x0) {
+        x0 -= 1;
+        wx[u] = 1.0f;
+      }
       o0[u] = x0 * 3 + ch;
-      o1[u] = x1 * 3 + ch;
+      o1[u] = o0[u] + 3;
     }
     k = PkK(a.nc);
 #pragma unroll

@@ -97,10 +97,10 @@ std::vector<Line> Tokenize(const std::string& text) {
   return out;
 }
 
-class Args {
+class StanzaArgs {
  public:
-  explicit Args(const Line& l) : l_(l), used_(l.args.size(), false) {}
-  std::optional<std::string> Find(const std::string& k) {
+  explicit StanzaArgs(const Line& l) : l_(l), used_(l.args.size(), false) {}
+  std::optional<std::string> Value(const std::string& k) {
     for (size_t i = 0; i < l_.args.size(); ++i)
       if (l_.args[i].key == k) {
         used_[i] = true;
@@ -108,7 +108,7 @@ class Args {
       }
     return std::nullopt;
   }
-  std::vector<std::string> FindAll(const std::string& k) {
+  std::vector<std::string> AllValues(const std::string& k) {
     std::vector<std::string> v;
     for (size_t i = 0; i < l_.args.size(); ++i)
       if (l_.args[i].key == k) {
@@ -117,16 +117,16 @@ class Args {
       }
     return v;
   }
-  int64_t Int(const std::string& k, std::optional<int64_t> fallback = {}) {
-    auto v = Find(k);
+  int64_t Integer(const std::string& k, std::optional<int64_t> fallback = {}) {
+    auto v = Value(k);
     if (!v) {
       if (fallback) return *fallback;
       Fail(l_.number, l_.column, l_.stanza + ": missing '" + k + "'");
     }
-    return ParseInt(*v, k);
+    return ToInt(*v, k);
   }
-  uint64_t Uint(const std::string& k, uint64_t fallback) {
-    auto v = Find(k);
+  uint64_t Unsigned(const std::string& k, uint64_t fallback) {
+    auto v = Value(k);
     if (!v) return fallback;
     try {
       size_t idx = 0;
@@ -134,33 +134,33 @@ class Args {
       if (idx != v->size()) throw std::invalid_argument("trailing");
       return x;
     } catch (const std::exception&) {
-      Fail(l_.number, Col(k), "'" + k + "' must be an unsigned integer, got '" + *v + "'");
+      Fail(l_.number, ColumnOfKey(k), "'" + k + "' must be an unsigned integer, got '" + *v + "'");
     }
   }
-  int64_t Tunable(const std::string& k, int64_t fallback) {
-    auto v = Find(k);
+  int64_t IntOrAuto(const std::string& k, int64_t fallback) {
+    auto v = Value(k);
     if (!v) return fallback;
     if (*v == "AUTO") return kAutotune;
-    return ParseInt(*v, k);
+    return ToInt(*v, k);
   }
-  bool Bool(const std::string& k, bool fallback) {
-    auto v = Find(k);
+  bool Flag(const std::string& k, bool fallback) {
+    auto v = Value(k);
     if (!v) return fallback;
     if (*v == "true" || *v == "1") return true;
     if (*v == "false" || *v == "0") return false;
-    Fail(l_.number, Col(k), "'" + k + "' must be true or false");
+    Fail(l_.number, ColumnOfKey(k), "'" + k + "' must be true or false");
   }
-  std::vector<int64_t> IntList(const std::string& k) {
-    auto v = Find(k);
+  std::vector<int64_t> Integers(const std::string& k) {
+    auto v = Value(k);
     if (!v) Fail(l_.number, l_.column, l_.stanza + ": missing '" + k + "'");
     std::vector<int64_t> out;
     std::stringstream ss(*v);
     std::string item;
-    while (std::getline(ss, item, ',')) out.push_back(ParseInt(item, k));
+    while (std::getline(ss, item, ',')) out.push_back(ToInt(item, k));
     return out;
   }
-  std::vector<float> FloatList(const std::string& k, std::vector<float> fallback) {
-    auto v = Find(k);
+  std::vector<float> Floats(const std::string& k, std::vector<float> fallback) {
+    auto v = Value(k);
     if (!v) return fallback;
     std::vector<float> out;
     std::stringstream ss(*v);
@@ -169,12 +169,12 @@ class Args {
       try {
         out.push_back(std::stof(item));
       } catch (const std::exception&) {
-        Fail(l_.number, Col(k), "'" + k + "' must be a list of numbers");
+        Fail(l_.number, ColumnOfKey(k), "'" + k + "' must be a list of numbers");
       }
     }
     return out;
   }
-  void RejectUnknown() {
+  void CheckAllUsed() {
     for (size_t i = 0; i < l_.args.size(); ++i)
       if (!used_[i]) Fail(l_.number, l_.args[i].column, l_.stanza + ": unknown argument '" + l_.args[i].key + "'");
     if (!l_.words.empty() && l_.stanza != "epochs")
@@ -182,17 +182,17 @@ class Args {
   }
 
  private:
-  int64_t ParseInt(const std::string& v, const std::string& k) {
+  int64_t ToInt(const std::string& v, const std::string& k) {
     try {
       size_t idx = 0;
       const int64_t x = std::stoll(v, &idx, 0);
       if (idx != v.size()) throw std::invalid_argument("trailing");
       return x;
     } catch (const std::exception&) {
-      Fail(l_.number, Col(k), "'" + k + "' must be an integer, got '" + v + "'");
+      Fail(l_.number, ColumnOfKey(k), "'" + k + "' must be an integer, got '" + v + "'");
     }
   }
-  int Col(const std::string& k) const {
+  int ColumnOfKey(const std::string& k) const {
     for (const auto& a : l_.args)
       if (a.key == k) return a.column;
     return l_.column;
@@ -208,7 +208,7 @@ ParsedPipeline ParsePipelineSpec(const std::string& text, UdfRegistry& reg, int 
   DatasetGraph g;
   bool have_source = false;
   for (const Line& line : Tokenize(text)) {
-    Args args(line);
+    StanzaArgs args(line);
     const int L = line.number, C = line.column;
     const std::string& s = line.stanza;
     auto need_source = [&] {
@@ -219,9 +219,9 @@ ParsedPipeline ParsePipelineSpec(const std::string& text, UdfRegistry& reg, int 
         if (have_source) Fail(L, C, "multiple source stanzas");
         const std::string& k = line.subkind;
         if (k == "range") {
-          g = ops::Range(args.Int("count"), reg);
+          g = ops::Range(args.Integer("count"), reg);
         } else if (k == "memory") {
-          auto v = args.Find("values");
+          auto v = args.Value("values");
           if (!v) Fail(L, C, "memory source requires values=1,2,3");
           std::vector<int64_t> vals;
           std::stringstream ss(*v);
@@ -235,14 +235,14 @@ ParsedPipeline ParsePipelineSpec(const std::string& text, UdfRegistry& reg, int 
           }
           g = ops::FromMemory(vals, reg, device);
         } else if (k == "images") {
-          const int64_t n = args.Int("count"), h = args.Int("h"), w = args.Int("w");
-          g = ops::TensorSlices(SynthImages(n, h, w, args.Uint("seed", 0x5EED), device), reg);
+          const int64_t n = args.Integer("count"), h = args.Integer("h"), w = args.Integer("w");
+          g = ops::TensorSlices(SynthImages(n, h, w, args.Unsigned("seed", 0x5EED), device), reg);
         } else if (k == "tokens") {
-          const int64_t n = args.Int("count"), m = args.Int("max_len");
-          const uint64_t seed = args.Uint("seed", 4);
+          const int64_t n = args.Integer("count"), m = args.Integer("max_len");
+          const uint64_t seed = args.Unsigned("seed", 4);
           g = ops::TokenSequences(SynthTokens(n, static_cast<uint32_t>(m), seed, seed, device), reg);
         } else if (k == "file") {
-          auto paths = args.FindAll("path");
+          auto paths = args.AllValues("path");
           if (paths.empty()) Fail(L, C, "file source requires path=...");
           g = ops::FromFile(paths, reg, device);
         } else {
@@ -254,46 +254,46 @@ ParsedPipeline ParsePipelineSpec(const std::string& text, UdfRegistry& reg, int 
         const std::string& k = line.subkind;
         std::string name;
         if (k == "affine") {
-          const int64_t a = args.Int("a"), b = args.Int("b", 0);
+          const int64_t a = args.Integer("a"), b = args.Integer("b", 0);
           name = "affine(" + std::to_string(a) + "," + std::to_string(b) + ")";
           if (!reg.Contains(name)) reg.RegisterAffine(name, a, b);
         } else if (k == "crop") {
-          const int64_t h = args.Int("h"), w = args.Int("w");
-          const uint64_t seed = args.Uint("seed", 7);
-          const bool flip = args.Bool("flip", true);
+          const int64_t h = args.Integer("h"), w = args.Integer("w");
+          const uint64_t seed = args.Unsigned("seed", 7);
+          const bool flip = args.Flag("flip", true);
           name = "crop(" + std::to_string(h) + "," + std::to_string(w) + "," + std::to_string(seed) + "," +
                  (flip ? "1" : "0") + ")";
           if (!reg.Contains(name)) reg.RegisterRandomCropFlip(name, h, w, seed, flip);
         } else if (k == "resize") {
-          const int64_t h = args.Int("h"), w = args.Int("w");
+          const int64_t h = args.Integer("h"), w = args.Integer("w");
           name = "resize(" + std::to_string(h) + "," + std::to_string(w) + ")";
           if (!reg.Contains(name)) reg.RegisterResizeBilinear(name, h, w);
         } else if (k == "normalize") {
-          auto m = args.FloatList("mean", {123.675f, 116.28f, 103.53f});
-          auto d = args.FloatList("std", {58.395f, 57.12f, 57.375f});
+          auto m = args.Floats("mean", {123.675f, 116.28f, 103.53f});
+          auto d = args.Floats("std", {58.395f, 57.12f, 57.375f});
           if (m.size() != 3 || d.size() != 3) Fail(L, C, "normalize: mean and std take 3 values");
           std::ostringstream nm;
           nm << "normalize(" << m[0] << "," << m[1] << "," << m[2] << ";" << d[0] << "," << d[1] << "," << d[2] << ")";
           name = nm.str();
           if (!reg.Contains(name)) reg.RegisterNormalize(name, {m[0], m[1], m[2]}, {d[0], d[1], d[2]});
         } else if (k == "decode") {
-          const int64_t h = args.Int("h"), w = args.Int("w");
+          const int64_t h = args.Integer("h"), w = args.Integer("w");
           name = "decode_raw(" + std::to_string(h) + "," + std::to_string(w) + ")";
           if (!reg.Contains(name)) reg.RegisterDecodeRaw(name, h, w);
         } else {
           Fail(L, C, "usage: map affine|crop|resize|normalize|decode ...");
         }
-        const int64_t p = args.Tunable("parallel", 1);
+        const int64_t p = args.IntOrAuto("parallel", 1);
         out.tunables.push_back({"map@" + std::to_string(out.tunables.size()) + ".parallel", "num_parallel_calls"});
         g = ops::Map(g, name, p, reg);
       } else if (s == "filter") {
         need_source();
         std::string name;
-        if (auto keep = args.Find("keep")) {
+        if (auto keep = args.Value("keep")) {
           reg.RegisterStandardPredicates();
           if (*keep != "even" && *keep != "odd" && *keep != "all") Fail(L, C, "filter requires keep=even|odd|all");
           name = "keep_" + *keep;
-        } else if (auto le = args.Find("len_le")) {
+        } else if (auto le = args.Value("len_le")) {
           name = "len_le(" + *le + ")";
           if (!reg.Contains(name)) reg.RegisterLengthFilter(name, std::stoll(*le));
         } else {
@@ -302,44 +302,44 @@ ParsedPipeline ParsePipelineSpec(const std::string& text, UdfRegistry& reg, int 
         g = ops::Filter(g, name, reg);
       } else if (s == "shuffle") {
         need_source();
-        const int64_t b = args.Int("buffer");
-        auto seed = args.Find("seed");
+        const int64_t b = args.Integer("buffer");
+        auto seed = args.Value("seed");
         g = ops::Shuffle(g, b, seed ? std::optional<uint64_t>(std::stoull(*seed, nullptr, 0)) : std::nullopt, reg);
       } else if (s == "shard") {
         need_source();
-        g = ops::Shard(g, args.Int("shards"), args.Int("index"), reg);
+        g = ops::Shard(g, args.Integer("shards"), args.Integer("index"), reg);
       } else if (s == "batch") {
         need_source();
-        g = ops::Batch(g, args.Int("size"), args.Bool("drop_remainder", false), reg);
+        g = ops::Batch(g, args.Integer("size"), args.Flag("drop_remainder", false), reg);
       } else if (s == "padded_batch") {
         need_source();
-        g = ops::PaddedBatch(g, args.Int("size"), args.Int("pad", 0), args.Bool("drop_remainder", false), reg);
+        g = ops::PaddedBatch(g, args.Integer("size"), args.Integer("pad", 0), args.Flag("drop_remainder", false), reg);
       } else if (s == "bucket") {
         need_source();
-        const auto b = args.IntList("boundaries"), z = args.IntList("sizes");
-        g = ops::BucketByLength(g, b, z, args.Int("pad", 0), args.Bool("drop_remainder", false), reg);
+        const auto b = args.Integers("boundaries"), z = args.Integers("sizes");
+        g = ops::BucketByLength(g, b, z, args.Integer("pad", 0), args.Flag("drop_remainder", false), reg);
       } else if (s == "prefetch") {
         need_source();
         out.tunables.push_back({"prefetch@" + std::to_string(out.tunables.size()) + ".buffer", "buffer_size"});
-        g = ops::Prefetch(g, args.Tunable("buffer", kAutotune), reg);
+        g = ops::Prefetch(g, args.IntOrAuto("buffer", kAutotune), reg);
       } else if (s == "repeat") {
         need_source();
-        g = ops::Repeat(g, args.Int("count"), reg);
+        g = ops::Repeat(g, args.Integer("count"), reg);
       } else if (s == "options") {
-        out.options.deterministic = args.Bool("deterministic", true);
-        if (auto seed = args.Find("seed")) out.options.seed_override = std::stoull(*seed, nullptr, 0);
+        out.options.deterministic = args.Flag("deterministic", true);
+        if (auto seed = args.Value("seed")) out.options.seed_override = std::stoull(*seed, nullptr, 0);
       } else if (s == "epochs") {
         if (line.words.size() != 1) Fail(L, C, "usage: epochs <n>");
         out.epochs = static_cast<int>(std::stoll(line.words[0]));
         if (out.epochs < 1) Fail(L, C, "epochs must be >= 1");
       } else if (s == "disable") {
-        auto rule = args.Find("rule");
+        auto rule = args.Value("rule");
         if (!rule) Fail(L, C, "usage: disable rule=<name>");
         out.disabled_rules.push_back(*rule);
       } else {
         Fail(L, C, "unknown stanza '" + s + "'");
       }
-      args.RejectUnknown();
+      args.CheckAllUsed();
     } catch (const PipelineError& e) {
       if (e.code() == ErrorCode::kParseError) throw;
       Fail(L, C, e.what());  // a builder's validation error, located

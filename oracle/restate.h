@@ -11,8 +11,9 @@
  *     C restatement of the reference runtime, pinned against the compiled
  *     reference (oracle/_ref, oracle/ref_shim.cpp) and against the known
  *     answers in SURVEY.md Appendix A (tests/golden/).
- *  2. map-UDF arithmetic (crop / flip / resize / normalize): the reference has
- *     no image UDFs, so this file DEFINES them.  The same C
+ *  2. map-UDF arithmetic (crop / flip / resize / normalize): PARITY UNPINNED
+ *     by the reference, which has no image UDFs, so this
+ *     file DEFINES them (as does orc_bucket_by_length for that new kind).  The same C
  *     functions are registered into the reference's UdfRegistry by
  *     oracle/ref_shim.cpp, so the compiled reference pipeline and this
  *     restatement agree by construction on the arithmetic; the order in which

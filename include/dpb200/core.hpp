@@ -99,6 +99,7 @@ class Value {
   static Value List(std::vector<Value> items);  // homogeneous (kValidationFailed)
   static Value Tuple(std::vector<Value> items) { return Value(Storage(TupleBox{std::move(items)})); }
   static Value FromTensor(Tensor t) { return Value(Storage(std::make_shared<Tensor>(std::move(t)))); }
+  static Value FromTensor(std::shared_ptr<Tensor> t) { return Value(Storage(std::move(t))); }
 
   Kind kind() const { return static_cast<Kind>(v_.index()); }
   int64_t int64() const { return std::get<int64_t>(v_); }

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <memory>
+#include <vector>
 #include <string>
 
 #include "dpb200/core.hpp"
@@ -82,5 +83,52 @@ template <typename T>
 T* P(const std::shared_ptr<void>& p) {
   return static_cast<T*>(p.get());
 }
+
+// Small-block recycling for the per-batch control blocks GetNext creates
+// (slot leases, Tensor views): a per-thread free list per 64-byte size
+// class, capped, falling back to operator new / delete.  Blocks freed on
+// another thread join that thread's list.
+struct BlockPool {
+  static constexpr int kClasses = 4, kCap = 4096;
+  static std::vector<void*>* Lists() {
+    thread_local std::vector<void*> lists[kClasses];
+    return lists;
+  }
+  static void* Get(size_t bytes) {
+    const size_t c = (bytes + 63) / 64 - 1;
+    if (c < kClasses) {
+      auto& l = Lists()[c];
+      if (!l.empty()) {
+        void* p = l.back();
+        l.pop_back();
+        return p;
+      }
+      return ::operator new((c + 1) * 64);
+    }
+    return ::operator new(bytes);
+  }
+  static void Put(void* p, size_t bytes) {
+    const size_t c = (bytes + 63) / 64 - 1;
+    if (c < kClasses) {
+      auto& l = Lists()[c];
+      if (l.size() < kCap) {
+        l.push_back(p);
+        return;
+      }
+    }
+    ::operator delete(p);
+  }
+};
+template <class T>
+struct PoolAllocator {
+  using value_type = T;
+  PoolAllocator() = default;
+  template <class U>
+  PoolAllocator(const PoolAllocator<U>&) {}
+  T* allocate(size_t n) { return static_cast<T*>(BlockPool::Get(n * sizeof(T))); }
+  void deallocate(T* p, size_t n) { BlockPool::Put(p, n * sizeof(T)); }
+  template <class U>
+  bool operator==(const PoolAllocator<U>&) const { return true; }
+};
 
 }  // namespace datapipe::b200::detail

@@ -88,7 +88,8 @@ struct Slot {
   cudaEvent_t ready = nullptr, release = nullptr, start = nullptr;
   bool release_recorded = false;
   // group bookkeeping
-  int64_t first_batch = 0, num_batches = 0, handed_out = 0;
+  int64_t first_batch = 0, num_batches = 0;
+  std::atomic<int64_t> handed_out{0};
   int64_t units = 0;  // what GetNext hands out from this slot: batches, or elements when unbatched
   std::atomic<int64_t> outstanding{0};
   bool busy = false;
@@ -206,7 +207,7 @@ class DevicePipeline {
           // after a Seek into the middle of a group, the skipped units count as handed out
           std::lock_guard lk(shared_->mu);
           const int64_t before = UnitsBefore(*cur_slot_, i, row);
-          if (cur_slot_->handed_out < before) cur_slot_->handed_out = before;
+          if (cur_slot_->handed_out.load() < before) cur_slot_->handed_out.store(before);
         }
         // one wait per group: the slot's ready event covers all its batches
         if (consumer_ != stream_ && !opt_.host_output)
@@ -983,27 +984,34 @@ class DevicePipeline {
     return 0;
   }
 
+  // A lease on `slot` for one handed-out unit.  Lock-free on the per-batch
+  // path: `outstanding` goes up before `handed_out`, so the drop that brings
+  // `outstanding` to 0 after the slot's last unit was handed out is the only
+  // one that sees both; it records the release event (one API call per
+  // group) under the lock.  The slot is reused only after that (TryIssueGroup),
+  // and the event orders every unit's consumer-stream work before the rewrite.
+  std::shared_ptr<void> Lease(const std::shared_ptr<Slot>& slot) {
+    slot->outstanding.fetch_add(1);
+    slot->handed_out.fetch_add(1);
+    return std::shared_ptr<void>(
+        nullptr,
+        [slot, consumer = consumer_, shared = shared_](void*) {
+          if (slot->outstanding.fetch_sub(1) == 1 && slot->handed_out.load() == slot->units) {
+            std::lock_guard lk(shared->mu);
+            if (shared->alive) {
+              cudaEventRecord(slot->release, consumer);
+              slot->release_recorded = true;
+              shared->slots_freed.fetch_add(1, std::memory_order_release);
+            }
+          }
+        },
+        PoolAllocator<char>());
+  }
+
   Element MakeElement(const std::shared_ptr<Slot>& slot, int64_t i) {
     const int64_t k = i - slot->first_batch;
     const int64_t rows = slot->batch_rows[k];
-    {
-      std::lock_guard lk(shared_->mu);
-      slot->handed_out++;
-      slot->outstanding++;
-    }
-    cudaStream_t consumer = consumer_;
-    std::shared_ptr<void> lease(nullptr, [slot, consumer, shared = shared_](void*) {
-      std::lock_guard lk(shared->mu);
-      // The slot is reused only after ALL its batches were handed out and
-      // dropped (TryIssueGroup), so one release event, recorded on the
-      // consumer stream by the last drop, orders every batch's consumer work
-      // before the rewrite (one API call per group, not per batch).
-      if (--slot->outstanding == 0 && slot->handed_out == slot->units && shared->alive) {
-        cudaEventRecord(slot->release, consumer);
-        slot->release_recorded = true;
-        shared->slots_freed.fetch_add(1, std::memory_order_release);
-      }
-    });
+    std::shared_ptr<void> lease = Lease(slot);
     const bool host = opt_.host_output;
     auto base_a = static_cast<uint8_t*>(host ? slot->ha.get() : slot->a.get()) + slot->batch_off_a[k];
     auto base_b = slot->b ? static_cast<uint8_t*>(host ? slot->hb.get() : slot->b.get()) + slot->batch_off_b[k] : nullptr;
@@ -1016,7 +1024,7 @@ class DevicePipeline {
       t.device = opt_.device;
       t.owner = lease;
       t.ready = slot->ready;
-      return Value::FromTensor(std::move(t));
+      return Value::FromTensor(std::allocate_shared<Tensor>(PoolAllocator<Tensor>(), std::move(t)));
     };
     std::vector<Value> comps;
     comps.reserve(2);
@@ -1050,20 +1058,7 @@ class DevicePipeline {
   // id, tensor [h, w, 3] view into the slot), as MapIterator delivers them
   Element MakeUnitElement(const std::shared_ptr<Slot>& slot, int64_t i, int64_t row) {
     const int64_t k = i - slot->first_batch;
-    {
-      std::lock_guard lk(shared_->mu);
-      slot->handed_out++;
-      slot->outstanding++;
-    }
-    cudaStream_t consumer = consumer_;
-    std::shared_ptr<void> lease(nullptr, [slot, consumer, shared = shared_](void*) {
-      std::lock_guard lk(shared->mu);
-      if (--slot->outstanding == 0 && slot->handed_out == slot->units && shared->alive) {
-        cudaEventRecord(slot->release, consumer);
-        slot->release_recorded = true;
-        shared->slots_freed.fetch_add(1, std::memory_order_release);
-      }
-    });
+    std::shared_ptr<void> lease = Lease(slot);
     if (L_.ragged) {  // one token sequence: a device view into the batch's values
       const int64_t* splits = reinterpret_cast<const int64_t*>(static_cast<const uint8_t*>(slot->hb.get()) +
                                                                slot->batch_off_b[k]);

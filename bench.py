@@ -46,6 +46,11 @@ CFG = {
                           "normalize fp32) -> Batch(256) -> Prefetch(AUTOTUNE)",
                  in_hw=(320, 320), out_hw=(224, 224), mode=1, batch=256, n=65536,
                  bytes_per_elem=320 * 320 * 3 + IMG_BYTES_WRITE, kernel="K4 resize_normalize_batch"),
+    "cfg5": dict(workload="Shard(N) over 32*N synthetic record files of 2048 256x256x3 u8 images (each GPU holds "
+                          "only its 32 files) -> Interleave(cycle 4, parallel 4) -> Shuffle(10k, seed 42) -> Map(random "
+                          "crop 224 + flip + normalize fp32) -> Batch(256) -> Prefetch(AUTOTUNE)",
+                 in_hw=(256, 256), out_hw=(224, 224), mode=0, batch=256, n=65536, files=32, cycle=4,
+                 bytes_per_elem=IMG_BYTES_READ + IMG_BYTES_WRITE, kernel="K3 crop_flip_normalize_batch"),
     "cfg1": dict(workload="Range(2^28) int64 -> Map(x*3+1) -> Batch(1024) (cfg1 shape at the roofline size "
                           "SURVEY.md 8(d) names; Range(1M) is the parity case)",
                  kind="range", batch=1024, n=1 << 28, bytes_per_elem=8, kernel="K1 range_affine_batch",
@@ -177,13 +182,26 @@ def cpu_reference(cfg, threads, warmup_batches, steps):
                                                              ctypes.c_void_p, ctypes.c_void_p]
     secs, elems = ctypes.c_double(), i64()
     sample = 2048
-    rc = L.ref_time_image_steps(cfg["mode"], *cfg["in_hw"], *cfg["out_hw"], 7, 0x5EED, sample, 10000, 42,
-                                cfg["batch"], threads, warmup_batches, steps, ctypes.byref(secs), ctypes.byref(elems))
+    if cfg.get("files"):  # cfg5: the reference's interleave over record readers
+        L.ref_time_interleave_image_steps.argtypes = [ctypes.c_int] * 5 + [u64, u64] + [i64] * 5 + [
+            i64, u64, i64, i64, i64, i64, ctypes.c_void_p, ctypes.c_void_p]
+        rec = cfg["n"] // cfg["files"]
+        rc = L.ref_time_interleave_image_steps(cfg["mode"], *cfg["in_hw"], *cfg["out_hw"], 7, 0x5EED, sample,
+                                               cfg["files"], rec, cfg["cycle"], cfg["cycle"], 10000, 42, cfg["batch"],
+                                               threads, warmup_batches, steps, ctypes.byref(secs),
+                                               ctypes.byref(elems))
+        what = (f"interleave(cycle {cfg['cycle']}, parallel {cfg['cycle']}) over {cfg['files']} readers of {rec} "
+                f"records copied from {sample} resident synthetic images")
+    else:
+        rc = L.ref_time_image_steps(cfg["mode"], *cfg["in_hw"], *cfg["out_hw"], 7, 0x5EED, sample, 10000, 42,
+                                    cfg["batch"], threads, warmup_batches, steps, ctypes.byref(secs),
+                                    ctypes.byref(elems))
+        what = f"{sample} resident synthetic images repeated"
     if rc != 0:
         raise RuntimeError(L.ref_last_error().decode())
     return {"value": elems.value / secs.value, "seconds": secs.value, "elements": elems.value, "cores": threads,
-            "sample": f"{sample} resident synthetic images repeated, {steps} timed batches of {cfg['batch']} after "
-                      f"{warmup_batches} warm-up, map_and_batch num_parallel_calls={threads}, prefetch(AUTOTUNE)"}
+            "sample": f"{what}, {steps} timed batches of {cfg['batch']} after {warmup_batches} warm-up, "
+                      f"map_and_batch num_parallel_calls={threads}, prefetch(AUTOTUNE)"}
 
 
 def cpu_reference_range(cfg):
@@ -236,14 +254,22 @@ def run_reference(args, cfg):
 
 
 # ---------------------------------------------------------------- GPU side --
-def build_graph(dp, cfg, src, repeat=True, shard=None):
+def build_graph(dp, cfg, src, repeat=True, shard=None, files=None):
     reg = dp.Registry()
     first = (reg.register_resize_bilinear("resize", *cfg["out_hw"]) if cfg["mode"] == 1
              else reg.register_random_crop_flip("crop", *cfg["out_hw"], seed=7, flip=True))
     reg.register_normalize("norm")
-    g = dp.Dataset.tensor_slices(reg, src)
-    if shard:
-        g = g.shard(*shard)  # Shard(k, rank) right after the source
+    if cfg.get("files"):  # cfg5: Shard over the record files, then Interleave their readers
+        files = files or cfg["files"] * (shard[0] if shard else 1)
+        reg.register_record_reader("reader", cfg["n"] // cfg["files"])
+        g = dp.Dataset.range(reg, files)
+        if shard:
+            g = g.shard(*shard)
+        g = g.interleave("reader", cfg["cycle"], cfg["cycle"], records=src)
+    else:
+        g = dp.Dataset.tensor_slices(reg, src)
+        if shard:
+            g = g.shard(*shard)  # Shard(k, rank) right after the source
     g = g.shuffle(10000, 42).map(first, -1).map("norm", -1).batch(cfg["batch"])
     if repeat:
         g = g.repeat(-1)
@@ -321,6 +347,10 @@ def run_ours(args, cfg):
     n = cfg["n"]
     if cfg["kind"] != "images":
         g, report = build_other_graph(dp, cfg, local, rank, world)
+    elif cfg.get("files"):  # cfg5: each rank holds only the record files of its shard
+        src = dp.Source.synthetic_records_sharded(cfg["files"] * world, n // cfg["files"], *cfg["in_hw"], world, rank,
+                                                  seed=0x5EED, device=local)
+        g, report = build_graph(dp, cfg, src, shard=(world, rank) if world > 1 else None)
     elif world > 1:  # each rank holds and processes shard `rank` of a world * n dataset
         lay = shard_layout(world, rank, n)
         src = dp.Source.synthetic_images_sharded(lay["global_count"], *cfg["in_hw"], world, rank, seed=0x5EED,
@@ -497,7 +527,14 @@ def run_e2e(dp, cfg, local, args, world=1, dev=None):
     h, w = cfg["in_hw"]
     host = np.random.default_rng(0).integers(0, 256, (n_host, h, w, 3), dtype=np.uint8)
     src = dp.Source.images_pinned_host(host, device=local)
-    g, _ = build_graph(dp, cfg, src)
+    if cfg.get("files"):  # cfg5: each rank's pinned records = its shard's files of R records
+        rec = cfg["n"] // cfg["files"]
+        files = n_host // rec
+        if world > 1:
+            src = src.as_shard(files * world * rec, world, dist_env()[0], rec)
+        g, _ = build_graph(dp, cfg, src, shard=(world, dist_env()[0]) if world > 1 else None, files=files * world)
+    else:
+        g, _ = build_graph(dp, cfg, src)
     # one batch per launch: each batch's D2H starts as soon as it is written
     it = dp.make_iterator(g, seed_override=1, device=local, host_output=True,
                           max_launch_bytes=int(os.environ.get("DP_E2E_LAUNCH_BYTES", 160 << 20)))

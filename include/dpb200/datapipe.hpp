@@ -76,7 +76,12 @@ struct SourceData {
   // `global_count`-element dataset, row r = position shard_index + r *
   // shard_count.  The graph must apply shard(shard_count, shard_index) to it
   // first (checked at MakeIterator).  shard_count 1 = fully resident.
-  int64_t global_count = 0, shard_count = 1, shard_index = 0;
+  // shard_block R > 1: the record blocks of an interleave's shard -- this
+  // process holds the R records of every interleave input (file) x with
+  // x % shard_count == shard_index, row r = record (x * R + r % R) of file
+  // x = (r / R) * shard_count + shard_index; the graph applies
+  // shard(shard_count, shard_index) to the interleave's inputs.
+  int64_t global_count = 0, shard_count = 1, shard_index = 0, shard_block = 1;
 };
 using SourcePtr = std::shared_ptr<const SourceData>;
 
@@ -86,6 +91,16 @@ SourcePtr SynthImages(int64_t count, int64_t h, int64_t w, uint64_t seed, int de
 // generated and held (pixels keyed by the global element id).
 SourcePtr SynthImagesSharded(int64_t global_count, int64_t h, int64_t w, uint64_t seed, int64_t num_shards,
                              int64_t index, int device = 0);
+// Synthetic records for interleave: `num_files` inputs of `records_per_file`
+// images (record r of file x = image id x * R + r); this process holds only
+// the files x % num_shards == index (all of them when num_shards is 1).
+SourcePtr SynthRecordsSharded(int64_t num_files, int64_t records_per_file, int64_t h, int64_t w, uint64_t seed,
+                              int64_t num_shards, int64_t index, int device = 0);
+// A view of `s` declaring its residency: it holds shard `index` of
+// `num_shards` of a `global_count`-element dataset in blocks of `block`
+// consecutive positions (block 1 = element shards; block R = the files of an
+// interleave's shard).  kInvalidAttr unless s->count is that shard's size.
+SourcePtr AsShard(const SourcePtr& s, int64_t global_count, int64_t num_shards, int64_t index, int64_t block = 1);
 SourcePtr SynthTokens(int64_t count, uint32_t max_len, uint64_t len_seed, uint64_t tok_seed, int device = 0);
 // Uploads host data (copied); images: u8 [count, h, w, 3].
 SourcePtr ImagesFromHost(const uint8_t* data, int64_t count, int64_t h, int64_t w, int device = 0);
@@ -96,7 +111,11 @@ SourcePtr Int64FromHost(const int64_t* values, int64_t count, int device = 0);
 SourcePtr TokensFromHost(const int32_t* lengths, int64_t count, const int32_t* tokens, int device = 0);
 // Length-prefixed record files (formats.md:67-74) read in order; payloads
 // packed into device memory.
-SourcePtr RecordsFromFiles(const std::vector<std::string>& paths, int device = 0);
+// num_shards > 1: read only the files f % num_shards == index (an
+// interleave's shard of the file list; every held file must hold the same
+// record count R -- the reader's).
+SourcePtr RecordsFromFiles(const std::vector<std::string>& paths, int device = 0, int64_t num_shards = 1,
+                           int64_t index = 0);
 // WriteRecordFile (runtime.hpp:102-107): [u32 LE length][payload] per record.
 void WriteRecordFile(const std::string& path, const std::vector<std::string>& payloads);
 

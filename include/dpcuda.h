@@ -124,17 +124,20 @@ int dp_k_resize_normalize_batch(const uint8_t* images, int64_t num_images,
                                 float* out, void* stream);
 
 /* Sharded residency (one process per GPU holds shard `id_base` of
- * `id_stride`): `images` row r is element id_base + r * id_stride; the
- * gather order indexes rows, ids (Philox counter, out_ids) are global. */
+ * `id_stride`, in blocks of `id_block` consecutive ids): `images` row r is
+ * element ((r / id_block) * id_stride + id_base) * id_block + r % id_block
+ * (id_block 1: id_base + r * id_stride); the gather order indexes rows, ids
+ * (Philox counter, out_ids) are global. */
 int dp_k_crop_flip_normalize_batch_ex(const uint8_t* images, int64_t num_images, int in_h, int in_w,
                                       const int64_t* order, int64_t first, int64_t rows, int64_t id_base,
-                                      int64_t id_stride, uint64_t udf_seed, int crop_h, int crop_w, int do_flip,
-                                      const float mean[3], const float stdv[3], int64_t* out_ids, float* out,
-                                      void* stream);
+                                      int64_t id_stride, int64_t id_block, uint64_t udf_seed, int crop_h,
+                                      int crop_w, int do_flip, const float mean[3], const float stdv[3],
+                                      int64_t* out_ids, float* out, void* stream);
 int dp_k_resize_normalize_batch_ex(const uint8_t* images, int64_t num_images, int in_h, int in_w,
                                    const int64_t* order, int64_t first, int64_t rows, int64_t id_base,
-                                   int64_t id_stride, int out_h, int out_w, const float mean[3],
-                                   const float stdv[3], int64_t* out_ids, float* out, void* stream);
+                                   int64_t id_stride, int64_t id_block, int out_h, int out_w,
+                                   const float mean[3], const float stdv[3], int64_t* out_ids, float* out,
+                                   void* stream);
 
 /* ---------------------------------------------------------------------- */
 /* K5  filter(len <= max_keep) stream compaction + padded_batch.           */

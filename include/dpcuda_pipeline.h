@@ -62,6 +62,18 @@ int dp_source_synthetic_images(int64_t count, int64_t h, int64_t w, uint64_t see
  * dataset are generated/held; graphs must start with shard(num_shards, index). */
 int dp_source_synthetic_images_sharded(int64_t global_count, int64_t h, int64_t w, uint64_t seed,
                                        int64_t num_shards, int64_t index, int device, dp_source** out);
+/* synthetic records of an interleave over `num_files` inputs of
+ * `records_per_file` images each (record r of file x = image id x * R + r);
+ * this process holds only the files x % num_shards == index (block residency:
+ * the graph applies shard(num_shards, index) to the interleave's inputs) */
+int dp_source_synthetic_records_sharded(int64_t num_files, int64_t records_per_file, int64_t h, int64_t w,
+                                        uint64_t seed, int64_t num_shards, int64_t index, int device,
+                                        dp_source** out);
+/* a view of `src` declaring that it holds shard `index` of `num_shards` of a
+ * `global_count`-element dataset, in blocks of `block` consecutive positions
+ * (1: element shards; R: the record files of an interleave's shard) */
+int dp_source_as_shard(const dp_source* src, int64_t global_count, int64_t num_shards, int64_t index,
+                       int64_t block, dp_source** out);
 int dp_source_images_from_host(const uint8_t* data, int64_t count, int64_t h, int64_t w, int device,
                                dp_source** out);
 /* pinned/registered host memory read by the kernels over PCIe (end-to-end runs; not copied) */
@@ -76,6 +88,10 @@ int dp_source_tokens_from_host(const int32_t* lengths, int64_t count, const int3
  * every file holding the reader's record count; ops::Interleave over
  * ops::FromFile readers, runtime.cpp:1044-1128) */
 int dp_source_records_from_files(const char* const* paths, int64_t num_paths, int device, dp_source** out);
+/* only the files f % num_shards == index are read (each process of a
+ * sharded interleave reads its own files; held files must hold equal counts) */
+int dp_source_records_from_files_sharded(const char* const* paths, int64_t num_paths, int64_t num_shards,
+                                         int64_t index, int device, dp_source** out);
 void dp_source_release(dp_source* src);
 
 /* ---- graph builders: include/datapipe/graph.hpp:134-165 (ops::*) ---- */

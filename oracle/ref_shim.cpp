@@ -466,6 +466,60 @@ int ref_time_image_steps(int mode, int in_h, int in_w, int out_h, int out_w, uin
   }
 }
 
+// CPU baseline for cfg5: from_memory(file ids 0..files-1) -> interleave(
+// reader: file s opens `records` images valued (s * records + r, image bytes),
+// cycle, parallel) -> shuffle -> repeat -> map(img udf, parallel) -> batch ->
+// prefetch(AUTOTUNE), optimized.  The readers copy their records out of a
+// resident sample of `sample` synthetic images (record i = sample[i % sample]).
+int ref_time_interleave_image_steps(int mode, int in_h, int in_w, int out_h, int out_w, uint64_t udf_seed,
+                                    uint64_t pix_seed, int64_t sample, int64_t files, int64_t records,
+                                    int64_t cycle, int64_t interleave_parallel, int64_t shuffle_buffer,
+                                    uint64_t shuffle_seed, int64_t batch, int64_t parallel, int64_t warmup,
+                                    int64_t steps, double* seconds, int64_t* elements) {
+  try {
+    UdfRegistry reg;
+    ImageUdfParams p{mode, in_h, in_w, out_h, out_w, udf_seed};
+    RegisterImageUdf(reg, p);
+    auto imgs = std::make_shared<std::vector<Element>>(SynthImages(sample, in_h, in_w, pix_seed));
+    reg.RegisterDataset(
+        "image_reader",
+        [&reg, imgs, records](const Element& e) {
+          const int64_t s = e.component(0).int64();
+          std::vector<Element> recs;
+          for (int64_t r = 0; r < records; ++r) {
+            const int64_t id = s * records + r;
+            std::vector<Value> c;
+            c.push_back(Value::Int64(id));
+            c.push_back(Value::Bytes((*imgs)[static_cast<size_t>(id) % imgs->size()].component(1).bytes()));
+            recs.push_back(Element(std::move(c)));
+          }
+          return ops::FromMemory(std::move(recs), reg);
+        },
+        ElementSpec({TypeSpec::Int64(), TypeSpec::Bytes()}));
+    DatasetGraph g = ops::FromMemory(IntRange(files), reg);
+    g = ops::Interleave(g, "image_reader", cycle, interleave_parallel, reg);
+    if (shuffle_buffer > 0) g = ops::Shuffle(g, shuffle_buffer, shuffle_seed, reg);
+    g = ops::Repeat(g, kInfiniteRepeat, reg);
+    g = ops::Map(g, ImageUdfName(p), parallel, reg);
+    g = ops::Batch(g, batch, false, reg);
+    g = ops::Prefetch(g, kAutotune, reg);
+    g = Optimize(g, RuleSet::Default(), reg).first;
+    auto it = MakeIterator(g, reg, Seeded(1));
+    for (int64_t i = 0; i < warmup; ++i) it->GetNext();
+    int64_t count = 0;
+    auto t0 = std::chrono::steady_clock::now();
+    for (int64_t i = 0; i < steps; ++i) {
+      auto e = it->GetNext();
+      count += static_cast<int64_t>(e->component(0).items().size());
+    }
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    *elements = count;
+    return 0;
+  } catch (const std::exception& e) {
+    return Fail(e);
+  }
+}
+
 // CPU baseline for cfg1 (range -> map -> batch, optimized).
 int ref_time_range_map_batch(int64_t n, int64_t batch, int64_t parallel,
                              int epochs, double* epoch_s) {

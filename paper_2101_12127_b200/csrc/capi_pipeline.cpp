@@ -129,6 +129,19 @@ int dp_source_synthetic_images_sharded(int64_t global_count, int64_t h, int64_t 
   DP_REQUIRE(out);
   return Guard([&] { *out = new dp_source{SynthImagesSharded(global_count, h, w, seed, num_shards, index, device)}; });
 }
+int dp_source_synthetic_records_sharded(int64_t num_files, int64_t records_per_file, int64_t h, int64_t w,
+                                        uint64_t seed, int64_t num_shards, int64_t index, int device,
+                                        dp_source** out) {
+  DP_REQUIRE(out);
+  return Guard([&] {
+    *out = new dp_source{SynthRecordsSharded(num_files, records_per_file, h, w, seed, num_shards, index, device)};
+  });
+}
+int dp_source_as_shard(const dp_source* src, int64_t global_count, int64_t num_shards, int64_t index,
+                       int64_t block, dp_source** out) {
+  DP_REQUIRE(src && out);
+  return Guard([&] { *out = new dp_source{AsShard(src->s, global_count, num_shards, index, block)}; });
+}
 int dp_source_images_from_host(const uint8_t* data, int64_t count, int64_t h, int64_t w, int device,
                                dp_source** out) {
   DP_REQUIRE(data && out);
@@ -150,6 +163,10 @@ int dp_source_tokens_from_host(const int32_t* lengths, int64_t count, const int3
   return Guard([&] { *out = new dp_source{TokensFromHost(lengths, count, tokens, device)}; });
 }
 int dp_source_records_from_files(const char* const* paths, int64_t num_paths, int device, dp_source** out) {
+  return dp_source_records_from_files_sharded(paths, num_paths, 1, 0, device, out);
+}
+int dp_source_records_from_files_sharded(const char* const* paths, int64_t num_paths, int64_t num_shards,
+                                         int64_t index, int device, dp_source** out) {
   DP_REQUIRE(out && (paths || num_paths == 0) && num_paths >= 0);
   return Guard([&] {
     std::vector<std::string> p;
@@ -157,7 +174,7 @@ int dp_source_records_from_files(const char* const* paths, int64_t num_paths, in
       if (!paths[i]) throw PipelineError(ErrorCode::kInvalidAttr, "records_from_files: null path");
       p.emplace_back(paths[i]);
     }
-    *out = new dp_source{RecordsFromFiles(p, device)};
+    *out = new dp_source{RecordsFromFiles(p, device, num_shards, index)};
   });
 }
 void dp_source_release(dp_source* src) { delete src; }

@@ -194,7 +194,40 @@ Lowered Lower(const DatasetGraph& g, const UdfRegistry& reg) {
     L.source_count = s.count;
   }
   if (seen_interleave) {
-    if (L.records && L.records->shard_count > 1) Unsupported("interleave records must be fully resident");
+    int64_t reader_records = 0;
+    for (const auto& op : L.chain)
+      if (op.kind == IndexOp::Kind::kInterleave) reader_records = op.b;
+    if (L.records && L.records->shard_count > 1) {
+      // block residency: this process holds the record files of the
+      // interleave inputs shard(k, g) keeps; the interleave then indexes the
+      // held files (local file j = input j of the shard)
+      const auto& rs = *L.records;
+      if (L.chain.size() < 2 || L.chain[0].kind != IndexOp::Kind::kShard || L.chain[0].a != rs.shard_count ||
+          L.chain[0].b != rs.shard_index || L.chain[1].kind != IndexOp::Kind::kInterleave)
+        Unsupported("records hold only the files of shard " + std::to_string(rs.shard_index) + " of " +
+                    std::to_string(rs.shard_count) + ": apply shard(" + std::to_string(rs.shard_count) + ", " +
+                    std::to_string(rs.shard_index) + ") to the interleave's inputs, directly");
+      if (reader_records != rs.shard_block)
+        Unsupported("sharded records hold files of " + std::to_string(rs.shard_block) +
+                    " records; the reader opens " + std::to_string(reader_records));
+      L.records_local = true;
+    }
+    if (L.records && !L.source && reader_records > 0) {
+      // every record the closed-form interleave names must be resident
+      int64_t first = 0, stride = 1, m = L.source_count;
+      for (const auto& op : L.chain) {
+        if (op.kind != IndexOp::Kind::kShard) break;
+        m = m > op.b ? (m - op.b + op.a - 1) / op.a : 0;
+        first += op.b * stride;
+        stride *= op.a;
+      }
+      const int64_t need = m == 0 ? 0 : L.records_local ? m * reader_records
+                                                         : (first + (m - 1) * stride + 1) * reader_records;
+      if (need > L.records->count)
+        throw PipelineError(ErrorCode::kMalformedInput,
+                            "interleave: the readers open " + std::to_string(need) + " records, the record source holds " +
+                                std::to_string(L.records->count));
+    }
     if (L.records && L.records->kind == SourceData::Kind::kRecords) {
       // interleave over record files: input element x opens file x.  A
       // reader of R > 0 records requires every file to hold R (records
@@ -254,6 +287,8 @@ Lowered Lower(const DatasetGraph& g, const UdfRegistry& reg) {
       Unsupported("a length predicate needs token sequences");
     if (op.pred.on == DevicePredicate::On::kValue && (sk != SourceData::Kind::kInt64 || op.opaque))
       Unsupported("a value predicate needs int64 elements (after affine maps only)");
+    if (op.pred.on == DevicePredicate::On::kValue && L.records_local)
+      Unsupported("a value predicate over sharded records");
   }
   if (sk == SourceData::Kind::kTokens && L.kind != BatchKind::kPadded) {
     if (!L.steps.empty()) Unsupported("map on token sequences");

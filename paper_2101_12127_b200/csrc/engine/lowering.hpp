@@ -49,8 +49,8 @@ struct Lowered {
   std::vector<IndexOp> chain;  // bottom-up
   SourcePtr source;            // element data (images / tokens / int64 values); null for range
   int64_t source_count = 0;    // positions entering the index chain
-  bool index_over_records = false;
   SourcePtr records;           // interleave record source
+  bool records_local = false;  // records hold only this shard's files (block residency): index held files
   std::vector<std::string> node_paths;  // root first
   std::string batch_node_path;
 };

@@ -478,6 +478,7 @@ class DevicePipeline {
           // arithmetic sequence here (identity or shards of it)
           int64_t first = 0, stride = 1;
           ArithmeticOf(count, first, stride);
+          if (L_.records_local) first = 0, stride = 1;  // block residency: input j of the shard = held file j
           if (op.b == 0 && L_.records && L_.records->kind == SourceData::Kind::kRecords) {
             BuildVarInterleave(first, stride, op.a, cur, count);
             break;
@@ -865,13 +866,13 @@ class DevicePipeline {
         if (L_.kind == BatchKind::kCrop)
           KCheck(dp_k_crop_flip_normalize_batch_ex(P<uint8_t>(src.values), src.count, static_cast<int>(src.h),
                                                    static_cast<int>(src.w), order, row0, rows_total, src.shard_index,
-                                                   src.shard_count, L_.crop.seed, oh, ow, L_.crop.flip ? 1 : 0, mean,
+                                                   src.shard_count, src.shard_block, L_.crop.seed, oh, ow, L_.crop.flip ? 1 : 0, mean,
                                                    stdv, P<int64_t>(slot->a), P<float>(slot->b), stream_),
                  "K3");
         else
           KCheck(dp_k_resize_normalize_batch_ex(P<uint8_t>(src.values), src.count, static_cast<int>(src.h),
                                                 static_cast<int>(src.w), order, row0, rows_total, src.shard_index,
-                                                src.shard_count, oh, ow, mean, stdv, P<int64_t>(slot->a),
+                                                src.shard_count, src.shard_block, oh, ow, mean, stdv, P<int64_t>(slot->a),
                                                 P<float>(slot->b), stream_),
                  "K4");
         launches_++;

@@ -124,7 +124,8 @@ void EncodeSource(const std::string& key, const SourceData& s, Out& w) {
   }
   w.Le<uint8_t>(kTagDeviceSource);
   w.Le<uint8_t>(static_cast<uint8_t>(s.kind));
-  for (int64_t v : {s.count, s.h, s.w, s.c, s.total_tokens, s.record_len, s.global_count, s.shard_count, s.shard_index})
+  for (int64_t v : {s.count, s.h, s.w, s.c, s.total_tokens, s.record_len, s.global_count, s.shard_count, s.shard_index,
+                    s.shard_block})
     w.Le<int64_t>(v);
 }
 
@@ -218,7 +219,7 @@ struct Decoder {
 
   SourcePtr BindSource(In& in) {
     const auto kind = static_cast<SourceData::Kind>(in.Le<uint8_t>());
-    int64_t d[9];
+    int64_t d[10];
     for (auto& v : d) v = in.Le<int64_t>();
     if (next_source >= sources.size())
       throw PipelineError(ErrorCode::kValidationFailed,
@@ -226,8 +227,8 @@ struct Decoder {
                               ": pass the sources (device data is not serialized)");
     SourcePtr s = sources[next_source++];
     if (!s) throw PipelineError(ErrorCode::kValidationFailed, "null device source");
-    const int64_t have[9] = {s->count, s->h, s->w, s->c, s->total_tokens, s->record_len,
-                             s->global_count, s->shard_count, s->shard_index};
+    const int64_t have[10] = {s->count, s->h, s->w, s->c, s->total_tokens, s->record_len,
+                              s->global_count, s->shard_count, s->shard_index, s->shard_block};
     if (s->kind != kind || std::memcmp(d, have, sizeof(d)) != 0)
       throw PipelineError(ErrorCode::kValidationFailed,
                           "device source #" + std::to_string(next_source - 1) + " does not match the serialized one");

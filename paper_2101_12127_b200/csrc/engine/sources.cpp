@@ -57,6 +57,57 @@ SourcePtr SynthImagesSharded(int64_t global_count, int64_t h, int64_t w, uint64_
   return s;
 }
 
+SourcePtr SynthRecordsSharded(int64_t num_files, int64_t records_per_file, int64_t h, int64_t w, uint64_t seed,
+                              int64_t num_shards, int64_t index, int device) {
+  if (num_shards < 1 || index < 0 || index >= num_shards || num_files <= index)
+    throw PipelineError(ErrorCode::kInvalidAttr, "synth records: shard index must be in [0, num_shards) and < files");
+  if (records_per_file < 1 || h < 1 || w < 1) throw PipelineError(ErrorCode::kInvalidAttr, "synth records: bad shape");
+  const int64_t files = (num_files - index + num_shards - 1) / num_shards, R = records_per_file;
+  auto s = std::make_shared<SourceData>();
+  s->kind = SourceData::Kind::kImages;
+  s->count = files * R;
+  s->h = h;
+  s->w = w;
+  s->c = 3;
+  s->device = device;
+  if (num_shards > 1) {
+    s->global_count = num_files * R;
+    s->shard_count = num_shards;
+    s->shard_index = index;
+    s->shard_block = R;
+  }
+  const size_t image = static_cast<size_t>(h) * w * 3;
+  s->values = DeviceAlloc(static_cast<size_t>(s->count) * image, device);
+  DeviceGuard g(device);
+  for (int64_t j = 0; j < files; ++j)  // held file j = file x: ids x * R .. x * R + R - 1 (setup, not timed)
+    KCheck(dp_k_synth_images(P<uint8_t>(s->values) + j * R * image, (index + j * num_shards) * R, R, image, seed,
+                             nullptr),
+           "synth records");
+  CudaCheck(cudaDeviceSynchronize(), "synth records");
+  return s;
+}
+
+SourcePtr AsShard(const SourcePtr& s, int64_t global_count, int64_t num_shards, int64_t index, int64_t block) {
+  if (!s) throw PipelineError(ErrorCode::kInvalidAttr, "as_shard: null source");
+  if (s->shard_count != 1) throw PipelineError(ErrorCode::kInvalidAttr, "as_shard: source is already a shard");
+  if (num_shards < 1 || index < 0 || index >= num_shards || block < 1 || global_count < 1)
+    throw PipelineError(ErrorCode::kInvalidAttr, "as_shard: need 0 <= index < num_shards, block >= 1");
+  const int64_t blocks = (global_count + block - 1) / block;
+  const int64_t mine = blocks > index ? (blocks - index + num_shards - 1) / num_shards : 0;
+  int64_t held = mine * block;
+  if (mine > 0 && (index + (mine - 1) * num_shards) == blocks - 1) held -= blocks * block - global_count;
+  if (held != s->count)
+    throw PipelineError(ErrorCode::kInvalidAttr, "as_shard: shard " + std::to_string(index) + " of " +
+                                                     std::to_string(num_shards) + " holds " + std::to_string(held) +
+                                                     " elements, the source " + std::to_string(s->count));
+  auto v = std::make_shared<SourceData>(*s);
+  v->global_count = global_count;
+  v->shard_count = num_shards;
+  v->shard_index = index;
+  v->shard_block = block;
+  return v;
+}
+
 SourcePtr SynthTokens(int64_t count, uint32_t max_len, uint64_t len_seed, uint64_t tok_seed, int device) {
   if (count < 1 || max_len < 1) throw PipelineError(ErrorCode::kInvalidAttr, "synth tokens: bad shape");
   // lengths: Pcg32(len_seed).Bounded(max_len) + 1 drawn in order (random.hpp:41-63)
@@ -142,8 +193,11 @@ SourcePtr ImagesFromPinnedHost(const uint8_t* data, int64_t count, int64_t h, in
 // FromFileIterator::Next (/root/reference/proj/src/runtime.cpp:416-474):
 // records are [u32 little-endian length][payload], files read in order; a
 // truncated length or payload is MalformedInput, a missing file MissingFile.
-SourcePtr RecordsFromFiles(const std::vector<std::string>& paths, int device) {
+SourcePtr RecordsFromFiles(const std::vector<std::string>& paths, int device, int64_t num_shards, int64_t index) {
   if (paths.empty()) throw PipelineError(ErrorCode::kInvalidAttr, "from_file: 'paths' must be non-empty");
+  if (num_shards < 1 || index < 0 || index >= num_shards || static_cast<int64_t>(paths.size()) <= index)
+    throw PipelineError(ErrorCode::kInvalidAttr, "records: shard index must be in [0, num_shards) and < files");
+  auto held = [&](size_t fi) { return static_cast<int64_t>(fi) % num_shards == index; };
   // Pass 1: walk the length headers (seeking over payloads) -- validates the
   // framing and sizes everything.  Pass 2 reads the payloads straight into
   // one pinned staging buffer (one host copy of the data), then one H2D copy.
@@ -157,6 +211,7 @@ SourcePtr RecordsFromFiles(const std::vector<std::string>& paths, int device) {
   std::vector<int64_t> per_file;
   int64_t uniform = -1;
   for (size_t fi = 0; fi < paths.size(); ++fi) {
+    if (!held(fi)) continue;
     const std::string& path = paths[fi];
     FILE* f = std::fopen(path.c_str(), "rb");
     if (!f) throw PipelineError(ErrorCode::kMissingFile, "no such file: " + path);
@@ -192,12 +247,24 @@ SourcePtr RecordsFromFiles(const std::vector<std::string>& paths, int device) {
   s->kind = SourceData::Kind::kRecords;
   s->count = static_cast<int64_t>(recs.size());
   s->record_len = uniform >= 0 ? uniform : 0;
+  if (num_shards > 1) {  // block residency: every held file holds R records
+    for (int64_t c : per_file)
+      if (c != per_file[0])
+        throw PipelineError(ErrorCode::kMalformedInput,
+                            "sharded records: held files hold " + std::to_string(per_file[0]) + " and " +
+                                std::to_string(c) + " records (block residency needs equal files)");
+    s->shard_count = num_shards;
+    s->shard_index = index;
+    s->shard_block = std::max<int64_t>(per_file[0], 1);
+    s->global_count = per_file[0] * static_cast<int64_t>(paths.size());
+  }
   s->file_records = std::move(per_file);
   s->device = device;
   const size_t total = static_cast<size_t>(offsets.back());
   auto staging = PinnedAlloc(std::max<size_t>(total, 16));
   char* dst = static_cast<char*>(staging.get());
   for (size_t fi = 0, r = 0; fi < paths.size(); ++fi) {
+    if (!held(fi)) continue;
     FILE* f = std::fopen(paths[fi].c_str(), "rb");
     if (!f) throw PipelineError(ErrorCode::kMissingFile, "no such file: " + paths[fi]);
     for (; r < recs.size() && recs[r].file == fi; ++r) {

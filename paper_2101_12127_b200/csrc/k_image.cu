@@ -35,6 +35,20 @@ constexpr size_t kSmemBudget = 200 * 1024;
 
 __device__ __forceinline__ float sel3(int c, float a, float b, float d) { return c == 0 ? a : (c == 1 ? b : d); }
 
+// Element id of resident row r (the Philox counter and the emitted id).
+// Fully resident: id = r.  Sharded residency (one process per GPU holds
+// blocks b % stride == base of `block` consecutive positions; block 1 =
+// element shards, block R = the record files of an interleave's shard):
+//   id = ((r / block) * stride + base) * block + r % block.
+struct RowIds {
+  int64_t base, stride, block;
+  __device__ __forceinline__ int64_t of(int64_t r) const {
+    if (block == 1) return base + r * stride;
+    const int64_t q = r / block;
+    return (q * stride + base) * block + (r - q * block);
+  }
+};
+
 struct ImageArgs {
   const uint8_t* images;
   const int64_t* order;
@@ -45,7 +59,7 @@ struct ImageArgs {
   int in_h, in_w, out_h, out_w;
   int bands;
   NormConsts nc;
-  int64_t id_base, id_stride;  // element id of row r = id_base + r * id_stride
+  RowIds ids;  // element id of resident row r = ids.of(r)
 };
 
 // ---------------------------------------------------------------- K3 ----
@@ -57,7 +71,7 @@ crop_generic_kernel(ImageArgs a, uint64_t seed, int do_flip, int sstride) {
   const int64_t j = blockIdx.x / a.bands;
   const int64_t row = a.order ? a.order[a.first + j] : a.first + j;
   if (row < 0 || row >= a.num_images) return;  // engine orders are in range by construction
-  const int64_t id = a.id_base + row * a.id_stride;  // element id (sharded residency)
+  const int64_t id = a.ids.of(row);  // element id (sharded residency)
   CropParams cp = crop_params(seed, id, a.in_h, a.in_w, a.out_h, a.out_w);
   if (!do_flip) cp.flip = 0;
   if (band == 0 && threadIdx.x == 0) a.out_ids[j] = id;
@@ -147,7 +161,7 @@ resize_generic_kernel(ImageArgs a) {
   const int64_t j = blockIdx.x / a.bands;
   const int64_t row = a.order ? a.order[a.first + j] : a.first + j;
   if (row < 0 || row >= a.num_images) return;  // engine orders are in range by construction
-  if (band == 0 && threadIdx.x == 0) a.out_ids[j] = a.id_base + row * a.id_stride;
+  if (band == 0 && threadIdx.x == 0) a.out_ids[j] = a.ids.of(row);
 
   const int y_begin = band * kResizeBandRows;
   const int nrows = min(kResizeBandRows, a.out_h - y_begin);
@@ -295,7 +309,7 @@ struct FastArgs {
   uint64_t seed;
   int do_flip;
   NormConsts nc;
-  int64_t id_base, id_stride;  // element id of row r = id_base + r * id_stride
+  RowIds ids;  // element id of resident row r = ids.of(r)
 };
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -340,7 +354,7 @@ struct CropOp {
     const int64_t row = a.order ? a.order[a.first + p.j] : a.first + p.j;
     const bool valid = row >= 0 && row < a.num_images;
     p.row = valid ? row : -1;
-    p.id = valid ? a.id_base + row * a.id_stride : -1;
+    p.id = valid ? a.ids.of(row) : -1;
     p.nrows = min(a.band_rows, a.out_h - p.band * a.band_rows);
     CropParams cp{0, 0, 0};
     if (valid) cp = crop_params(a.seed, p.id, a.in_h, a.in_w, a.out_h, a.out_w);
@@ -433,7 +447,7 @@ struct ResizeOp {
     const int64_t row = a.order ? a.order[a.first + p.j] : a.first + p.j;
     const bool valid = row >= 0 && row < a.num_images;
     p.row = valid ? row : -1;
-    p.id = valid ? a.id_base + row * a.id_stride : -1;
+    p.id = valid ? a.ids.of(row) : -1;
     const int y_begin = p.band * a.band_rows;
     p.nrows = min(a.band_rows, a.out_h - y_begin);
     p.src_row = taps[y_begin].y0;
@@ -672,8 +686,7 @@ using namespace dpk;
 
 static int crop_impl(const uint8_t* images, int64_t num_images, int in_h, int in_w, const int64_t* order, int64_t first,
                      int64_t rows, uint64_t udf_seed, int crop_h, int crop_w, int do_flip, const float mean[3],
-                     const float stdv[3], int64_t* out_ids, float* out, void* stream, int64_t id_base,
-                     int64_t id_stride) {
+                     const float stdv[3], int64_t* out_ids, float* out, void* stream, RowIds ids) {
   int st = check_common(images, num_images, in_h, in_w, rows, crop_h, crop_w, out_ids, out, "crop_flip_normalize");
   if (st) return st;
   if (crop_h > in_h || crop_w > in_w)
@@ -683,8 +696,7 @@ static int crop_impl(const uint8_t* images, int64_t num_images, int in_h, int in
   if (fast_ok(images, in_w, crop_w, out)) {
     FastArgs f = make_fast(images, num_images, in_h, in_w, order, first, rows, crop_h, crop_w, mean, stdv, out_ids,
                            out, env_int("DP_DEV_CROP_BAND", kFastCropBandRows), kCropStages);
-    f.id_base = id_base;
-    f.id_stride = id_stride;
+    f.ids = ids;
     f.seed = udf_seed;
     f.do_flip = do_flip;
     f.stage_stride = ((crop_w * 3 + 15 + 15) / 16) * 16;
@@ -695,7 +707,7 @@ static int crop_impl(const uint8_t* images, int64_t num_images, int in_h, int in
     if (smem <= kSmemBudget) return launch_persistent(pipeline_kernel<CropOp>, f, smem, s, "crop_flip_normalize");
   }
   ImageArgs a{images, order, first, out_ids, out, num_images, in_h, in_w, crop_h, crop_w,
-              (crop_h + kCropBandRows - 1) / kCropBandRows, make_norm(mean, stdv), id_base, id_stride};
+              (crop_h + kCropBandRows - 1) / kCropBandRows, make_norm(mean, stdv), ids};
   const size_t row_bytes = static_cast<size_t>(in_w) * 3;
   const bool aligned = (row_bytes % 16 == 0) && (reinterpret_cast<uintptr_t>(images) % 16 == 0) &&
                        (crop_w % 4 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
@@ -716,7 +728,7 @@ static int crop_impl(const uint8_t* images, int64_t num_images, int in_h, int in
 
 static int resize_impl(const uint8_t* images, int64_t num_images, int in_h, int in_w, const int64_t* order,
                        int64_t first, int64_t rows, int out_h, int out_w, const float mean[3], const float stdv[3],
-                       int64_t* out_ids, float* out, void* stream, int64_t id_base, int64_t id_stride) {
+                       int64_t* out_ids, float* out, void* stream, RowIds ids) {
   int st = check_common(images, num_images, in_h, in_w, rows, out_h, out_w, out_ids, out, "resize_normalize");
   if (st) return st;
   if (rows == 0) return DP_OK;
@@ -724,8 +736,7 @@ static int resize_impl(const uint8_t* images, int64_t num_images, int in_h, int 
   if (fast_ok(images, in_w, out_w, out)) {
     FastArgs f = make_fast(images, num_images, in_h, in_w, order, first, rows, out_h, out_w, mean, stdv, out_ids, out,
                            env_int("DP_DEV_RESIZE_BAND", kFastResizeBandRows), kResizeStages);
-    f.id_base = id_base;
-    f.id_stride = id_stride;
+    f.ids = ids;
     const double sc = static_cast<double>(in_h) / out_h;
     int src_rows = static_cast<int>(f.band_rows * sc) + 3;
     if (src_rows > in_h) src_rows = in_h;
@@ -738,7 +749,7 @@ static int resize_impl(const uint8_t* images, int64_t num_images, int in_h, int 
       return launch_persistent(pipeline_kernel<ResizeOp>, f, smem, s, "resize_normalize");
   }
   ImageArgs a{images, order, first, out_ids, out, num_images, in_h, in_w, out_h, out_w,
-              (out_h + kResizeBandRows - 1) / kResizeBandRows, make_norm(mean, stdv), id_base, id_stride};
+              (out_h + kResizeBandRows - 1) / kResizeBandRows, make_norm(mean, stdv), ids};
   const size_t row_bytes = static_cast<size_t>(in_w) * 3;
   const bool aligned = (row_bytes % 16 == 0) && (reinterpret_cast<uintptr_t>(images) % 16 == 0) &&
                        (out_w % 4 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
@@ -765,16 +776,18 @@ extern "C" int dp_k_crop_flip_normalize_batch(const uint8_t* images, int64_t num
                                               int crop_h, int crop_w, int do_flip, const float mean[3],
                                               const float stdv[3], int64_t* out_ids, float* out, void* stream) {
   return crop_impl(images, num_images, in_h, in_w, order, first, rows, udf_seed, crop_h, crop_w, do_flip, mean, stdv,
-                   out_ids, out, stream, 0, 1);
+                   out_ids, out, stream, RowIds{0, 1, 1});
 }
 
 extern "C" int dp_k_crop_flip_normalize_batch_ex(const uint8_t* images, int64_t num_images, int in_h, int in_w,
                                                  const int64_t* order, int64_t first, int64_t rows, int64_t id_base,
-                                                 int64_t id_stride, uint64_t udf_seed, int crop_h, int crop_w,
-                                                 int do_flip, const float mean[3], const float stdv[3],
+                                                 int64_t id_stride, int64_t id_block, uint64_t udf_seed, int crop_h,
+                                                 int crop_w, int do_flip, const float mean[3], const float stdv[3],
                                                  int64_t* out_ids, float* out, void* stream) {
+  if (id_stride < 1 || id_block < 1 || id_base < 0 || id_base >= id_stride)
+    return fail(DP_ERR_INVALID_ATTR, "crop_flip_normalize: bad sharded residency (id_base/id_stride/id_block)");
   return crop_impl(images, num_images, in_h, in_w, order, first, rows, udf_seed, crop_h, crop_w, do_flip, mean, stdv,
-                   out_ids, out, stream, id_base, id_stride);
+                   out_ids, out, stream, RowIds{id_base, id_stride, id_block});
 }
 
 extern "C" int dp_k_resize_normalize_batch(const uint8_t* images, int64_t num_images, int in_h, int in_w,
@@ -782,13 +795,16 @@ extern "C" int dp_k_resize_normalize_batch(const uint8_t* images, int64_t num_im
                                            const float mean[3], const float stdv[3], int64_t* out_ids, float* out,
                                            void* stream) {
   return resize_impl(images, num_images, in_h, in_w, order, first, rows, out_h, out_w, mean, stdv, out_ids, out,
-                     stream, 0, 1);
+                     stream, RowIds{0, 1, 1});
 }
 
 extern "C" int dp_k_resize_normalize_batch_ex(const uint8_t* images, int64_t num_images, int in_h, int in_w,
                                               const int64_t* order, int64_t first, int64_t rows, int64_t id_base,
-                                              int64_t id_stride, int out_h, int out_w, const float mean[3],
-                                              const float stdv[3], int64_t* out_ids, float* out, void* stream) {
+                                              int64_t id_stride, int64_t id_block, int out_h, int out_w,
+                                              const float mean[3], const float stdv[3], int64_t* out_ids, float* out,
+                                              void* stream) {
+  if (id_stride < 1 || id_block < 1 || id_base < 0 || id_base >= id_stride)
+    return fail(DP_ERR_INVALID_ATTR, "resize_normalize: bad sharded residency (id_base/id_stride/id_block)");
   return resize_impl(images, num_images, in_h, in_w, order, first, rows, out_h, out_w, mean, stdv, out_ids, out,
-                     stream, id_base, id_stride);
+                     stream, RowIds{id_base, id_stride, id_block});
 }

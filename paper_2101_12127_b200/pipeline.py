@@ -67,6 +67,9 @@ _SIGS = {
     "dp_source_synthetic_tokens": [c_i64, ctypes.c_uint32, c_u64, c_u64, c_int, PP],
     "dp_source_tokens_from_host": [c_vp, c_i64, c_vp, c_int, PP],
     "dp_source_records_from_files": [ctypes.POINTER(ctypes.c_char_p), c_i64, c_int, PP],
+    "dp_source_records_from_files_sharded": [ctypes.POINTER(ctypes.c_char_p), c_i64, c_i64, c_i64, c_int, PP],
+    "dp_source_as_shard": [c_vp, c_i64, c_i64, c_i64, c_i64, PP],
+    "dp_source_synthetic_records_sharded": [c_i64, c_i64, c_i64, c_i64, c_u64, c_i64, c_i64, c_int, PP],
     "dp_source_release": [c_vp],
     "dp_graph_range": [c_vp, c_i64, PP],
     "dp_graph_from_memory_i64": [c_vp, c_vp, c_i64, c_int, PP],
@@ -217,11 +220,32 @@ class Source:
         _rel(self, "dp_source_release")
 
     @staticmethod
-    def records_from_files(paths, device=0):
-        """Record files read into device memory: the records of an interleave over files."""
+    def records_from_files(paths, device=0, num_shards=1, index=0):
+        """Record files read into device memory: the records of an interleave
+        over files.  num_shards > 1 reads only the files f % num_shards ==
+        index (graphs apply .shard(num_shards, index) to the interleave's
+        inputs)."""
         arr = (ctypes.c_char_p * max(1, len(paths)))(*[os.fsencode(p) for p in paths])
         out = c_vp()
-        _check(L().dp_source_records_from_files(arr, len(paths), device, ctypes.byref(out)))
+        _check(L().dp_source_records_from_files_sharded(arr, len(paths), num_shards, index, device,
+                                                        ctypes.byref(out)))
+        return Source(out)
+
+    def as_shard(self, global_count, num_shards, index, block=1):
+        """A view of this source holding shard `index` of `num_shards` of a
+        `global_count`-element dataset, in blocks of `block` positions."""
+        out = c_vp()
+        _check(L().dp_source_as_shard(self.h, global_count, num_shards, index, block, ctypes.byref(out)))
+        return Source(out, self)
+
+    @staticmethod
+    def synthetic_records_sharded(num_files, records_per_file, h, w, num_shards=1, index=0, seed=0x5EED, device=0):
+        """Interleave records: `num_files` inputs of `records_per_file` images
+        (record r of file x = image id x * R + r); holds only the files
+        x % num_shards == index."""
+        out = c_vp()
+        _check(L().dp_source_synthetic_records_sharded(num_files, records_per_file, h, w, seed, num_shards, index,
+                                                       device, ctypes.byref(out)))
         return Source(out)
 
     @staticmethod

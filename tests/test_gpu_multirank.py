@@ -9,6 +9,7 @@ import os
 import subprocess
 import sys
 
+import numpy as np
 import pytest
 
 pytestmark = pytest.mark.gpu
@@ -34,4 +35,27 @@ def test_two_rank_bench_order_check_matches_oracle(orc):
         # the bench graph repeats above the batch: epoch 0's shuffle is salted
         # MixSeeds(base, 0) (RepeatIterator::MakeChild, runtime.cpp:1175-1177)
         ids = pos[orc.shuffle_order(pos.size, 10000, orc.shuffle_seed(orc.mix_seeds(1, 0), 42))]
+        assert digests[r] == f"{orc.order_digest(ids[:8 * 256]):016x}", r
+
+
+def test_two_rank_cfg5_block_residency_order_check(orc):
+    """cfg5 on two ranks: each holds only the record files of its
+    shard(2, rank) of the interleave's inputs; its digest equals the oracle's
+    interleave (closed form) -> shuffle(10k, 42) of those files."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    n, files = 8192, 32  # per rank: 32 files of 256 records
+    env = dict(os.environ, DP_BENCH_ONE_GPU="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", "29534", os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "32",
+           "--warmup", "16", "--elements-per-gpu", str(n), "--config", "cfg5"]
+    out = subprocess.run(cmd, capture_output=True, text=True, env=env, cwd=ROOT, timeout=900)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
+    line = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["batches_in_window"] == 32 and line["e2e"]["value"] > 0
+    digests = line["order_check"]["per_rank"]
+    for r in range(2):
+        inter = orc.interleave_order(np.arange(r, 2 * files, 2), 4, n // files)
+        ids = inter[orc.shuffle_order(inter.size, 10000, orc.shuffle_seed(orc.mix_seeds(1, 0), 42))]
         assert digests[r] == f"{orc.order_digest(ids[:8 * 256]):016x}", r

@@ -596,6 +596,71 @@ def test_cfg5_interleave_shuffle_map_and_batch(dp, orc):
         assert np.array_equal(pix[r], orc.crop_flip_normalize(orc.images(p, 1, 48, 48)[0], p, 32, 32))
 
 
+def test_cfg5_sharded_record_residency(dp, orc, tmp_path):
+    """cfg5 with block residency: process g of k holds only the record files
+    of the interleave inputs shard(k, g) keeps (synthetic or read from its own
+    files); its output equals the same graph over fully resident records,
+    the shards' ids partition the dataset, and a mismatched shard / reader is
+    rejected."""
+    m, rec, k, cycle = 11, 6, 3, 4
+    reg = image_registry(dp, 0, crop=(32, 32))
+    reg.register_record_reader("reader", rec)
+    reg.register_decode_raw("decode", 48, 48)
+    imgs = orc.images(0, m * rec, 48, 48)
+    paths = [str(tmp_path / f"part-{x}.rec") for x in range(m)]
+    for x, p in enumerate(paths):
+        dp.write_record_file(p, [im.tobytes() for im in imgs[x * rec:(x + 1) * rec]])
+
+    def run(recs, g, par, decode=False):
+        d = dp.Dataset.range(reg, m).shard(k, g).interleave("reader", cycle, par, records=recs)
+        if decode:
+            d = d.map("decode")
+        d, _ = d.shuffle(20, 42).map("crop").map("norm").batch(8).prefetch(-1).optimize()
+        return drain(dp.make_iterator(d, seed_override=1), comps=(0, 1))
+
+    full = dp.Source.synthetic_records_sharded(m, rec, 48, 48)
+    seen = []
+    for g in range(k):
+        for par in (1, cycle):
+            want = run(full, g, par)
+            got = run(dp.Source.synthetic_records_sharded(m, rec, 48, 48, k, g), g, par)
+            files = run(dp.Source.records_from_files(paths, num_shards=k, index=g), g, par, decode=True)
+            held = np.concatenate([imgs[x * rec:(x + 1) * rec] for x in range(g, m, k)])
+            view = run(dp.Source.images_from_host(held).as_shard(m * rec, k, g, rec), g, par)
+            assert len(got) == len(want) == len(files) == len(view)
+            for a, b, c, v in zip(got, want, files, view):
+                assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+                assert np.array_equal(c[0], b[0]) and np.array_equal(c[1], b[1])
+                assert np.array_equal(v[0], b[0]) and np.array_equal(v[1], b[1])
+        ids = np.concatenate([b[0] for b in got])
+        assert sorted(ids.tolist()) == sorted(x * rec + r for x in range(g, m, k) for r in range(rec))
+        p = int(got[-1][0][-1])
+        assert np.array_equal(got[-1][1][-1], orc.crop_flip_normalize(imgs[p], p, 32, 32))
+        seen += ids.tolist()
+    assert sorted(seen) == list(range(m * rec))
+    mine = dp.Source.synthetic_records_sharded(m, rec, 48, 48, k, 1)
+    bad = [dp.Dataset.range(reg, m).shard(k, 0).interleave("reader", cycle, 1, records=mine),
+           dp.Dataset.range(reg, m).interleave("reader", cycle, 1, records=mine)]
+    reg.register_record_reader("reader5", rec - 1)
+    bad.append(dp.Dataset.range(reg, m).shard(k, 1).interleave("reader5", cycle, 1, records=mine))
+    for d in bad:
+        with pytest.raises(dp.DpError) as e:
+            dp.make_iterator(d.map("crop").map("norm").batch(8))
+        assert e.value.code == dp.ERR["InvalidAttr"]
+    with pytest.raises(dp.DpError) as e:  # wrong size for shard 0's files
+        dp.Source.images_from_host(imgs[:rec * 3]).as_shard(m * rec, k, 0, rec)
+    assert e.value.code == dp.ERR["InvalidAttr"]
+    with pytest.raises(dp.DpError) as e:  # an input past the resident records
+        dp.make_iterator(dp.Dataset.range(reg, m + 1).interleave("reader", cycle, 1, records=full).map("crop")
+                         .map("norm").batch(8))
+    assert e.value.code == dp.ERR["MalformedInput"]
+    dp.write_record_file(paths[4], [imgs[0].tobytes()])  # held by shard 1: unequal held files
+    with pytest.raises(dp.DpError) as e:
+        dp.Source.records_from_files(paths, num_shards=k, index=1)
+    assert e.value.code == dp.ERR["MalformedInput"]
+    dp.Source.records_from_files(paths, num_shards=k, index=0)  # shard 0 does not read it
+
+
 def test_interleave_over_record_files_equals_cfg5(dp, orc, tmp_path):
     """Interleave over record files (from_file +
     Interleave): input element x opens file x; equals the same pipeline over

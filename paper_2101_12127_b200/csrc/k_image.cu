@@ -323,6 +323,7 @@ struct RowTap {
 
 // ---- K3 stage operations ----
 struct CropOp {
+  static constexpr bool kWarpWide = false;
   float mu[4], sd[4], rc[4];
   int off_n[4], off_f[4];
   f32x2 mu2[2], nsd2[2], rc2[2];
@@ -404,6 +405,7 @@ struct CropOp {
 
 // ---- K4 stage operations ----
 struct ResizeOp {
+  static constexpr bool kWarpWide = false;
   float mu[4], sd[4], rc[4], wx[4];
   int o0[4], o1[4];
   f32x2 mu2[2], nsd2[2], rc2[2], wx2[2];
@@ -504,6 +506,146 @@ struct ResizeOp {
   }
 };
 
+// K4 over a PERIODIC horizontal map: in_w = PI * G, out_w = PO * G, and
+// every output column x takes source columns x0 = PI * (x / PO) + T(x % PO)
+// and x0 + 1 (checked on the host against resize_coord for every x:
+// periodic_ok).  One lane owns one period ("group": PO output pixels = 3 * PO
+// floats from a window of source bytes it loads as 32-bit words), one warp
+// one output row (G <= 32 groups).  The bytes are picked out of registers
+// with PRMT at compile-time positions instead of one shared-memory byte load
+// per tap (ResizeOp: 16 per float4, ~1.8-way bank conflicts), and the row is
+// transposed through a per-warp shared buffer (stride 3 * PO words, odd:
+// conflict-free) into coalesced float4 stores.  Same lerp / normalize ops,
+// same order, as ResizeOp and the oracle (orc_resize_normalize).
+template <int PO, int PI>
+struct ResizePOp {
+  __host__ __device__ static constexpr int T(int x) { return ((2 * x + 1) * PI - PO) / (2 * PO); }
+  static constexpr int kF = 3 * PO;                       // floats per group
+  static constexpr int kPairs = (kF + 1) / 2;
+  static constexpr int kSpan = 3 * (T(PO - 1) + 2);       // window bytes
+  static constexpr int kOmax = (3 * PI) % 4 == 0 ? 0 : ((3 * PI) % 2 == 0 ? 2 : 3);
+  static constexpr int kNW = (kOmax + kSpan + 3) / 4;     // 32-bit words per window
+  static constexpr bool kWarpWide = true;
+  f32x2 wx2[kPairs];
+  f32x2 mu2[3], nsd2[3], rc2[3];  // by pair pattern (channel of the pair's first float: 0, 2, 1)
+  PkK k;
+  float* stg;  // this warp's row buffer: G * kF floats
+  int byte0;   // the group's first source byte in a row
+
+  __device__ void init(const FastArgs& a, int q, uint8_t* taps) {
+    float wx[kF];
+#pragma unroll
+    for (int e = 0; e < kF; e += 3) {
+      int x0, x1;
+      resize_coord(q * PO + e / 3, a.in_w, a.out_w, x0, x1, wx[e]);
+      wx[e + 1] = wx[e];
+      wx[e + 2] = wx[e];
+    }
+#pragma unroll
+    for (int i = 0; i < kPairs; ++i) wx2[i] = pk2(wx[2 * i], wx[2 * i + 1 < kF ? 2 * i + 1 : 2 * i]);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const int c1 = (c + 1) % 3;
+      mu2[c] = pk2(a.nc.mean[c], a.nc.mean[c1]);
+      nsd2[c] = pk2(-a.nc.stdv[c], -a.nc.stdv[c1]);
+      rc2[c] = pk2(a.nc.rcp[c], a.nc.rcp[c1]);
+    }
+    k = PkK(a.nc);
+    const size_t taps_bytes = ((static_cast<size_t>(a.out_h) * sizeof(RowTap) + 15) / 16) * 16;
+    stg = reinterpret_cast<float*>(taps + taps_bytes) + static_cast<size_t>(threadIdx.x >> 5) * a.q_per_row * kF;
+    byte0 = q * PI * 3;
+  }
+
+  static __device__ Plan plan(const FastArgs& a, int64_t item, const uint8_t* taps_raw) {
+    return ResizeOp::plan(a, item, taps_raw);
+  }
+  static __device__ void issue(const FastArgs& a, const Plan& p, uint8_t* dst, StageMeta* meta, uint64_t* full,
+                               int lane, uint64_t pol) {
+    ResizeOp::issue(a, p, dst, meta, full, lane, pol);
+  }
+
+  // byte b of the (shifted) window as an exact fp32 (the 2^23 magic-number
+  // conversion; PRMT builds 0x4B0000bb directly)
+  static __device__ __forceinline__ uint32_t pick(const uint32_t* w, int b) {
+    return __byte_perm(w[b >> 2], 0x4B000000u, 0x7440u | static_cast<uint32_t>(b & 3));
+  }
+  __device__ __forceinline__ f32x2 px2(const uint32_t* w, int b0, int b1) const {
+    return fma2(pk2(__uint_as_float(pick(w, b0)), __uint_as_float(pick(w, b1))), k.one, k.neg_magic);
+  }
+
+  __device__ void consume(const FastArgs& a, const StageMeta& m, const uint8_t* st, int q, int rsub,
+                          const uint8_t* taps_raw) const {
+    const RowTap* taps = reinterpret_cast<const RowTap*>(taps_raw);
+    const size_t row_bytes = static_cast<size_t>(a.in_w) * 3;
+    const int lane = threadIdx.x & 31;
+    const int y_begin = m.band * a.band_rows;
+    const int row_f4 = a.out_w * 3 / 4;
+    float4* ob = reinterpret_cast<float4*>(a.out) + (static_cast<size_t>(m.j) * a.out_h + y_begin) * row_f4;
+    const int sh = (byte0 & 3) * 8;
+    const bool mine = q < a.q_per_row;  // a group of this row (else: store helper only)
+    for (int r = rsub; r < m.nrows; r += a.rpp) {
+      const RowTap t = taps[y_begin + r];
+      if (mine) {
+        const uint32_t* s0 =
+            reinterpret_cast<const uint32_t*>(st + static_cast<size_t>(t.y0 - m.ys0) * row_bytes + (byte0 & ~3));
+        const uint32_t* s1 =
+            reinterpret_cast<const uint32_t*>(st + static_cast<size_t>(t.y1 - m.ys0) * row_bytes + (byte0 & ~3));
+        uint32_t w0[kNW + 1], w1[kNW + 1];
+#pragma unroll
+        for (int i = 0; i < kNW; ++i) {
+          w0[i] = s0[i];
+          w1[i] = s1[i];
+        }
+        w0[kNW] = w1[kNW] = 0;
+        if (kOmax) {
+#pragma unroll
+          for (int i = 0; i < kNW; ++i) {
+            w0[i] = __funnelshift_r(w0[i], w0[i + 1], sh);
+            w1[i] = __funnelshift_r(w1[i], w1[i + 1], sh);
+          }
+        }
+        const f32x2 wy2 = splat2(t.wy);
+        float* my = stg + lane * kF;
+#pragma unroll
+        for (int i = 0; i < kPairs; ++i) {
+          const int e0 = 2 * i, e1 = 2 * i + 1 < kF ? 2 * i + 1 : 2 * i;
+          const int l0 = 3 * T(e0 / 3) + e0 % 3, l1 = 3 * T(e1 / 3) + e1 % 3;  // left taps; right = +3
+          const f32x2 top = k.lerp(px2(w0, l0, l1), px2(w0, l0 + 3, l1 + 3), wx2[i]);
+          const f32x2 bot = k.lerp(px2(w1, l0, l1), px2(w1, l0 + 3, l1 + 3), wx2[i]);
+          const float2 v = up2(k.normalize(k.lerp(top, bot, wy2), mu2[e0 % 3], nsd2[e0 % 3], rc2[e0 % 3]));
+          my[e0] = v.x;
+          if (e1 != e0) my[e1] = v.y;
+        }
+      }
+      __syncwarp();
+      const float4* src = reinterpret_cast<const float4*>(stg);
+      float4* orow = ob + static_cast<size_t>(r) * row_f4;
+#pragma unroll
+      for (int i = 0; i < (32 * kF + 127) / 128; ++i) {  // <= 32 groups per row
+        const int c = lane + 32 * i;
+        if (c < row_f4) st_cs_f4(orow + c, src[c]);
+      }
+      __syncwarp();
+    }
+  }
+};
+
+// Host twin of resize_coord's column taps: the periodic form holds when
+// every x0 = PI * (x / PO) + T(x % PO) and x1 = x0 + 1 (no edge clamps).
+template <int PO, int PI>
+bool periodic_ok(int in_w, int out_w) {
+  if (in_w % PI || out_w % PO || in_w / PI != out_w / PO || out_w / PO > 32) return false;
+  const float scale = static_cast<float>(in_w) / static_cast<float>(out_w);
+  for (int x = 0; x < out_w; ++x) {
+    float sx = (static_cast<float>(x) + 0.5f) * scale - 0.5f;
+    if (sx < 0.0f) sx = 0.0f;
+    int a = static_cast<int>(sx);
+    if (a > in_w - 1) a = in_w - 1;
+    if (a + 1 >= in_w || a != PI * (x / PO) + ResizePOp<PO, PI>::T(x % PO)) return false;
+  }
+  return true;
+}
+
 template <class Op>
 __global__ void __launch_bounds__(kFastConsumers + 32, 1) pipeline_kernel(FastArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -549,7 +691,9 @@ __global__ void __launch_bounds__(kFastConsumers + 32, 1) pipeline_kernel(FastAr
   }
   // ---- consumer warps ----
   const int q = tid % a.q_stride, rsub = tid / a.q_stride;
-  const bool active = tid < consumers && q < a.q_per_row;
+  // warp-wide ops (ResizePOp) run every lane of a consumer warp: lanes past
+  // the row's groups take part in the warp's transposed store
+  const bool active = tid < consumers && (Op::kWarpWide || q < a.q_per_row);
   Op op;
   op.init(a, active ? q : 0, taps);
   int k = 0;
@@ -745,6 +889,28 @@ static int resize_impl(const uint8_t* images, int64_t num_images, int in_h, int 
     const size_t taps = static_cast<size_t>(out_h) * sizeof(RowTap);
     while (f.stages > 2 && static_cast<size_t>(f.stages) * f.stage_bytes + taps > kSmemBudget) --f.stages;
     const size_t smem = static_cast<size_t>(f.stages) * f.stage_bytes + taps;
+    // periodic column taps (320 -> 224, 256 -> 224): one period per lane
+    const bool p710 = periodic_ok<7, 10>(in_w, out_w), p78 = !p710 && periodic_ok<7, 8>(in_w, out_w);
+    if ((p710 || p78) && env_int("DP_DEV_RESIZE_PERIODIC", 1)) {
+      FastArgs p = f;
+      p.q_per_row = out_w / 7;  // groups per row (one lane each)
+      p.q_stride = 32;
+      p.rpp = kFastConsumers / 32;
+      p.band_rows = env_int("DP_DEV_RESIZE_PBAND", p.rpp);
+      if (p.band_rows > out_h) p.band_rows = out_h;
+      p.bands = (out_h + p.band_rows - 1) / p.band_rows;
+      p.stages = env_int("DP_DEV_STAGES", kResizeStages);
+      int prow = static_cast<int>(p.band_rows * sc) + 3;
+      if (prow > in_h) prow = in_h;
+      p.stage_bytes = static_cast<int>(((static_cast<size_t>(prow) * in_w * 3 + 127) / 128) * 128);
+      const size_t taps16 = ((taps + 15) / 16) * 16;
+      const size_t stg = static_cast<size_t>(p.rpp) * out_w * 3 * sizeof(float);
+      while (p.stages > 2 && static_cast<size_t>(p.stages) * p.stage_bytes + taps16 + stg > kSmemBudget) --p.stages;
+      const size_t psmem = static_cast<size_t>(p.stages) * p.stage_bytes + taps16 + stg;
+      if (psmem <= kSmemBudget)
+        return p710 ? launch_persistent(pipeline_kernel<ResizePOp<7, 10>>, p, psmem, s, "resize_normalize")
+                    : launch_persistent(pipeline_kernel<ResizePOp<7, 8>>, p, psmem, s, "resize_normalize");
+    }
     if (smem <= kSmemBudget)
       return launch_persistent(pipeline_kernel<ResizeOp>, f, smem, s, "resize_normalize");
   }

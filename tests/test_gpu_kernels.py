@@ -202,8 +202,22 @@ def test_k4_resize_normalize_within_1ulp(K, orc, dev):
     assert nonzero == 0, f"{nonzero} values differ by 1 ulp"  # design goal: 0 ulp
 
 
+def test_k4_periodic_and_general_paths_agree(K, dev, monkeypatch):
+    """320 -> 224 runs the periodic-tap consumer (ResizePOp<7, 10>); the
+    general ResizeOp (DP_DEV_RESIZE_PERIODIC=0) must give the same bits."""
+    imgs = device_images(K, dev, 24, 320, 320)
+    order = gpu_shuffle(K, 24, 8, 99)
+    _, a = run_resize(K, imgs, order, 0, 24)
+    monkeypatch.setenv("DP_DEV_RESIZE_PERIODIC", "0")
+    _, b = run_resize(K, imgs, order, 0, 24)
+    assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
 def test_k4_other_shapes(K, orc, dev):
-    for (ih, iw, oh, ow) in ((100, 160, 224, 224), (480, 360, 224, 224), (33, 57, 17, 23)):
+    # (256, 256) and (160, 160) -> periodic column taps (ResizePOp 7/8, 7/10
+    # with 16 groups per row), the rest the general ResizeOp / generic kernel
+    for (ih, iw, oh, ow) in ((100, 160, 224, 224), (480, 360, 224, 224), (33, 57, 17, 23), (256, 256, 224, 224),
+                             (160, 160, 112, 112), (200, 320, 96, 224)):
         imgs = device_images(K, dev, 3, ih, iw)
         ids, out = run_resize(K, imgs, None, 0, 3, (oh, ow))
         host = imgs.cpu().numpy()

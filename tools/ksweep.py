@@ -1,4 +1,5 @@
-"""Tuning sweep for the K3/K4 fast path (stages x band rows), CUDA events."""
+"""Tuning sweep for the K3/K4 fast path (stages x band rows), CUDA events.
+    python tools/ksweep.py k3|k4|k4p STAGES,.. BANDS,..   (k4p: periodic-tap K4)"""
 import ctypes, json, os, sys
 import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -26,7 +27,8 @@ res = []
 for stages in sys.argv[2].split(","):
     for band in sys.argv[3].split(","):
         os.environ["DP_DEV_STAGES"] = stages
-        os.environ["DP_DEV_CROP_BAND" if which == "k3" else "DP_DEV_RESIZE_BAND"] = band
+        os.environ[{"k3": "DP_DEV_CROP_BAND", "k4": "DP_DEV_RESIZE_BAND", "k4p": "DP_DEV_RESIZE_PBAND"}[which]] = band
+        os.environ["DP_DEV_RESIZE_PERIODIC"] = "1" if which == "k4p" else "0"
         for i in range(5): run(i)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)

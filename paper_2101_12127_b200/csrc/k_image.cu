@@ -32,6 +32,8 @@ constexpr int kFastResizeBandRows = 16;
 constexpr int kCropStages = 8;
 constexpr int kResizeStages = 4;
 constexpr size_t kSmemBudget = 200 * 1024;
+constexpr size_t kSmemBudgetMax = 224 * 1024;  // 227 KB opt-in minus static + reserved
+constexpr int kResizePWarps = 25;              // ResizePOp consumer warps (21 / 25 / 29 instantiated)
 
 __device__ __forceinline__ float sel3(int c, float a, float b, float d) { return c == 0 ? a : (c == 1 ? b : d); }
 
@@ -266,6 +268,7 @@ int check_common(const uint8_t* images, int64_t num_images, int in_h, int in_w, 
 constexpr int kMaxStages = 16;
 constexpr int kFastConsumers = 672;  // 21 warps; + 1 producer warp
 
+
 struct StageMeta {
   int64_t id;
   int64_t j;
@@ -324,6 +327,7 @@ struct RowTap {
 // ---- K3 stage operations ----
 struct CropOp {
   static constexpr bool kWarpWide = false;
+  static constexpr int kConsumers = kFastConsumers;
   float mu[4], sd[4], rc[4];
   int off_n[4], off_f[4];
   f32x2 mu2[2], nsd2[2], rc2[2];
@@ -406,6 +410,7 @@ struct CropOp {
 // ---- K4 stage operations ----
 struct ResizeOp {
   static constexpr bool kWarpWide = false;
+  static constexpr int kConsumers = kFastConsumers;
   float mu[4], sd[4], rc[4], wx[4];
   int o0[4], o1[4];
   f32x2 mu2[2], nsd2[2], rc2[2], wx2[2];
@@ -517,7 +522,7 @@ struct ResizeOp {
 // transposed through a per-warp shared buffer (stride 3 * PO words, odd:
 // conflict-free) into coalesced float4 stores.  Same lerp / normalize ops,
 // same order, as ResizeOp and the oracle (orc_resize_normalize).
-template <int PO, int PI>
+template <int PO, int PI, int W>
 struct ResizePOp {
   __host__ __device__ static constexpr int T(int x) { return ((2 * x + 1) * PI - PO) / (2 * PO); }
   static constexpr int kF = 3 * PO;                       // floats per group
@@ -526,6 +531,7 @@ struct ResizePOp {
   static constexpr int kOmax = (3 * PI) % 4 == 0 ? 0 : ((3 * PI) % 2 == 0 ? 2 : 3);
   static constexpr int kNW = (kOmax + kSpan + 3) / 4;     // 32-bit words per window
   static constexpr bool kWarpWide = true;
+  static constexpr int kConsumers = W * 32;  // W consumer warps, one output row each
   f32x2 wx2[kPairs];
   f32x2 mu2[3], nsd2[3], rc2[3];  // by pair pattern (channel of the pair's first float: 0, 2, 1)
   PkK k;
@@ -569,7 +575,7 @@ struct ResizePOp {
   static __device__ __forceinline__ uint32_t pick(const uint32_t* w, int b) {
     return __byte_perm(w[b >> 2], 0x4B000000u, 0x7440u | static_cast<uint32_t>(b & 3));
   }
-  __device__ __forceinline__ f32x2 px2(const uint32_t* w, int b0, int b1) const {
+  static __device__ __forceinline__ f32x2 px2(const PkK& k, const uint32_t* w, int b0, int b1) {
     return fma2(pk2(__uint_as_float(pick(w, b0)), __uint_as_float(pick(w, b1))), k.one, k.neg_magic);
   }
 
@@ -610,8 +616,8 @@ struct ResizePOp {
         for (int i = 0; i < kPairs; ++i) {
           const int e0 = 2 * i, e1 = 2 * i + 1 < kF ? 2 * i + 1 : 2 * i;
           const int l0 = 3 * T(e0 / 3) + e0 % 3, l1 = 3 * T(e1 / 3) + e1 % 3;  // left taps; right = +3
-          const f32x2 top = k.lerp(px2(w0, l0, l1), px2(w0, l0 + 3, l1 + 3), wx2[i]);
-          const f32x2 bot = k.lerp(px2(w1, l0, l1), px2(w1, l0 + 3, l1 + 3), wx2[i]);
+          const f32x2 top = k.lerp(px2(k, w0, l0, l1), px2(k, w0, l0 + 3, l1 + 3), wx2[i]);
+          const f32x2 bot = k.lerp(px2(k, w1, l0, l1), px2(k, w1, l0 + 3, l1 + 3), wx2[i]);
           const float2 v = up2(k.normalize(k.lerp(top, bot, wy2), mu2[e0 % 3], nsd2[e0 % 3], rc2[e0 % 3]));
           my[e0] = v.x;
           if (e1 != e0) my[e1] = v.y;
@@ -641,13 +647,13 @@ bool periodic_ok(int in_w, int out_w) {
     if (sx < 0.0f) sx = 0.0f;
     int a = static_cast<int>(sx);
     if (a > in_w - 1) a = in_w - 1;
-    if (a + 1 >= in_w || a != PI * (x / PO) + ResizePOp<PO, PI>::T(x % PO)) return false;
+    if (a + 1 >= in_w || a != PI * (x / PO) + ResizePOp<PO, PI, 1>::T(x % PO)) return false;
   }
   return true;
 }
 
 template <class Op>
-__global__ void __launch_bounds__(kFastConsumers + 32, 1) pipeline_kernel(FastArgs a) {
+__global__ void __launch_bounds__(Op::kConsumers + 32, 1) pipeline_kernel(FastArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t full[kMaxStages], empty[kMaxStages];
   __shared__ StageMeta meta[kMaxStages];
@@ -892,10 +898,11 @@ static int resize_impl(const uint8_t* images, int64_t num_images, int in_h, int 
     // periodic column taps (320 -> 224, 256 -> 224): one period per lane
     const bool p710 = periodic_ok<7, 10>(in_w, out_w), p78 = !p710 && periodic_ok<7, 8>(in_w, out_w);
     if ((p710 || p78) && env_int("DP_DEV_RESIZE_PERIODIC", 1)) {
+      const int warps = env_int("DP_DEV_RESIZEP_WARPS", kResizePWarps);
       FastArgs p = f;
       p.q_per_row = out_w / 7;  // groups per row (one lane each)
       p.q_stride = 32;
-      p.rpp = kFastConsumers / 32;
+      p.rpp = warps;
       p.band_rows = env_int("DP_DEV_RESIZE_PBAND", p.rpp);
       if (p.band_rows > out_h) p.band_rows = out_h;
       p.bands = (out_h + p.band_rows - 1) / p.band_rows;
@@ -905,11 +912,18 @@ static int resize_impl(const uint8_t* images, int64_t num_images, int in_h, int 
       p.stage_bytes = static_cast<int>(((static_cast<size_t>(prow) * in_w * 3 + 127) / 128) * 128);
       const size_t taps16 = ((taps + 15) / 16) * 16;
       const size_t stg = static_cast<size_t>(p.rpp) * out_w * 3 * sizeof(float);
-      while (p.stages > 2 && static_cast<size_t>(p.stages) * p.stage_bytes + taps16 + stg > kSmemBudget) --p.stages;
+      while (p.stages > 2 && static_cast<size_t>(p.stages) * p.stage_bytes + taps16 + stg > kSmemBudgetMax) --p.stages;
       const size_t psmem = static_cast<size_t>(p.stages) * p.stage_bytes + taps16 + stg;
-      if (psmem <= kSmemBudget)
-        return p710 ? launch_persistent(pipeline_kernel<ResizePOp<7, 10>>, p, psmem, s, "resize_normalize")
-                    : launch_persistent(pipeline_kernel<ResizePOp<7, 8>>, p, psmem, s, "resize_normalize");
+      if (psmem <= kSmemBudgetMax) {
+#define DP_LAUNCH_P(W)                                                                                   \
+  if (warps == W)                                                                                        \
+    return p710 ? launch_persistent(pipeline_kernel<ResizePOp<7, 10, W>>, p, psmem, s, "resize_normalize") \
+                : launch_persistent(pipeline_kernel<ResizePOp<7, 8, W>>, p, psmem, s, "resize_normalize");
+        DP_LAUNCH_P(21)
+        DP_LAUNCH_P(25)
+        DP_LAUNCH_P(29)
+#undef DP_LAUNCH_P
+      }
     }
     if (smem <= kSmemBudget)
       return launch_persistent(pipeline_kernel<ResizeOp>, f, smem, s, "resize_normalize");

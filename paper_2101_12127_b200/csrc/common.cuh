@@ -200,6 +200,33 @@ __device__ __forceinline__ void st_cs_f4(float4* p, float4 v) {
                : "memory");
 }
 
+// One warp streams two token rows at once (kLoads loads per lane per row in
+// flight before the stores): row a/b copies len tokens, then pads with `pad`
+// up to lm (lm = len: no padding; len = lm = 0: no row).  Two independent
+// rows per warp double the bytes in flight of the short (~1 KB) rows.
+template <int kLoads>
+__device__ __forceinline__ void stream_row_pair(const int32_t* __restrict__ src_a, int len_a, int lm_a,
+                                                int32_t* __restrict__ dst_a, const int32_t* __restrict__ src_b,
+                                                int len_b, int lm_b, int32_t* __restrict__ dst_b, int32_t pad,
+                                                int lane) {
+  const int lm = lm_a > lm_b ? lm_a : lm_b;
+  for (int c = lane; c < lm; c += 32 * kLoads) {
+    int32_t va[kLoads], vb[kLoads];
+#pragma unroll
+    for (int u = 0; u < kLoads; ++u) {
+      const int k = c + 32 * u;
+      va[u] = k < len_a ? __ldcs(src_a + k) : pad;
+      vb[u] = k < len_b ? __ldcs(src_b + k) : pad;
+    }
+#pragma unroll
+    for (int u = 0; u < kLoads; ++u) {
+      const int k = c + 32 * u;
+      if (k < lm_a) __stcs(dst_a + k, va[u]);
+      if (k < lm_b) __stcs(dst_b + k, vb[u]);
+    }
+  }
+}
+
 __device__ __forceinline__ uint4 ld_nc_na_u4(const void* p) {
   uint4 v;
   asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"

@@ -242,18 +242,10 @@ bucket_batches_kernel(const int32_t* __restrict__ tokens, const int64_t* __restr
   }
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  for (int t = threadIdx.x >> 5; t < n; t += kWarps) {
-    const int32_t len = s_len[t], lm = s_lm[t];
-    const int32_t* src = tokens + s_src[t];
-    int32_t* dst = out + s_dst[t];
-    for (int c = lane; c < lm; c += 32 * kLoads) {
-      int32_t v[kLoads];
-#pragma unroll
-      for (int u = 0; u < kLoads; ++u) v[u] = c + 32 * u < len ? __ldcs(src + c + 32 * u) : pad;
-#pragma unroll
-      for (int u = 0; u < kLoads; ++u)
-        if (c + 32 * u < lm) __stcs(dst + c + 32 * u, v[u]);
-    }
+  for (int t = threadIdx.x >> 5; t < n; t += 2 * kWarps) {  // rows t and t + kWarps
+    const int b = t + kWarps, has_b = b < n;
+    stream_row_pair<kLoads>(tokens + s_src[t], s_len[t], s_lm[t], out + s_dst[t], has_b ? tokens + s_src[b] : tokens,
+                            has_b ? s_len[b] : 0, has_b ? s_lm[b] : 0, has_b ? out + s_dst[b] : out, pad, lane);
   }
 }
 

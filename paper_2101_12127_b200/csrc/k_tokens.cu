@@ -229,18 +229,12 @@ padded_batches_kernel(const int32_t* __restrict__ tokens, const int64_t* __restr
   }
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  for (int t = threadIdx.x >> 5; t < n; t += kThreads / 32) {
-    const int32_t len = s_len[t], lm = s_lm[t];
-    const int32_t* src = tokens + s_src[t];
-    int32_t* dst = out + s_dst[t];
-    for (int c = lane; c < lm; c += 32 * kLoadsInFlight) {
-      int32_t v[kLoadsInFlight];
-#pragma unroll
-      for (int u = 0; u < kLoadsInFlight; ++u) v[u] = c + 32 * u < len ? __ldcs(src + c + 32 * u) : pad;
-#pragma unroll
-      for (int u = 0; u < kLoadsInFlight; ++u)
-        if (c + 32 * u < lm) __stcs(dst + c + 32 * u, v[u]);
-    }
+  constexpr int kW = kThreads / 32;
+  for (int t = threadIdx.x >> 5; t < n; t += 2 * kW) {  // rows t and t + kW
+    const int b = t + kW, has_b = b < n;
+    stream_row_pair<kLoadsInFlight>(tokens + s_src[t], s_len[t], s_lm[t], out + s_dst[t],
+                                    has_b ? tokens + s_src[b] : tokens, has_b ? s_len[b] : 0,
+                                    has_b ? s_lm[b] : 0, has_b ? out + s_dst[b] : out, pad, lane);
   }
 }
 
@@ -333,18 +327,12 @@ ragged_batches_kernel(const int32_t* __restrict__ tokens, const int64_t* __restr
   }
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  for (int t = threadIdx.x >> 5; t < n; t += kThreads / 32) {
-    const int32_t len = s_len[t];
-    const int32_t* src = tokens + s_src[t];
-    int32_t* dst = values + s_dst[t];
-    for (int c = lane; c < len; c += 32 * kLoadsInFlight) {
-      int32_t v[kLoadsInFlight];
-#pragma unroll
-      for (int u = 0; u < kLoadsInFlight; ++u) v[u] = c + 32 * u < len ? __ldcs(src + c + 32 * u) : 0;
-#pragma unroll
-      for (int u = 0; u < kLoadsInFlight; ++u)
-        if (c + 32 * u < len) __stcs(dst + c + 32 * u, v[u]);
-    }
+  constexpr int kW = kThreads / 32;
+  for (int t = threadIdx.x >> 5; t < n; t += 2 * kW) {  // rows t and t + kW
+    const int b = t + kW, has_b = b < n;
+    const int la = s_len[t], lb = has_b ? s_len[b] : 0;
+    stream_row_pair<kLoadsInFlight>(tokens + s_src[t], la, la, values + s_dst[t], has_b ? tokens + s_src[b] : tokens,
+                                    lb, lb, has_b ? values + s_dst[b] : values, 0, lane);
   }
 }
 

@@ -312,6 +312,37 @@ def test_cfg2_shape_value_parity_20k(dp, orc):
     assert k == n
 
 
+@pytest.mark.parametrize("mode,hw", [(0, 256), (1, 320)])
+def test_full_size_image_epoch(dp, orc, mode, hw):
+    """cfg2 / cfg3 at BASELINE.json's full size (65,536 images of 256x256 /
+    320x320 resident in HBM, shuffle(10k, 42), batch 256): the epoch's ids are
+    exactly the reference's shuffle order (so a permutation of the dataset)
+    and sampled images of every 16th batch equal the oracle bit for bit."""
+    n, buf, b = 65536, 10_000, 256
+    reg = image_registry(dp, mode)
+    src = dp.Source.synthetic_images(n, hw, hw)
+    op = "resize" if mode == 1 else "crop"
+    g, _ = dp.Dataset.tensor_slices(reg, src).shuffle(buf, 42).map(op).map("norm").batch(b).prefetch(-1).optimize()
+    order = orc.shuffle_order(n, buf, orc.shuffle_seed(1, 42))
+    assert np.array_equal(np.sort(order), np.arange(n))
+    it = dp.make_iterator(g, seed_override=1)
+    rng = np.random.default_rng(mode)
+    k = 0
+    for j, bt in enumerate(it):
+        ids = bt.numpy(0)
+        assert np.array_equal(ids, order[k:k + ids.size])
+        if j % 16 == 0:
+            pix = bt.numpy(1)
+            for r in rng.choice(ids.size, 2, replace=False):
+                img = orc.images(int(ids[r]), 1, hw, hw)[0]
+                want = orc.resize_normalize(img) if mode == 1 else orc.crop_flip_normalize(img, int(ids[r]))
+                assert np.array_equal(pix[r].view(np.uint32), want.view(np.uint32))
+        k += ids.size
+        bt.release()
+    assert k == n
+    del it, g, src
+
+
 def test_consumer_may_hold_batches(dp):
     """Holding every Element (the reference returns owned copies) grows the
     slot ring instead of overwriting held batches."""
@@ -465,6 +496,79 @@ def test_cfg4_filter_padded_batch(dp, orc):
             assert (b[0][r, b[1][r]:] == 0).all()
     assert fnv(orc, lens) == c["fnv_row_lengths"] and fnv(orc, toks) == c["fnv_tokens"]
     assert fnv(orc, sizes) == c["fnv_batch_sizes"]
+
+
+def test_full_size_cfg4_epoch(dp, orc):
+    """cfg4 at full size (1M sequences, len U[1,1024], filter len <= 512,
+    padded_batch 128): every batch's row lengths are the reference filter's
+    kept sequences in order, padding is 0 to the batch max, and sampled rows
+    of every 64th batch hold the oracle's tokens."""
+    n, max_keep, b = 1_000_000, 512, 128
+    lens = orc.lengths(n)
+    kept = orc.filter_len_le(lens, max_keep)
+    reg = dp.Registry()
+    reg.register_length_filter("len<=512", max_keep)
+    src = dp.Source.synthetic_tokens(n, 1024, 4, 4)
+    g = dp.Dataset.token_sequences(reg, src).filter("len<=512").padded_batch(b)
+    it = dp.make_iterator(g, seed_override=1)
+    rng = np.random.default_rng(4)
+    k = j = 0
+    for bt in it:
+        toks, got = bt.numpy(0), bt.numpy(1)
+        want = lens[kept[k:k + got.size]]
+        assert np.array_equal(got, want) and toks.shape == (got.size, want.max())
+        if j % 64 == 0:
+            assert all((toks[r, got[r]:] == 0).all() for r in range(got.size))
+            for r in rng.choice(got.size, 2, replace=False):
+                i = int(kept[k + r])
+                assert toks[r, :got[r]].tolist() == [orc.token(4, i, c) for c in range(int(got[r]))]
+        k += got.size
+        j += 1
+        bt.release()
+    assert k == kept.size and j == (kept.size + b - 1) // b
+
+
+@pytest.mark.parametrize("kind", ["ragged", "bucket"])
+def test_full_size_cfg4r_cfg4b_epoch(dp, orc, kind):
+    """cfg4r (the reference graph: filter -> ragged batch 128) and cfg4b
+    (filter -> shuffle(10k, 42) -> bucket_by_length) at full size (1M
+    sequences): row lengths / bucket membership follow the oracle batch for
+    batch over the whole epoch; sampled rows hold the oracle's tokens."""
+    n, max_keep = 1_000_000, 512
+    lens = orc.lengths(n)
+    kept = orc.filter_len_le(lens, max_keep)
+    reg = dp.Registry()
+    reg.register_length_filter("len<=512", max_keep)
+    src = dp.Source.synthetic_tokens(n, 1024, 4, 4)
+    g = dp.Dataset.token_sequences(reg, src).filter("len<=512")
+    if kind == "ragged":
+        g = g.batch(128)
+        expect = [kept[i:i + 128] for i in range(0, kept.size, 128)]
+    else:
+        bounds, sizes = [128, 256, 384], [256, 128, 96, 64]
+        g = g.shuffle(10000, 42).bucket_by_length(bounds, sizes)
+        order = kept[orc.shuffle_order(kept.size, 10000, orc.shuffle_seed(1, 42))]
+        expect = orc.bucket_by_length(lens, order, bounds, sizes)
+    it = dp.make_iterator(g, seed_override=1)
+    rng = np.random.default_rng(5)
+    j = 0
+    for bt in it:
+        pos = expect[j]
+        if kind == "ragged":
+            vals, splits = bt.numpy(0), bt.numpy(1)
+            got = np.diff(splits)
+            rows = [vals[splits[r]:splits[r + 1]] for r in range(got.size)]
+        else:
+            toks, got = bt.numpy(0), bt.numpy(1)
+            assert toks.shape == (pos.size, lens[pos].max())
+            rows = [toks[r, :got[r]] for r in range(got.size)]
+        assert np.array_equal(got, lens[pos])
+        if j % 64 == 0:
+            for r in rng.choice(got.size, 2, replace=False):
+                assert rows[r].tolist() == [orc.token(4, int(pos[r]), c) for c in range(int(got[r]))]
+        j += 1
+        bt.release()
+    assert j == len(expect)
 
 
 def test_cfg4_reference_graph_filter_then_ragged_batch(dp, orc):

@@ -202,9 +202,15 @@ bucket_lmax_kernel(const int32_t* __restrict__ lengths, const int64_t* __restric
 // offset, destination) into shared memory, then warps stream the tile with
 // kLoads token loads in flight per lane.
 constexpr int kRowTile = 128;
-constexpr int kLoads = 8;
+#ifndef DP_TOK_LOADS
+#define DP_TOK_LOADS 16
+#endif
+#ifndef DP_TOK_MINB
+#define DP_TOK_MINB 1
+#endif
+constexpr int kLoads = DP_TOK_LOADS;
 
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, DP_TOK_MINB)
 bucket_batches_kernel(const int32_t* __restrict__ tokens, const int64_t* __restrict__ offsets,
                       const int32_t* __restrict__ lengths, const int64_t* __restrict__ perm,
                       const int64_t* __restrict__ start, const int32_t* __restrict__ lmax_of,

@@ -204,9 +204,15 @@ padded_batch_kernel(const int32_t* __restrict__ tokens, const int64_t* __restric
 // shared memory; then each warp streams its rows with kLoadsInFlight token
 // loads per lane issued before their stores.
 constexpr int kRowTile = 128;
-constexpr int kLoadsInFlight = 8;
+#ifndef DP_TOK_LOADS
+#define DP_TOK_LOADS 16
+#endif
+#ifndef DP_TOK_MINB
+#define DP_TOK_MINB 1
+#endif
+constexpr int kLoadsInFlight = DP_TOK_LOADS;
 
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, DP_TOK_MINB)
 padded_batches_kernel(const int32_t* __restrict__ tokens, const int64_t* __restrict__ offsets,
                       const int32_t* __restrict__ lengths, const int64_t* __restrict__ order, int64_t first_row,
                       int64_t rows, int64_t batch, const int32_t* __restrict__ lmax, const int64_t* __restrict__ boff,
@@ -303,7 +309,7 @@ len_prefix_apply_kernel(const int32_t* __restrict__ lengths, const int64_t* __re
 // row R's tokens go to values[prefix[R] - prefix[first_row]]; batch j's
 // row splits (rows_j + 1 int64, relative to the batch) follow the splits of
 // the batches before it in the launch group.  Row tiles as padded_batches.
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, DP_TOK_MINB)
 ragged_batches_kernel(const int32_t* __restrict__ tokens, const int64_t* __restrict__ offsets,
                       const int32_t* __restrict__ lengths, const int64_t* __restrict__ order, int64_t first_row,
                       int64_t rows, int64_t batch, int64_t n_rows, const int64_t* __restrict__ prefix,

@@ -213,6 +213,9 @@ class UdfRegistry {
   void RegisterRandomCropFlip(const std::string& name, int64_t crop_h, int64_t crop_w, uint64_t seed, bool flip);
   void RegisterResizeBilinear(const std::string& name, int64_t out_h, int64_t out_w);
   void RegisterNormalize(const std::string& name, std::array<float, 3> mean, std::array<float, 3> stdv);
+  // cast: u8 image -> fp32 (exact), lowered as normalize(mean 0, std 1) --
+  // (x - 0) / 1 is x exactly under the kernels' IEEE-exact normalize
+  void RegisterCast(const std::string& name);
   void RegisterDecodeRaw(const std::string& name, int64_t h, int64_t w);
   void RegisterLengthFilter(const std::string& name, int64_t max_len);  // keep len <= max_len
   void RegisterValueFilter(const std::string& name, std::vector<PredicateTerm> terms);

@@ -41,6 +41,8 @@ int dp_registry_register_random_crop_flip(dp_registry* reg, const char* name, in
 int dp_registry_register_resize_bilinear(dp_registry* reg, const char* name, int64_t out_h, int64_t out_w);
 /* per-channel (x - mean[c]) / std[c] to fp32 */
 int dp_registry_register_normalize(dp_registry* reg, const char* name, const float mean[3], const float stdv[3]);
+/* cast u8 -> fp32 (the north star's Map library "cast"): exact, = normalize(mean 0, std 1) */
+int dp_registry_register_cast(dp_registry* reg, const char* name);
 /* predicate: keep sequences with length <= max_len */
 int dp_registry_register_length_filter(dp_registry* reg, const char* name, int64_t max_len);
 /* predicate on int64 element values (after the maps beneath the filter):

@@ -86,6 +86,10 @@ int dp_registry_register_normalize(dp_registry* reg, const char* name, const flo
   DP_REQUIRE(reg && name && mean && stdv);
   return Guard([&] { reg->reg.RegisterNormalize(name, {mean[0], mean[1], mean[2]}, {stdv[0], stdv[1], stdv[2]}); });
 }
+int dp_registry_register_cast(dp_registry* reg, const char* name) {
+  DP_REQUIRE(reg && name);
+  return Guard([&] { reg->reg.RegisterCast(name); });
+}
 int dp_registry_register_length_filter(dp_registry* reg, const char* name, int64_t max_len) {
   DP_REQUIRE(reg && name);
   return Guard([&] { reg->reg.RegisterLengthFilter(name, max_len); });

@@ -161,6 +161,8 @@ void UdfRegistry::RegisterNormalize(const std::string& name, std::array<float, 3
   Register(name, std::move(e));
 }
 
+void UdfRegistry::RegisterCast(const std::string& name) { RegisterNormalize(name, {0.f, 0.f, 0.f}, {1.f, 1.f, 1.f}); }
+
 void UdfRegistry::RegisterDecodeRaw(const std::string& name, int64_t h, int64_t w) {
   if (h < 1 || w < 1) throw PipelineError(ErrorCode::kInvalidAttr, "decode_raw: shape must be >= 1");
   Entry e;

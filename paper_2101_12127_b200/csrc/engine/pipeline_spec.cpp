@@ -17,6 +17,7 @@
 //   map crop h=<h> w=<w> [seed=<s>] [flip=true|false]
 //   map resize h=<h> w=<w>
 //   map normalize [mean=<m0,m1,m2>] [std=<s0,s1,s2>]
+//   map cast                              (u8 -> fp32)
 //   map decode h=<h> w=<w>
 //   filter keep=even|odd|all | filter len_le=<n>
 //   shuffle buffer=<n> [seed=<s>]        shard shards=<k> index=<i>
@@ -276,12 +277,15 @@ ParsedPipeline ParsePipelineSpec(const std::string& text, UdfRegistry& reg, int 
           nm << "normalize(" << m[0] << "," << m[1] << "," << m[2] << ";" << d[0] << "," << d[1] << "," << d[2] << ")";
           name = nm.str();
           if (!reg.Contains(name)) reg.RegisterNormalize(name, {m[0], m[1], m[2]}, {d[0], d[1], d[2]});
+        } else if (k == "cast") {
+          name = "cast";
+          if (!reg.Contains(name)) reg.RegisterCast(name);
         } else if (k == "decode") {
           const int64_t h = args.Integer("h"), w = args.Integer("w");
           name = "decode_raw(" + std::to_string(h) + "," + std::to_string(w) + ")";
           if (!reg.Contains(name)) reg.RegisterDecodeRaw(name, h, w);
         } else {
-          Fail(L, C, "usage: map affine|crop|resize|normalize|decode ...");
+          Fail(L, C, "usage: map affine|crop|resize|normalize|cast|decode ...");
         }
         const int64_t p = args.IntOrAuto("parallel", 1);
         out.tunables.push_back({"map@" + std::to_string(out.tunables.size()) + ".parallel", "num_parallel_calls"});

@@ -55,6 +55,7 @@ _SIGS = {
     "dp_registry_register_normalize": [c_vp, ctypes.c_char_p, ctypes.POINTER(ctypes.c_float),
                                        ctypes.POINTER(ctypes.c_float)],
     "dp_registry_register_length_filter": [c_vp, ctypes.c_char_p, c_i64],
+    "dp_registry_register_cast": [c_vp, ctypes.c_char_p],
     "dp_registry_register_record_reader": [c_vp, ctypes.c_char_p, c_i64],
     "dp_registry_register_value_filter": [c_vp, ctypes.c_char_p, c_vp, c_int],
     "dp_registry_register_standard_predicates": [c_vp],
@@ -171,6 +172,11 @@ class Registry:
 
     def register_resize_bilinear(self, name, out_h=224, out_w=224):
         _check(L().dp_registry_register_resize_bilinear(self.h, _b(name), out_h, out_w))
+        return name
+
+    def register_cast(self, name):
+        """u8 image -> fp32 values, exact (normalize with mean 0, std 1)."""
+        _check(L().dp_registry_register_cast(self.h, _b(name)))
         return name
 
     def register_normalize(self, name, mean=MEAN, std=STD):

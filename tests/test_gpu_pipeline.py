@@ -416,6 +416,33 @@ def test_resize_alone_and_normalize_alone(dp, orc):
     assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
 
 
+def test_cast_u8_to_f32(dp, orc):
+    """The Map library's cast (u8 -> fp32, exact): alone, after a random
+    crop + flip (the cropped, flipped window as floats) and after a resize;
+    also through the pipeline text format (`map cast`)."""
+    imgs = orc.images(0, 24, 48, 64)
+    src = dp.Source.images_from_host(imgs)
+    reg = dp.Registry()
+    reg.register_cast("cast")
+    reg.register_random_crop_flip("crop", 32, 40, seed=9, flip=True)
+    reg.register_resize_bilinear("rs", 30, 44)
+    base = dp.Dataset.tensor_slices(reg, src).shuffle(10, 4)
+    alone = drain(dp.make_iterator(base.map("cast").batch(8), seed_override=1), comps=(0, 1))
+    crop = drain(dp.make_iterator(base.map("crop").map("cast").batch(8), seed_override=1), comps=(0, 1))
+    rs = drain(dp.make_iterator(base.map("rs").map("cast").batch(8), seed_override=1), comps=(0, 1))
+    for a, c, r in zip(alone, crop, rs):
+        for k, i in enumerate(a[0]):
+            assert np.array_equal(a[1][k], imgs[i].astype(np.float32))
+            oy, ox, fl = orc.crop_params(9, int(i), 48, 64, 32, 40)
+            win = imgs[i][oy:oy + 32, ox:ox + 40]
+            assert np.array_equal(c[1][k], (win[:, ::-1] if fl else win).astype(np.float32))
+            assert np.array_equal(r[1][k].view(np.uint32), orc.resize(imgs[i], 30, 44).view(np.uint32))
+    g, _ = dp.Dataset.from_spec(dp.Registry(), "source images count=24 h=48 w=64\nmap cast\nbatch size=8\n")
+    out = drain(dp.make_iterator(g, seed_override=1), comps=(0, 1))
+    pix = orc.images(0, 24, 48, 64)
+    assert all(np.array_equal(b[1][k], pix[int(i)].astype(np.float32)) for b in out for k, i in enumerate(b[0]))
+
+
 def test_host_output_equals_device_output(dp):
     reg = image_registry(dp, 0, crop=(64, 64))
     src = dp.Source.synthetic_images(200, 96, 96)

@@ -575,8 +575,16 @@ struct ResizePOp {
   static __device__ __forceinline__ uint32_t pick(const uint32_t* w, int b) {
     return __byte_perm(w[b >> 2], 0x4B000000u, 0x7440u | static_cast<uint32_t>(b & 3));
   }
-  static __device__ __forceinline__ f32x2 px2(const PkK& k, const uint32_t* w, int b0, int b1) {
-    return fma2(pk2(__uint_as_float(pick(w, b0)), __uint_as_float(pick(w, b1))), k.one, k.neg_magic);
+  // two tap bytes as 2^23 + byte (exact "magic" floats, not yet converted)
+  static __device__ __forceinline__ f32x2 raw2(const uint32_t* w, int b0, int b1) {
+    return pk2(__uint_as_float(pick(w, b0)), __uint_as_float(pick(w, b1)));
+  }
+  // lerp_rn(p, q, wx) from the magic floats p' = 2^23 + p, q' = 2^23 + q:
+  // q' - p' == q - p exactly (|q - p| <= 255), so only p is converted
+  // (p' - 2^23); the same three rounded ops as the oracle's p + w * (q - p).
+  __device__ __forceinline__ f32x2 hlerp(f32x2 p_raw, f32x2 q_raw, f32x2 w) const {
+    const f32x2 p = fma2(p_raw, k.one, k.neg_magic);
+    return k.add(p, k.mul(w, k.sub(q_raw, p_raw)));
   }
 
   __device__ void consume(const FastArgs& a, const StageMeta& m, const uint8_t* st, int q, int rsub,
@@ -616,8 +624,8 @@ struct ResizePOp {
         for (int i = 0; i < kPairs; ++i) {
           const int e0 = 2 * i, e1 = 2 * i + 1 < kF ? 2 * i + 1 : 2 * i;
           const int l0 = 3 * T(e0 / 3) + e0 % 3, l1 = 3 * T(e1 / 3) + e1 % 3;  // left taps; right = +3
-          const f32x2 top = k.lerp(px2(k, w0, l0, l1), px2(k, w0, l0 + 3, l1 + 3), wx2[i]);
-          const f32x2 bot = k.lerp(px2(k, w1, l0, l1), px2(k, w1, l0 + 3, l1 + 3), wx2[i]);
+          const f32x2 top = hlerp(raw2(w0, l0, l1), raw2(w0, l0 + 3, l1 + 3), wx2[i]);
+          const f32x2 bot = hlerp(raw2(w1, l0, l1), raw2(w1, l0 + 3, l1 + 3), wx2[i]);
           const float2 v = up2(k.normalize(k.lerp(top, bot, wy2), mu2[e0 % 3], nsd2[e0 % 3], rc2[e0 % 3]));
           my[e0] = v.x;
           if (e1 != e0) my[e1] = v.y;

@@ -241,6 +241,22 @@ int dp_k_bucket_batches(const int32_t* tokens, const int64_t* offsets,
                         int64_t num_rows, int32_t pad_value, int32_t* out,
                         int32_t* out_lengths, void* stream);
 
+/* The same batches from per-row tables of a plan (dp_k_bucket_rows, once  */
+/* per epoch): row R reads position row_src[R], writes row_lm[R] tokens at */
+/* row_dst[R] - first_elem; rows [first_row, first_row + num_rows).  The    */
+/* engine's path (a shallower per-row dependency chain than the search).   */
+int dp_k_bucket_rows(const int64_t* perm, const int64_t* batch_start,
+                     const int32_t* batch_lmax, const int64_t* boff,
+                     const int64_t* roff, int64_t num_batches,
+                     int64_t* row_src, int64_t* row_dst, int32_t* row_lm,
+                     void* stream);
+int dp_k_bucket_rows_batches(const int32_t* tokens, const int64_t* offsets,
+                             const int32_t* lengths, const int64_t* row_src,
+                             const int64_t* row_dst, const int32_t* row_lm,
+                             int64_t first_row, int64_t first_elem,
+                             int64_t num_rows, int32_t pad_value,
+                             int32_t* out, int32_t* out_lengths, void* stream);
+
 /* ---------------------------------------------------------------------- */
 /* K6  shard + interleave index mapping -- ShardIterator (runtime.cpp:     */
 /*     770-800) + (Parallel)InterleaveIterator (1044-1128, 1727-2021) over */

@@ -76,8 +76,9 @@ struct EpochPlan {
   std::shared_ptr<void> lmax_dev, boff_dev;
   // bucket_by_length: order = the bucket-grouped positions; per batch its
   // start in order, rows and the exclusive row prefix
-  std::vector<int64_t> rows;
+  std::vector<int64_t> rows, roff;
   std::shared_ptr<void> bstart_dev, rows_dev, roff_dev;
+  std::shared_ptr<void> row_src_dev, row_dst_dev, row_lm_dev;  // per emitted row (dp_k_bucket_rows)
   cudaEvent_t ready = nullptr;
 };
 
@@ -676,8 +677,19 @@ class DevicePipeline {
               "boff");
     CudaCheck(cudaMemcpyAsync(p.roff_dev.get(), roff.data(), sizeof(int64_t) * (nb + 1), cudaMemcpyHostToDevice, s),
               "roff");
+    // per-row tables for the batch kernel (one pass per epoch, plan stream)
+    const int64_t nrows = roff[nb];
+    p.row_src_dev = dalloc(sizeof(int64_t) * std::max<int64_t>(nrows, 1));
+    p.row_dst_dev = dalloc(sizeof(int64_t) * std::max<int64_t>(nrows, 1));
+    p.row_lm_dev = dalloc(sizeof(int32_t) * std::max<int64_t>(nrows, 1));
+    KCheck(dp_k_bucket_rows(P<int64_t>(perm), P<int64_t>(bstart), P<int32_t>(blmax), P<int64_t>(p.boff_dev),
+                            P<int64_t>(p.roff_dev), nb, P<int64_t>(p.row_src_dev), P<int64_t>(p.row_dst_dev),
+                            P<int32_t>(p.row_lm_dev), s),
+           "bucket_rows");
+    launches_++;
     // the host vectors are read by the copies: keep them alive until done
     CudaCheck(cudaStreamSynchronize(s), "bucket upload");
+    p.roff = std::move(roff);
     p.order = perm;
     p.bstart_dev = bstart;
     p.rows_dev = brows;
@@ -889,11 +901,11 @@ class DevicePipeline {
         if (L_.bucketed) {
           int64_t group_rows = 0;
           for (int64_t k = 0; k < nb; ++k) group_rows += slot->batch_rows[k] = plan.rows[j0 + k];
-          KCheck(dp_k_bucket_batches(P<int32_t>(L_.source->tokens), P<int64_t>(L_.source->offsets),
-                                     P<int32_t>(L_.source->lengths), order, P<int64_t>(plan.bstart_dev),
-                                     P<int32_t>(plan.rows_dev), P<int32_t>(plan.lmax_dev), P<int64_t>(plan.boff_dev),
-                                     P<int64_t>(plan.roff_dev), j0, nb, group_rows, static_cast<int32_t>(L_.pad),
-                                     P<int32_t>(slot->a), P<int32_t>(slot->b), stream_),
+          KCheck(dp_k_bucket_rows_batches(P<int32_t>(L_.source->tokens), P<int64_t>(L_.source->offsets),
+                                          P<int32_t>(L_.source->lengths), P<int64_t>(plan.row_src_dev),
+                                          P<int64_t>(plan.row_dst_dev), P<int32_t>(plan.row_lm_dev), plan.roff[j0],
+                                          plan.boff[j0], group_rows, static_cast<int32_t>(L_.pad),
+                                          P<int32_t>(slot->a), P<int32_t>(slot->b), stream_),
                  "K8");
         } else if (L_.ragged) {
           KCheck(dp_k_ragged_batches(P<int32_t>(L_.source->tokens), P<int64_t>(L_.source->offsets),

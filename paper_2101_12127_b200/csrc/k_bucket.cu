@@ -255,6 +255,55 @@ bucket_batches_kernel(const int32_t* __restrict__ tokens, const int64_t* __restr
   }
 }
 
+// Per-row tables of an epoch's bucket plan (built once per epoch on the plan
+// stream): emitted row R of batch e, row r, reads source position
+// perm[start_e + r] and lands at boff_e + r * lmax_e, width lmax_e.  The
+// batch kernel's preamble then needs one coalesced read per table plus the
+// (length, offset) gather, as K5 padded_batches, instead of a batch search,
+// a forward walk over roff and the dependent perm read per row.
+__global__ void __launch_bounds__(kThreads)
+bucket_rows_kernel(const int64_t* __restrict__ perm, const int64_t* __restrict__ start,
+                   const int32_t* __restrict__ lmax_of, const int64_t* __restrict__ boff,
+                   const int64_t* __restrict__ roff, int64_t* __restrict__ row_src, int64_t* __restrict__ row_dst,
+                   int32_t* __restrict__ row_lm) {
+  const int64_t e = blockIdx.x, r0 = roff[e], rows = roff[e + 1] - r0, s0 = start[e], b0 = boff[e];
+  const int32_t lm = lmax_of[e];
+  for (int64_t r = threadIdx.x; r < rows; r += blockDim.x) {
+    row_src[r0 + r] = perm[s0 + r];
+    row_dst[r0 + r] = b0 + r * lm;
+    row_lm[r0 + r] = lm;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, DP_TOK_MINB)
+bucket_rows_batches_kernel(const int32_t* __restrict__ tokens, const int64_t* __restrict__ offsets,
+                           const int32_t* __restrict__ lengths, const int64_t* __restrict__ row_src,
+                           const int64_t* __restrict__ row_dst, const int32_t* __restrict__ row_lm, int64_t r_first,
+                           int64_t b_first, int64_t rows, int32_t pad, int32_t* __restrict__ out,
+                           int32_t* __restrict__ out_lengths) {
+  __shared__ int64_t s_src[kRowTile], s_dst[kRowTile];
+  __shared__ int32_t s_len[kRowTile], s_lm[kRowTile];
+  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * kRowTile;
+  const int n = static_cast<int>(rows - t0 < kRowTile ? rows - t0 : kRowTile);
+  for (int t = threadIdx.x; t < n; t += kThreads) {
+    const int64_t R = r_first + t0 + t;
+    const int64_t p = __ldcs(row_src + R);
+    const int32_t len = lengths[p];
+    s_src[t] = offsets[p];
+    s_len[t] = len;
+    s_lm[t] = __ldcs(row_lm + R);
+    s_dst[t] = __ldcs(row_dst + R) - b_first;
+    out_lengths[t0 + t] = len;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  for (int t = threadIdx.x >> 5; t < n; t += 2 * kWarps) {  // rows t and t + kWarps
+    const int b = t + kWarps, has_b = b < n;
+    stream_row_pair<kLoads>(tokens + s_src[t], s_len[t], s_lm[t], out + s_dst[t], has_b ? tokens + s_src[b] : tokens,
+                            has_b ? s_len[b] : 0, has_b ? s_lm[b] : 0, has_b ? out + s_dst[b] : out, pad, lane);
+  }
+}
+
 struct PlanScratch {
   int64_t* tile_counts;
   int64_t* meta;
@@ -349,6 +398,30 @@ extern "C" int dp_k_bucket_plan(const int32_t* lengths, const int64_t* order, in
   bucket_lmax_kernel<<<static_cast<int>((max_batches + kWarps - 1) / kWarps), kThreads, 0, s>>>(
       lengths, perm, batch_start, batch_rows, num_batches_dev, batch_lmax);
   return launch_status("bucket_plan");
+}
+
+extern "C" int dp_k_bucket_rows(const int64_t* perm, const int64_t* batch_start, const int32_t* batch_lmax,
+                                const int64_t* boff, const int64_t* roff, int64_t num_batches, int64_t* row_src,
+                                int64_t* row_dst, int32_t* row_lm, void* stream) {
+  if (num_batches < 0 || num_batches > 0x7fffffff) return fail(DP_ERR_INVALID_ATTR, "bucket_rows: bad batch count");
+  if (num_batches == 0) return DP_OK;
+  bucket_rows_kernel<<<static_cast<int>(num_batches), kThreads, 0, as_stream(stream)>>>(
+      perm, batch_start, batch_lmax, boff, roff, row_src, row_dst, row_lm);
+  return launch_status("bucket_rows");
+}
+
+extern "C" int dp_k_bucket_rows_batches(const int32_t* tokens, const int64_t* offsets, const int32_t* lengths,
+                                        const int64_t* row_src, const int64_t* row_dst, const int32_t* row_lm,
+                                        int64_t first_row, int64_t first_elem, int64_t num_rows, int32_t pad_value,
+                                        int32_t* out, int32_t* out_lengths, void* stream) {
+  if (first_row < 0 || first_elem < 0 || num_rows < 0) return fail(DP_ERR_INVALID_ATTR, "bucket_batches: bad range");
+  if (num_rows == 0) return DP_OK;
+  const int64_t blocks = (num_rows + kRowTile - 1) / kRowTile;
+  if (blocks > 0x7fffffff) return fail(DP_ERR_INVALID_ATTR, "bucket_batches: too many rows");
+  bucket_rows_batches_kernel<<<static_cast<int>(blocks), kThreads, 0, as_stream(stream)>>>(
+      tokens, offsets, lengths, row_src, row_dst, row_lm, first_row, first_elem, num_rows, pad_value, out,
+      out_lengths);
+  return launch_status("bucket_batches");
 }
 
 extern "C" int dp_k_bucket_batches(const int32_t* tokens, const int64_t* offsets, const int32_t* lengths,

@@ -769,7 +769,19 @@ def test_cfg5_sharded_record_residency(dp, orc, tmp_path):
         assert np.array_equal(got[-1][1][-1], orc.crop_flip_normalize(imgs[p], p, 32, 32))
         seen += ids.tolist()
     assert sorted(seen) == list(range(m * rec))
+    # checkpoint / restore (seek) and DPG1 round trip over block-resident records
     mine = dp.Source.synthetic_records_sharded(m, rec, 48, 48, k, 1)
+    d = dp.Dataset.range(reg, m).shard(k, 1).interleave("reader", cycle, cycle, records=mine)
+    d = d.shuffle(20, 42).map("crop").map("norm").batch(4).repeat(2)
+    whole = drain(dp.make_iterator(d, seed_override=3), comps=(0, 1))
+    it = dp.make_iterator(d, seed_override=3)
+    for _ in range(5):
+        it.get_next().release()
+    rest = drain(dp.restore(d, it.save()), comps=(0, 1))
+    assert len(rest) == len(whole) - 5
+    assert all(np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) for a, b in zip(rest, whole[5:]))
+    again = dp.Dataset.deserialize(reg, d.serialize(), sources=[mine])
+    assert np.array_equal(drain(dp.make_iterator(again, seed_override=3))[0][0], whole[0][0])
     bad = [dp.Dataset.range(reg, m).shard(k, 0).interleave("reader", cycle, 1, records=mine),
            dp.Dataset.range(reg, m).interleave("reader", cycle, 1, records=mine)]
     reg.register_record_reader("reader5", rec - 1)

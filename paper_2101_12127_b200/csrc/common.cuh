@@ -192,6 +192,15 @@ struct PkK {  // opaque packed constants, built from NormConsts in registers
   }
   // p + w * (q - p), each op rounded (lerp_rn) on a pair
   __device__ f32x2 lerp(f32x2 p, f32x2 q, f32x2 w) const { return add(p, mul(w, sub(q, p))); }
+  // lerp_rn of two uint8 taps given as magic floats p' = 2^23 + p, q' = 2^23 + q:
+  // q' - p' == q - p exactly (|q - p| <= 255), so only p is converted -- the
+  // same three rounded ops as lerp(u8x2(p), u8x2(q), w), one FFMA2 fewer.
+  __device__ f32x2 lerp_u8(f32x2 p_raw, f32x2 q_raw, f32x2 w) const {
+    return add(fma2(p_raw, one, neg_magic), mul(w, sub(q_raw, p_raw)));
+  }
+  static __device__ f32x2 raw_u8x2(uint32_t a, uint32_t b) {
+    return pk2(__uint_as_float(0x4B000000u | a), __uint_as_float(0x4B000000u | b));
+  }
 };
 
 __device__ __forceinline__ void st_cs_f4(float4* p, float4 v) {

@@ -500,10 +500,10 @@ struct ResizeOp {
 #pragma unroll
       for (int p = 0; p < 2; ++p) {
         const int u = 2 * p;
-        const f32x2 top =
-            k.lerp(k.u8x2(row0[o0[u]], row0[o0[u + 1]]), k.u8x2(row0[o1[u]], row0[o1[u + 1]]), wx2[p]);
-        const f32x2 bot =
-            k.lerp(k.u8x2(row1[o0[u]], row1[o0[u + 1]]), k.u8x2(row1[o1[u]], row1[o1[u + 1]]), wx2[p]);
+        const f32x2 top = k.lerp_u8(PkK::raw_u8x2(row0[o0[u]], row0[o0[u + 1]]),
+                                    PkK::raw_u8x2(row0[o1[u]], row0[o1[u + 1]]), wx2[p]);
+        const f32x2 bot = k.lerp_u8(PkK::raw_u8x2(row1[o0[u]], row1[o0[u + 1]]),
+                                    PkK::raw_u8x2(row1[o1[u]], row1[o1[u + 1]]), wx2[p]);
         v[p] = up2(k.normalize(k.lerp(top, bot, wy2), mu2[p], nsd2[p], rc2[p]));
       }
       st_cs_f4(ob + static_cast<size_t>(r) * a.q_per_row + q, make_float4(v[0].x, v[0].y, v[1].x, v[1].y));
@@ -579,13 +579,7 @@ struct ResizePOp {
   static __device__ __forceinline__ f32x2 raw2(const uint32_t* w, int b0, int b1) {
     return pk2(__uint_as_float(pick(w, b0)), __uint_as_float(pick(w, b1)));
   }
-  // lerp_rn(p, q, wx) from the magic floats p' = 2^23 + p, q' = 2^23 + q:
-  // q' - p' == q - p exactly (|q - p| <= 255), so only p is converted
-  // (p' - 2^23); the same three rounded ops as the oracle's p + w * (q - p).
-  __device__ __forceinline__ f32x2 hlerp(f32x2 p_raw, f32x2 q_raw, f32x2 w) const {
-    const f32x2 p = fma2(p_raw, k.one, k.neg_magic);
-    return k.add(p, k.mul(w, k.sub(q_raw, p_raw)));
-  }
+
 
   __device__ void consume(const FastArgs& a, const StageMeta& m, const uint8_t* st, int q, int rsub,
                           const uint8_t* taps_raw) const {
@@ -624,8 +618,9 @@ struct ResizePOp {
         for (int i = 0; i < kPairs; ++i) {
           const int e0 = 2 * i, e1 = 2 * i + 1 < kF ? 2 * i + 1 : 2 * i;
           const int l0 = 3 * T(e0 / 3) + e0 % 3, l1 = 3 * T(e1 / 3) + e1 % 3;  // left taps; right = +3
-          const f32x2 top = hlerp(raw2(w0, l0, l1), raw2(w0, l0 + 3, l1 + 3), wx2[i]);
-          const f32x2 bot = hlerp(raw2(w1, l0, l1), raw2(w1, l0 + 3, l1 + 3), wx2[i]);
+          // only the left tap is converted (PkK::lerp_u8)
+          const f32x2 top = k.lerp_u8(raw2(w0, l0, l1), raw2(w0, l0 + 3, l1 + 3), wx2[i]);
+          const f32x2 bot = k.lerp_u8(raw2(w1, l0, l1), raw2(w1, l0 + 3, l1 + 3), wx2[i]);
           const float2 v = up2(k.normalize(k.lerp(top, bot, wy2), mu2[e0 % 3], nsd2[e0 % 3], rc2[e0 % 3]));
           my[e0] = v.x;
           if (e1 != e0) my[e1] = v.y;

@@ -16,15 +16,17 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def test_two_rank_bench_order_check_matches_oracle(orc):
+@pytest.mark.parametrize("config,port", [("cfg2", 29533), ("cfg3", 29535)])
+def test_two_rank_bench_order_check_matches_oracle(orc, config, port):
+    """cfg2 (crop) and cfg3 (resize, "1/2/4/8 GPUs via Shard") on two ranks."""
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     n = 8192
     env = dict(os.environ, DP_BENCH_ONE_GPU="1")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
-           "127.0.0.1", "--master-port", "29533", os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "32",
-           "--warmup", "16", "--elements-per-gpu", str(n)]
+           "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "32",
+           "--warmup", "16", "--elements-per-gpu", str(n), "--config", config]
     out = subprocess.run(cmd, capture_output=True, text=True, env=env, cwd=ROOT, timeout=900)
     assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
     line = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])

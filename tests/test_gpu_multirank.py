@@ -1,6 +1,7 @@
 """The multi-rank bench path on the one GPU of the test box: two torchrun
 ranks (gloo for the 8-byte collectives, DP_BENCH_ONE_GPU=1) each run the
-cfg2 pipeline on its own shard(2, rank) with sharded residency.  The final
+cfg2 / cfg3 pipeline on its own shard(2, rank) with sharded residency (and
+cfg5 with block residency of its record files).  The final
 ordering check's per-rank K7 digests must equal the oracle's digest of
 shard(2, rank) -> shuffle(10k, 42) for that rank.  The
 ranks' kernels never wait on one another (no data-path collective)."""

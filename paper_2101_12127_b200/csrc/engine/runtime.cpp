@@ -1028,14 +1028,15 @@ class DevicePipeline {
     const bool host = opt_.host_output;
     auto base_a = static_cast<uint8_t*>(host ? slot->ha.get() : slot->a.get()) + slot->batch_off_a[k];
     auto base_b = slot->b ? static_cast<uint8_t*>(host ? slot->hb.get() : slot->b.get()) + slot->batch_off_b[k] : nullptr;
-    auto mk = [&](DType dt, std::vector<int64_t> shape, void* data) {
+    // the last component takes the lease itself (one refcount round trip fewer)
+    auto mk = [&](DType dt, std::vector<int64_t> shape, void* data, bool last = false) {
       Tensor t;
       t.dtype = dt;
       t.shape = std::move(shape);
       t.data = data;
       t.residency = host ? Residency::kHost : Residency::kDevice;
       t.device = opt_.device;
-      t.owner = lease;
+      t.owner = last ? std::move(lease) : lease;
       t.ready = slot->ready;
       return Value::FromTensor(std::allocate_shared<Tensor>(PoolAllocator<Tensor>(), std::move(t)));
     };
@@ -1044,24 +1045,24 @@ class DevicePipeline {
     switch (L_.kind) {
       case BatchKind::kAffine:
       case BatchKind::kIdentityInt:
-        comps.push_back(mk(DType::kInt64, {rows}, base_a));
+        comps.push_back(mk(DType::kInt64, {rows}, base_a, true));
         break;
       case BatchKind::kCrop:
         comps.push_back(mk(DType::kInt64, {rows}, base_a));
-        comps.push_back(mk(DType::kFloat32, {rows, L_.crop.out_h, L_.crop.out_w, 3}, base_b));
+        comps.push_back(mk(DType::kFloat32, {rows, L_.crop.out_h, L_.crop.out_w, 3}, base_b, true));
         break;
       case BatchKind::kResize:
         comps.push_back(mk(DType::kInt64, {rows}, base_a));
-        comps.push_back(mk(DType::kFloat32, {rows, L_.resize.out_h, L_.resize.out_w, 3}, base_b));
+        comps.push_back(mk(DType::kFloat32, {rows, L_.resize.out_h, L_.resize.out_w, 3}, base_b, true));
         break;
       case BatchKind::kPadded:
         if (L_.ragged) {  // (values, row splits)
           comps.push_back(mk(DType::kInt32, {slot->batch_cols[k]}, base_a));
-          comps.push_back(mk(DType::kInt64, {rows + 1}, base_b));
+          comps.push_back(mk(DType::kInt64, {rows + 1}, base_b, true));
           break;
         }
         comps.push_back(mk(DType::kInt32, {rows, slot->batch_cols[k]}, base_a));
-        comps.push_back(mk(DType::kInt32, {rows}, base_b));
+        comps.push_back(mk(DType::kInt32, {rows}, base_b, true));
         break;
     }
     return Element(std::move(comps));

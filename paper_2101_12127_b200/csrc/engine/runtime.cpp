@@ -1082,7 +1082,7 @@ class DevicePipeline {
       t.data = static_cast<uint8_t*>(slot->a.get()) + slot->batch_off_a[k] + splits[row] * sizeof(int32_t);
       t.residency = Residency::kDevice;
       t.device = opt_.device;
-      t.owner = lease;
+      t.owner = std::move(lease);
       t.ready = slot->ready;
       std::vector<Value> one;
       one.push_back(Value::FromTensor(std::move(t)));
@@ -1102,7 +1102,7 @@ class DevicePipeline {
       t.data = static_cast<uint8_t*>(slot->b.get()) + slot->batch_off_b[k] + row * oh * ow * 3 * sizeof(float);
       t.residency = Residency::kDevice;
       t.device = opt_.device;
-      t.owner = lease;
+      t.owner = std::move(lease);
       t.ready = slot->ready;
       comps.push_back(Value::FromTensor(std::move(t)));
     } else {

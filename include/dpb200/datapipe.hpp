@@ -109,6 +109,9 @@ SourcePtr ImagesFromHost(const uint8_t* data, int64_t count, int64_t h, int64_t 
 SourcePtr ImagesFromPinnedHost(const uint8_t* data, int64_t count, int64_t h, int64_t w, int device = 0);
 SourcePtr Int64FromHost(const int64_t* values, int64_t count, int device = 0);
 SourcePtr TokensFromHost(const int32_t* lengths, int64_t count, const int32_t* tokens, int device = 0);
+// Token sequences copied into pinned, device-mapped host memory: the kernels
+// read them over PCIe (end-to-end runs of the token configs).
+SourcePtr TokensFromPinnedHost(const int32_t* lengths, int64_t count, const int32_t* tokens, int device = 0);
 // Length-prefixed record files (formats.md:67-74) read in order; payloads
 // packed into device memory.
 // num_shards > 1: read only the files f % num_shards == index (an

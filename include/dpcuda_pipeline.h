@@ -85,6 +85,9 @@ int dp_source_synthetic_tokens(int64_t count, uint32_t max_len, uint64_t len_see
                                dp_source** out);
 int dp_source_tokens_from_host(const int32_t* lengths, int64_t count, const int32_t* tokens, int device,
                                dp_source** out);
+/* token sequences in pinned, device-mapped host memory (copied in), read by the kernels over PCIe */
+int dp_source_tokens_pinned_host(const int32_t* lengths, int64_t count, const int32_t* tokens, int device,
+                                 dp_source** out);
 /* length-prefixed record files (formats.md:67-74) read in order into device
  * memory: the records of an interleave over files (file x = input element x,
  * every file holding the reader's record count; ops::Interleave over

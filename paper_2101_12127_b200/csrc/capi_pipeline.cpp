@@ -166,6 +166,11 @@ int dp_source_tokens_from_host(const int32_t* lengths, int64_t count, const int3
   DP_REQUIRE(lengths && out);
   return Guard([&] { *out = new dp_source{TokensFromHost(lengths, count, tokens, device)}; });
 }
+int dp_source_tokens_pinned_host(const int32_t* lengths, int64_t count, const int32_t* tokens, int device,
+                                 dp_source** out) {
+  DP_REQUIRE(out && count >= 0 && (lengths || count == 0));
+  return Guard([&] { *out = new dp_source{TokensFromPinnedHost(lengths, count, tokens, device)}; });
+}
 int dp_source_records_from_files(const char* const* paths, int64_t num_paths, int device, dp_source** out) {
   return dp_source_records_from_files_sharded(paths, num_paths, 1, 0, device, out);
 }

@@ -319,6 +319,28 @@ SourcePtr Int64FromHost(const int64_t* values, int64_t count, int device) {
   return s;
 }
 
+SourcePtr TokensFromPinnedHost(const int32_t* lengths, int64_t count, const int32_t* tokens, int device) {
+  auto s = std::make_shared<SourceData>();
+  s->kind = SourceData::Kind::kTokens;
+  s->count = count;
+  s->device = device;
+  s->residency = Residency::kHost;
+  DeviceGuard g(device);
+  s->lengths = PinnedAlloc(sizeof(int32_t) * std::max<int64_t>(count, 1));
+  s->offsets = PinnedAlloc(sizeof(int64_t) * (count + 1));
+  int64_t* offs = P<int64_t>(s->offsets);
+  offs[0] = 0;
+  for (int64_t i = 0; i < count; ++i) {
+    if (lengths[i] < 0) throw PipelineError(ErrorCode::kInvalidAttr, "token lengths must be >= 0");
+    offs[i + 1] = offs[i] + lengths[i];
+  }
+  s->total_tokens = offs[count];
+  s->tokens = PinnedAlloc(sizeof(int32_t) * std::max<int64_t>(s->total_tokens, 1));
+  if (count) std::memcpy(s->lengths.get(), lengths, sizeof(int32_t) * count);
+  if (s->total_tokens) std::memcpy(s->tokens.get(), tokens, sizeof(int32_t) * s->total_tokens);
+  return s;  // mapped + portable pinned memory: under UVA the host pointers are the device pointers
+}
+
 SourcePtr TokensFromHost(const int32_t* lengths, int64_t count, const int32_t* tokens, int device) {
   auto s = std::make_shared<SourceData>();
   s->kind = SourceData::Kind::kTokens;

@@ -67,6 +67,7 @@ _SIGS = {
     "dp_source_images_pinned_host": [c_vp, c_i64, c_i64, c_i64, c_int, PP],
     "dp_source_synthetic_tokens": [c_i64, ctypes.c_uint32, c_u64, c_u64, c_int, PP],
     "dp_source_tokens_from_host": [c_vp, c_i64, c_vp, c_int, PP],
+    "dp_source_tokens_pinned_host": [c_vp, c_i64, c_vp, c_int, PP],
     "dp_source_records_from_files": [ctypes.POINTER(ctypes.c_char_p), c_i64, c_int, PP],
     "dp_source_records_from_files_sharded": [ctypes.POINTER(ctypes.c_char_p), c_i64, c_i64, c_i64, c_int, PP],
     "dp_source_as_shard": [c_vp, c_i64, c_i64, c_i64, c_i64, PP],
@@ -293,12 +294,15 @@ class Source:
         return Source(out)
 
     @staticmethod
-    def tokens_from_host(lengths, tokens, device=0):
+    def tokens_from_host(lengths, tokens, device=0, pinned=False):
+        """Token sequences (lengths + concatenated tokens) copied to the device,
+        or (pinned=True) into pinned host memory the kernels read over PCIe."""
         lengths = np.ascontiguousarray(lengths, np.int32)
         tokens = np.ascontiguousarray(tokens, np.int32)
         out = c_vp()
-        _check(L().dp_source_tokens_from_host(lengths.ctypes.data, lengths.size,
-                                              tokens.ctypes.data if tokens.size else None, device, ctypes.byref(out)))
+        fn = L().dp_source_tokens_pinned_host if pinned else L().dp_source_tokens_from_host
+        _check(fn(lengths.ctypes.data, lengths.size, tokens.ctypes.data if tokens.size else None, device,
+                  ctypes.byref(out)))
         return Source(out)
 
 

@@ -443,6 +443,32 @@ def test_cast_u8_to_f32(dp, orc):
     assert all(np.array_equal(b[1][k], pix[int(i)].astype(np.float32)) for b in out for k, i in enumerate(b[0]))
 
 
+def test_pinned_host_token_source_equals_device_source(dp, orc):
+    """Token sequences in pinned host memory (read over PCIe by the filter,
+    padded / ragged and bucket kernels) give the same batches as the same
+    sequences in HBM, with host_output on and off."""
+    lens = orc.lengths(3000)
+    toks, _ = orc.tokens(lens)
+    reg = dp.Registry()
+    reg.register_length_filter("len<=512", 512)
+    outs = []
+    for pinned, host in ((False, False), (True, False), (True, True)):
+        src = dp.Source.tokens_from_host(lens, toks, pinned=pinned)
+        base = dp.Dataset.token_sequences(reg, src).filter("len<=512")
+        got = []
+        for g in (base.padded_batch(64), base.batch(50), base.shuffle(300, 5).bucket_by_length([200], [32, 16])):
+            it = dp.make_iterator(g, seed_override=1, host_output=host)
+            while (b := it.get_next()) is not None:
+                if host:
+                    b.wait()
+                got.append([b.numpy(0), b.numpy(1)])
+                b.release()
+        outs.append(got)
+    for other in outs[1:]:
+        assert len(other) == len(outs[0])
+        assert all(np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) for a, b in zip(outs[0], other))
+
+
 def test_host_output_equals_device_output(dp):
     reg = image_registry(dp, 0, crop=(64, 64))
     src = dp.Source.synthetic_images(200, 96, 96)

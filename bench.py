@@ -126,6 +126,50 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def config_dict(cfg, world):
+    """The `config` object of both arms' JSON lines (same keys and values)."""
+    if cfg["kind"] == "images":
+        l2 = (f"inputs {cfg['n'] * cfg['in_hw'][0] * cfg['in_hw'][1] * 3 / 1e9:.1f} GB/GPU and the rotating output "
+              f"slots exceed the 126 MB L2 (no flush needed)")
+    else:
+        l2 = "one launch = one epoch of output (> 126 MB L2); no flush needed"
+    return {"workload": cfg["workload"], "global_batch": cfg["batch"] * world, "elements_per_gpu": cfg["n"],
+            "parallelism": f"dp{world} (Shard, no data-path collective)", "l2": l2}
+
+
+def expected_order_digest(config, n, world, rank):
+    """tests/golden/order_check.json (generated by the oracle restatement)."""
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "order_check.json")) as f:
+            return json.load(f)["entries"].get(f"{config}/n{n}/w{world}/r{rank}")
+    except (OSError, ValueError, KeyError):
+        return None
+
+
+def launch_group_for(warmup, steps, default_group, batches_per_epoch):
+    """Largest launch group d <= default_group whose launch boundaries fall
+    on both ends of the timed window [warmup, warmup + steps): groups tile
+    each epoch from its start (the last one may be shorter), so the window
+    holds exactly `steps` batches."""
+    def on_boundary(x, d):
+        return (x % batches_per_epoch) % d == 0
+    for d in range(min(default_group, batches_per_epoch), 0, -1):
+        if on_boundary(warmup, d) and on_boundary(warmup + steps, d):
+            return d
+    return 1
+
+
 def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
@@ -245,9 +289,10 @@ def run_reference(args, cfg):
             "unit": cfg["unit"], "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(1e3 * r["seconds"] / args.steps, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": cfg.get("dtype", "u8->f32"), "data": "synthetic",
-            "config": {"workload": cfg["workload"], "global_batch": cfg["batch"], "host_threads": threads},
+            "config": config_dict(cfg, world),
             "cpu_baseline": {"value": round(r["value"], 2), "unit": cfg["unit"], "cores": threads,
-                             "kind": "reference", "sample": r["sample"]},
+                             "kind": "reference", "sample": r["sample"], "cpu_model": cpu_model(),
+                             "host_threads": os.cpu_count()},
             "e2e": {"value": round(r["value"], 2), "unit": cfg["unit"], "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -336,12 +381,17 @@ def run_ours(args, cfg):
     rehearsal = os.environ.get("DP_BENCH_ONE_GPU") == "1"
     if rehearsal:
         local = 0
+    if not rehearsal and torch.cuda.device_count() < world:
+        raise SystemExit(f"bench.py --gpus {world}: only {torch.cuda.device_count()} CUDA device(s) visible")
     torch.cuda.set_device(local)
+    comm = None
     if world > 1:
         if rehearsal:
             distr.init_process_group("gloo")
         else:
             distr.init_process_group("nccl", device_id=torch.device("cuda", local))
+        comm = {"backend": distr.get_backend(), "world_size": distr.get_world_size(),
+                "data_path_collectives": 0, "use": "barrier, max-over-ranks time, 8-byte digest all_gather"}
     dev = torch.device("cuda", local)
 
     # ---- device-resident workload (not timed) ----
@@ -361,18 +411,28 @@ def run_ours(args, cfg):
         src = dp.Source.synthetic_images(n, *cfg["in_hw"], seed=0x5EED, device=local)
         g, report = build_graph(dp, cfg, src)
     it = dp.make_iterator(g, seed_override=1, device=local)
-    stream = torch.cuda.ExternalStream(it.stream, device=dev)
     desc = it.describe()
     per_launch = int(re.search(r"(\d+) batch\(es\) per launch", desc).group(1))
     per_epoch = int(re.search(r"epoch: \d+ elements, (\d+) batches", desc).group(1))
-    if per_epoch % per_launch:  # ragged last group per epoch: whole epochs keep the window exact
-        per_launch = per_epoch
-    if cfg["kind"] != "images":  # small batches: whole epochs
+    steps_requested, warmup_requested = args.steps, args.warmup
+    if cfg["kind"] == "images":
+        # exactly K timed and W warm-up steps: a launch group that tiles the
+        # window (largest divisor-compatible group up to the default size)
+        group = launch_group_for(args.warmup, args.steps, per_launch, per_epoch)
+        if group != per_launch:
+            del it
+            it = dp.make_iterator(g, seed_override=1, device=local, launch_batches=group)
+            per_launch = group
+    else:
+        # token / range configs launch a whole epoch of tiny batches at once:
+        # the window is whole epochs (steps and warmup rounded up to them)
+        if per_epoch % per_launch:
+            per_launch = per_epoch
         args.steps = max(args.steps, per_launch)
         args.warmup = max(args.warmup, per_launch)
-    # W and K whole launch groups, so the event window holds exactly K batches
-    args.warmup = -(-args.warmup // per_launch) * per_launch
-    args.steps = -(-args.steps // per_launch) * per_launch
+        args.warmup = -(-args.warmup // per_launch) * per_launch
+        args.steps = -(-args.steps // per_launch) * per_launch
+    stream = torch.cuda.ExternalStream(it.stream, device=dev)
     it.skip(args.warmup)  # GetNext in C++, batches dropped (no-op consumer)
     torch.cuda.synchronize(dev)
     if world > 1:
@@ -430,6 +490,8 @@ def run_ours(args, cfg):
         b.release()
     torch.cuda.synchronize(dev)
     order_digests = gather_digests(digest, world)
+    expected = [expected_order_digest(args.config, n, world, r) for r in range(world)]
+    order_ok = None if None in expected else all(a == b for a, b in zip(order_digests, expected))
     del vit
 
     if rank != 0:
@@ -459,18 +521,18 @@ def run_ours(args, cfg):
             traffic = None if t is None else int(t["bytes"] * batches_per_launch / t["batches"])
         except Exception:
             traffic = None
-    l2 = (f"inputs {n * cfg['in_hw'][0] * cfg['in_hw'][1] * 3 / 1e9:.1f} GB/GPU and the rotating output slots "
-          f"exceed the 126 MB L2 (no flush needed)" if cfg["kind"] == "images" else
-          "one launch = one epoch of output (> 126 MB L2); no flush needed")
     line = {
         "metric": "pipeline elements/sec", "value": round(value, 1), "unit": cfg["unit"], "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 5),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": cfg["dtype"],
         "data": "synthetic (device-generated, SplitMix64 / PCG32 keyed)",
-        "config": {"workload": cfg["workload"], "global_batch": cfg["batch"] * world,
-                   "elements_per_gpu": n, "parallelism": f"dp{world} (Shard, no data-path collective)",
-                   "l2": l2,
-                   "optimized": "map_and_batch" in report or "map_batch_fusion" in report},
+        "config": config_dict(cfg, world),
+        "lowering": {"optimized": "map_and_batch" in report or "map_batch_fusion" in report,
+                     "batches_per_launch": per_launch, "prefetch_depth": "AUTOTUNE"},
+        **({} if (steps_requested, warmup_requested) == (args.steps, args.warmup) else
+           {"steps_requested": steps_requested, "warmup_requested": warmup_requested,
+            "steps_note": "whole epochs of tiny batches (one launch per epoch)"}),
+        "comm": comm,
         "roofline": {"bound": "hbm", "kernel": cfg["kernel"], "achieved": round(achieved, 1), "peak": peak,
                      "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
                      "algorithmic_bytes_per_launch": int(bytes_per_batch * batches_per_launch),
@@ -481,11 +543,13 @@ def run_ours(args, cfg):
                                  "write-only HBM traffic runs above the read+write copy figure used as peak"}
                         if cfg["kind"] == "range" else {})},
         "batches_in_window": batches_in_window, "steps_per_launch_group": per_launch,
-        "order_check": {"digest": "K7 position-keyed digest of each rank's first 8 batches of ids",
-                        "per_rank": order_digests},
+        "order_check": {"digest": "K7 position-keyed digest of each rank's first 8 batches (ids / values / row "
+                                  "lengths), vs tests/golden/order_check.json (oracle restatement)",
+                        "per_rank": order_digests, "expected": expected, "ok": order_ok},
         "cpu_baseline": {"value": None if cpu is None else (round(cpu["value"], 2) if cpu["value"] else None),
                          "unit": cfg["unit"], "cores": (cpu or {}).get("cores", os.cpu_count()), "kind": "reference",
-                         "sample": None if cpu is None else cpu["sample"], "one_core": one_core},
+                         "sample": None if cpu is None else cpu["sample"], "one_core": one_core,
+                         "cpu_model": cpu_model(), "host_threads": os.cpu_count()},
         "e2e": e2e,
         "gpu_launches": launches,
         "clocks": clocks.summary(),
@@ -624,6 +688,37 @@ def run_e2e_tokens(dp, cfg, local, args, world=1, dev=None):
                      "(128 B per warp request); staging the dataset per epoch by bulk DMA is not done yet"}
 
 
+def relaunch(n):
+    """`bench.py --gpus N` outside torchrun: re-run this command as N ranks
+    (one process per GPU) under torch.distributed.run on this node."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def probe_launch(args):
+    """The rank plumbing of `--gpus N` without a GPU (tests/test_multiproc.py):
+    every rank joins a gloo group, the max-over-ranks and digest gather run,
+    rank 0 prints what it saw."""
+    import torch
+    import torch.distributed as distr
+    rank, world, local = dist_env()
+    if world > 1:
+        distr.init_process_group("gloo")
+    ms = max_over_ranks(1.0 + rank, world, "cpu")
+    digests = gather_digests(torch.tensor([rank * 1000 + local], dtype=torch.int64), world)
+    expected = [expected_order_digest(args.config, CFG[args.config]["n"], world, r) for r in range(world)]
+    if rank == 0:
+        print(json.dumps({"probe": True, "n_gpus": world, "gpus_requested": args.gpus, "ms_max": ms,
+                          "per_rank": digests, "expected": expected}), flush=True)
+    if world > 1:
+        distr.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -632,9 +727,17 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CFG), default="cfg2")
     ap.add_argument("--elements-per-gpu", type=int, default=0, help="override the per-GPU dataset size (tests)")
+    ap.add_argument("--probe-launch", action="store_true", help=argparse.SUPPRESS)  # CPU test of the launcher
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
+    if "WORLD_SIZE" in os.environ:
+        if int(os.environ["WORLD_SIZE"]) != args.gpus:
+            ap.error(f"--gpus {args.gpus} but WORLD_SIZE={os.environ['WORLD_SIZE']}")
+    elif args.gpus > 1 and args.impl == "ours":
+        sys.exit(relaunch(args.gpus))
+    if args.probe_launch:
+        return probe_launch(args)
     cfg = dict(CFG[args.config])
     if args.elements_per_gpu:
         cfg["n"] = args.elements_per_gpu

@@ -324,6 +324,10 @@ struct IteratorOptions {
   // grouped into one launch up to this size); 0 = 3.2 GB (512 MB with
   // host_output).
   size_t max_launch_bytes = 0;
+  // Batches per fused launch, exactly (0 = from max_launch_bytes, rounded
+  // down to a power of two).  Launch groups never straddle an epoch of a
+  // per-epoch batch stage, so the last group of an epoch may be shorter.
+  int64_t launch_batches = 0;
 };
 
 struct NodeMetricsRow {
@@ -355,6 +359,10 @@ class PipelineIterator {
   int64_t prefetch_depth() const;       // device slots in use (autotuned)
   int64_t kernel_launches() const;      // sm_100a kernels issued so far
   int64_t batches_launched() const;     // batches covered by issued batch-stage launches
+  struct Stats {
+    int64_t live_plans = 0, slots = 0, slot_bytes = 0, prefetch_depth = 0, group_batches = 0;
+  };
+  Stats stats() const;
   // Checkpoint in the reference's DPC1 layout (checkpoint.hpp:36-49,
   // formats.md:76-94).  Restore() seeks instead of replaying.
   std::string Save() const;

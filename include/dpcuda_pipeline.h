@@ -171,6 +171,7 @@ typedef struct {
   int host_output;            /* copy batches to pinned host memory */
   uint64_t slot_memory_budget;/* bytes of device prefetch slots (0: default 8 GiB) */
   uint64_t max_launch_bytes;  /* output bytes per fused launch (0: default) */
+  int64_t launch_batches;     /* batches per fused launch, exactly (0: from max_launch_bytes) */
 } dp_iterator_options;
 
 typedef enum { DP_U8 = 0, DP_I32 = 1, DP_I64 = 2, DP_F32 = 3 } dp_dtype;
@@ -226,6 +227,16 @@ int64_t dp_iterator_batches_launched(const dp_iterator* it);
  * each launch on the launching stream; waits for issued launches). */
 int dp_iterator_batch_stage_timing(const dp_iterator* it, int64_t* total_ns, int64_t* launches);
 int64_t dp_iterator_prefetch_depth(const dp_iterator* it);
+/* Resource counters of the device pipeline (no reference counterpart: the
+ * reference's buffers are per-element heap objects). */
+typedef struct {
+  int64_t live_plans;     /* epoch plans held (current, next, one back) */
+  int64_t slots;          /* device batch slots allocated (prefetch ring) */
+  int64_t slot_bytes;     /* their device bytes */
+  int64_t prefetch_depth; /* groups kept in flight */
+  int64_t group_batches;  /* batches per fused launch */
+} dp_iterator_stats;
+int dp_iterator_get_stats(const dp_iterator* it, dp_iterator_stats* out);
 int64_t dp_iterator_root_delivered(const dp_iterator* it);
 uint64_t dp_iterator_base_seed(const dp_iterator* it);
 int dp_iterator_describe(const dp_iterator* it, char* buf, size_t len);

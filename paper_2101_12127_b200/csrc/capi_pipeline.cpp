@@ -365,6 +365,7 @@ int dp_iterator_create(const dp_graph* g, const dp_registry* reg, const dp_itera
       o.host_output = opt->host_output != 0;
       if (opt->slot_memory_budget) o.slot_memory_budget = opt->slot_memory_budget;
       o.max_launch_bytes = opt->max_launch_bytes;
+      o.launch_batches = opt->launch_batches;
     }
     *out = new dp_iterator{MakeIterator(g->g, reg->reg, o)};
   });
@@ -437,6 +438,7 @@ int dp_iterator_restore(const dp_graph* g, const dp_registry* reg, const void* b
       o.host_output = opt->host_output != 0;
       if (opt->slot_memory_budget) o.slot_memory_budget = opt->slot_memory_budget;
       o.max_launch_bytes = opt->max_launch_bytes;
+      o.launch_batches = opt->launch_batches;
     }
     std::string b(static_cast<const char*>(blob), len);
     *out = new dp_iterator{Restore(g->g, reg->reg, b, o)};
@@ -502,6 +504,13 @@ int dp_iterator_batch_stage_timing(const dp_iterator* it, int64_t* total_ns, int
   });
 }
 int64_t dp_iterator_prefetch_depth(const dp_iterator* it) { return it ? it->it->prefetch_depth() : 0; }
+int dp_iterator_get_stats(const dp_iterator* it, dp_iterator_stats* out) {
+  DP_REQUIRE(it && out);
+  return Guard([&] {
+    const auto st = it->it->stats();
+    *out = dp_iterator_stats{st.live_plans, st.slots, st.slot_bytes, st.prefetch_depth, st.group_batches};
+  });
+}
 int64_t dp_iterator_root_delivered(const dp_iterator* it) { return it ? it->it->root_delivered() : 0; }
 uint64_t dp_iterator_base_seed(const dp_iterator* it) { return it ? it->it->base_seed() : 0; }
 int dp_iterator_describe(const dp_iterator* it, char* buf, size_t len) {

@@ -87,20 +87,35 @@ T* P(const std::shared_ptr<void>& p) {
 // Small-block recycling for the per-batch control blocks GetNext creates
 // (slot leases, Tensor views): a per-thread free list per 64-byte size
 // class, capped, falling back to operator new / delete.  Blocks freed on
-// another thread join that thread's list.
+// another thread join that thread's list.  A thread's lists are returned to
+// the heap when the thread exits; blocks freed during or after that teardown
+// (a lease dropped by a thread_local destructor) go straight to the heap.
 struct BlockPool {
   static constexpr int kClasses = 4, kCap = 4096;
-  static std::vector<void*>* Lists() {
-    thread_local std::vector<void*> lists[kClasses];
-    return lists;
+  struct Lists {
+    std::vector<void*> l[kClasses];
+    ~Lists() {
+      Dead() = true;
+      for (auto& v : l)
+        for (void* p : v) ::operator delete(p);
+    }
+  };
+  // trivially destructible, so still readable while the thread tears down
+  static bool& Dead() {
+    thread_local bool dead = false;
+    return dead;
+  }
+  static std::vector<void*>* ThreadLists() {
+    if (Dead()) return nullptr;
+    thread_local Lists lists;
+    return lists.l;
   }
   static void* Get(size_t bytes) {
     const size_t c = (bytes + 63) / 64 - 1;
     if (c < kClasses) {
-      auto& l = Lists()[c];
-      if (!l.empty()) {
-        void* p = l.back();
-        l.pop_back();
+      if (auto* lists = ThreadLists(); lists && !lists[c].empty()) {
+        void* p = lists[c].back();
+        lists[c].pop_back();
         return p;
       }
       return ::operator new((c + 1) * 64);
@@ -110,9 +125,8 @@ struct BlockPool {
   static void Put(void* p, size_t bytes) {
     const size_t c = (bytes + 63) / 64 - 1;
     if (c < kClasses) {
-      auto& l = Lists()[c];
-      if (l.size() < kCap) {
-        l.push_back(p);
+      if (auto* lists = ThreadLists(); lists && lists[c].size() < kCap) {
+        lists[c].push_back(p);
         return;
       }
     }

@@ -135,6 +135,7 @@ class DevicePipeline {
     // (padded kinds launch a whole epoch when it fits: their epochs have an
     // arbitrary batch count, so a power of two would leave a ragged tail group)
     if (L_.kind != BatchKind::kPadded || group_ < batches_per_epoch_) group_ = pow2;
+    if (opt_.launch_batches > 0) group_ = opt_.launch_batches;
     group_ = std::min(group_, std::max<int64_t>(1, batches_per_epoch_));
     // the prefetch depth must fit the slot budget (at least double buffering)
     const size_t group_bytes = (batch_bytes_.first + batch_bytes_.second) * group_;
@@ -296,7 +297,7 @@ class DevicePipeline {
     if (L_.kind == BatchKind::kPadded) {
       // max sequence length over the source, for slot sizing
       std::vector<int32_t> lens(L_.source->count);
-      CudaCheck(cudaMemcpy(lens.data(), L_.source->lengths.get(), sizeof(int32_t) * lens.size(), cudaMemcpyDeviceToHost),
+      CudaCheck(cudaMemcpy(lens.data(), L_.source->lengths.get(), sizeof(int32_t) * lens.size(), cudaMemcpyDefault),
                 "lengths");
       max_len_ = lens.empty() ? 0 : *std::max_element(lens.begin(), lens.end());
       for (const auto& op : L_.chain)
@@ -417,6 +418,7 @@ class DevicePipeline {
   // Builds epoch e's plan on a helper thread (plan stream); Plan() joins it.
   void PrefetchPlan(int64_t e) {
     JoinPendingPlan();
+    RetirePlansBefore(e);
     if (plans_.count(e)) return;
     pending_plan_ = std::async(std::launch::async, [this, e] {
       DeviceGuard g(opt_.device);
@@ -428,24 +430,40 @@ class DevicePipeline {
     });
   }
 
+  // Retire the plans of epochs before `e - 1` (called whenever plan e is
+  // asked for or prefetched; groups are issued in epoch order, so nothing
+  // issued later reads them).  Their buffers are freed on the plan stream,
+  // ordered after every batch kernel queued so far on the batch stream (the
+  // last readers) -- no host synchronisation.
+  void RetirePlansBefore(int64_t e) {
+    for (auto jt = plans_.begin(); jt != plans_.end() && jt->first < e - 1;) {
+      if (!retire_ev_) CudaCheck(cudaEventCreateWithFlags(&retire_ev_, cudaEventDisableTiming), "event");
+      CudaCheck(cudaEventRecord(retire_ev_, stream_), "event");
+      CudaCheck(cudaStreamWaitEvent(plan_stream_, retire_ev_, 0), "wait");
+      if (jt->second.ready) cudaEventDestroy(jt->second.ready);
+      for (auto at = appended_.begin(); at != appended_.end();)
+        at = *at / 1000003 == jt->first ? appended_.erase(at) : std::next(at);
+      jt = plans_.erase(jt);
+    }
+  }
+
+ public:
+  PipelineIterator::Stats stats() const {
+    PipelineIterator::Stats st;
+    st.live_plans = static_cast<int64_t>(plans_.size());
+    st.slots = static_cast<int64_t>(slots_.size());
+    st.slot_bytes = static_cast<int64_t>(slot_bytes_total_);
+    st.prefetch_depth = depth_;
+    st.group_batches = group_;
+    return st;
+  }
+
+ private:
   EpochPlan& Plan(int64_t e) {
     JoinPendingPlan();
+    RetirePlansBefore(e);
     auto it = plans_.find(e);
     if (it != plans_.end()) return it->second;
-    // Retire plans two epochs back.  Their buffers are freed on the plan
-    // stream, ordered after every batch kernel queued so far on the batch
-    // stream (the last readers) -- no host synchronisation.
-    for (auto jt = plans_.begin(); jt != plans_.end();) {
-      if (jt->first < e - 1) {
-        if (!retire_ev_) CudaCheck(cudaEventCreateWithFlags(&retire_ev_, cudaEventDisableTiming), "event");
-        CudaCheck(cudaEventRecord(retire_ev_, stream_), "event");
-        CudaCheck(cudaStreamWaitEvent(plan_stream_, retire_ev_, 0), "wait");
-        if (jt->second.ready) cudaEventDestroy(jt->second.ready);
-        jt = plans_.erase(jt);
-      } else {
-        ++jt;
-      }
-    }
     EpochPlan& p = plans_[e];
     p.epoch = e;
     BuildPlan(p, e);
@@ -777,8 +795,10 @@ class DevicePipeline {
 
   std::shared_ptr<Slot> FindFreeSlot(bool may_grow) {
     for (auto& s : slots_) {
+      // free = never used, or its release event was recorded (which happens
+      // only after every unit was handed out and dropped, see Lease)
       std::lock_guard lk(shared_->mu);
-      if (!s->busy || (s->handed_out == s->units && s->outstanding.load() == 0)) return s;
+      if (!s->busy || s->release_recorded) return s;
     }
     const size_t need = (batch_bytes_.first + batch_bytes_.second) * group_;
     if (static_cast<int64_t>(slots_.size()) < depth_ || may_grow) {
@@ -1010,8 +1030,14 @@ class DevicePipeline {
         nullptr,
         [slot, consumer = consumer_, shared = shared_](void*) {
           if (slot->outstanding.fetch_sub(1) == 1 && slot->handed_out.load() == slot->units) {
+            // Re-checked under the lock: a Lease() of the group's last unit
+            // may have run between the fetch_sub and the handed_out load (its
+            // outstanding++ precedes its handed_out++, so it is visible here);
+            // that unit's own drop releases the slot.  Every drop that reaches
+            // outstanding == 0 after the last hand-out gets here, and the
+            // first one under the lock records the event.
             std::lock_guard lk(shared->mu);
-            if (shared->alive) {
+            if (shared->alive && !slot->release_recorded && slot->outstanding.load() == 0) {
               cudaEventRecord(slot->release, consumer);
               slot->release_recorded = true;
               shared->slots_freed.fetch_add(1, std::memory_order_release);
@@ -1277,6 +1303,10 @@ std::vector<NodeMetricsRow> PipelineIterator::Metrics() const {
 
 void* PipelineIterator::stream() const { return impl_->stream(); }
 int64_t PipelineIterator::prefetch_depth() const { return impl_->depth(); }
+PipelineIterator::Stats PipelineIterator::stats() const {
+  std::lock_guard lock(mu_);
+  return impl_->stats();
+}
 int64_t PipelineIterator::kernel_launches() const { return impl_->launches(); }
 int64_t PipelineIterator::batches_launched() const { return impl_->batches_launched(); }
 void PipelineIterator::Seek(int64_t batches) {

@@ -335,6 +335,9 @@ SourcePtr TokensFromPinnedHost(const int32_t* lengths, int64_t count, const int3
     offs[i + 1] = offs[i] + lengths[i];
   }
   s->total_tokens = offs[count];
+  if (s->total_tokens > 0 && tokens == nullptr)
+    throw PipelineError(ErrorCode::kInvalidAttr, "token sequences: tokens is null but the lengths sum to " +
+                                                     std::to_string(s->total_tokens));
   s->tokens = PinnedAlloc(sizeof(int32_t) * std::max<int64_t>(s->total_tokens, 1));
   if (count) std::memcpy(s->lengths.get(), lengths, sizeof(int32_t) * count);
   if (s->total_tokens) std::memcpy(s->tokens.get(), tokens, sizeof(int32_t) * s->total_tokens);
@@ -352,6 +355,9 @@ SourcePtr TokensFromHost(const int32_t* lengths, int64_t count, const int32_t* t
     offs[i + 1] = offs[i] + lengths[i];
   }
   s->total_tokens = offs[count];
+  if (s->total_tokens > 0 && tokens == nullptr)
+    throw PipelineError(ErrorCode::kInvalidAttr, "token sequences: tokens is null but the lengths sum to " +
+                                                     std::to_string(s->total_tokens));
   s->lengths = DeviceAlloc(sizeof(int32_t) * std::max<int64_t>(count, 1), device);
   s->offsets = DeviceAlloc(sizeof(int64_t) * (count + 1), device);
   s->tokens = DeviceAlloc(sizeof(int32_t) * std::max<int64_t>(s->total_tokens, 1), device);

@@ -44,7 +44,12 @@ class dp_batch(ctypes.Structure):
 class dp_iterator_options(ctypes.Structure):
     _fields_ = [("deterministic", c_int), ("has_seed_override", c_int), ("seed_override", c_u64), ("device", c_int),
                 ("consumer_stream", c_vp), ("host_output", c_int), ("slot_memory_budget", c_u64),
-                ("max_launch_bytes", c_u64)]
+                ("max_launch_bytes", c_u64), ("launch_batches", c_i64)]
+
+
+class dp_iterator_stats(ctypes.Structure):
+    _fields_ = [("live_plans", c_i64), ("slots", c_i64), ("slot_bytes", c_i64), ("prefetch_depth", c_i64),
+                ("group_batches", c_i64)]
 
 
 _SIGS = {
@@ -109,7 +114,7 @@ _SIGS = {
     "dp_tensor_copy_to_host": [ctypes.POINTER(dp_batch), c_int, c_vp, c_size],
     "dp_iterator_stream": [c_vp], "dp_iterator_kernel_launches": [c_vp], "dp_iterator_prefetch_depth": [c_vp],
     "dp_iterator_batch_stage_timing": [c_vp, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64)],
-    "dp_iterator_batches_launched": [c_vp],
+    "dp_iterator_batches_launched": [c_vp], "dp_iterator_get_stats": [c_vp, ctypes.POINTER(dp_iterator_stats)],
     "dp_iterator_root_delivered": [c_vp], "dp_iterator_base_seed": [c_vp],
     "dp_iterator_describe": [c_vp, ctypes.c_char_p, c_size], "dp_iterator_destroy": [c_vp],
 }
@@ -299,6 +304,9 @@ class Source:
         or (pinned=True) into pinned host memory the kernels read over PCIe."""
         lengths = np.ascontiguousarray(lengths, np.int32)
         tokens = np.ascontiguousarray(tokens, np.int32)
+        if tokens.size != int(lengths.astype(np.int64).sum()):
+            raise DpError(2, f"token sequences: {tokens.size} tokens but the lengths sum to "
+                          f"{int(lengths.astype(np.int64).sum())}")
         out = c_vp()
         fn = L().dp_source_tokens_pinned_host if pinned else L().dp_source_tokens_from_host
         _check(fn(lengths.ctypes.data, lengths.size, tokens.ctypes.data if tokens.size else None, device,
@@ -475,6 +483,18 @@ class Batch:
         _check(L().dp_tensor_copy_to_host(ctypes.byref(self.b), c, arr.ctypes.data, arr.nbytes))
         return arr
 
+    def torch(self, c):
+        """Zero-copy torch view of a device component (valid until release;
+        ready on the iterator's consumer_stream)."""
+        import torch
+        dt, shape, ptr, on_host = self.components[c]
+        assert not on_host, "torch() views device components"
+
+        class _View:
+            __cuda_array_interface__ = {"shape": shape, "typestr": np.dtype(dt).str, "data": (ptr, False),
+                                        "version": 2, "strides": None}
+        return torch.as_tensor(_View(), device="cuda")
+
     def wait(self):
         """Host-blocking wait until the batch is written (and copied, with host_output)."""
         _check(L().dp_batch_wait(ctypes.byref(self.b)))
@@ -560,6 +580,12 @@ class Iterator:
     def prefetch_depth(self):
         return L().dp_iterator_prefetch_depth(self.h)
 
+    def stats(self) -> dict:
+        """dp_iterator_get_stats: live epoch plans, slots, slot bytes, depth, batches per launch."""
+        st = dp_iterator_stats()
+        _check(L().dp_iterator_get_stats(self.h, ctypes.byref(st)))
+        return {f: int(getattr(st, f)) for f, _ in dp_iterator_stats._fields_}
+
     @property
     def root_delivered(self):
         return L().dp_iterator_root_delivered(self.h)
@@ -587,7 +613,7 @@ def restore(ds: Dataset, blob: bytes, device=0, consumer_stream=None, host_outpu
 
 
 def make_iterator(ds: Dataset, seed_override=None, device=0, consumer_stream=None, host_output=False,
-                  slot_memory_budget=0, deterministic=True, max_launch_bytes=0):
+                  slot_memory_budget=0, deterministic=True, max_launch_bytes=0, launch_batches=0):
     """MakeIterator(graph, registry, IteratorOptions) (runtime.hpp:98-100)."""
     o = dp_iterator_options()
     L().dp_iterator_options_default(ctypes.byref(o))
@@ -600,6 +626,7 @@ def make_iterator(ds: Dataset, seed_override=None, device=0, consumer_stream=Non
     o.host_output = int(host_output)
     o.slot_memory_budget = slot_memory_budget
     o.max_launch_bytes = max_launch_bytes
+    o.launch_batches = launch_batches
     out = c_vp()
     _check(L().dp_iterator_create(ds.h, ds.reg.h, ctypes.byref(o), ctypes.byref(out)))
     return Iterator(out, ds)

@@ -62,3 +62,22 @@ def test_two_rank_cfg5_block_residency_order_check(orc):
         inter = orc.interleave_order(np.arange(r, 2 * files, 2), 4, n // files)
         ids = inter[orc.shuffle_order(inter.size, 10000, orc.shuffle_seed(orc.mix_seeds(1, 0), 42))]
         assert digests[r] == f"{orc.order_digest(ids[:8 * 256]):016x}", r
+
+
+def test_self_launched_two_ranks_full_size_order_check():
+    """the driver's own command shape, `bench.py --gpus 2`
+    with no torchrun around it, spawns two ranks; at the full cfg3 size
+    (65,536 images per rank) each rank's digest equals the golden oracle
+    digest (tests/golden/order_check.json) and the line says so."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env["DP_BENCH_ONE_GPU"] = "1"
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "20", "--warmup",
+                          "5", "--config", "cfg3"], capture_output=True, text=True, env=env, cwd=ROOT, timeout=1200)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
+    line = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["comm"]["world_size"] == 2
+    assert line["steps"] == 20 and line["warmup"] == 5 and line["batches_in_window"] == 20
+    assert line["order_check"]["ok"] is True, line["order_check"]

@@ -1,0 +1,142 @@
+"""Device-pipeline runtime properties on the GPU: bounded per-epoch state
+under repeat(-1), slot reuse ordered after consumer-stream work when
+batches are dropped on other threads, and output independent of the
+prefetch depth and of the launch-group size (the reference's
+P/tests/test_parallel.cpp:297-312: settings do not change the sequence).
+"""
+import queue
+import threading
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dp():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2101_12127_b200 import pipeline
+    return pipeline
+
+
+def _token_graph(dp, kind, n=4000):
+    reg = dp.Registry()
+    reg.register_length_filter("len<=100", 100)
+    src = dp.Source.synthetic_tokens(n, 200, 3, 3)
+    g = dp.Dataset.token_sequences(reg, src).filter("len<=100").shuffle(500, 5)
+    if kind == "padded":
+        g = g.padded_batch(64)
+    elif kind == "ragged":
+        g = g.batch(64)
+    else:
+        g = g.bucket_by_length([30, 60], [32, 16, 8])
+    return g.repeat(-1).prefetch(2), src
+
+
+@pytest.mark.parametrize("kind", ["padded", "ragged", "bucket"])
+def test_epoch_plans_are_retired_under_repeat(dp, kind):
+    """the padded kinds prefetch the next epoch's plan; the
+    old ones must still be retired.  25 epochs, <= 3 live plans throughout."""
+    g, _ = _token_graph(dp, kind)
+    it = dp.make_iterator(g, seed_override=1)
+    per_epoch = int(__import__("re").search(r"elements, (\d+) batches", it.describe()).group(1))
+    peak = 0
+    for k in range(25 * per_epoch):
+        it.get_next().release()
+        if k % per_epoch == 0:
+            peak = max(peak, it.stats()["live_plans"])
+    assert peak <= 3, peak
+
+
+def test_image_plans_are_retired_under_repeat(dp):
+    reg = dp.Registry()
+    reg.register_random_crop_flip("crop", 16, 16, seed=1, flip=True)
+    reg.register_normalize("norm")
+    src = dp.Source.synthetic_images(640, 24, 24)
+    g, _ = (dp.Dataset.tensor_slices(reg, src).shuffle(100, 2).map("crop").map("norm").batch(64).repeat(-1)
+            .optimize())
+    it = dp.make_iterator(g, seed_override=1)
+    for _ in range(30 * 10):
+        it.get_next().release()
+    assert it.stats()["live_plans"] <= 3
+
+
+def test_slot_reuse_waits_for_consumer_stream_work_dropped_on_other_threads(dp):
+    """batches are read by slow kernels on a consumer
+    stream and dropped by worker threads; a slot may be rewritten only after
+    the consumer work queued before its drop.  One batch per launch group
+    and a depth-2 ring make reuse immediate; the per-batch checksums taken
+    on the consumer stream must equal those of an undisturbed run."""
+    import torch
+    reg = dp.Registry()
+    reg.register_random_crop_flip("crop", 32, 32, seed=3, flip=True)
+    reg.register_normalize("norm")
+    src = dp.Source.synthetic_images(4096, 40, 40)
+    g, _ = (dp.Dataset.tensor_slices(reg, src).shuffle(1000, 9).map("crop").map("norm").batch(64).prefetch(2)
+            .optimize())
+    want = []
+    for b in dp.make_iterator(g, seed_override=4, launch_batches=1):
+        b.wait()
+        want.append(float(b.torch(1).double().sum()))
+        b.release()
+    cs = torch.cuda.Stream()
+    it = dp.make_iterator(g, seed_override=4, consumer_stream=cs.cuda_stream, launch_batches=1)
+    assert it.stats()["group_batches"] == 1
+    drops = queue.Queue()
+    sums = []
+
+    def dropper():
+        while (b := drops.get()) is not None:
+            b.release()
+
+    workers = [threading.Thread(target=dropper) for _ in range(3)]
+    for w in workers:
+        w.start()
+    with torch.cuda.stream(cs):
+        while (b := it.get_next()) is not None:
+            torch.cuda._sleep(200_000)  # the consumer is slower than the producer
+            sums.append(b.torch(1).double().sum())
+            drops.put(b)
+    for _ in workers:
+        drops.put(None)
+    for w in workers:
+        w.join()
+    torch.cuda.synchronize()
+    assert [float(s) for s in sums] == want
+
+
+@pytest.mark.parametrize("depth", [1, 2, 8, -1])
+@pytest.mark.parametrize("launch_batches", [0, 1, 3, 7])
+def test_output_independent_of_prefetch_and_launch_group(dp, depth, launch_batches):
+    """The same batches (ids and pixels, bit for bit) for prefetch 1/2/8/
+    AUTOTUNE and any launch-group size (DP max_launch_bytes), across epoch
+    boundaries (repeat 3, batches spanning epochs)."""
+    reg = dp.Registry()
+    reg.register_random_crop_flip("crop", 24, 24, seed=5, flip=True)
+    reg.register_normalize("norm")
+    src = dp.Source.synthetic_images(1000, 32, 32)
+    g, _ = (dp.Dataset.tensor_slices(reg, src).shuffle(300, 1).map("crop").map("norm").repeat(3).batch(48)
+            .prefetch(depth).optimize())
+    key = ("base",)
+    if key not in _REF:
+        base = dp.make_iterator(g, seed_override=7)
+        _REF[key] = [(b.numpy(0), b.numpy(1)) for b in base]
+    # launch_batches 0: the default group, or (depth 8) 5 batches' bytes of max_launch_bytes
+    mlb = 5 * 48 * (24 * 24 * 3 * 4 + 8) if (launch_batches == 0 and depth == 8) else 0
+    got = []
+    it = dp.make_iterator(g, seed_override=7, max_launch_bytes=mlb, launch_batches=launch_batches)
+    if launch_batches:
+        assert it.stats()["group_batches"] == launch_batches
+    for b in it:
+        got.append((b.numpy(0), b.numpy(1)))
+        b.release()
+    ref = _REF[key]
+    assert len(got) == len(ref) == -(-3000 // 48)
+    for (i0, p0), (i1, p1) in zip(ref, got):
+        assert np.array_equal(i0, i1) and np.array_equal(p0.view(np.uint32), p1.view(np.uint32))
+
+
+_REF = {}

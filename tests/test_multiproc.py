@@ -61,3 +61,47 @@ def test_two_rank_shard_layout_timing_and_order_check(orc):
         ids = pos[orc.shuffle_order(pos.size, 300, orc.shuffle_seed(1, 42))]
         assert res["digests"][r] == f"{orc.order_digest(ids[:8 * 64]):016x}"
     assert res["digests"][0] != res["digests"][1]
+
+
+def test_bench_gpus_n_launches_n_ranks():
+    """`bench.py --gpus N` outside torchrun re-runs itself as N ranks
+    (torch.distributed.run, 127.0.0.1); rank 0 sees the whole group, the
+    max over ranks and every rank's digest, plus the golden order digests
+    of that world size."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--probe-launch",
+                          "--config", "cfg3"], capture_output=True, text=True, env=env, cwd=root, timeout=300)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
+    line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["ms_max"] == 2.0
+    assert line["per_rank"] == [f"{0:016x}", f"{1001:016x}"]
+    assert None not in line["expected"] and line["expected"][0] != line["expected"][1]
+
+
+def test_bench_rejects_world_size_mismatch():
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, WORLD_SIZE="2", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "4", "--probe-launch"],
+                         capture_output=True, text=True, env=env, cwd=root, timeout=120)
+    assert out.returncode != 0 and "WORLD_SIZE=2" in out.stderr
+
+
+def test_golden_order_check_table_matches_the_oracle(orc):
+    """tests/golden/order_check.json (what bench.py compares each rank's
+    device digest with) recomputed from the oracle for a sample of keys."""
+    import json
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path.insert(0, os.path.join(here, "golden"))
+    import make_order_check as m
+    table = json.load(open(os.path.join(here, "golden", "order_check.json")))["entries"]
+    for config, world, rank in [("cfg2", 1, 0), ("cfg3", 8, 5), ("cfg5", 4, 3), ("cfg1", 2, 1), ("cfg4", 1, 0),
+                                ("cfg4r", 2, 1), ("cfg4b", 1, 0)]:
+        n = m.SIZES[config]
+        assert table[f"{config}/n{n}/w{world}/r{rank}"] == f"{m.expected(orc, config, world, rank, n):016x}"

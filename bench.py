@@ -157,17 +157,31 @@ def expected_order_digest(config, n, world, rank):
         return None
 
 
-def launch_group_for(warmup, steps, default_group, batches_per_epoch):
-    """Largest launch group d <= default_group whose launch boundaries fall
-    on both ends of the timed window [warmup, warmup + steps): groups tile
-    each epoch from its start (the last one may be shorter), so the window
-    holds exactly `steps` batches."""
-    def on_boundary(x, d):
-        return (x % batches_per_epoch) % d == 0
-    for d in range(min(default_group, batches_per_epoch), 0, -1):
-        if on_boundary(warmup, d) and on_boundary(warmup + steps, d):
-            return d
-    return 1
+def group_boundary(x, d, head, batches_per_epoch):
+    """Is batch x the first batch of a launch group?  Groups of d batches tile
+    each epoch from its start; with a head, epoch 0's first group holds
+    `head` batches (IteratorOptions::first_launch_batches)."""
+    e, k = divmod(x, batches_per_epoch)
+    if k == 0:
+        return True
+    if e == 0 and head:
+        return k == head or (k > head and (k - head) % d == 0)
+    return k % d == 0
+
+
+def launch_tiling_for(warmup, steps, max_group, batches_per_epoch):
+    """(batches per launch, first-launch batches) with launch boundaries on
+    both ends of the timed window [warmup, warmup + steps), so the window
+    holds exactly `steps` batches: the largest group up to max_group, the
+    warm-up as a head group when that is what makes it fit."""
+    for d in range(min(max_group, batches_per_epoch), 0, -1):
+        for head in (0, warmup):
+            if head >= batches_per_epoch:
+                continue
+            if group_boundary(warmup, d, head, batches_per_epoch) and \
+                    group_boundary(warmup + steps, d, head, batches_per_epoch):
+                return d, head
+    return 1, 0
 
 
 def dist_env():
@@ -415,14 +429,18 @@ def run_ours(args, cfg):
     per_launch = int(re.search(r"(\d+) batch\(es\) per launch", desc).group(1))
     per_epoch = int(re.search(r"epoch: \d+ elements, (\d+) batches", desc).group(1))
     steps_requested, warmup_requested = args.steps, args.warmup
+    head_batches = 0
     if cfg["kind"] == "images":
         # exactly K timed and W warm-up steps: a launch group that tiles the
         # window (largest divisor-compatible group up to the default size)
-        group = launch_group_for(args.warmup, args.steps, per_launch, per_epoch)
-        if group != per_launch:
+        out_bytes = cfg["batch"] * (cfg["out_hw"][0] * cfg["out_hw"][1] * 3 * 4 + 8)
+        group, head = launch_tiling_for(args.warmup, args.steps, max(per_launch, (3200 << 20) // out_bytes),
+                                        per_epoch)
+        if (group, head) != (per_launch, 0):
             del it
-            it = dp.make_iterator(g, seed_override=1, device=local, launch_batches=group)
+            it = dp.make_iterator(g, seed_override=1, device=local, launch_batches=group, first_launch_batches=head)
             per_launch = group
+        head_batches = head
     else:
         # token / range configs launch a whole epoch of tiny batches at once:
         # the window is whole epochs (steps and warmup rounded up to them)
@@ -528,7 +546,8 @@ def run_ours(args, cfg):
         "data": "synthetic (device-generated, SplitMix64 / PCG32 keyed)",
         "config": config_dict(cfg, world),
         "lowering": {"optimized": "map_and_batch" in report or "map_batch_fusion" in report,
-                     "batches_per_launch": per_launch, "prefetch_depth": "AUTOTUNE"},
+                     "batches_per_launch": per_launch, "first_launch_batches": head_batches or per_launch,
+                     "prefetch_depth": "AUTOTUNE"},
         **({} if (steps_requested, warmup_requested) == (args.steps, args.warmup) else
            {"steps_requested": steps_requested, "warmup_requested": warmup_requested,
             "steps_note": "whole epochs of tiny batches (one launch per epoch)"}),

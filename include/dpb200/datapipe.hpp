@@ -328,6 +328,9 @@ struct IteratorOptions {
   // down to a power of two).  Launch groups never straddle an epoch of a
   // per-epoch batch stage, so the last group of an epoch may be shorter.
   int64_t launch_batches = 0;
+  // Batches of the stream's first launch group only (0 = launch_batches);
+  // the groups after it tile the stream (or epoch 0) from there.
+  int64_t first_launch_batches = 0;
 };
 
 struct NodeMetricsRow {

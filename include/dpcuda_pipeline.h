@@ -172,6 +172,7 @@ typedef struct {
   uint64_t slot_memory_budget;/* bytes of device prefetch slots (0: default 8 GiB) */
   uint64_t max_launch_bytes;  /* output bytes per fused launch (0: default) */
   int64_t launch_batches;     /* batches per fused launch, exactly (0: from max_launch_bytes) */
+  int64_t first_launch_batches; /* batches of the first launch only (0: launch_batches) */
 } dp_iterator_options;
 
 typedef enum { DP_U8 = 0, DP_I32 = 1, DP_I64 = 2, DP_F32 = 3 } dp_dtype;

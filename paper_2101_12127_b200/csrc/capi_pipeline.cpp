@@ -366,6 +366,7 @@ int dp_iterator_create(const dp_graph* g, const dp_registry* reg, const dp_itera
       if (opt->slot_memory_budget) o.slot_memory_budget = opt->slot_memory_budget;
       o.max_launch_bytes = opt->max_launch_bytes;
       o.launch_batches = opt->launch_batches;
+      o.first_launch_batches = opt->first_launch_batches;
     }
     *out = new dp_iterator{MakeIterator(g->g, reg->reg, o)};
   });
@@ -439,6 +440,7 @@ int dp_iterator_restore(const dp_graph* g, const dp_registry* reg, const void* b
       if (opt->slot_memory_budget) o.slot_memory_budget = opt->slot_memory_budget;
       o.max_launch_bytes = opt->max_launch_bytes;
       o.launch_batches = opt->launch_batches;
+      o.first_launch_batches = opt->first_launch_batches;
     }
     std::string b(static_cast<const char*>(blob), len);
     *out = new dp_iterator{Restore(g->g, reg->reg, b, o)};

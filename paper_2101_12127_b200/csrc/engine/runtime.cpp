@@ -80,6 +80,7 @@ struct EpochPlan {
   std::shared_ptr<void> bstart_dev, rows_dev, roff_dev;
   std::shared_ptr<void> row_src_dev, row_dst_dev, row_lm_dev;  // per emitted row (dp_k_bucket_rows)
   cudaEvent_t ready = nullptr;
+  int64_t ready_gen = 0;  // bumped whenever `ready` is recorded again (a head appended)
 };
 
 struct Slot {
@@ -122,7 +123,7 @@ class DevicePipeline {
     // the persistent kernel's ramp-up / drain), at most one epoch of batches
     // Per-launch fixed costs (kernel ramp-up, tail imbalance, launch gap)
     // are ~10% of a 150 MB batch; 16 cfg2 batches per launch put the batch
-    // stage at the HBM roofline (tools/groupsweep.py).  Pinned host slots
+    // stage at the HBM roofline (tools/dev/groupsweep.py).  Pinned host slots
     // (host_output) are kept smaller.
     size_t target = opt_.max_launch_bytes ? opt_.max_launch_bytes
                                           : (opt_.host_output ? size_t(512) << 20 : size_t(3200) << 20);
@@ -142,6 +143,9 @@ class DevicePipeline {
     depth_ = std::max<int64_t>(2, std::min<int64_t>(depth_, static_cast<int64_t>(opt_.slot_memory_budget /
                                                                                  std::max<size_t>(group_bytes, 1))));
     if (span_epochs_) group_ = std::min<int64_t>(group_, std::max<int64_t>(1, epoch_count_ / std::max<int64_t>(L_.batch, 1)));
+    // a first launch group of another size (then groups of group_ again)
+    head_ = opt_.first_launch_batches;
+    if (head_ <= 0 || head_ == group_ || (span_epochs_ ? head_ > group_ : head_ >= batches_per_epoch_)) head_ = 0;
     if (group_ > 1) {  // epoch 0 was planned with a one-group tail: re-plan lazily
       for (auto& [e, p] : plans_)
         if (p.ready) cudaEventDestroy(p.ready);
@@ -363,11 +367,28 @@ class DevicePipeline {
     return n;
   }
 
+  // Groups tile the batch stream (spanning epochs) or each epoch from its
+  // start; with a head (IteratorOptions::first_launch_batches) the first
+  // group of the stream holds head_ batches and the tiling restarts after it.
+  int64_t SegGroups(int64_t batches, int64_t head) const {
+    if (batches <= 0) return 0;
+    return head ? 1 + (batches - head + group_ - 1) / group_ : (batches + group_ - 1) / group_;
+  }
+  int64_t GroupInSeg(int64_t k, int64_t head) const {
+    return head ? (k < head ? 0 : 1 + (k - head) / group_) : k / group_;
+  }
+  std::pair<int64_t, int64_t> SegRange(int64_t grp, int64_t head) const {  // (first, n) within the segment
+    if (!head) return {grp * group_, group_};
+    if (grp == 0) return {0, head};
+    return {head + (grp - 1) * group_, group_};
+  }
+
   int64_t GroupOf(int64_t i) const {
-    if (span_epochs_) return i / group_;
+    if (span_epochs_) return GroupInSeg(i, head_);
     const int64_t bpe = std::max<int64_t>(batches_per_epoch_, 1);
-    const int64_t gpe = (bpe + group_ - 1) / group_;
-    return (i / bpe) * gpe + (i % bpe) / group_;
+    const int64_t e = i / bpe, k = i % bpe;
+    if (e == 0) return GroupInSeg(k, head_);
+    return SegGroups(bpe, head_) + (e - 1) * SegGroups(bpe, 0) + k / group_;
   }
 
  public:
@@ -390,16 +411,21 @@ class DevicePipeline {
  private:
   std::pair<int64_t, int64_t> GroupRange(int64_t g) const {
     if (span_epochs_) {
-      int64_t first = g * group_;
-      int64_t n = group_;
+      auto [first, n] = SegRange(g, head_);
       if (total_batches_ >= 0) n = std::min(n, total_batches_ - first);
       return {first, std::max<int64_t>(n, 0)};
     }
-    const int64_t gpe = (batches_per_epoch_ + group_ - 1) / group_;
+    const int64_t bpe = batches_per_epoch_;
+    const int64_t gpe0 = SegGroups(bpe, head_), gpe = SegGroups(bpe, 0);
     if (gpe == 0) return {0, 0};
-    const int64_t e = g / gpe, k = g % gpe;
-    int64_t first = e * batches_per_epoch_ + k * group_;
-    int64_t n = std::min(group_, batches_per_epoch_ - k * group_);
+    int64_t e = 0, k = g;
+    if (g >= gpe0) {
+      e = 1 + (g - gpe0) / gpe;
+      k = (g - gpe0) % gpe;
+    }
+    auto [off, n] = SegRange(k, e == 0 ? head_ : 0);
+    const int64_t first = e * bpe + off;
+    n = std::min(n, bpe - off);
     if (total_batches_ >= 0 && first >= total_batches_) n = 0;
     return {first, n};
   }
@@ -585,6 +611,7 @@ class DevicePipeline {
     }
     CudaCheck(cudaEventCreateWithFlags(&p.ready, cudaEventDisableTiming), "event");
     CudaCheck(cudaEventRecord(p.ready, s), "event");
+    p.ready_gen = 1;
   }
 
   // Interleave over record files of unequal sizes: the host schedules the
@@ -749,6 +776,7 @@ class DevicePipeline {
                                   cudaMemcpyDeviceToDevice, plan_stream_),
                   "append head");
         CudaCheck(cudaEventRecord(p.ready, plan_stream_), "event");
+        p.ready_gen++;
         appended_.insert(e0 * 1000003 + e);
       }
     }
@@ -773,8 +801,9 @@ class DevicePipeline {
   std::shared_ptr<Slot> NewSlot() {
     auto slot = std::make_shared<Slot>();
     slot->device = opt_.device;
-    slot->a_bytes = batch_bytes_.first * group_;
-    slot->b_bytes = batch_bytes_.second * group_;
+    const int64_t cap = std::max(group_, head_);  // batches a slot holds (the head group may be larger)
+    slot->a_bytes = batch_bytes_.first * cap;
+    slot->b_bytes = batch_bytes_.second * cap;
     slot->a = DeviceAlloc(slot->a_bytes, opt_.device);
     if (slot->b_bytes) slot->b = DeviceAlloc(slot->b_bytes, opt_.device);
     if (opt_.host_output) {
@@ -800,7 +829,7 @@ class DevicePipeline {
       std::lock_guard lk(shared_->mu);
       if (!s->busy || s->release_recorded) return s;
     }
-    const size_t need = (batch_bytes_.first + batch_bytes_.second) * group_;
+    const size_t need = (batch_bytes_.first + batch_bytes_.second) * std::max(group_, head_);
     if (static_cast<int64_t>(slots_.size()) < depth_ || may_grow) {
       if (slot_bytes_total_ + need > opt_.slot_memory_budget && !slots_.empty())
         throw PipelineError(ErrorCode::kInternal,
@@ -826,7 +855,14 @@ class DevicePipeline {
     const auto t0 = std::chrono::steady_clock::now();
     {
       std::lock_guard lk(shared_->mu);
-      if (slot->busy && slot->release_recorded) CudaCheck(cudaStreamWaitEvent(stream_, slot->release, 0), "wait release");
+      if (slot->busy) {
+        // host_output: the previous D2H copy out of this slot (copy stream)
+        if (opt_.host_output) CudaCheck(cudaStreamWaitEvent(stream_, slot->ready, 0), "wait copy");
+        // consumer-stream work queued before the last drop; a release
+        // recorded on this very stream is already ordered before the launch
+        if (slot->release_recorded && consumer_ != stream_)
+          CudaCheck(cudaStreamWaitEvent(stream_, slot->release, 0), "wait release");
+      }
       slot->busy = true;
       slot->release_recorded = false;
       slot->first_batch = first;
@@ -841,7 +877,10 @@ class DevicePipeline {
     const int64_t epoch = span_epochs_ ? (epoch_count_ ? first * L_.batch / epoch_count_ : 0)
                                        : first / std::max<int64_t>(batches_per_epoch_, 1);
     EpochPlan& plan = Plan(epoch);
-    CudaCheck(cudaStreamWaitEvent(stream_, plan.ready, 0), "wait plan");
+    if (waited_plan_ != std::make_pair(epoch, plan.ready_gen)) {  // once per plan (re)record
+      CudaCheck(cudaStreamWaitEvent(stream_, plan.ready, 0), "wait plan");
+      waited_plan_ = {epoch, plan.ready_gen};
+    }
     // Plan the next epoch on the side stream now, so its index kernels
     // overlap this epoch's batch kernels instead of stalling the next one.
     if (MoreEpochsAfter(epoch)) {
@@ -1227,10 +1266,12 @@ class DevicePipeline {
   std::pair<size_t, size_t> batch_bytes_;
   int64_t max_len_ = 0;
   int64_t group_ = 1;
+  int64_t head_ = 0;  // batches of the stream's first launch group (0: group_)
   bool span_epochs_ = false;
   int64_t epoch_count_ = 0, batches_per_epoch_ = 0, total_batches_ = 0, total_groups_ = -1;
   int64_t total_units_ = 0;  // unbatched: elements (-1 = infinite)
   std::map<int64_t, EpochPlan> plans_;
+  std::pair<int64_t, int64_t> waited_plan_{-1, -1};  // (epoch, ready_gen) the batch stream last waited on
   cudaEvent_t retire_ev_ = nullptr;
   int64_t batches_launched_ = 0;
   std::set<int64_t> appended_;

@@ -27,7 +27,7 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kCropBandRows = 16;
 constexpr int kResizeBandRows = 16;
-constexpr int kFastCropBandRows = 16;   // tools/ksweep.py: 16 rows x 8 stages best on B200
+constexpr int kFastCropBandRows = 16;   // tools/dev/ksweep.py: 16 rows x 8 stages best on B200
 constexpr int kFastResizeBandRows = 16;
 constexpr int kCropStages = 8;
 constexpr int kResizeStages = 4;
@@ -657,6 +657,10 @@ bool periodic_ok(int in_w, int out_w) {
 
 template <class Op>
 __global__ void __launch_bounds__(Op::kConsumers + 32, 1) pipeline_kernel(FastArgs a) {
+  // The next launch on the stream (the next launch group, another slot) may
+  // start as SMs free up: it reads only the read-only dataset and plan and
+  // writes a different slot (programmatic dependent launch).
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t full[kMaxStages], empty[kMaxStages];
   __shared__ StageMeta meta[kMaxStages];
@@ -730,6 +734,8 @@ int sm_count() {
   return n;
 }
 
+int env_int(const char* name, int fallback);
+
 template <typename K>
 int launch_persistent(K kernel, const FastArgs& a, size_t smem, cudaStream_t s, const char* what) {
   // cudaFuncSetAttribute / the occupancy query are host-synchronous-ish and
@@ -774,6 +780,20 @@ int launch_persistent(K kernel, const FastArgs& a, size_t smem, cudaStream_t s, 
   if (per_sm < 1) return fail(DP_ERR_INVALID_ATTR, std::string(what) + ": kernel does not fit on an SM");
   const int64_t items = a.rows * a.bands;
   const int64_t grid = std::min<int64_t>(items, static_cast<int64_t>(per_sm) * sm_count());
+  static const int pdl = env_int("DP_DEV_PDL", 0);
+  if (pdl) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid));
+    cfg.blockDim = dim3(static_cast<unsigned>(threads));
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cuda_status(cudaLaunchKernelEx(&cfg, kernel, a), what);
+  }
   kernel<<<static_cast<int>(grid), threads, smem, s>>>(a);
   return launch_status(what);
 }
@@ -798,7 +818,7 @@ bool fast_ok(const uint8_t* images, int in_w, int out_w, const float* out) {
          in_device_memory(images);
 }
 
-// Development-only overrides for tuning sweeps (tools/kbench.py).
+// Development-only overrides for tuning sweeps (tools/dev/kbench.py).
 int env_int(const char* name, int fallback) {
   const char* v = std::getenv(name);
   return v && *v ? std::atoi(v) : fallback;

@@ -44,7 +44,8 @@ class dp_batch(ctypes.Structure):
 class dp_iterator_options(ctypes.Structure):
     _fields_ = [("deterministic", c_int), ("has_seed_override", c_int), ("seed_override", c_u64), ("device", c_int),
                 ("consumer_stream", c_vp), ("host_output", c_int), ("slot_memory_budget", c_u64),
-                ("max_launch_bytes", c_u64), ("launch_batches", c_i64)]
+                ("max_launch_bytes", c_u64), ("launch_batches", c_i64),
+                ("first_launch_batches", c_i64)]
 
 
 class dp_iterator_stats(ctypes.Structure):
@@ -600,20 +601,24 @@ class Iterator:
         return buf.value.decode()
 
 
-def restore(ds: Dataset, blob: bytes, device=0, consumer_stream=None, host_output=False):
+def restore(ds: Dataset, blob: bytes, device=0, consumer_stream=None, host_output=False, launch_batches=0,
+            first_launch_batches=0):
     """Restore(graph, registry, blob) (checkpoint.hpp:44-49): seeks, never replays."""
     o = dp_iterator_options()
     L().dp_iterator_options_default(ctypes.byref(o))
     o.device = device
     o.consumer_stream = consumer_stream
     o.host_output = int(host_output)
+    o.launch_batches = launch_batches
+    o.first_launch_batches = first_launch_batches
     out = c_vp()
     _check(L().dp_iterator_restore(ds.h, ds.reg.h, blob, len(blob), ctypes.byref(o), ctypes.byref(out)))
     return Iterator(out, ds)
 
 
 def make_iterator(ds: Dataset, seed_override=None, device=0, consumer_stream=None, host_output=False,
-                  slot_memory_budget=0, deterministic=True, max_launch_bytes=0, launch_batches=0):
+                  slot_memory_budget=0, deterministic=True, max_launch_bytes=0, launch_batches=0,
+                  first_launch_batches=0):
     """MakeIterator(graph, registry, IteratorOptions) (runtime.hpp:98-100)."""
     o = dp_iterator_options()
     L().dp_iterator_options_default(ctypes.byref(o))
@@ -627,6 +632,7 @@ def make_iterator(ds: Dataset, seed_override=None, device=0, consumer_stream=Non
     o.slot_memory_budget = slot_memory_budget
     o.max_launch_bytes = max_launch_bytes
     o.launch_batches = launch_batches
+    o.first_launch_batches = first_launch_batches
     out = c_vp()
     _check(L().dp_iterator_create(ds.h, ds.reg.h, ctypes.byref(o), ctypes.byref(out)))
     return Iterator(out, ds)

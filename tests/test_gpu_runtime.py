@@ -140,3 +140,33 @@ def test_output_independent_of_prefetch_and_launch_group(dp, depth, launch_batch
 
 
 _REF = {}
+
+
+@pytest.mark.parametrize("span", [False, True])
+@pytest.mark.parametrize("tiling", [(4, 3), (5, 1), (2, 7)])
+def test_output_independent_of_a_first_launch_head(dp, span, tiling):
+    """IteratorOptions::first_launch_batches (the bench's exact-window
+    tiling): a first launch of another size, then groups of launch_batches,
+    per-epoch (batch -> repeat) and spanning (repeat -> batch) stages; also
+    a checkpoint seek into the tiled stream."""
+    reg = dp.Registry()
+    reg.register_random_crop_flip("crop", 16, 16, seed=2, flip=True)
+    reg.register_normalize("norm")
+    src = dp.Source.synthetic_images(700, 20, 20)
+    g = dp.Dataset.tensor_slices(reg, src).shuffle(200, 4).map("crop").map("norm")
+    g = g.repeat(3).batch(32) if span else g.batch(32).repeat(3)
+    g, _ = g.prefetch(-1).optimize()
+    ref = [(b.numpy(0), b.numpy(1)) for b in dp.make_iterator(g, seed_override=3)]
+    lb, head = tiling
+    it = dp.make_iterator(g, seed_override=3, launch_batches=lb, first_launch_batches=head)
+    got = [(b.numpy(0), b.numpy(1)) for b in it]
+    assert len(got) == len(ref)
+    for (i0, p0), (i1, p1) in zip(ref, got):
+        assert np.array_equal(i0, i1) and np.array_equal(p0.view(np.uint32), p1.view(np.uint32))
+    it = dp.make_iterator(g, seed_override=3, launch_batches=lb, first_launch_batches=head)
+    for _ in range(11):
+        it.get_next().release()
+    rest = [(b.numpy(0), b.numpy(1)) for b in dp.restore(g, it.save(), launch_batches=lb, first_launch_batches=head)]
+    assert len(rest) == len(ref) - 11
+    for (i0, p0), (i1, p1) in zip(ref[11:], rest):
+        assert np.array_equal(i0, i1) and np.array_equal(p0.view(np.uint32), p1.view(np.uint32))

@@ -105,3 +105,29 @@ def test_golden_order_check_table_matches_the_oracle(orc):
                                 ("cfg4r", 2, 1), ("cfg4b", 1, 0)]:
         n = m.SIZES[config]
         assert table[f"{config}/n{n}/w{world}/r{rank}"] == f"{m.expected(orc, config, world, rank, n):016x}"
+
+
+def test_bench_launch_tiling_puts_the_window_on_group_boundaries():
+    """bench.py honours --steps/--warmup exactly: the chosen tiling has launch
+    boundaries at both ends of the timed window (simulated group starts,
+    same rule as DevicePipeline::GroupRange)."""
+    import bench
+
+    def starts(d, head, bpe, upto):
+        out, e = set(), 0
+        while e * bpe <= upto:
+            k = 0
+            while k < bpe:
+                out.add(e * bpe + k)
+                k += head if (e == 0 and head and k == 0) else d
+            e += 1
+        return out
+
+    for w, k, gmax, bpe in [(5, 20, 21, 256), (32, 512, 21, 256), (3, 7, 16, 256), (16, 16, 16, 256), (5, 300, 21, 256),
+                            (7, 1000, 21, 100), (4, 4, 1, 10)]:
+        d, head = bench.launch_tiling_for(w, k, gmax, bpe)
+        st = starts(d, head, bpe, w + k + bpe)
+        assert w in st and (w + k) in st, (w, k, d, head)
+        assert 1 <= d <= gmax
+    assert bench.launch_tiling_for(5, 20, 21, 256) == (20, 5)
+    assert bench.launch_tiling_for(32, 512, 21, 256) == (16, 0)

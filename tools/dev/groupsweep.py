@@ -1,5 +1,5 @@
 import sys, os, time, ctypes
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import torch
 from paper_2101_12127_b200 import pipeline as dp
 src = dp.Source.synthetic_images(65536, 256, 256)

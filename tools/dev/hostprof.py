@@ -1,6 +1,6 @@
 """Host-side cost of GetNext through the Python/ctypes binding vs device time."""
 import sys, os, time
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import torch
 from paper_2101_12127_b200 import pipeline as dp
 import bench

@@ -1,7 +1,7 @@
 """Kernel micro-timings (CUDA events on the launch stream) -- development aid."""
 import ctypes, json, sys, time
 import torch
-sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__))))
+sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__)))))
 from paper_2101_12127_b200 import _capi as K
 
 MEAN = (123.675, 116.28, 103.53); STD = (58.395, 57.12, 57.375)

@@ -1,7 +1,7 @@
 """Runs one kernel family a few times on cfg-sized inputs (for ncu captures)."""
 import ctypes, sys, os
 import torch
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 from paper_2101_12127_b200 import _capi as K
 MEAN = (123.675, 116.28, 103.53); STD = (58.395, 57.12, 57.375)
 vp = lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None

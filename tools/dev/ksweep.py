@@ -1,8 +1,8 @@
 """Tuning sweep for the K3/K4 fast path (stages x band rows), CUDA events.
-    python tools/ksweep.py k3|k4|k4p STAGES,.. BANDS,..   (k4p: periodic-tap K4)"""
+    python tools/dev/ksweep.py k3|k4|k4p STAGES,.. BANDS,..   (k4p: periodic-tap K4)"""
 import ctypes, json, os, sys
 import torch
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 from paper_2101_12127_b200 import _capi as K
 MEAN = (123.675, 116.28, 103.53); STD = (58.395, 57.12, 57.375)
 vp = lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None

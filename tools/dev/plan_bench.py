@@ -1,6 +1,6 @@
 """K2 shuffle_plan timing: device-wide plan vs single-warp kernel (CUDA events)."""
 import ctypes, os, sys
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import torch
 from paper_2101_12127_b200 import _capi as K
 L = K.lib(); s = torch.cuda.current_stream(); S = ctypes.c_void_p(s.cuda_stream)

@@ -130,6 +130,35 @@ uint64_t orc_interleave_var(uint64_t m_inputs, const uint64_t* inputs,
                             uint64_t cycle, const uint64_t* lengths,
                             const uint64_t* starts, uint64_t* out);
 
+/* ---- image map UDF chain (oracle/chain.c): each step a MapFn on the whole
+ * element, applied in order; u8 stays u8 through crops, resize / normalize /
+ * affine / cast make fp32. ---- */
+enum {
+  ORC_STEP_RANDOM_CROP = 1, /* h, w, seed, flip: Philox offsets (orc_crop_params) */
+  ORC_STEP_CENTER_CROP = 2, /* h, w: offsets ((H - h) / 2, (W - w) / 2), no flip */
+  ORC_STEP_RESIZE = 3,      /* h, w: bilinear, half-pixel centres (orc_resize) */
+  ORC_STEP_NORMALIZE = 4,   /* a = mean[3], b = std[3]: (x - a_c) / b_c */
+  ORC_STEP_AFFINE = 5,      /* a = scale[3], b = shift[3]: x * a_c + b_c */
+  ORC_STEP_CAST = 6         /* u8 -> fp32, exact */
+};
+typedef struct {
+  int op, h, w, flip;
+  uint64_t seed;
+  float a[3], b[3];
+} orc_map_step;
+/* output dims / dtype of a chain over an in_h x in_w x 3 u8 image; -1 if invalid */
+int orc_chain_output(const orc_map_step* steps, int nsteps, int in_h, int in_w, int* out_h, int* out_w,
+                     int* out_f32);
+/* element (id, img) through the chain; out holds the result (u8 or fp32) */
+int orc_apply_chain(const uint8_t* img, int in_h, int in_w, int64_t id, const orc_map_step* steps, int nsteps,
+                    void* out);
+/* Whole-epoch output digest: images ids[0..n) (synthetic pixels, seed
+ * pix_seed) through the chain, output k's little-endian u32 words w hashed
+ * at position k * words + w with K7's position hash and summed mod 2^64
+ * (the device's dp_k_word_digest over the epoch's batches). */
+uint64_t orc_epoch_image_digest(const orc_map_step* steps, int nsteps, uint64_t pix_seed, const int64_t* ids,
+                                int64_t n, int in_h, int in_w, int threads, int* err);
+
 #ifdef __cplusplus
 }
 #endif

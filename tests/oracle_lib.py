@@ -29,6 +29,31 @@ PIX_SEED = 0x5EED
 UDF_SEED = 7
 
 
+class orc_map_step(ctypes.Structure):
+    _fields_ = [("op", c_int), ("h", c_int), ("w", c_int), ("flip", c_int), ("seed", u64),
+                ("a", ctypes.c_float * 3), ("b", ctypes.c_float * 3)]
+
+
+STEP = {"random_crop": 1, "center_crop": 2, "resize": 3, "normalize": 4, "affine": 5, "cast": 6}
+
+
+def steps_array(steps):
+    """[("random_crop", h, w, seed, flip) | ("center_crop", h, w) | ("resize", h, w) |
+    ("normalize", mean3, std3) | ("affine", scale3, shift3) | ("cast",)] -> orc_map_step[]"""
+    arr = (orc_map_step * max(len(steps), 1))()
+    for i, st in enumerate(steps):
+        o = arr[i]
+        o.op = STEP[st[0]]
+        if st[0] in ("random_crop", "center_crop", "resize"):
+            o.h, o.w = st[1], st[2]
+        if st[0] == "random_crop":
+            o.seed, o.flip = st[3], int(st[4])
+        if st[0] in ("normalize", "affine"):
+            o.a[:] = [float(x) for x in st[1]]
+            o.b[:] = [float(x) for x in st[2]]
+    return arr
+
+
 def P(a: np.ndarray):
     assert a.flags["C_CONTIGUOUS"]
     return a.ctypes.data_as(vp)
@@ -58,6 +83,9 @@ class Oracle:
             "orc_bucket_by_length": (i64, [vp, vp, i64, vp, c_int, vp, c_int, vp, vp]),
             "orc_shard_positions": (u64, [u64, u64, u64, vp]),
             "orc_interleave_order": (u64, [u64, vp, u64, u64, vp]),
+            "orc_chain_output": (c_int, [vp, c_int, c_int, c_int, vp, vp, vp]),
+            "orc_apply_chain": (c_int, [vp, c_int, c_int, i64, vp, c_int, vp]),
+            "orc_epoch_image_digest": (u64, [vp, c_int, u64, vp, i64, c_int, c_int, c_int, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -147,6 +175,34 @@ class Oracle:
         out = np.zeros((out_h, out_w, 3), np.float32)
         self.L.orc_resize_normalize(P(img), img.shape[0], img.shape[1], out_h, out_w, P(out))
         return out
+
+    def chain_output(self, steps, in_h, in_w):
+        """(out_h, out_w, np dtype) of an image map chain (oracle/chain.c)."""
+        h, w, f = c_int(), c_int(), c_int()
+        arr = steps_array(steps)
+        if self.L.orc_chain_output(arr, len(steps), in_h, in_w, ctypes.byref(h), ctypes.byref(w), ctypes.byref(f)):
+            raise ValueError("invalid chain")
+        return h.value, w.value, (np.float32 if f.value else np.uint8)
+
+    def chain(self, img, ident, steps):
+        """One element (id, img) through the image map chain, as MapFns in order."""
+        img = np.ascontiguousarray(img, np.uint8)
+        oh, ow, dt = self.chain_output(steps, img.shape[0], img.shape[1])
+        out = np.zeros((oh, ow, 3), dt)
+        if self.L.orc_apply_chain(P(img), img.shape[0], img.shape[1], ident, steps_array(steps), len(steps), P(out)):
+            raise ValueError("chain failed")
+        return out
+
+    def epoch_image_digest(self, steps, ids, in_h, in_w, threads=None, seed=PIX_SEED):
+        """K7 word digest of every output image of `ids` through the chain
+        (position = running u32 word index across the epoch)."""
+        ids = np.ascontiguousarray(ids, np.int64)
+        err = c_int()
+        d = self.L.orc_epoch_image_digest(steps_array(steps), len(steps), seed, P(ids), ids.size, in_h, in_w,
+                                          threads or os.cpu_count() or 1, ctypes.byref(err))
+        if err.value:
+            raise ValueError("chain failed")
+        return d
 
     # ---- filter / shard / interleave ----
     def filter_len_le(self, lengths, max_keep):

@@ -313,3 +313,24 @@ def test_interleave_schedule_closed_form(orc):
                 pos = int(np.minimum(end, r).sum()) + int(((np.arange(c) < slot[i]) & (end > r)).sum())
                 out[pos] = first[i] + j
         assert out.tolist() == orc.interleave_var(np.arange(m), c, lens).tolist(), (lens.tolist(), c)
+
+
+def test_chain_restatement_equals_the_fused_restatements_and_digest(orc):
+    """oracle/chain.c (each UDF a MapFn on the whole element, in order) equals
+    the fused crop+flip+normalize / resize+normalize restatements, and its
+    epoch digest equals K7's position hash over the chained outputs."""
+    from tests.oracle_lib import MEAN, STD, Oracle
+    for ident in (0, 5, 77, 1 << 33):
+        img = orc.images(ident, 1, 256, 256)[0]
+        a = orc.chain(img, ident, [("random_crop", 224, 224, 7, True), ("normalize", MEAN, STD)])
+        assert np.array_equal(a.view(np.uint32), orc.crop_flip_normalize(img, ident).view(np.uint32))
+        img = orc.images(ident, 1, 320, 320)[0]
+        a = orc.chain(img, ident, [("resize", 224, 224), ("normalize", MEAN, STD)])
+        assert np.array_equal(a.view(np.uint32), orc.resize_normalize(img).view(np.uint32))
+        a = orc.chain(img, ident, [("resize", 200, 150)])
+        assert np.array_equal(a.view(np.uint32), orc.resize(img, 200, 150).view(np.uint32))
+    ids = np.array([3, 1, 4, 1, 5, 9, 2, 6], np.int64)
+    steps = [("random_crop", 24, 20, 7, True), ("normalize", MEAN, STD)]
+    outs = np.concatenate([orc.chain(orc.images(int(i), 1, 32, 40)[0], int(i), steps).reshape(-1).view(np.uint32)
+                           for i in ids])
+    assert orc.epoch_image_digest(steps, ids, 32, 40, threads=3) == Oracle.order_digest(outs)

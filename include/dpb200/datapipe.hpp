@@ -82,6 +82,10 @@ struct SourceData {
   // x = (r / R) * shard_count + shard_index; the graph applies
   // shard(shard_count, shard_index) to the interleave's inputs.
   int64_t global_count = 0, shard_count = 1, shard_index = 0, shard_block = 1;
+  // kImages: an int64 label per held row (the element is then (int64 id,
+  // image, int64 label), FromMemory's tuple elements, element.hpp:30-184);
+  // same residency as the images
+  std::shared_ptr<void> labels;
 };
 using SourcePtr = std::shared_ptr<const SourceData>;
 
@@ -101,6 +105,9 @@ SourcePtr SynthRecordsSharded(int64_t num_files, int64_t records_per_file, int64
 // consecutive positions (block 1 = element shards; block R = the files of an
 // interleave's shard).  kInvalidAttr unless s->count is that shard's size.
 SourcePtr AsShard(const SourcePtr& s, int64_t global_count, int64_t num_shards, int64_t index, int64_t block = 1);
+// A view of image source `s` carrying an int64 label per held row (copied to
+// the device, or to pinned host memory when `s` is host resident).
+SourcePtr WithLabels(const SourcePtr& s, const int64_t* labels, int64_t count);
 SourcePtr SynthTokens(int64_t count, uint32_t max_len, uint64_t len_seed, uint64_t tok_seed, int device = 0);
 // Uploads host data (copied); images: u8 [count, h, w, 3].
 SourcePtr ImagesFromHost(const uint8_t* data, int64_t count, int64_t h, int64_t w, int device = 0);
@@ -170,12 +177,15 @@ class DatasetGraph {
 struct MapStep {
   // kDecodeRaw: a from_file record (bytes) holding a raw uint8 HWC image of
   // out_h x out_w x 3 -> (int64 record ordinal, tensor u8[out_h, out_w, 3])
-  enum class Op { kAffine, kRandomCropFlip, kResizeBilinear, kNormalize, kDecodeRaw } op;
+  // kCenterCrop: out_h x out_w window at ((H - out_h) / 2, (W - out_w) / 2)
+  // kImageAffine: fp32 x * scale_c + shift_c per channel (two rounded ops)
+  enum class Op { kAffine, kRandomCropFlip, kResizeBilinear, kNormalize, kDecodeRaw, kCenterCrop, kImageAffine } op;
   int64_t a = 1, b = 0;                 // affine
   int64_t out_h = 0, out_w = 0;         // crop / resize
   uint64_t seed = 0;                    // crop: Philox key
   bool flip = true;                     // crop: random horizontal flip
   std::array<float, 3> mean{}, stdv{};  // normalize
+  std::array<float, 3> scale{}, shift{};  // image affine
 };
 
 // Device predicate for Filter: a conjunction of terms on one quantity of
@@ -220,6 +230,10 @@ class UdfRegistry {
   // (x - 0) / 1 is x exactly under the kernels' IEEE-exact normalize
   void RegisterCast(const std::string& name);
   void RegisterDecodeRaw(const std::string& name, int64_t h, int64_t w);
+  // center crop (no randomness, no flip), dtype preserved
+  void RegisterCenterCrop(const std::string& name, int64_t crop_h, int64_t crop_w);
+  // per-channel x * scale_c + shift_c on an image (u8 or fp32) -> fp32
+  void RegisterImageAffine(const std::string& name, std::array<float, 3> scale, std::array<float, 3> shift);
   void RegisterLengthFilter(const std::string& name, int64_t max_len);  // keep len <= max_len
   void RegisterValueFilter(const std::string& name, std::vector<PredicateTerm> terms);
   // keep_even / keep_odd / keep_all on int64 elements (the reference's

@@ -289,6 +289,42 @@ int dp_k_shard_index(int64_t n, int64_t num_shards, int64_t shard_index,
                      const int64_t* in_map, int64_t* out, void* stream);
 
 /* ---------------------------------------------------------------------- */
+/* ---------------------------------------------------------------------- */
+/* K9  general image map chain + Batch (MapAndBatchIterator, src/runtime.  */
+/*     cpp:1467-1721, over the device UDF library's chains that K3 / K4 do  */
+/*     not cover): [crop A][pixel ops][resize][crop B][pixel ops], each    */
+/*     value from its source taps with the sequential chain's rounded fp32 */
+/*     ops (oracle/chain.c).  Crop modes: 0 none, 1 random (Philox key =   */
+/*     seed, counter = element id; flip bit used when *_flip), 2 center.   */
+/*     Pixel ops (op_kind): 0 normalize (x - a_c) / b_c, 1 affine          */
+/*     x * a_c + b_c; the first num_pre_ops act on source taps (before the */
+/*     resize), the next num_post_ops on the blend.  out_f32 = resize or   */
+/*     any op (else u8 output: crops only).                                */
+typedef struct {
+  int in_h, in_w;
+  int pre_mode, pre_h, pre_w, pre_flip;
+  uint64_t pre_seed;
+  int resize, rs_h, rs_w;
+  int post_mode, post_h, post_w, post_flip;
+  uint64_t post_seed;
+  int num_pre_ops, num_post_ops;
+  int op_kind[4];
+  float op_a[4][3], op_b[4][3];
+  int out_f32;
+} dp_image_chain;
+/* Output shape / dtype of a chain (validates it). */
+int dp_image_chain_output(const dp_image_chain* chain, int* out_h, int* out_w, int* out_f32);
+/* out[j] = chain(images[p_j]), p_j = order ? order[first + j] : first + j;
+ * out_ids[j] = the element id of p_j (sharded residency as K3's _ex). */
+int dp_k_image_chain_batch(const uint8_t* images, int64_t num_images, const int64_t* order, int64_t first,
+                           int64_t rows, int64_t id_base, int64_t id_stride, int64_t id_block,
+                           const dp_image_chain* chain, int64_t* out_ids, void* out, void* stream);
+/* Batch with no map (BatchIterator over (id, u8 image), runtime.cpp:579-
+ * 637): out[j] = images[p_j] byte for byte (image_bytes each). */
+int dp_k_gather_copy_batch(const uint8_t* images, int64_t num_images, int64_t image_bytes, const int64_t* order,
+                           int64_t first, int64_t rows, int64_t id_base, int64_t id_stride, int64_t id_block,
+                           int64_t* out_ids, uint8_t* out, void* stream);
+
 /* K7  order digest (the multi-GPU "final ordering check") */
 /*     position-keyed, parallel: D = sum_i SplitMix64Next(v_i ^ (i *      */
 /*     0x9e3779b97f4a7c15)) mod 2^64 (state passed by value).  Accumulates */

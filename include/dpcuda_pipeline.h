@@ -43,6 +43,10 @@ int dp_registry_register_resize_bilinear(dp_registry* reg, const char* name, int
 int dp_registry_register_normalize(dp_registry* reg, const char* name, const float mean[3], const float stdv[3]);
 /* cast u8 -> fp32 (the north star's Map library "cast"): exact, = normalize(mean 0, std 1) */
 int dp_registry_register_cast(dp_registry* reg, const char* name);
+/* center crop (offsets ((H - h) / 2, (W - w) / 2), no flip; dtype kept) */
+int dp_registry_register_center_crop(dp_registry* reg, const char* name, int64_t crop_h, int64_t crop_w);
+/* per-channel x * scale[c] + shift[c] on an image -> fp32 (two rounded ops) */
+int dp_registry_register_image_affine(dp_registry* reg, const char* name, const float scale[3], const float shift[3]);
 /* predicate: keep sequences with length <= max_len */
 int dp_registry_register_length_filter(dp_registry* reg, const char* name, int64_t max_len);
 /* predicate on int64 element values (after the maps beneath the filter):
@@ -78,6 +82,11 @@ int dp_source_as_shard(const dp_source* src, int64_t global_count, int64_t num_s
                        int64_t block, dp_source** out);
 int dp_source_images_from_host(const uint8_t* data, int64_t count, int64_t h, int64_t w, int device,
                                dp_source** out);
+/* `images` with an int64 label per held row (copied): tensor_slices over it
+ * yields (int64 id, u8 image, int64 label) elements -- FromMemory's tuple
+ * elements (include/datapipe/graph.hpp:136, element.hpp:30-184); maps
+ * transform the image and pass the label through, Batch stacks it. */
+int dp_source_with_labels(const dp_source* images, const int64_t* labels, int64_t count, dp_source** out);
 /* pinned/registered host memory read by the kernels over PCIe (end-to-end runs; not copied) */
 int dp_source_images_pinned_host(const uint8_t* data, int64_t count, int64_t h, int64_t w, int device,
                                  dp_source** out);

@@ -139,6 +139,24 @@ static int chain_step(orc_img* cur, const orc_map_step* s, int64_t id) {
   return 0;
 }
 
+int orc_apply_step(const void* in, int in_h, int in_w, int in_f32, int64_t id, const orc_map_step* step,
+                   void* out) {
+  orc_img cur;
+  img_alloc(&cur, in_h, in_w, in_f32);
+  const size_t n = (size_t)in_h * in_w * 3;
+  if (in_f32) memcpy(cur.f, in, sizeof(float) * n);
+  else memcpy(cur.u8, in, n);
+  if (chain_step(&cur, step, id)) {
+    img_free(&cur);
+    return -1;
+  }
+  const size_t m = (size_t)cur.h * cur.w * 3;
+  if (cur.f32) memcpy(out, cur.f, sizeof(float) * m);
+  else memcpy(out, cur.u8, m);
+  img_free(&cur);
+  return 0;
+}
+
 int orc_chain_output(const orc_map_step* steps, int nsteps, int in_h, int in_w, int* out_h, int* out_w,
                      int* out_f32) {
   int h = in_h, w = in_w, f = 0;

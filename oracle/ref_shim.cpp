@@ -149,9 +149,82 @@ DatasetGraph BuildImageGraph(UdfRegistry& reg, const ImagePipelineArgs& a,
   return opt;
 }
 
+// One image-chain step as its own reference map UDF: (int64 id, bytes img
+// [, int64 label]) -> the same with the step applied (oracle/chain.c); the
+// input dims / dtype of the step are fixed by the chain prefix.
+std::string RegisterChainStep(UdfRegistry& reg, const orc_map_step& s, int index, int in_h, int in_w, int in_f32) {
+  std::string name = "chain_step(" + std::to_string(index) + ",op=" + std::to_string(s.op) + ")";
+  reg.RegisterMap(name, [s, in_h, in_w, in_f32](const Element& e) {
+    int oh = 0, ow = 0, of = 0;
+    if (orc_chain_output(&s, 1, in_h, in_w, &oh, &ow, &of)) throw std::runtime_error("chain step: bad shape");
+    of = of || in_f32;
+    const int64_t id = e.component(0).int64();
+    std::string out(static_cast<size_t>(oh) * ow * 3 * (of ? sizeof(float) : 1), '\0');
+    if (orc_apply_step(e.component(1).bytes().data(), in_h, in_w, in_f32, id, &s, out.data()))
+      throw std::runtime_error("chain step failed");
+    std::vector<Value> c;
+    c.push_back(Value::Int64(id));
+    c.push_back(Value::Bytes(std::move(out)));
+    if (e.arity() == 3) c.push_back(e.component(2));
+    return Element(std::move(c));
+  });
+  return name;
+}
+
 }  // namespace
 
 extern "C" {
+
+// from_memory(n synthetic images [, labels]) -> [shuffle] -> map(step_0) ->
+// ... -> map(step_k) -> batch(b), optimized (map_map_fusion composes the
+// steps, map_batch_fusion fuses the batch), drained by GetNext.  Outputs the
+// ids, the output image bytes back to back, the labels and the batch sizes.
+int ref_image_chain_pipeline(const orc_map_step* steps, int nsteps, int in_h, int in_w, uint64_t pix_seed, int64_t n,
+                             const int64_t* labels, int64_t shuffle_buffer, uint64_t shuffle_seed, int64_t batch,
+                             int drop_remainder, uint64_t base_seed, int64_t* out_ids, uint8_t* out_images,
+                             int64_t* out_labels, int64_t* out_batch_sizes, int64_t* num_batches) {
+  try {
+    UdfRegistry reg;
+    std::vector<Element> elems = SynthImages(n, in_h, in_w, pix_seed);
+    if (labels)
+      for (int64_t i = 0; i < n; ++i) {
+        std::vector<Value> c{elems[i].component(0), elems[i].component(1), Value::Int64(labels[i])};
+        elems[i] = Element(std::move(c));
+      }
+    DatasetGraph g = ops::FromMemory(std::move(elems), reg);
+    if (shuffle_buffer > 0) g = ops::Shuffle(g, shuffle_buffer, shuffle_seed, reg);
+    int h = in_h, w = in_w, f = 0;
+    for (int i = 0; i < nsteps; ++i) {
+      g = ops::Map(g, RegisterChainStep(reg, steps[i], i, h, w, f), 1, reg);
+      int oh, ow, of;
+      if (orc_chain_output(&steps[i], 1, h, w, &oh, &ow, &of)) throw std::runtime_error("bad chain");
+      h = oh;
+      w = ow;
+      f = f || of;
+    }
+    g = ops::Batch(g, batch, drop_remainder != 0, reg);
+    g = Optimize(g, RuleSet::Default(), reg).first;
+    auto it = MakeIterator(g, reg, Seeded(base_seed));
+    const size_t per = static_cast<size_t>(h) * w * 3 * (f ? sizeof(float) : 1);
+    int64_t k = 0, nb = 0;
+    while (auto e = it->GetNext()) {
+      const auto& ids = e->component(0).items();
+      const auto& imgs = e->component(1).items();
+      for (size_t i = 0; i < ids.size(); ++i, ++k) {
+        out_ids[k] = ids[i].int64();
+        if (imgs[i].bytes().size() != per) throw std::runtime_error("chain output size");
+        std::memcpy(out_images + static_cast<size_t>(k) * per, imgs[i].bytes().data(), per);
+        if (labels) out_labels[k] = e->component(2).items()[i].int64();
+      }
+      out_batch_sizes[nb++] = static_cast<int64_t>(ids.size());
+    }
+    *num_batches = nb;
+    return 0;
+  } catch (const std::exception& e) {
+    return Fail(e);
+  }
+}
+
 
 const char* ref_last_error(void) { return g_err.c_str(); }
 

@@ -146,6 +146,9 @@ typedef struct {
   uint64_t seed;
   float a[3], b[3];
 } orc_map_step;
+/* one step on an element image (u8 or fp32 HWC); out sized for its output */
+int orc_apply_step(const void* in, int in_h, int in_w, int in_f32, int64_t id, const orc_map_step* step,
+                   void* out);
 /* output dims / dtype of a chain over an in_h x in_w x 3 u8 image; -1 if invalid */
 int orc_chain_output(const orc_map_step* steps, int nsteps, int in_h, int in_w, int* out_h, int* out_w,
                      int* out_f32);

@@ -90,6 +90,16 @@ int dp_registry_register_cast(dp_registry* reg, const char* name) {
   DP_REQUIRE(reg && name);
   return Guard([&] { reg->reg.RegisterCast(name); });
 }
+int dp_registry_register_center_crop(dp_registry* reg, const char* name, int64_t crop_h, int64_t crop_w) {
+  DP_REQUIRE(reg && name);
+  return Guard([&] { reg->reg.RegisterCenterCrop(name, crop_h, crop_w); });
+}
+int dp_registry_register_image_affine(dp_registry* reg, const char* name, const float scale[3],
+                                      const float shift[3]) {
+  DP_REQUIRE(reg && name && scale && shift);
+  return Guard(
+      [&] { reg->reg.RegisterImageAffine(name, {scale[0], scale[1], scale[2]}, {shift[0], shift[1], shift[2]}); });
+}
 int dp_registry_register_length_filter(dp_registry* reg, const char* name, int64_t max_len) {
   DP_REQUIRE(reg && name);
   return Guard([&] { reg->reg.RegisterLengthFilter(name, max_len); });
@@ -145,6 +155,10 @@ int dp_source_as_shard(const dp_source* src, int64_t global_count, int64_t num_s
                        int64_t block, dp_source** out) {
   DP_REQUIRE(src && out);
   return Guard([&] { *out = new dp_source{AsShard(src->s, global_count, num_shards, index, block)}; });
+}
+int dp_source_with_labels(const dp_source* images, const int64_t* labels, int64_t count, dp_source** out) {
+  DP_REQUIRE(images && out && (labels || count == 0));
+  return Guard([&] { *out = new dp_source{WithLabels(images->s, labels, count)}; });
 }
 int dp_source_images_from_host(const uint8_t* data, int64_t count, int64_t h, int64_t w, int device,
                                dp_source** out) {

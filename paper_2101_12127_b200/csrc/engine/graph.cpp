@@ -163,6 +163,27 @@ void UdfRegistry::RegisterNormalize(const std::string& name, std::array<float, 3
 
 void UdfRegistry::RegisterCast(const std::string& name) { RegisterNormalize(name, {0.f, 0.f, 0.f}, {1.f, 1.f, 1.f}); }
 
+void UdfRegistry::RegisterCenterCrop(const std::string& name, int64_t crop_h, int64_t crop_w) {
+  if (crop_h < 1 || crop_w < 1) throw PipelineError(ErrorCode::kInvalidAttr, "crop size must be >= 1");
+  Entry e;
+  MapStep s{MapStep::Op::kCenterCrop};
+  s.out_h = crop_h;
+  s.out_w = crop_w;
+  s.flip = false;
+  e.map.push_back(s);
+  Register(name, std::move(e));
+}
+
+void UdfRegistry::RegisterImageAffine(const std::string& name, std::array<float, 3> scale,
+                                      std::array<float, 3> shift) {
+  Entry e;
+  MapStep s{MapStep::Op::kImageAffine};
+  s.scale = scale;
+  s.shift = shift;
+  e.map.push_back(s);
+  Register(name, std::move(e));
+}
+
 void UdfRegistry::RegisterDecodeRaw(const std::string& name, int64_t h, int64_t w) {
   if (h < 1 || w < 1) throw PipelineError(ErrorCode::kInvalidAttr, "decode_raw: shape must be >= 1");
   Entry e;
@@ -225,12 +246,20 @@ const UdfRegistry::Entry& UdfRegistry::Get(const std::string& name) const {
 
 ElementSpec ApplyMapSteps(const std::vector<MapStep>& steps, const ElementSpec& in) {
   ElementSpec cur = in;
+  // (int64 id, tensor[h, w, 3]) or (int64 id, tensor[h, w, 3], int64 label):
+  // image maps transform the tensor and pass the other components through
   auto image_spec = [&](const char* what) -> const TypeSpec& {
-    if (cur.arity() != 2 || cur.components()[0].kind() != Value::Kind::kInt64 ||
+    if ((cur.arity() != 2 && cur.arity() != 3) || cur.components()[0].kind() != Value::Kind::kInt64 ||
         cur.components()[1].kind() != Value::Kind::kTensor || cur.components()[1].shape().size() != 3 ||
-        cur.components()[1].shape()[2] != 3)
+        cur.components()[1].shape()[2] != 3 ||
+        (cur.arity() == 3 && cur.components()[2].kind() != Value::Kind::kInt64))
       throw TypeMismatchError(what, cur);
     return cur.components()[1];
+  };
+  auto with_image = [&](TypeSpec t) {
+    std::vector<TypeSpec> c{TypeSpec::Int64(), std::move(t)};
+    if (cur.arity() == 3) c.push_back(TypeSpec::Int64());
+    return ElementSpec(std::move(c));
   };
   for (const auto& s : steps) {
     switch (s.op) {
@@ -242,12 +271,24 @@ ElementSpec ApplyMapSteps(const std::vector<MapStep>& steps, const ElementSpec& 
         const TypeSpec& t = image_spec("random_crop expects (int64 id, tensor[h,w,3])");
         if (t.shape()[0] < s.out_h || t.shape()[1] < s.out_w)
           throw PipelineError(ErrorCode::kTypeMismatch, "random_crop: crop larger than the image");
-        cur = ElementSpec({TypeSpec::Int64(), TypeSpec::OfTensor(t.dtype(), {s.out_h, s.out_w, 3})});
+        cur = with_image(TypeSpec::OfTensor(t.dtype(), {s.out_h, s.out_w, 3}));
+        break;
+      }
+      case MapStep::Op::kCenterCrop: {
+        const TypeSpec& t = image_spec("center_crop expects (int64 id, tensor[h,w,3])");
+        if (t.shape()[0] < s.out_h || t.shape()[1] < s.out_w)
+          throw PipelineError(ErrorCode::kTypeMismatch, "center_crop: crop larger than the image");
+        cur = with_image(TypeSpec::OfTensor(t.dtype(), {s.out_h, s.out_w, 3}));
         break;
       }
       case MapStep::Op::kResizeBilinear: {
         image_spec("resize expects (int64 id, tensor[h,w,3])");
-        cur = ElementSpec({TypeSpec::Int64(), TypeSpec::OfTensor(DType::kFloat32, {s.out_h, s.out_w, 3})});
+        cur = with_image(TypeSpec::OfTensor(DType::kFloat32, {s.out_h, s.out_w, 3}));
+        break;
+      }
+      case MapStep::Op::kImageAffine: {
+        const TypeSpec& t = image_spec("image affine expects (int64 id, tensor[h,w,3])");
+        cur = with_image(TypeSpec::OfTensor(DType::kFloat32, t.shape()));
         break;
       }
       case MapStep::Op::kDecodeRaw:
@@ -257,7 +298,7 @@ ElementSpec ApplyMapSteps(const std::vector<MapStep>& steps, const ElementSpec& 
         break;
       case MapStep::Op::kNormalize: {
         const TypeSpec& t = image_spec("normalize expects (int64 id, tensor[h,w,3])");
-        cur = ElementSpec({TypeSpec::Int64(), TypeSpec::OfTensor(DType::kFloat32, t.shape())});
+        cur = with_image(TypeSpec::OfTensor(DType::kFloat32, t.shape()));
         break;
       }
     }
@@ -331,6 +372,9 @@ ElementSpec SourceSpec(const SourceData& s) {
   switch (s.kind) {
     case SourceData::Kind::kInt64: return ElementSpec({TypeSpec::Int64()});
     case SourceData::Kind::kImages:
+      if (s.labels)
+        return ElementSpec(
+            {TypeSpec::Int64(), TypeSpec::OfTensor(DType::kUInt8, {s.h, s.w, s.c}), TypeSpec::Int64()});
       return ElementSpec({TypeSpec::Int64(), TypeSpec::OfTensor(DType::kUInt8, {s.h, s.w, s.c})});
     case SourceData::Kind::kTokens: return ElementSpec({TypeSpec::OfTensor(DType::kInt32, {-1})});
     case SourceData::Kind::kRecords: return ElementSpec({TypeSpec::Bytes()});

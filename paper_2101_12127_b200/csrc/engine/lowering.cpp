@@ -11,6 +11,67 @@ namespace {
   throw PipelineError(ErrorCode::kInvalidAttr, "device lowering: " + why);
 }
 
+// A chain of image map steps -> K9's descriptor: the first crop (before any
+// resize) is crop A, a crop after the resize -- or a second crop without one
+// -- is crop B; pixel ops (normalize, cast = normalize(0, 1), image affine)
+// act on the source taps before the resize and on the blend after it.  They
+// commute with crops and flips (pointwise, per channel), so only their place
+// relative to the resize matters.
+dp_image_chain LowerImageChain(const std::vector<MapStep>& steps, int64_t in_h, int64_t in_w) {
+  dp_image_chain c{};
+  c.in_h = static_cast<int>(in_h);
+  c.in_w = static_cast<int>(in_w);
+  int ops = 0;
+  for (const auto& s : steps) {
+    switch (s.op) {
+      case MapStep::Op::kRandomCropFlip:
+      case MapStep::Op::kCenterCrop: {
+        const int mode = s.op == MapStep::Op::kRandomCropFlip ? 1 : 2;
+        const bool flip = s.op == MapStep::Op::kRandomCropFlip && s.flip;
+        if (!c.resize && !c.pre_mode) {
+          c.pre_mode = mode;
+          c.pre_h = static_cast<int>(s.out_h);
+          c.pre_w = static_cast<int>(s.out_w);
+          c.pre_flip = flip;
+          c.pre_seed = s.seed;
+        } else if (!c.post_mode) {
+          c.post_mode = mode;
+          c.post_h = static_cast<int>(s.out_h);
+          c.post_w = static_cast<int>(s.out_w);
+          c.post_flip = flip;
+          c.post_seed = s.seed;
+        } else {
+          Unsupported("image UDF chain: at most one crop before and one after the resize (or two crops)");
+        }
+        break;
+      }
+      case MapStep::Op::kResizeBilinear:
+        if (c.resize || c.post_mode) Unsupported("image UDF chain: one resize, before any second crop");
+        c.resize = 1;
+        c.rs_h = static_cast<int>(s.out_h);
+        c.rs_w = static_cast<int>(s.out_w);
+        break;
+      case MapStep::Op::kNormalize:
+      case MapStep::Op::kImageAffine: {
+        if (ops == 4) Unsupported("image UDF chain: at most 4 pixel ops");
+        const bool norm = s.op == MapStep::Op::kNormalize;
+        c.op_kind[ops] = norm ? 0 : 1;
+        for (int ch = 0; ch < 3; ++ch) {
+          c.op_a[ops][ch] = norm ? s.mean[ch] : s.scale[ch];
+          c.op_b[ops][ch] = norm ? s.stdv[ch] : s.shift[ch];
+        }
+        ++ops;
+        (c.resize ? c.num_post_ops : c.num_pre_ops)++;
+        break;
+      }
+      default:
+        Unsupported("image UDF chain: unsupported map step on images");
+    }
+  }
+  c.out_f32 = c.resize || ops > 0;
+  return c;
+}
+
 }  // namespace
 
 Lowered Lower(const DatasetGraph& g, const UdfRegistry& reg) {
@@ -332,8 +393,20 @@ Lowered Lower(const DatasetGraph& g, const UdfRegistry& reg) {
       L.crop.out_w = L.source->w;
       L.crop.flip = false;
       L.norm = st[0];
+    } else if (st.empty()) {
+      // Batch with no map: the u8 images themselves (K9 gather)
+      L.kind = BatchKind::kCopy;
+      L.img_h = L.source->h;
+      L.img_w = L.source->w;
     } else {
-      Unsupported("image UDF chain must be random_crop_flip>>normalize, resize_bilinear[>>normalize] or normalize");
+      L.kind = BatchKind::kChain;
+      L.img_chain = LowerImageChain(st, L.source->h, L.source->w);
+      int oh = 0, ow = 0, f32 = 0;
+      if (dp_image_chain_output(&L.img_chain, &oh, &ow, &f32) != DP_OK)
+        Unsupported(std::string("image UDF chain: ") + dp_last_error());
+      L.img_h = oh;
+      L.img_w = ow;
+      L.img_f32 = f32 != 0;
     }
     if (L.source->c != 3) Unsupported("images must have 3 channels");
   }

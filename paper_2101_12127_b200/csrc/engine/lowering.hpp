@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "dpb200/datapipe.hpp"
+#include "dpcuda.h"
 
 namespace datapipe::b200::detail {
 
@@ -23,7 +24,8 @@ struct IndexOp {
   bool opaque = false;  // a non-affine map lies beneath the filter
 };
 
-enum class BatchKind { kAffine, kCrop, kResize, kPadded, kIdentityInt };
+// kChain: K9's general image map chain; kCopy: images batched with no map
+enum class BatchKind { kAffine, kCrop, kResize, kPadded, kIdentityInt, kChain, kCopy };
 
 struct Lowered {
   int64_t prefetch = 0;  // 0: none, -1: AUTOTUNE, else depth
@@ -46,6 +48,9 @@ struct Lowered {
   std::vector<MapStep> steps;
   int64_t affine_a = 1, affine_b = 0;
   MapStep crop{}, resize{}, norm{};
+  dp_image_chain img_chain{};      // kChain
+  int64_t img_h = 0, img_w = 0;    // kChain / kCopy: output image dims
+  bool img_f32 = false;            // kChain: fp32 output (else u8)
   std::vector<IndexOp> chain;  // bottom-up
   SourcePtr source;            // element data (images / tokens / int64 values); null for range
   int64_t source_count = 0;    // positions entering the index chain

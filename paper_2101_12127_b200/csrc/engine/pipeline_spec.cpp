@@ -18,6 +18,8 @@
 //   map resize h=<h> w=<w>
 //   map normalize [mean=<m0,m1,m2>] [std=<s0,s1,s2>]
 //   map cast                              (u8 -> fp32)
+//   map center_crop h=<h> w=<w>
+//   map scale scale=<a0,a1,a2> [shift=<b0,b1,b2>]   (x * a_c + b_c -> fp32)
 //   map decode h=<h> w=<w>
 //   filter keep=even|odd|all | filter len_le=<n>
 //   shuffle buffer=<n> [seed=<s>]        shard shards=<k> index=<i>
@@ -280,12 +282,24 @@ ParsedPipeline ParsePipelineSpec(const std::string& text, UdfRegistry& reg, int 
         } else if (k == "cast") {
           name = "cast";
           if (!reg.Contains(name)) reg.RegisterCast(name);
+        } else if (k == "center_crop") {
+          const int64_t h = args.Integer("h"), w = args.Integer("w");
+          name = "center_crop(" + std::to_string(h) + "," + std::to_string(w) + ")";
+          if (!reg.Contains(name)) reg.RegisterCenterCrop(name, h, w);
+        } else if (k == "scale") {
+          auto a = args.Floats("scale", {1.f, 1.f, 1.f});
+          auto b = args.Floats("shift", {0.f, 0.f, 0.f});
+          if (a.size() != 3 || b.size() != 3) Fail(L, C, "scale: scale and shift take 3 values");
+          std::ostringstream nm;
+          nm << "scale(" << a[0] << "," << a[1] << "," << a[2] << ";" << b[0] << "," << b[1] << "," << b[2] << ")";
+          name = nm.str();
+          if (!reg.Contains(name)) reg.RegisterImageAffine(name, {a[0], a[1], a[2]}, {b[0], b[1], b[2]});
         } else if (k == "decode") {
           const int64_t h = args.Integer("h"), w = args.Integer("w");
           name = "decode_raw(" + std::to_string(h) + "," + std::to_string(w) + ")";
           if (!reg.Contains(name)) reg.RegisterDecodeRaw(name, h, w);
         } else {
-          Fail(L, C, "usage: map affine|crop|resize|normalize|cast|decode ...");
+          Fail(L, C, "usage: map affine|crop|center_crop|resize|normalize|scale|cast|decode ...");
         }
         const int64_t p = args.IntOrAuto("parallel", 1);
         out.tunables.push_back({"map@" + std::to_string(out.tunables.size()) + ".parallel", "num_parallel_calls"});

@@ -85,8 +85,8 @@ struct EpochPlan {
 
 struct Slot {
   int device = 0;
-  std::shared_ptr<void> a, b, ha, hb;  // device outputs (+ pinned host mirrors)
-  size_t a_bytes = 0, b_bytes = 0;
+  std::shared_ptr<void> a, b, c, ha, hb, hc;  // device outputs (+ pinned host mirrors); c: labels
+  size_t a_bytes = 0, b_bytes = 0, c_bytes = 0;
   cudaEvent_t ready = nullptr, release = nullptr, start = nullptr;
   bool release_recorded = false;
   // group bookkeeping
@@ -119,6 +119,8 @@ class DevicePipeline {
     autotune_ = L_.prefetch == kAutotune;
     PlanEpochSizes();          // also finds the max sequence length (padded slots)
     batch_bytes_ = BatchBytes();
+    labels_ = L_.source && L_.source->labels && L_.kind != BatchKind::kPadded;
+    if (labels_) batch_bytes_.first += sizeof(int64_t) * L_.batch;  // counted with the ids for group sizing
     // group size: >= 256 MB of output per launch (amortises launch latency and
     // the persistent kernel's ramp-up / drain), at most one epoch of batches
     // Per-launch fixed costs (kernel ramp-up, tail imbalance, launch gap)
@@ -259,7 +261,8 @@ class DevicePipeline {
   std::string Describe() const {
     std::ostringstream os;
     const char* kinds[] = {"K1 gather_affine_batch", "K3 crop_flip_normalize_batch", "K4 resize_normalize_batch",
-                           "K5 padded_batches", "K1 gather_affine_batch"};
+                           "K5 padded_batches",     "K1 gather_affine_batch",       "K9 image_chain_batch",
+                           "K9 gather_copy_batch"};
     os << "batch stage: " << kinds[static_cast<int>(L_.kind)] << " (batch " << L_.batch << (L_.drop ? ", drop" : "")
        << ", " << group_ << " batch(es) per launch, depth " << depth_ << (autotune_ ? " autotuned" : "") << ")\n";
     os << "index chain (bottom-up):";
@@ -281,6 +284,9 @@ class DevicePipeline {
       case BatchKind::kIdentityInt: return {sizeof(int64_t) * b, 0};
       case BatchKind::kCrop: return {sizeof(int64_t) * b, sizeof(float) * b * L_.crop.out_h * L_.crop.out_w * 3};
       case BatchKind::kResize: return {sizeof(int64_t) * b, sizeof(float) * b * L_.resize.out_h * L_.resize.out_w * 3};
+      case BatchKind::kChain:
+      case BatchKind::kCopy:
+        return {sizeof(int64_t) * b, (L_.img_f32 ? sizeof(float) : 1) * b * L_.img_h * L_.img_w * 3};
       case BatchKind::kPadded:
         if (L_.ragged) return {sizeof(int32_t) * b * std::max<int64_t>(max_len_, 1), sizeof(int64_t) * (b + 1)};
         return {sizeof(int32_t) * b * std::max<int64_t>(max_len_, 1), sizeof(int32_t) * b};
@@ -802,22 +808,27 @@ class DevicePipeline {
     auto slot = std::make_shared<Slot>();
     slot->device = opt_.device;
     const int64_t cap = std::max(group_, head_);  // batches a slot holds (the head group may be larger)
-    slot->a_bytes = batch_bytes_.first * cap;
+    const size_t label_bytes = labels_ ? sizeof(int64_t) * L_.batch : 0;
+    slot->a_bytes = (batch_bytes_.first - label_bytes) * cap;
     slot->b_bytes = batch_bytes_.second * cap;
+    slot->c_bytes = label_bytes * cap;
     slot->a = DeviceAlloc(slot->a_bytes, opt_.device);
     if (slot->b_bytes) slot->b = DeviceAlloc(slot->b_bytes, opt_.device);
+    if (slot->c_bytes) slot->c = DeviceAlloc(slot->c_bytes, opt_.device);
     if (opt_.host_output) {
       slot->ha = PinnedAlloc(slot->a_bytes);
       if (slot->b_bytes) slot->hb = PinnedAlloc(slot->b_bytes);
+      if (slot->c_bytes) slot->hc = PinnedAlloc(slot->c_bytes);
     } else if (L_.unbatched && L_.ragged) {
       slot->hb = PinnedAlloc(slot->b_bytes);  // host copy of the row splits
     } else if (L_.unbatched) {
       slot->ha = PinnedAlloc(slot->a_bytes);  // host copy of the values / ids
+      if (slot->c_bytes) slot->hc = PinnedAlloc(slot->c_bytes);  // and of the labels
     }
     CudaCheck(cudaEventCreateWithFlags(&slot->ready, cudaEventDisableTiming), "event");
     CudaCheck(cudaEventCreateWithFlags(&slot->release, cudaEventDisableTiming), "event");
     CudaCheck(cudaEventCreate(&slot->start), "event");
-    slot_bytes_total_ += slot->a_bytes + slot->b_bytes;
+    slot_bytes_total_ += slot->a_bytes + slot->b_bytes + slot->c_bytes;
     slots_.push_back(slot);
     return slot;
   }
@@ -955,6 +966,29 @@ class DevicePipeline {
         }
         break;
       }
+      case BatchKind::kChain:
+      case BatchKind::kCopy: {
+        const auto& src = *L_.source;
+        if (L_.kind == BatchKind::kChain)
+          KCheck(dp_k_image_chain_batch(P<uint8_t>(src.values), src.count, order, row0, rows_total, src.shard_index,
+                                        src.shard_count, src.shard_block, &L_.img_chain, P<int64_t>(slot->a),
+                                        slot->b.get(), stream_),
+                 "K9 image chain");
+        else
+          KCheck(dp_k_gather_copy_batch(P<uint8_t>(src.values), src.count, src.h * src.w * 3, order, row0, rows_total,
+                                        src.shard_index, src.shard_count, src.shard_block, P<int64_t>(slot->a),
+                                        P<uint8_t>(slot->b), stream_),
+                 "K9 gather");
+        launches_++;
+        const size_t img_bytes = (L_.img_f32 ? sizeof(float) : 1) * L_.img_h * L_.img_w * 3;
+        int64_t off = 0;
+        for (int64_t k = 0; k < nb; ++k) {
+          slot->batch_off_a[k] = off * sizeof(int64_t);
+          slot->batch_off_b[k] = off * img_bytes;
+          off += slot->batch_rows[k];
+        }
+        break;
+      }
       case BatchKind::kPadded: {
         const int64_t j0 = row0 / L_.batch;
         if (L_.bucketed) {
@@ -989,6 +1023,12 @@ class DevicePipeline {
         break;
       }
     }
+    if (labels_) {  // the label component: labels[p] of every gathered row (K1 gather)
+      KCheck(dp_k_gather_affine_batch(P<int64_t>(L_.source->labels), order, row0, rows_total, 1, 0,
+                                      P<int64_t>(slot->c), stream_),
+             "labels");
+      launches_++;
+    }
     const auto tC = std::chrono::steady_clock::now();
     dbg_[5] += std::chrono::duration<double>(tC - tB).count();
     CudaCheck(cudaEventRecord(tl.end, stream_), "event");
@@ -1000,8 +1040,10 @@ class DevicePipeline {
       const size_t a_used = UsedBytesA(*slot), b_used = UsedBytesB(*slot);
       CudaCheck(cudaMemcpyAsync(slot->ha.get(), slot->a.get(), a_used, cudaMemcpyDeviceToHost, copy_stream_), "d2h");
       if (b_used) CudaCheck(cudaMemcpyAsync(slot->hb.get(), slot->b.get(), b_used, cudaMemcpyDeviceToHost, copy_stream_), "d2h");
+      const size_t c_used = labels_ ? a_used : 0;  // one int64 label per row, like the ids
+      if (c_used) CudaCheck(cudaMemcpyAsync(slot->hc.get(), slot->c.get(), c_used, cudaMemcpyDeviceToHost, copy_stream_), "d2h");
       CudaCheck(cudaEventRecord(slot->ready, copy_stream_), "event");
-      d2h_bytes_ += a_used + b_used;
+      d2h_bytes_ += a_used + b_used + c_used;
     } else if (L_.unbatched && L_.ragged) {
       // single token sequences: the row splits locate them in the values
       CudaCheck(cudaMemcpyAsync(slot->hb.get(), slot->b.get(), UsedBytesB(*slot), cudaMemcpyDeviceToHost, stream_),
@@ -1011,6 +1053,9 @@ class DevicePipeline {
       // element values / ids are served as host int64 values
       CudaCheck(cudaMemcpyAsync(slot->ha.get(), slot->a.get(), UsedBytesA(*slot), cudaMemcpyDeviceToHost, stream_),
                 "d2h values");
+      if (labels_)
+        CudaCheck(cudaMemcpyAsync(slot->hc.get(), slot->c.get(), UsedBytesA(*slot), cudaMemcpyDeviceToHost, stream_),
+                  "d2h labels");
       CudaCheck(cudaEventRecord(slot->ready, stream_), "event");
     } else {
       CudaCheck(cudaEventRecord(slot->ready, stream_), "event");
@@ -1053,6 +1098,8 @@ class DevicePipeline {
     if (L_.kind == BatchKind::kPadded) return rows * sizeof(int32_t);
     if (L_.kind == BatchKind::kCrop) return rows * sizeof(float) * L_.crop.out_h * L_.crop.out_w * 3;
     if (L_.kind == BatchKind::kResize) return rows * sizeof(float) * L_.resize.out_h * L_.resize.out_w * 3;
+    if (L_.kind == BatchKind::kChain || L_.kind == BatchKind::kCopy)
+      return rows * (L_.img_f32 ? sizeof(float) : 1) * L_.img_h * L_.img_w * 3;
     return 0;
   }
 
@@ -1093,6 +1140,7 @@ class DevicePipeline {
     const bool host = opt_.host_output;
     auto base_a = static_cast<uint8_t*>(host ? slot->ha.get() : slot->a.get()) + slot->batch_off_a[k];
     auto base_b = slot->b ? static_cast<uint8_t*>(host ? slot->hb.get() : slot->b.get()) + slot->batch_off_b[k] : nullptr;
+    auto base_c = slot->c ? static_cast<uint8_t*>(host ? slot->hc.get() : slot->c.get()) + slot->batch_off_a[k] : nullptr;
     // the last component takes the lease itself (one refcount round trip fewer)
     auto mk = [&](DType dt, std::vector<int64_t> shape, void* data, bool last = false) {
       Tensor t;
@@ -1114,11 +1162,17 @@ class DevicePipeline {
         break;
       case BatchKind::kCrop:
         comps.push_back(mk(DType::kInt64, {rows}, base_a));
-        comps.push_back(mk(DType::kFloat32, {rows, L_.crop.out_h, L_.crop.out_w, 3}, base_b, true));
+        comps.push_back(mk(DType::kFloat32, {rows, L_.crop.out_h, L_.crop.out_w, 3}, base_b, !labels_));
         break;
       case BatchKind::kResize:
         comps.push_back(mk(DType::kInt64, {rows}, base_a));
-        comps.push_back(mk(DType::kFloat32, {rows, L_.resize.out_h, L_.resize.out_w, 3}, base_b, true));
+        comps.push_back(mk(DType::kFloat32, {rows, L_.resize.out_h, L_.resize.out_w, 3}, base_b, !labels_));
+        break;
+      case BatchKind::kChain:
+      case BatchKind::kCopy:
+        comps.push_back(mk(DType::kInt64, {rows}, base_a));
+        comps.push_back(mk(L_.img_f32 ? DType::kFloat32 : DType::kUInt8, {rows, L_.img_h, L_.img_w, 3}, base_b,
+                           !labels_));
         break;
       case BatchKind::kPadded:
         if (L_.ragged) {  // (values, row splits)
@@ -1130,6 +1184,7 @@ class DevicePipeline {
         comps.push_back(mk(DType::kInt32, {rows}, base_b, true));
         break;
     }
+    if (labels_) comps.push_back(mk(DType::kInt64, {rows}, base_c, true));
     return Element(std::move(comps));
   }
 
@@ -1156,27 +1211,37 @@ class DevicePipeline {
     const int64_t idx = slot->batch_off_a[k] / static_cast<int64_t>(sizeof(int64_t)) + row;
     const int64_t value = static_cast<const int64_t*>(slot->ha.get())[idx];
     std::vector<Value> comps;
-    comps.reserve(2);
+    comps.reserve(3);
     comps.push_back(Value::Int64(value));
-    if (L_.kind == BatchKind::kCrop || L_.kind == BatchKind::kResize) {
-      const int64_t oh = L_.kind == BatchKind::kCrop ? L_.crop.out_h : L_.resize.out_h;
-      const int64_t ow = L_.kind == BatchKind::kCrop ? L_.crop.out_w : L_.resize.out_w;
+    if (IsImageKind()) {
+      const int64_t oh = ImgH(), ow = ImgW();
+      const size_t el = L_.kind == BatchKind::kCopy || (L_.kind == BatchKind::kChain && !L_.img_f32) ? 1 : sizeof(float);
       Tensor t;
-      t.dtype = DType::kFloat32;
+      t.dtype = el == 1 ? DType::kUInt8 : DType::kFloat32;
       t.shape = {oh, ow, 3};
-      t.data = static_cast<uint8_t*>(slot->b.get()) + slot->batch_off_b[k] + row * oh * ow * 3 * sizeof(float);
+      t.data = static_cast<uint8_t*>(slot->b.get()) + slot->batch_off_b[k] + row * oh * ow * 3 * el;
       t.residency = Residency::kDevice;
       t.device = opt_.device;
       t.owner = std::move(lease);
       t.ready = slot->ready;
       comps.push_back(Value::FromTensor(std::move(t)));
-    } else {
-      // the value was copied out: the slot can go as soon as this returns
-      comps.reserve(1);
+      if (labels_) comps.push_back(Value::Int64(static_cast<const int64_t*>(slot->hc.get())[idx]));
     }
+    // (int64 values were copied out: the slot can go as soon as this returns)
     Element e(std::move(comps));
-    if (L_.kind != BatchKind::kCrop && L_.kind != BatchKind::kResize) lease.reset();
+    if (!IsImageKind()) lease.reset();
     return e;
+  }
+
+  bool IsImageKind() const {
+    return L_.kind == BatchKind::kCrop || L_.kind == BatchKind::kResize || L_.kind == BatchKind::kChain ||
+           L_.kind == BatchKind::kCopy;
+  }
+  int64_t ImgH() const {
+    return L_.kind == BatchKind::kCrop ? L_.crop.out_h : L_.kind == BatchKind::kResize ? L_.resize.out_h : L_.img_h;
+  }
+  int64_t ImgW() const {
+    return L_.kind == BatchKind::kCrop ? L_.crop.out_w : L_.kind == BatchKind::kResize ? L_.resize.out_w : L_.img_w;
   }
 
   // AUTOTUNE prefetch: depth = ceil(host issue time / device time per group)
@@ -1266,6 +1331,7 @@ class DevicePipeline {
   std::pair<size_t, size_t> batch_bytes_;
   int64_t max_len_ = 0;
   int64_t group_ = 1;
+  bool labels_ = false;  // images with labels: a third component (int64 per row)
   int64_t head_ = 0;  // batches of the stream's first launch group (0: group_)
   bool span_epochs_ = false;
   int64_t epoch_count_ = 0, batches_per_epoch_ = 0, total_batches_ = 0, total_groups_ = -1;

@@ -123,7 +123,8 @@ void EncodeSource(const std::string& key, const SourceData& s, Out& w) {
     return;
   }
   w.Le<uint8_t>(kTagDeviceSource);
-  w.Le<uint8_t>(static_cast<uint8_t>(s.kind));
+  // kind, bit 7 = the images carry labels (a third element component)
+  w.Le<uint8_t>(static_cast<uint8_t>(static_cast<uint8_t>(s.kind) | (s.labels ? 0x80 : 0)));
   for (int64_t v : {s.count, s.h, s.w, s.c, s.total_tokens, s.record_len, s.global_count, s.shard_count, s.shard_index,
                     s.shard_block})
     w.Le<int64_t>(v);
@@ -218,7 +219,9 @@ struct Decoder {
   uint32_t nodes = 0;
 
   SourcePtr BindSource(In& in) {
-    const auto kind = static_cast<SourceData::Kind>(in.Le<uint8_t>());
+    const uint8_t kind_byte = in.Le<uint8_t>();
+    const auto kind = static_cast<SourceData::Kind>(kind_byte & 0x7f);
+    const bool labels = (kind_byte & 0x80) != 0;
     int64_t d[10];
     for (auto& v : d) v = in.Le<int64_t>();
     if (next_source >= sources.size())
@@ -229,7 +232,7 @@ struct Decoder {
     if (!s) throw PipelineError(ErrorCode::kValidationFailed, "null device source");
     const int64_t have[10] = {s->count, s->h, s->w, s->c, s->total_tokens, s->record_len,
                               s->global_count, s->shard_count, s->shard_index, s->shard_block};
-    if (s->kind != kind || std::memcmp(d, have, sizeof(d)) != 0)
+    if (s->kind != kind || (s->labels != nullptr) != labels || std::memcmp(d, have, sizeof(d)) != 0)
       throw PipelineError(ErrorCode::kValidationFailed,
                           "device source #" + std::to_string(next_source - 1) + " does not match the serialized one");
     return s;

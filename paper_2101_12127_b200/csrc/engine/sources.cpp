@@ -108,6 +108,27 @@ SourcePtr AsShard(const SourcePtr& s, int64_t global_count, int64_t num_shards, 
   return v;
 }
 
+SourcePtr WithLabels(const SourcePtr& s, const int64_t* labels, int64_t count) {
+  if (!s || s->kind != SourceData::Kind::kImages)
+    throw PipelineError(ErrorCode::kInvalidAttr, "labels: the source must hold images");
+  if (count != s->count)
+    throw PipelineError(ErrorCode::kInvalidAttr, "labels: " + std::to_string(count) + " labels for " +
+                                                     std::to_string(s->count) + " images");
+  if (count > 0 && !labels) throw PipelineError(ErrorCode::kInvalidAttr, "labels: null");
+  auto v = std::make_shared<SourceData>(*s);
+  const size_t bytes = sizeof(int64_t) * std::max<int64_t>(count, 1);
+  DeviceGuard g(s->device);
+  if (s->residency == Residency::kHost) {
+    v->labels = PinnedAlloc(bytes);  // mapped: the kernels read it over PCIe like the images
+    if (count) std::memcpy(v->labels.get(), labels, sizeof(int64_t) * count);
+  } else {
+    v->labels = DeviceAlloc(bytes, s->device);
+    if (count)
+      CudaCheck(cudaMemcpy(v->labels.get(), labels, sizeof(int64_t) * count, cudaMemcpyHostToDevice), "labels");
+  }
+  return v;
+}
+
 SourcePtr SynthTokens(int64_t count, uint32_t max_len, uint64_t len_seed, uint64_t tok_seed, int device) {
   if (count < 1 || max_len < 1) throw PipelineError(ErrorCode::kInvalidAttr, "synth tokens: bad shape");
   // lengths: Pcg32(len_seed).Bounded(max_len) + 1 drawn in order (random.hpp:41-63)

@@ -77,6 +77,10 @@ _SIGS = {
     "dp_source_records_from_files": [ctypes.POINTER(ctypes.c_char_p), c_i64, c_int, PP],
     "dp_source_records_from_files_sharded": [ctypes.POINTER(ctypes.c_char_p), c_i64, c_i64, c_i64, c_int, PP],
     "dp_source_as_shard": [c_vp, c_i64, c_i64, c_i64, c_i64, PP],
+    "dp_source_with_labels": [c_vp, c_vp, c_i64, PP],
+    "dp_registry_register_center_crop": [c_vp, ctypes.c_char_p, c_i64, c_i64],
+    "dp_registry_register_image_affine": [c_vp, ctypes.c_char_p, ctypes.POINTER(ctypes.c_float),
+                                          ctypes.POINTER(ctypes.c_float)],
     "dp_source_synthetic_records_sharded": [c_i64, c_i64, c_i64, c_i64, c_u64, c_i64, c_i64, c_int, PP],
     "dp_source_release": [c_vp],
     "dp_graph_range": [c_vp, c_i64, PP],
@@ -186,6 +190,16 @@ class Registry:
         _check(L().dp_registry_register_cast(self.h, _b(name)))
         return name
 
+    def register_center_crop(self, name, crop_h, crop_w):
+        _check(L().dp_registry_register_center_crop(self.h, _b(name), crop_h, crop_w))
+        return name
+
+    def register_image_affine(self, name, scale, shift):
+        """x * scale[c] + shift[c] per channel -> fp32."""
+        _check(L().dp_registry_register_image_affine(self.h, _b(name), (ctypes.c_float * 3)(*map(float, scale)),
+                                                     (ctypes.c_float * 3)(*map(float, shift))))
+        return name
+
     def register_normalize(self, name, mean=MEAN, std=STD):
         m = (ctypes.c_float * 3)(*mean)
         s = (ctypes.c_float * 3)(*std)
@@ -275,6 +289,14 @@ class Source:
         _check(L().dp_source_synthetic_images_sharded(global_count, h, w, seed, num_shards, index, device,
                                                       ctypes.byref(out)))
         return Source(out)
+
+    def with_labels(self, labels):
+        """This image source with an int64 label per row: elements (id, image, label)."""
+        labels = np.ascontiguousarray(labels, np.int64)
+        out = c_vp()
+        _check(L().dp_source_with_labels(self.h, labels.ctypes.data if labels.size else None, labels.size,
+                                         ctypes.byref(out)))
+        return Source(out, keepalive=self)
 
     @staticmethod
     def images_from_host(arr: np.ndarray, device=0):

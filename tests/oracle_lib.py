@@ -271,6 +271,8 @@ class Reference:
         L.ref_image_pipeline.argtypes = [c_int, c_int, c_int, c_int, c_int, u64, u64, i64, i64, i64, i64, c_int, u64,
                                          i64, c_int, i64, i64, u64, vp, vp, vp, vp]
         L.ref_filter_batch_tokens.argtypes = [i64, u64, u32, u64, i32, i64, c_int, vp, vp, vp, vp, vp, vp]
+        L.ref_image_chain_pipeline.argtypes = [vp, c_int, c_int, c_int, u64, i64, vp, i64, u64, i64, c_int, u64, vp,
+                                               vp, vp, vp, vp]
         L.ref_interleave_ids.argtypes = [i64, i64, i64, i64, i64, i64, i64, u64, u64, vp, vp]
         L.ref_time_image_pipeline.argtypes = [c_int, c_int, c_int, c_int, c_int, u64, u64, i64, i64, u64, i64, i64,
                                               i64, u64, c_int, vp, vp]
@@ -317,6 +319,27 @@ class Reference:
         sizes = sizes[: nb[0]]
         t = int(sizes.sum())
         return ids[:t], pix[:t], sizes
+
+    def image_chain_pipeline(self, steps, n, in_hw, labels=None, shuffle_buffer=0, shuffle_seed=42, batch=32,
+                             drop_remainder=False, base_seed=1, pix_seed=PIX_SEED):
+        """from_memory(synthetic images [, labels]) -> [shuffle] -> one map per
+        chain step -> batch, optimized, through the reference runtime.
+        -> (ids, images [n, h, w, 3] u8/f32, labels or None, batch sizes)"""
+        orc = Oracle()
+        oh, ow, dt = orc.chain_output(steps, *in_hw)
+        ids = np.zeros(max(n, 1), np.int64)
+        imgs = np.zeros((max(n, 1), oh, ow, 3), dt)
+        lab_out = np.zeros(max(n, 1), np.int64)
+        sizes = np.zeros(max(n, 1) + 1, np.int64)
+        nb = i64()
+        lab = None if labels is None else np.ascontiguousarray(labels, np.int64)
+        self._check(self.L.ref_image_chain_pipeline(steps_array(steps), len(steps), in_hw[0], in_hw[1], pix_seed, n,
+                                                    None if lab is None else P(lab), shuffle_buffer, shuffle_seed,
+                                                    batch, int(drop_remainder), base_seed, P(ids), P(imgs),
+                                                    P(lab_out), P(sizes), ctypes.byref(nb)))
+        sizes = sizes[:nb.value]
+        k = int(sizes.sum())
+        return ids[:k], imgs[:k], (None if lab is None else lab_out[:k]), sizes
 
     def filter_batch_tokens(self, n, max_keep=512, batch=128, len_seed=4, max_len=1024, tok_seed=4,
                             drop_remainder=False):

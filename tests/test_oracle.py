@@ -334,3 +334,21 @@ def test_chain_restatement_equals_the_fused_restatements_and_digest(orc):
     outs = np.concatenate([orc.chain(orc.images(int(i), 1, 32, 40)[0], int(i), steps).reshape(-1).view(np.uint32)
                            for i in ids])
     assert orc.epoch_image_digest(steps, ids, 32, 40, threads=3) == Oracle.order_digest(outs)
+
+
+def test_chain_goldens_equal_the_restatement(orc):
+    """tests/golden/chains.json (the compiled reference running the chain
+    steps as MapFns) equals the oracle's shuffle order + chain restatement."""
+    import json
+    import os
+    from tests.oracle_lib import Oracle
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "chains.json")))
+    n, (buf, seed) = gold["n"], gold["shuffle"]
+    order = orc.shuffle_order(n, buf, orc.shuffle_seed(gold["base_seed"], seed))
+    for case in gold["cases"]:
+        steps = [tuple(s) for s in case["steps"]]
+        assert f"{orc.fnv_digest(order):016x}" == case["ids"]
+        imgs = np.stack([orc.chain(orc.images(int(i), 1, *case["in_hw"])[0], int(i), steps) for i in order])
+        assert f"{Oracle.order_digest(imgs.reshape(-1).view(np.uint32)):016x}" == case["images"], case["name"]
+        b = gold["batch"]
+        assert case["batch_sizes"] == [min(b, n - k) for k in range(0, n, b)]

@@ -51,6 +51,23 @@ CFG = {
                           "crop 224 + flip + normalize fp32) -> Batch(256) -> Prefetch(AUTOTUNE)",
                  in_hw=(256, 256), out_hw=(224, 224), mode=0, batch=256, n=65536, files=32, cycle=4,
                  bytes_per_elem=IMG_BYTES_READ + IMG_BYTES_WRITE, kernel="K3 crop_flip_normalize_batch"),
+    # the widened UDF library (K9): no map, RandomResizedCrop, ResNet eval
+    "cfg2u8": dict(workload="synthetic 256x256x3 u8 images -> Shuffle(10k, seed 42) -> Batch(256) (no map: the u8 "
+                            "images themselves)",
+                   in_hw=(256, 256), out_hw=(256, 256), batch=256, n=65536, udfs=[], out_f32=False,
+                   bytes_per_elem=2 * 196608, kernel="K9 gather_copy_batch", dtype="u8"),
+    "cfg2rrc": dict(workload="synthetic 256x256x3 u8 images -> Shuffle(10k, seed 42) -> Map(random crop 160x160 + "
+                             "flip) -> Map(bilinear resize 224) -> Map(normalize fp32) -> Batch(256) "
+                             "(RandomResizedCrop at a fixed scale)",
+                    in_hw=(256, 256), out_hw=(224, 224), batch=256, n=65536,
+                    udfs=[("random_crop", 160, 160, 7, True), ("resize", 224, 224), ("normalize",)],
+                    bytes_per_elem=160 * 160 * 3 + IMG_BYTES_WRITE, kernel="K9 image_chain_batch"),
+    "cfg3e": dict(workload="synthetic 320x320x3 u8 images -> Shuffle(10k, seed 42) -> Map(bilinear resize 256) -> "
+                           "Map(center crop 224) -> Map(normalize fp32) -> Batch(256) (ResNet eval)",
+                  in_hw=(320, 320), out_hw=(224, 224), batch=256, n=65536,
+                  udfs=[("resize", 256, 256), ("center_crop", 224, 224), ("normalize",)],
+                  # source rows / columns 20..299 feed the center window: 280 x 280 x 3 read
+                  bytes_per_elem=280 * 280 * 3 + IMG_BYTES_WRITE, kernel="K9 image_chain_batch"),
     "cfg1": dict(workload="Range(2^28) int64 -> Map(x*3+1) -> Batch(1024) (cfg1 shape at the roofline size "
                           "SURVEY.md 8(d) names; Range(1M) is the parity case)",
                  kind="range", batch=1024, n=1 << 28, bytes_per_elem=8, kernel="K1 range_affine_batch",
@@ -240,7 +257,15 @@ def cpu_reference(cfg, threads, warmup_batches, steps):
                                                              ctypes.c_void_p, ctypes.c_void_p]
     secs, elems = ctypes.c_double(), i64()
     sample = 2048
-    if cfg.get("files"):  # cfg5: the reference's interleave over record readers
+    if "udfs" in cfg:  # the chain configs: one reference map node per step
+        from tests.oracle_lib import steps_array
+        st = chain_steps(cfg["udfs"])
+        L.ref_time_chain_steps.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, u64, i64, i64,
+                                           u64, i64, i64, i64, i64, ctypes.c_void_p, ctypes.c_void_p]
+        rc = L.ref_time_chain_steps(steps_array(st), len(st), *cfg["in_hw"], 0x5EED, sample, 10000, 42, cfg["batch"],
+                                    threads, warmup_batches, steps, ctypes.byref(secs), ctypes.byref(elems))
+        what = f"{sample} resident synthetic images repeated, one reference map per chain step"
+    elif cfg.get("files"):  # cfg5: the reference's interleave over record readers
         L.ref_time_interleave_image_steps.argtypes = [ctypes.c_int] * 5 + [u64, u64] + [i64] * 5 + [
             i64, u64, i64, i64, i64, i64, ctypes.c_void_p, ctypes.c_void_p]
         rec = cfg["n"] // cfg["files"]
@@ -313,11 +338,36 @@ def run_reference(args, cfg):
 
 
 # ---------------------------------------------------------------- GPU side --
+def register_udfs(dp, reg, udfs):
+    names = []
+    for i, st in enumerate(udfs):
+        name = f"u{i}_{st[0]}"
+        if st[0] == "random_crop":
+            reg.register_random_crop_flip(name, st[1], st[2], seed=st[3], flip=st[4])
+        elif st[0] == "center_crop":
+            reg.register_center_crop(name, st[1], st[2])
+        elif st[0] == "resize":
+            reg.register_resize_bilinear(name, st[1], st[2])
+        elif st[0] == "normalize":
+            reg.register_normalize(name)
+        names.append(name)
+    return names
+
+
+def chain_steps(udfs):
+    """bench udfs -> the oracle's step tuples (tests/oracle_lib.steps_array)."""
+    from tests.oracle_lib import MEAN, STD
+    return [(st[0], MEAN, STD) if st[0] == "normalize" else st for st in udfs]
+
+
 def build_graph(dp, cfg, src, repeat=True, shard=None, files=None):
     reg = dp.Registry()
-    first = (reg.register_resize_bilinear("resize", *cfg["out_hw"]) if cfg["mode"] == 1
-             else reg.register_random_crop_flip("crop", *cfg["out_hw"], seed=7, flip=True))
-    reg.register_normalize("norm")
+    if "udfs" in cfg:
+        names = register_udfs(dp, reg, cfg["udfs"])
+    else:
+        names = [reg.register_resize_bilinear("resize", *cfg["out_hw"]) if cfg["mode"] == 1
+                 else reg.register_random_crop_flip("crop", *cfg["out_hw"], seed=7, flip=True),
+                 reg.register_normalize("norm")]
     if cfg.get("files"):  # cfg5: Shard over the record files, then Interleave their readers
         files = files or cfg["files"] * (shard[0] if shard else 1)
         reg.register_record_reader("reader", cfg["n"] // cfg["files"])
@@ -329,7 +379,10 @@ def build_graph(dp, cfg, src, repeat=True, shard=None, files=None):
         g = dp.Dataset.tensor_slices(reg, src)
         if shard:
             g = g.shard(*shard)  # Shard(k, rank) right after the source
-    g = g.shuffle(10000, 42).map(first, -1).map("norm", -1).batch(cfg["batch"])
+    g = g.shuffle(10000, 42)
+    for nm in names:
+        g = g.map(nm, -1)
+    g = g.batch(cfg["batch"])
     if repeat:
         g = g.repeat(-1)
     g, report = g.prefetch(-1).optimize()
@@ -433,7 +486,8 @@ def run_ours(args, cfg):
     if cfg["kind"] == "images":
         # exactly K timed and W warm-up steps: a launch group that tiles the
         # window (largest divisor-compatible group up to the default size)
-        out_bytes = cfg["batch"] * (cfg["out_hw"][0] * cfg["out_hw"][1] * 3 * 4 + 8)
+        out_bytes = cfg["batch"] * (cfg["out_hw"][0] * cfg["out_hw"][1] * 3 * (4 if cfg.get("out_f32", True) else 1)
+                                    + 8)
         group, head = launch_tiling_for(args.warmup, args.steps, max(per_launch, (3200 << 20) // out_bytes),
                                         per_epoch)
         if (group, head) != (per_launch, 0):
@@ -636,8 +690,9 @@ def run_e2e(dp, cfg, local, args, world=1, dev=None):
     secs = time.perf_counter() - t0
     if world > 1:
         secs = max_over_ranks(secs * 1e3, world, dev) / 1e3
-    b_out = cfg["batch"] * (cfg["out_hw"][0] * cfg["out_hw"][1] * 3 * 4 + 8)
-    b_in = cfg["batch"] * (cfg["out_hw"][0] * cfg["out_hw"][1] * 3 if cfg["mode"] != 1 else h * w * 3)
+    b_out = cfg["batch"] * (cfg["out_hw"][0] * cfg["out_hw"][1] * 3 * (4 if cfg.get("out_f32", True) else 1) + 8)
+    b_in = cfg["batch"] * (cfg["bytes_per_elem"] - cfg["out_hw"][0] * cfg["out_hw"][1] * 3 *
+                           (4 if cfg.get("out_f32", True) else 1))
     d2h_gbs = steps * b_out / secs / 1e9  # per rank
     return {"value": round(steps * cfg["batch"] * world / secs, 1), "unit": "images/s",
             "h2d_bytes_per_step": b_in * world, "d2h_bytes_per_step": b_out * world, "steps": steps,

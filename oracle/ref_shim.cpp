@@ -539,6 +539,46 @@ int ref_time_image_steps(int mode, int in_h, int in_w, int out_h, int out_w, uin
   }
 }
 
+// CPU baseline for the chain configs: from_memory(n synthetic images) ->
+// shuffle -> repeat -> one map node per chain step (num_parallel_calls =
+// parallel; map_map_fusion composes them) -> batch -> prefetch(AUTOTUNE),
+// optimized; `steps` timed GetNext calls after `warmup`.
+int ref_time_chain_steps(const orc_map_step* chain, int nsteps, int in_h, int in_w, uint64_t pix_seed, int64_t n,
+                         int64_t shuffle_buffer, uint64_t shuffle_seed, int64_t batch, int64_t parallel,
+                         int64_t warmup, int64_t steps, double* seconds, int64_t* elements) {
+  try {
+    UdfRegistry reg;
+    DatasetGraph g = ops::FromMemory(SynthImages(n, in_h, in_w, pix_seed), reg);
+    if (shuffle_buffer > 0) g = ops::Shuffle(g, shuffle_buffer, shuffle_seed, reg);
+    g = ops::Repeat(g, kInfiniteRepeat, reg);
+    int h = in_h, w = in_w, f = 0;
+    for (int i = 0; i < nsteps; ++i) {
+      g = ops::Map(g, RegisterChainStep(reg, chain[i], i, h, w, f), parallel, reg);
+      int oh, ow, of;
+      if (orc_chain_output(&chain[i], 1, h, w, &oh, &ow, &of)) throw std::runtime_error("bad chain");
+      h = oh;
+      w = ow;
+      f = f || of;
+    }
+    g = ops::Batch(g, batch, false, reg);
+    g = ops::Prefetch(g, kAutotune, reg);
+    g = Optimize(g, RuleSet::Default(), reg).first;
+    auto it = MakeIterator(g, reg, Seeded(1));
+    for (int64_t i = 0; i < warmup; ++i) it->GetNext();
+    int64_t count = 0;
+    auto t0 = std::chrono::steady_clock::now();
+    for (int64_t i = 0; i < steps; ++i) {
+      auto e = it->GetNext();
+      count += static_cast<int64_t>(e->component(0).items().size());
+    }
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    *elements = count;
+    return 0;
+  } catch (const std::exception& e) {
+    return Fail(e);
+  }
+}
+
 // CPU baseline for cfg5: from_memory(file ids 0..files-1) -> interleave(
 // reader: file s opens `records` images valued (s * records + r, image bytes),
 // cycle, parallel) -> shuffle -> repeat -> map(img udf, parallel) -> batch ->

@@ -30,7 +30,7 @@ def expected(orc, config, world, rank, n):
     """The values the bench digests for rank `rank` of `world` (bench.py run_ours)."""
     o = Oracle.order_digest
     salt0 = orc.mix_seeds(1, 0)  # repeat(-1) above the batch: epoch 0 is salted MixSeeds(base, 0)
-    if config in ("cfg2", "cfg3"):
+    if config in ("cfg2", "cfg3", "cfg2u8", "cfg2rrc", "cfg3e"):
         pos = orc.shard_positions(world * n, world, rank) if world > 1 else np.arange(n)
         ids = pos[orc.shuffle_order(pos.size, 10000, orc.shuffle_seed(salt0, 42))]
         return o(ids[:FIRST_BATCHES * 256])
@@ -66,7 +66,8 @@ def expected(orc, config, world, rank, n):
     raise KeyError(config)
 
 
-SIZES = {"cfg1": 1 << 28, "cfg2": 65536, "cfg3": 65536, "cfg5": 65536, "cfg4": 1_000_000, "cfg4r": 1_000_000,
+SIZES = {"cfg1": 1 << 28, "cfg2": 65536, "cfg3": 65536, "cfg5": 65536, "cfg2u8": 65536, "cfg2rrc": 65536,
+         "cfg3e": 65536, "cfg4": 1_000_000, "cfg4r": 1_000_000,
          "cfg4b": 1_000_000}
 
 

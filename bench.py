@@ -723,22 +723,29 @@ def run_e2e_tokens(dp, cfg, local, args, world=1, dev=None):
     it = make()
     per_epoch = int(re.search(r"elements, (\d+) batches", it.describe()).group(1))
     steps = per_epoch * 2
-    for _ in range(min(8, per_epoch)):
+    for _ in range(per_epoch):  # one warm-up epoch on the same iterator (slots allocated, plans built ahead)
         it.get_next().wait().release()
-    it = make()
-    if world > 1:
-        max_over_ranks(0.0, world, dev)  # barrier: start together
-    t0 = time.perf_counter()
-    rows = 0
-    for _ in range(steps):
-        b = it.get_next().wait()
-        rows += b.components[1][1][0] - (1 if cfg.get("ragged") else 0)
-        b.release()
-    secs = time.perf_counter() - t0
-    if world > 1:
-        secs = max_over_ranks(secs * 1e3, world, dev) / 1e3
+    # three timed windows of 2 epochs each on the same iterator; the median
+    # is reported (a window takes ~20 ms: one host hiccup would dominate it)
+    windows = []
+    for _ in range(3):
+        if world > 1:
+            max_over_ranks(0.0, world, dev)  # barrier: start together
+        t0 = time.perf_counter()
+        rows = 0
+        for _ in range(steps):
+            b = it.get_next().wait()
+            rows += b.components[1][1][0] - (1 if cfg.get("ragged") else 0)
+            b.release()
+        secs = time.perf_counter() - t0
+        if world > 1:
+            secs = max_over_ranks(secs * 1e3, world, dev) / 1e3
+        windows.append((secs, rows))
+    secs, rows = sorted(windows)[1]
     # bytes per step, from the same batches (untimed pass)
     it = make()
+    for _ in range(per_epoch):
+        it.get_next().release()
     b_in = b_out = 0
     for _ in range(steps):
         b = it.get_next().wait()
@@ -755,11 +762,15 @@ def run_e2e_tokens(dp, cfg, local, args, world=1, dev=None):
         b.release()
     return {"value": round(rows * world / secs, 1), "unit": cfg["unit"],
             "h2d_bytes_per_step": int(b_in / steps) * world, "d2h_bytes_per_step": int(b_out / steps) * world,
-            "steps": steps, "host_dataset": f"{n_host} sequences, len U[1,1024], pinned host memory",
+            "steps": steps, "windows_ms": [round(w[0] * 1e3, 2) for w in windows],
+            "pcie": {"h2d_gbs_achieved": round(b_in / secs / 1e9, 1), "d2h_gbs_achieved": round(b_out / secs / 1e9, 1),
+                     "d2h_gbs_measured": pcie_d2h_gbs(local)},
+            "host_dataset": f"{n_host} sequences, len U[1,1024], pinned host memory",
             "how": "pinned host token source read over PCIe by the kernels (lengths, offsets, tokens) + D2H of every "
-                   "batch into pinned host slots; host wall clock over 2 epochs, each batch waited on by the host",
-            "bound": "PCIe read requests: the batch kernels gather rows from host memory with 4-byte loads "
-                     "(128 B per warp request); staging the dataset per epoch by bulk DMA is not done yet"}
+                   "batch into pinned host slots; host wall clock over 2 epochs after a warm-up epoch on the same "
+                   "iterator (median of 3 such windows), each batch waited on by the host",
+            "bound": "PCIe: each epoch plan stages exactly the rows it consumes from pinned host memory into HBM "
+                     "(dp_k_stage_rows, one pass), the batch kernels stream HBM, every batch is copied back"}
 
 
 def relaunch(n):

@@ -195,6 +195,14 @@ int dp_k_padded_batches(const int32_t* tokens, const int64_t* offsets, const int
 /* Ragged Batch of token sequences (the reference's Filter -> Batch lists, */
 /* runtime.cpp:579-637): prefix[i] = sum of lengths[order[j]], j < i, and  */
 /* prefix[n] = the total (int64 [n + 1]; order null = identity).          */
+/* Stages plan rows into device memory (token configs with a pinned host
+ * source, end to end): staged[prefix[i] ..] = tokens[offsets[p_i] ..
+ * + lengths[p_i]), staged_lengths[i] = lengths[p_i], p_i = order ? order[i]
+ * : i; prefix from dp_k_len_prefix over the same order.  The batch kernels
+ * then read the staged rows (order = identity, offsets = prefix) from HBM
+ * instead of gathering 4-byte words over PCIe. */
+int dp_k_stage_rows(const int32_t* tokens, const int64_t* offsets, const int32_t* lengths, const int64_t* order,
+                    int64_t n, const int64_t* prefix, int32_t* staged, int32_t* staged_lengths, void* stream);
 size_t dp_k_len_prefix_scratch_bytes(int64_t n);
 int dp_k_len_prefix(const int32_t* lengths, const int64_t* order, int64_t n,
                     int64_t* prefix, void* scratch, void* stream);

@@ -79,6 +79,11 @@ struct EpochPlan {
   std::vector<int64_t> rows, roff;
   std::shared_ptr<void> bstart_dev, rows_dev, roff_dev;
   std::shared_ptr<void> row_src_dev, row_dst_dev, row_lm_dev;  // per emitted row (dp_k_bucket_rows)
+  // token sources in pinned host memory: the plan's rows staged into device
+  // memory in consumption order (dp_k_stage_rows), read by the batch kernels
+  // with the identity order
+  bool staged = false;
+  std::shared_ptr<void> st_tokens, st_offsets, st_lengths;
   cudaEvent_t ready = nullptr;
   int64_t ready_gen = 0;  // bumped whenever `ready` is recorded again (a head appended)
 };
@@ -615,9 +620,49 @@ class DevicePipeline {
                   "boff");
       }
     }
+    if (L_.kind == BatchKind::kPadded && L_.source->residency == Residency::kHost) StageRows(p);
     CudaCheck(cudaEventCreateWithFlags(&p.ready, cudaEventDisableTiming), "event");
     CudaCheck(cudaEventRecord(p.ready, s), "event");
     p.ready_gen = 1;
+  }
+
+  // Pinned-host token source (end-to-end runs): one PCIe pass per epoch
+  // moves exactly the rows the plan consumes, in consumption order, into a
+  // packed device buffer (warp-per-row kernel with 8 loads in flight per
+  // lane); the batch kernels then stream HBM.  Rows: the plan order
+  // (padded / ragged) or the bucket plan's emitted rows (then re-indexed
+  // 0..n-1).
+  void StageRows(EpochPlan& p) {
+    cudaStream_t s = plan_stream_;
+    auto dalloc = [&](size_t bytes) { return DeviceAllocAsync(bytes, opt_.device, plan_stream_, plan_stream_); };
+    const int64_t* ord = L_.bucketed ? P<int64_t>(p.row_src_dev) : P<int64_t>(p.order);
+    const int64_t n = L_.bucketed ? (p.roff.empty() ? 0 : p.roff.back()) : p.count;
+    std::shared_ptr<void> prefix;
+    if (L_.ragged) {
+      prefix = p.roff_dev;  // the ragged plan's length prefix over the same order
+    } else {
+      prefix = dalloc(sizeof(int64_t) * (n + 1));
+      auto scratch = dalloc(dp_k_len_prefix_scratch_bytes(n));
+      KCheck(dp_k_len_prefix(P<int32_t>(L_.source->lengths), ord, n, P<int64_t>(prefix), scratch.get(), s),
+             "stage prefix");
+      launches_ += 3;
+    }
+    int64_t total = 0;
+    CudaCheck(cudaMemcpyAsync(&total, P<int64_t>(prefix) + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s), "staged");
+    CudaCheck(cudaStreamSynchronize(s), "staged size");
+    p.st_tokens = dalloc(sizeof(int32_t) * std::max<int64_t>(total, 1));
+    p.st_lengths = dalloc(sizeof(int32_t) * std::max<int64_t>(n, 1));
+    p.st_offsets = prefix;
+    KCheck(dp_k_stage_rows(P<int32_t>(L_.source->tokens), P<int64_t>(L_.source->offsets),
+                           P<int32_t>(L_.source->lengths), ord, n, P<int64_t>(prefix), P<int32_t>(p.st_tokens),
+                           P<int32_t>(p.st_lengths), s),
+           "stage rows");
+    launches_++;
+    if (L_.bucketed && n > 0) {  // emitted row k is staged row k
+      KCheck(dp_k_range_affine_batch(0, n, 1, 0, P<int64_t>(p.row_src_dev), s), "stage iota");
+      launches_++;
+    }
+    p.staged = true;
   }
 
   // Interleave over record files of unequal sizes: the host schedules the
@@ -991,23 +1036,25 @@ class DevicePipeline {
       }
       case BatchKind::kPadded: {
         const int64_t j0 = row0 / L_.batch;
+        // staged plans: rows in consumption order in device memory
+        const int32_t* tok = plan.staged ? P<int32_t>(plan.st_tokens) : P<int32_t>(L_.source->tokens);
+        const int64_t* offs = plan.staged ? P<int64_t>(plan.st_offsets) : P<int64_t>(L_.source->offsets);
+        const int32_t* lens = plan.staged ? P<int32_t>(plan.st_lengths) : P<int32_t>(L_.source->lengths);
+        const int64_t* ord = plan.staged ? nullptr : order;
         if (L_.bucketed) {
           int64_t group_rows = 0;
           for (int64_t k = 0; k < nb; ++k) group_rows += slot->batch_rows[k] = plan.rows[j0 + k];
-          KCheck(dp_k_bucket_rows_batches(P<int32_t>(L_.source->tokens), P<int64_t>(L_.source->offsets),
-                                          P<int32_t>(L_.source->lengths), P<int64_t>(plan.row_src_dev),
+          KCheck(dp_k_bucket_rows_batches(tok, offs, lens, P<int64_t>(plan.row_src_dev),
                                           P<int64_t>(plan.row_dst_dev), P<int32_t>(plan.row_lm_dev), plan.roff[j0],
                                           plan.boff[j0], group_rows, static_cast<int32_t>(L_.pad),
                                           P<int32_t>(slot->a), P<int32_t>(slot->b), stream_),
                  "K8");
         } else if (L_.ragged) {
-          KCheck(dp_k_ragged_batches(P<int32_t>(L_.source->tokens), P<int64_t>(L_.source->offsets),
-                                     P<int32_t>(L_.source->lengths), order, row0, rows_total, L_.batch, plan.count,
+          KCheck(dp_k_ragged_batches(tok, offs, lens, ord, row0, rows_total, L_.batch, plan.count,
                                      P<int64_t>(plan.roff_dev), P<int32_t>(slot->a), P<int64_t>(slot->b), stream_),
                  "K5 ragged");
         } else {
-          KCheck(dp_k_padded_batches(P<int32_t>(L_.source->tokens), P<int64_t>(L_.source->offsets),
-                                     P<int32_t>(L_.source->lengths), order, row0, rows_total, L_.batch,
+          KCheck(dp_k_padded_batches(tok, offs, lens, ord, row0, rows_total, L_.batch,
                                      P<int32_t>(plan.lmax_dev), P<int64_t>(plan.boff_dev),
                                      static_cast<int32_t>(L_.pad), P<int32_t>(slot->a), P<int32_t>(slot->b), stream_),
                  "K5");

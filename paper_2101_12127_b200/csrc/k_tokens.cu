@@ -347,6 +347,54 @@ ragged_batches_kernel(const int32_t* __restrict__ tokens, const int64_t* __restr
 
 using namespace dpk;
 
+namespace dpk {
+namespace {
+// Stages the rows of an epoch plan out of (mapped, pinned) host memory into
+// a packed device buffer: row i of the plan = source row order[i] (or i),
+// its tokens land at staged + prefix[i].  One warp per row, kStageLoads
+// 4-byte loads per lane issued before their stores: every warp keeps
+// kStageLoads x 128 B of PCIe reads in flight, so thousands of resident
+// warps cover the PCIe round trip (the batch kernels then read HBM).
+constexpr int kStageLoads = 8;
+__global__ void __launch_bounds__(kThreads)
+stage_rows_kernel(const int32_t* __restrict__ tokens, const int64_t* __restrict__ offsets,
+                  const int32_t* __restrict__ lengths, const int64_t* __restrict__ order, int64_t n,
+                  const int64_t* __restrict__ prefix, int32_t* __restrict__ staged,
+                  int32_t* __restrict__ staged_lengths) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (kThreads / 32);
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * (kThreads / 32) + (threadIdx.x >> 5); i < n; i += warps) {
+    const int64_t p = order ? order[i] : i;
+    const int32_t len = lengths[p];
+    const int32_t* src = tokens + offsets[p];
+    int32_t* dst = staged + prefix[i];
+    if (lane == 0) staged_lengths[i] = len;
+    for (int c = lane; c < len; c += 32 * kStageLoads) {
+      int32_t v[kStageLoads];
+#pragma unroll
+      for (int u = 0; u < kStageLoads; ++u) v[u] = c + 32 * u < len ? __ldcs(src + c + 32 * u) : 0;
+#pragma unroll
+      for (int u = 0; u < kStageLoads; ++u)
+        if (c + 32 * u < len) dst[c + 32 * u] = v[u];
+    }
+  }
+}
+}  // namespace
+}  // namespace dpk
+
+extern "C" int dp_k_stage_rows(const int32_t* tokens, const int64_t* offsets, const int32_t* lengths,
+                               const int64_t* order, int64_t n, const int64_t* prefix, int32_t* staged,
+                               int32_t* staged_lengths, void* stream) {
+  if (n < 0) return dpk::fail(DP_ERR_INVALID_ATTR, "stage_rows: n must be >= 0");
+  if (n == 0) return DP_OK;
+  if (!tokens || !offsets || !lengths || !prefix || !staged || !staged_lengths)
+    return dpk::fail(DP_ERR_INVALID_ATTR, "stage_rows: null buffer");
+  const int64_t blocks = std::min<int64_t>((n + 7) / 8, 148LL * 8 * 4);
+  dpk::stage_rows_kernel<<<static_cast<int>(blocks), dpk::kThreads, 0, dpk::as_stream(stream)>>>(
+      tokens, offsets, lengths, order, n, prefix, staged, staged_lengths);
+  return dpk::launch_status("stage_rows");
+}
+
 extern "C" int dp_k_padded_batches(const int32_t* tokens, const int64_t* offsets, const int32_t* lengths,
                                    const int64_t* order, int64_t first_row, int64_t rows, int64_t batch,
                                    const int32_t* lmax_dev, const int64_t* boff_dev, int32_t pad_value, int32_t* out,

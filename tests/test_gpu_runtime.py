@@ -170,3 +170,29 @@ def test_output_independent_of_a_first_launch_head(dp, span, tiling):
     assert len(rest) == len(ref) - 11
     for (i0, p0), (i1, p1) in zip(ref[11:], rest):
         assert np.array_equal(i0, i1) and np.array_equal(p0.view(np.uint32), p1.view(np.uint32))
+
+
+def test_pinned_token_staging_across_epochs(dp, orc):
+    """Pinned-host token sources are staged into device memory once per
+    epoch plan (dp_k_stage_rows): over repeated epochs (plans built ahead
+    on the helper thread, retired behind) and a checkpoint restore, the
+    batches equal those of the same sequences in HBM."""
+    lens = orc.lengths(2500, 700, 9)
+    toks, _ = orc.tokens(lens, 9)
+    reg = dp.Registry()
+    reg.register_length_filter("len<=400", 400)
+    outs = []
+    for pinned in (False, True):
+        src = dp.Source.tokens_from_host(lens, toks, pinned=pinned)
+        base = dp.Dataset.token_sequences(reg, src).filter("len<=400").shuffle(500, 3)
+        got = []
+        for g in (base.padded_batch(40).repeat(3), base.batch(33).repeat(3),
+                  base.bucket_by_length([100, 250], [24, 16, 8]).repeat(3)):
+            got += [[b.numpy(0), b.numpy(1)] for b in dp.make_iterator(g, seed_override=2)]
+            it = dp.make_iterator(g, seed_override=2)
+            for _ in range(17):
+                it.get_next().release()
+            got += [[b.numpy(0), b.numpy(1)] for b in dp.restore(g, it.save())]
+        outs.append(got)
+    assert len(outs[0]) == len(outs[1])
+    assert all(np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) for a, b in zip(*outs))

@@ -377,7 +377,8 @@ class PipelineIterator {
   int64_t kernel_launches() const;      // sm_100a kernels issued so far
   int64_t batches_launched() const;     // batches covered by issued batch-stage launches
   struct Stats {
-    int64_t live_plans = 0, slots = 0, slot_bytes = 0, prefetch_depth = 0, group_batches = 0;
+    int64_t live_plans = 0, slots = 0, slot_bytes = 0, prefetch_depth = 0, group_batches = 0, max_depth = 0;
+    double producer_groups_per_s = 0, consumer_groups_per_s = 0, p_empty = 0;
   };
   Stats stats() const;
   // Checkpoint in the reference's DPC1 layout (checkpoint.hpp:36-49,

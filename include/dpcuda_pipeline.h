@@ -245,7 +245,21 @@ typedef struct {
   int64_t slot_bytes;     /* their device bytes */
   int64_t prefetch_depth; /* groups kept in flight */
   int64_t group_batches;  /* batches per fused launch */
+  /* AUTOTUNE (the reference's M/M/1/k model, model.cpp:29-42, 262-266) */
+  int64_t max_depth;              /* slots pre-allocated for the tuner */
+  double producer_groups_per_s;   /* device rate (CUDA-event self time, EWMA) */
+  double consumer_groups_per_s;   /* host request rate (EWMA) */
+  double p_empty;                 /* PEmpty(depth - 1, producer, consumer) */
 } dp_iterator_stats;
+/* Metrics() (runtime.hpp:46-51, 76): one row per graph node, root first. */
+typedef struct {
+  char path[192];
+  char label[96];
+  int64_t self_time_ns;
+  int64_t elements_produced;
+} dp_node_metrics;
+/* Fills up to cap rows; *count = the node count (rows beyond cap dropped). */
+int dp_iterator_metrics(const dp_iterator* it, dp_node_metrics* rows, int cap, int* count);
 int dp_iterator_get_stats(const dp_iterator* it, dp_iterator_stats* out);
 int64_t dp_iterator_root_delivered(const dp_iterator* it);
 uint64_t dp_iterator_base_seed(const dp_iterator* it);

@@ -524,7 +524,25 @@ int dp_iterator_get_stats(const dp_iterator* it, dp_iterator_stats* out) {
   DP_REQUIRE(it && out);
   return Guard([&] {
     const auto st = it->it->stats();
-    *out = dp_iterator_stats{st.live_plans, st.slots, st.slot_bytes, st.prefetch_depth, st.group_batches};
+    *out = dp_iterator_stats{st.live_plans,    st.slots,
+                             st.slot_bytes,    st.prefetch_depth,
+                             st.group_batches, st.max_depth,
+                             st.producer_groups_per_s, st.consumer_groups_per_s,
+                             st.p_empty};
+  });
+}
+int dp_iterator_metrics(const dp_iterator* it, dp_node_metrics* rows, int cap, int* count) {
+  DP_REQUIRE(it && count && (rows || cap == 0));
+  return Guard([&] {
+    const auto m = it->it->Metrics();
+    *count = static_cast<int>(m.size());
+    for (int i = 0; i < cap && i < static_cast<int>(m.size()); ++i) {
+      std::memset(&rows[i], 0, sizeof(rows[i]));
+      std::strncpy(rows[i].path, m[i].path.c_str(), sizeof(rows[i].path) - 1);
+      std::strncpy(rows[i].label, m[i].label.c_str(), sizeof(rows[i].label) - 1);
+      rows[i].self_time_ns = m[i].self_time_ns;
+      rows[i].elements_produced = m[i].elements_produced;
+    }
   });
 }
 int64_t dp_iterator_root_delivered(const dp_iterator* it) { return it ? it->it->root_delivered() : 0; }

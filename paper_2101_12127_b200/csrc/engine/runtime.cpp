@@ -37,6 +37,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <cmath>
 #include <condition_variable>
 #include <cstdio>
 #include <cstdlib>
@@ -149,6 +150,10 @@ class DevicePipeline {
     const size_t group_bytes = (batch_bytes_.first + batch_bytes_.second) * group_;
     depth_ = std::max<int64_t>(2, std::min<int64_t>(depth_, static_cast<int64_t>(opt_.slot_memory_budget /
                                                                                  std::max<size_t>(group_bytes, 1))));
+    max_depth_ = autotune_ ? std::clamp<int64_t>(static_cast<int64_t>(opt_.slot_memory_budget /
+                                                                      std::max<size_t>(group_bytes, 1)),
+                                                 2, 4)
+                           : depth_;
     if (span_epochs_) group_ = std::min<int64_t>(group_, std::max<int64_t>(1, epoch_count_ / std::max<int64_t>(L_.batch, 1)));
     // a first launch group of another size (then groups of group_ again)
     head_ = opt_.first_launch_batches;
@@ -158,6 +163,9 @@ class DevicePipeline {
         if (p.ready) cudaEventDestroy(p.ready);
       cudaStreamSynchronize(plan_stream_);
       plans_.clear();
+      DrainOpTimings(true);  // the sizing plan is not part of the stream's work
+      op_ns_total_.clear();
+      op_produced_.clear();
     }
   }
 
@@ -181,6 +189,10 @@ class DevicePipeline {
     plans_.clear();  // stream-ordered frees: before the streams go away
     cudaStreamSynchronize(plan_stream_);
     if (retire_ev_) cudaEventDestroy(retire_ev_);
+    for (auto& t : op_timed_) {
+      cudaEventDestroy(t.start);
+      cudaEventDestroy(t.end);
+    }
     cudaStreamDestroy(stream_);
     cudaStreamDestroy(plan_stream_);
     if (copy_stream_) cudaStreamDestroy(copy_stream_);
@@ -492,12 +504,41 @@ class DevicePipeline {
     st.slot_bytes = static_cast<int64_t>(slot_bytes_total_);
     st.prefetch_depth = depth_;
     st.group_batches = group_;
+    const TunerState t = Tuner();
+    st.max_depth = t.max_depth;
+    st.producer_groups_per_s = t.producer_groups_per_s;
+    st.consumer_groups_per_s = t.consumer_groups_per_s;
+    st.p_empty = t.p_empty;
     return st;
   }
 
  private:
+  // Folds the completed index-op timings into op_ns_total_ (wait: all).
+  void DrainOpTimings(bool wait) {
+    std::lock_guard lk(metrics_mu_);
+    size_t k = 0;
+    for (; k < op_timed_.size(); ++k) {
+      auto& t = op_timed_[k];
+      if (wait) cudaEventSynchronize(t.end);
+      else if (cudaEventQuery(t.end) != cudaSuccess) {
+        cudaGetLastError();
+        break;
+      }
+      float ms = 0;
+      if (cudaEventElapsedTime(&ms, t.start, t.end) == cudaSuccess) {
+        op_ns_total_.resize(L_.chain.size(), 0);
+        op_ns_total_[t.op] += static_cast<int64_t>(static_cast<double>(ms) * 1e6);
+      }
+      cudaGetLastError();
+      cudaEventDestroy(t.start);
+      cudaEventDestroy(t.end);
+    }
+    op_timed_.erase(op_timed_.begin(), op_timed_.begin() + static_cast<std::ptrdiff_t>(k));
+  }
+
   EpochPlan& Plan(int64_t e) {
     JoinPendingPlan();
+    DrainOpTimings(false);
     RetirePlansBefore(e);
     auto it = plans_.find(e);
     if (it != plans_.end()) return it->second;
@@ -518,7 +559,13 @@ class DevicePipeline {
     // how retirement orders the free after the batch kernels' last use)
     auto dalloc = [&](size_t bytes) { return DeviceAllocAsync(bytes, opt_.device, plan_stream_, plan_stream_); };
     auto alloc = [&](int64_t n) { return dalloc(sizeof(int64_t) * (n + tail)); };
-    for (const auto& op : L_.chain) {
+    for (size_t oi = 0; oi < L_.chain.size(); ++oi) {
+      const auto& op = L_.chain[oi];
+      // self time of this index op (its plan kernels; Metrics())
+      cudaEvent_t t0 = nullptr, t1 = nullptr;
+      CudaCheck(cudaEventCreate(&t0), "event");
+      CudaCheck(cudaEventCreate(&t1), "event");
+      CudaCheck(cudaEventRecord(t0, s), "event");
       switch (op.kind) {
         case IndexOp::Kind::kShard: {
           const int64_t m = count > op.b ? (count - op.b + op.a - 1) / op.a : 0;
@@ -585,6 +632,11 @@ class DevicePipeline {
         case IndexOp::Kind::kRepeat:
           break;
       }
+      CudaCheck(cudaEventRecord(t1, s), "event");
+      std::lock_guard lk(metrics_mu_);
+      op_timed_.push_back({static_cast<int>(oi), t0, t1});
+      if (op_produced_.size() < L_.chain.size()) op_produced_.resize(L_.chain.size(), 0);
+      op_produced_[oi] += count;
     }
     if (!cur && (span_epochs_ || L_.kind == BatchKind::kPadded)) {
       // materialise the identity so spanning batches can append the next head
@@ -879,6 +931,11 @@ class DevicePipeline {
   }
 
   std::shared_ptr<Slot> FindFreeSlot(bool may_grow) {
+    if (autotune_ && !slots_preallocated_) {
+      // every slot the tuner may use, once, so a depth change never allocates
+      slots_preallocated_ = true;
+      while (static_cast<int64_t>(slots_.size()) < max_depth_) NewSlot();
+    }
     for (auto& s : slots_) {
       // free = never used, or its release event was recorded (which happens
       // only after every unit was handed out and dropped, see Lease)
@@ -886,7 +943,7 @@ class DevicePipeline {
       if (!s->busy || s->release_recorded) return s;
     }
     const size_t need = (batch_bytes_.first + batch_bytes_.second) * std::max(group_, head_);
-    if (static_cast<int64_t>(slots_.size()) < depth_ || may_grow) {
+    if (static_cast<int64_t>(slots_.size()) < std::max(depth_, max_depth_) || may_grow) {
       if (slot_bytes_total_ + need > opt_.slot_memory_budget && !slots_.empty())
         throw PipelineError(ErrorCode::kInternal,
                             "prefetch slots exhausted: every device batch slot is still held by the consumer "
@@ -1340,18 +1397,120 @@ class DevicePipeline {
   }
 
  private:
+  // AUTOTUNE prefetch depth from the reference's model (SURVEY.md 8(f)
+  // next #3): the ring is an M/M/1/k queue (model.cpp:262-266, the kAsyncQueue
+  // case) with producer rate x = launch groups/s the device writes (CUDA-
+  // event self time of the batch stage, EWMA) and consumer rate y = groups/s
+  // the consumer asks for (host time between group boundaries, EWMA), both
+  // with RecordSelfTime's one-second half-life (model.cpp:47-64).  The
+  // buffered groups n are the smallest whose PEmpty (model.cpp:29-42) is
+  // <= 2%, or past which one more group lowers it by < 0.5% (a producer-
+  // bound ring); depth = n + 1 (the group being consumed), capped by the
+  // slots pre-allocated within slot_memory_budget at the first issue, so
+  // a depth change never allocates.
+  static double PEmpty(double n, double x, double y) {
+    const double r = x / y;
+    if (std::abs(r - 1.0) < 1e-9) return 1.0 / (n + 1.0);
+    return std::clamp((1.0 - r) / (1.0 - std::pow(r, n + 1.0)), 0.0, 1.0);
+  }
+  static void Ewma(double& acc, bool& has, std::chrono::steady_clock::time_point& last, double sample) {
+    const auto now = std::chrono::steady_clock::now();
+    if (!has) {
+      acc = sample;
+      has = true;
+    } else {
+      const double dt = std::chrono::duration<double, std::nano>(now - last).count();
+      const double w = std::min(std::exp2(-std::max(dt, 0.0) / 1e9), 0.95);
+      acc = w * acc + (1.0 - w) * sample;
+    }
+    last = now;
+  }
   void MaybeAutotune() {
+    const int64_t done_before = timed_groups_;
+    const int64_t ns_before = batch_ns_total_;
     DrainTimings(false);
-    if (!autotune_ || issued_count_ < 16 || issued_count_ % 16 != 0 || timed_groups_ == 0) return;
-    const double dev = static_cast<double>(batch_ns_total_) / timed_groups_;
-    const double host = static_cast<double>(host_issue_ns_) / issued_count_;
-    const size_t per = (batch_bytes_.first + batch_bytes_.second) * group_;
-    const int64_t by_mem = std::max<int64_t>(2, static_cast<int64_t>(opt_.slot_memory_budget / std::max<size_t>(per, 1)));
-    depth_ = std::clamp<int64_t>(static_cast<int64_t>(host / std::max(dev, 1.0)) + 2, 2, std::min<int64_t>(by_mem, 512));
+    if (timed_groups_ > done_before)
+      Ewma(prod_ns_, has_prod_, prod_last_, static_cast<double>(batch_ns_total_ - ns_before) /
+                                                static_cast<double>(timed_groups_ - done_before));
+    const auto now = std::chrono::steady_clock::now();
+    if (has_boundary_)
+      Ewma(cons_ns_, has_cons_, cons_last_, std::chrono::duration<double, std::nano>(now - last_boundary_).count());
+    last_boundary_ = now;
+    has_boundary_ = true;
+    if (!autotune_ || !has_prod_ || !has_cons_) return;
+    const double x = 1e9 / std::max(prod_ns_, 1.0), y = 1e9 / std::max(cons_ns_, 1.0);
+    int64_t n = 1;
+    while (n + 1 < max_depth_) {
+      const double p = PEmpty(static_cast<double>(n), x, y);
+      if (p <= 0.02 || p - PEmpty(static_cast<double>(n + 1), x, y) < 0.005) break;
+      ++n;
+    }
+    depth_ = std::clamp<int64_t>(n + 1, 2, max_depth_);
+    last_pempty_ = PEmpty(static_cast<double>(depth_ - 1), x, y);
   }
 
  public:
+  struct TunerState {
+    double producer_groups_per_s = 0, consumer_groups_per_s = 0, p_empty = 0;
+    int64_t depth = 0, max_depth = 0;
+  };
+  TunerState Tuner() const {
+    TunerState t;
+    t.producer_groups_per_s = has_prod_ ? 1e9 / std::max(prod_ns_, 1.0) : 0;
+    t.consumer_groups_per_s = has_cons_ ? 1e9 / std::max(cons_ns_, 1.0) : 0;
+    t.p_empty = last_pempty_;
+    t.depth = depth_;
+    t.max_depth = max_depth_;
+    return t;
+  }
+
+ private:
+
+ public:
   int64_t d2h_bytes() const { return d2h_bytes_; }
+
+  // Per-node rows in the reference's shape (runtime.hpp:46-51, Metrics()):
+  // path, label, self time, elements produced.  Self time is device time
+  // from CUDA events for the stages that run kernels (the fused batch stage;
+  // each index op's per-epoch plan kernels), host issue time for prefetch;
+  // maps fused into the batch stage report 0 (their work is the batch
+  // stage's).
+  std::vector<NodeMetricsRow> Metrics() {
+    DeviceGuard g(opt_.device);
+    DrainTimings(true);
+    DrainOpTimings(true);
+    std::vector<int64_t> op_ns(L_.chain.size(), 0);
+    {
+      std::lock_guard lk(metrics_mu_);
+      for (size_t i = 0; i < op_ns_total_.size() && i < op_ns.size(); ++i) op_ns[i] = op_ns_total_[i];
+    }
+    std::vector<NodeMetricsRow> rows;
+    for (const auto& path : L_.node_paths) {
+      const std::string label = path.substr(path.rfind('/') + 1, path.rfind('@') - path.rfind('/') - 1);
+      NodeMetricsRow r{path, label, 0, 0};
+      if (path == L_.batch_node_path) {
+        r.label += " (device: fused batch stage)";
+        r.self_time_ns = batch_ns_total_;
+        r.elements_produced = produced_;
+      } else if (label == "prefetch") {
+        r.label += " (device ring, depth " + std::to_string(depth_) + ")";
+        r.self_time_ns = host_issue_ns_;
+        r.elements_produced = produced_;
+      } else if (label == "repeat" && path == L_.node_paths.front()) {
+        r.elements_produced = produced_;
+      } else {
+        for (size_t i = 0; i < L_.chain.size(); ++i)
+          if (L_.chain[i].path == path) {
+            r.label += " (device: epoch plan)";
+            r.self_time_ns = op_ns[i];
+            std::lock_guard lk(metrics_mu_);
+            r.elements_produced = i < op_produced_.size() ? op_produced_[i] : 0;
+          }
+      }
+      rows.push_back(std::move(r));
+    }
+    return rows;
+  }
   // State shared with outstanding slot leases (they may outlive the pipeline).
   struct Shared {
     std::mutex mu;
@@ -1370,7 +1529,13 @@ class DevicePipeline {
   IteratorOptions opt_;
   cudaStream_t stream_ = nullptr, plan_stream_ = nullptr, copy_stream_ = nullptr, consumer_ = nullptr;
   int64_t depth_ = 2;
+  int64_t max_depth_ = 2;  // AUTOTUNE ceiling: the slots pre-allocated within the budget
   bool autotune_ = false;
+  bool slots_preallocated_ = false;
+  // AUTOTUNE model state (EWMAs of device ns per group, host ns per group)
+  double prod_ns_ = 0, cons_ns_ = 0, last_pempty_ = 0;
+  bool has_prod_ = false, has_cons_ = false, has_boundary_ = false;
+  std::chrono::steady_clock::time_point prod_last_{}, cons_last_{}, last_boundary_{};
   const bool debug_timing_ = std::getenv("DP_DEBUG_TIMING") != nullptr;
   int64_t cur_group_ = -1;            // group of the last batch handed out
   uint64_t seen_freed_ = 0;           // Shared::slots_freed at the last issue attempt
@@ -1402,6 +1567,14 @@ class DevicePipeline {
   std::vector<TimedLaunch> event_pool_;
   int64_t d2h_bytes_ = 0;
   bool done_ = false;
+  // index-op self time (plan kernels, built on the helper thread too)
+  struct OpTimed {
+    int op;
+    cudaEvent_t start, end;
+  };
+  std::mutex metrics_mu_;
+  std::vector<OpTimed> op_timed_;
+  std::vector<int64_t> op_ns_total_, op_produced_;
 };
 
 // ---------------------------------------------------------- PipelineIterator --
@@ -1450,9 +1623,7 @@ int64_t PipelineIterator::root_delivered() const {
 
 std::vector<NodeMetricsRow> PipelineIterator::Metrics() const {
   std::lock_guard lock(mu_);
-  std::vector<NodeMetricsRow> rows;
-  rows.push_back({"/", "device batch stage", impl_->batch_time_ns(), impl_->delivered()});
-  return rows;
+  return impl_->Metrics();
 }
 
 void* PipelineIterator::stream() const { return impl_->stream(); }

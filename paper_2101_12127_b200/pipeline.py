@@ -50,7 +50,13 @@ class dp_iterator_options(ctypes.Structure):
 
 class dp_iterator_stats(ctypes.Structure):
     _fields_ = [("live_plans", c_i64), ("slots", c_i64), ("slot_bytes", c_i64), ("prefetch_depth", c_i64),
-                ("group_batches", c_i64)]
+                ("group_batches", c_i64), ("max_depth", c_i64), ("producer_groups_per_s", ctypes.c_double),
+                ("consumer_groups_per_s", ctypes.c_double), ("p_empty", ctypes.c_double)]
+
+
+class dp_node_metrics(ctypes.Structure):
+    _fields_ = [("path", ctypes.c_char * 192), ("label", ctypes.c_char * 96), ("self_time_ns", c_i64),
+                ("elements_produced", c_i64)]
 
 
 _SIGS = {
@@ -120,6 +126,7 @@ _SIGS = {
     "dp_iterator_stream": [c_vp], "dp_iterator_kernel_launches": [c_vp], "dp_iterator_prefetch_depth": [c_vp],
     "dp_iterator_batch_stage_timing": [c_vp, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64)],
     "dp_iterator_batches_launched": [c_vp], "dp_iterator_get_stats": [c_vp, ctypes.POINTER(dp_iterator_stats)],
+    "dp_iterator_metrics": [c_vp, ctypes.POINTER(dp_node_metrics), c_int, ctypes.POINTER(c_int)],
     "dp_iterator_root_delivered": [c_vp], "dp_iterator_base_seed": [c_vp],
     "dp_iterator_describe": [c_vp, ctypes.c_char_p, c_size], "dp_iterator_destroy": [c_vp],
 }
@@ -607,7 +614,16 @@ class Iterator:
         """dp_iterator_get_stats: live epoch plans, slots, slot bytes, depth, batches per launch."""
         st = dp_iterator_stats()
         _check(L().dp_iterator_get_stats(self.h, ctypes.byref(st)))
-        return {f: int(getattr(st, f)) for f, _ in dp_iterator_stats._fields_}
+        return {f: (getattr(st, f) if t is ctypes.c_double else int(getattr(st, f)))
+                for f, t in dp_iterator_stats._fields_}
+
+    def metrics(self) -> list:
+        """Metrics() (runtime.hpp:76): [(path, label, self_time_ns, elements_produced)] root first."""
+        rows = (dp_node_metrics * 32)()
+        n = c_int()
+        _check(L().dp_iterator_metrics(self.h, rows, 32, ctypes.byref(n)))
+        return [(r.path.decode(), r.label.decode(), int(r.self_time_ns), int(r.elements_produced))
+                for r in rows[:min(n.value, 32)]]
 
     @property
     def root_delivered(self):

@@ -196,3 +196,77 @@ def test_pinned_token_staging_across_epochs(dp, orc):
         outs.append(got)
     assert len(outs[0]) == len(outs[1])
     assert all(np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) for a, b in zip(*outs))
+
+
+def test_autotuned_depth_follows_the_queue_model(dp):
+    """AUTOTUNE: the ring depth comes from the
+    reference's M/M/1/k model (PEmpty, model.cpp:29-42, 262-266) over the
+    measured producer (CUDA-event device time per group) and consumer (host
+    time per group) rates, inside slots pre-allocated at the first issue --
+    a consumer at about the producer's rate gets the deepest ring, a much
+    slower one the minimum and (the reference's test_parallel.cpp:169-190)
+    no wait: the ring refills while it works.  Slots never grow."""
+    import time
+    reg = dp.Registry()
+    reg.register_random_crop_flip("crop", 224, 224, seed=7, flip=True)
+    reg.register_normalize("norm")
+    src = dp.Source.synthetic_images(2048, 256, 256)
+    g, _ = (dp.Dataset.tensor_slices(reg, src).shuffle(1000, 42).map("crop").map("norm").batch(64).repeat(-1)
+            .prefetch(-1).optimize())
+
+    def run(sleep_s, n=240):
+        it = dp.make_iterator(g, seed_override=1, launch_batches=2)
+        waits = []
+        for k in range(n):
+            b = it.get_next()
+            t = time.perf_counter()
+            b.wait()
+            waits.append(time.perf_counter() - t)
+            b.release()
+            if sleep_s:
+                time.sleep(sleep_s)
+        return it.stats(), float(np.mean(waits[n // 2:]))
+
+    fast, _ = run(0)
+    assert fast["slots"] == fast["max_depth"] >= 3  # pre-allocated, never grown
+    per_group = 1.0 / fast["producer_groups_per_s"]  # device seconds per launch group (2 batches)
+    equal, _ = run(per_group / 2)  # the consumer takes a group about as fast as the device writes one
+    slow, slow_wait = run(per_group * 10)
+    def pempty(n, x, y):  # model.cpp:29-42
+        r = x / y
+        return 1.0 / (n + 1.0) if abs(r - 1.0) < 1e-9 else min(max((1.0 - r) / (1.0 - r ** (n + 1.0)), 0.0), 1.0)
+
+    def model_depth(st):
+        x, y, n = st["producer_groups_per_s"], st["consumer_groups_per_s"], 1
+        while n + 1 < st["max_depth"]:
+            p = pempty(n, x, y)
+            if p <= 0.02 or p - pempty(n + 1, x, y) < 0.005:
+                break
+            n += 1
+        return min(max(n + 1, 2), st["max_depth"])
+
+    for st in (fast, equal, slow):
+        assert st["slots"] == st["max_depth"]
+        assert st["prefetch_depth"] == model_depth(st), st
+    assert equal["prefetch_depth"] == equal["max_depth"] > slow["prefetch_depth"], (equal, slow)
+    assert slow["p_empty"] < 0.02 and slow_wait < per_group / 4, (slow, slow_wait, per_group)
+
+
+def test_metrics_rows_per_node(dp):
+    """Metrics() (runtime.hpp:76): one row per graph node, root first, with
+    CUDA-event self time for the device stages."""
+    reg = dp.Registry()
+    reg.register_random_crop_flip("crop", 24, 24, seed=1, flip=True)
+    reg.register_normalize("norm")
+    src = dp.Source.synthetic_images(1000, 32, 32)
+    g, _ = (dp.Dataset.tensor_slices(reg, src).shard(2, 1).shuffle(300, 5).map("crop").map("norm").batch(50)
+            .repeat(2).prefetch(-1).optimize())
+    it = dp.make_iterator(g, seed_override=1)
+    n = sum(1 for b in it)
+    rows = it.metrics()
+    paths = [r[0] for r in rows]
+    assert paths[0].startswith("/prefetch@0") and paths[-1].endswith("tensor_slices@0"), paths
+    by = {r[0].rsplit("/", 1)[1].split("@")[0]: r for r in rows}
+    assert by["map_and_batch"][2] > 0 and by["map_and_batch"][3] == n == 20
+    assert by["shuffle"][2] > 0 and by["shuffle"][3] == 1000  # 500 per epoch, 2 epochs planned
+    assert by["shard"][3] == 1000

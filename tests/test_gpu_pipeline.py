@@ -1011,9 +1011,8 @@ def test_edge_cases(dp, orc):
 
 def test_unsupported_graph_fails_loudly(dp):
     reg = dp.Registry()
-    reg.register_random_crop_flip("crop", 16, 16)
-    src = dp.Source.synthetic_images(10, 32, 32)
-    g = dp.Dataset.tensor_slices(reg, src).map("crop").batch(4)  # a u8 crop alone: no device kernel
+    src = dp.Source.synthetic_tokens(100, 50, 1, 1)
+    g = dp.Dataset.token_sequences(reg, src).repeat(2).padded_batch(8)  # batches across epochs: not lowered
     with pytest.raises(Exception) as e:
         dp.make_iterator(g)
     assert "device lowering" in str(e.value)

@@ -926,17 +926,25 @@ static int resize_impl(const uint8_t* images, int64_t num_images, int in_h, int 
       p.q_per_row = out_w / 7;  // groups per row (one lane each)
       p.q_stride = 32;
       p.rpp = warps;
-      p.band_rows = env_int("DP_DEV_RESIZE_PBAND", p.rpp);
-      if (p.band_rows > out_h) p.band_rows = out_h;
-      p.bands = (out_h + p.band_rows - 1) / p.band_rows;
-      p.stages = env_int("DP_DEV_STAGES", kResizeStages);
-      int prow = static_cast<int>(p.band_rows * sc) + 3;
-      if (prow > in_h) prow = in_h;
-      p.stage_bytes = static_cast<int>(((static_cast<size_t>(prow) * in_w * 3 + 127) / 128) * 128);
+      // two output rows per consumer warp per band (tools/dev/k4sweep*.sh:
+      // 43.0 vs 44.8 us per 256-image batch at 320 -> 224), one when the
+      // larger stage does not fit
       const size_t taps16 = ((taps + 15) / 16) * 16;
       const size_t stg = static_cast<size_t>(p.rpp) * out_w * 3 * sizeof(float);
-      while (p.stages > 2 && static_cast<size_t>(p.stages) * p.stage_bytes + taps16 + stg > kSmemBudgetMax) --p.stages;
-      const size_t psmem = static_cast<size_t>(p.stages) * p.stage_bytes + taps16 + stg;
+      size_t psmem = 0;
+      for (int rows_per_warp : {2, 1}) {
+        p.band_rows = env_int("DP_DEV_RESIZE_PBAND", rows_per_warp * p.rpp);
+        if (p.band_rows > out_h) p.band_rows = out_h;
+        p.bands = (out_h + p.band_rows - 1) / p.band_rows;
+        p.stages = env_int("DP_DEV_STAGES", kResizeStages);
+        int prow = static_cast<int>(p.band_rows * sc) + 3;
+        if (prow > in_h) prow = in_h;
+        p.stage_bytes = static_cast<int>(((static_cast<size_t>(prow) * in_w * 3 + 127) / 128) * 128);
+        while (p.stages > 2 && static_cast<size_t>(p.stages) * p.stage_bytes + taps16 + stg > kSmemBudgetMax)
+          --p.stages;
+        psmem = static_cast<size_t>(p.stages) * p.stage_bytes + taps16 + stg;
+        if (psmem <= kSmemBudgetMax) break;
+      }
       if (psmem <= kSmemBudgetMax) {
 #define DP_LAUNCH_P(W)                                                                                   \
   if (warps == W)                                                                                        \

@@ -133,6 +133,13 @@ int dp_k_crop_flip_normalize_batch_ex(const uint8_t* images, int64_t num_images,
                                       int64_t id_stride, int64_t id_block, uint64_t udf_seed, int crop_h,
                                       int crop_w, int do_flip, const float mean[3], const float stdv[3],
                                       int64_t* out_ids, float* out, void* stream);
+/* K3 with center_crop offsets ((in_h - crop_h) / 2, (in_w - crop_w) / 2), no
+ * flip: center_crop >> normalize (an eval-time chain). */
+int dp_k_center_crop_normalize_batch_ex(const uint8_t* images, int64_t num_images, int in_h, int in_w,
+                                        const int64_t* order, int64_t first, int64_t rows, int64_t id_base,
+                                        int64_t id_stride, int64_t id_block, int crop_h, int crop_w,
+                                        const float mean[3], const float stdv[3], int64_t* out_ids, float* out,
+                                        void* stream);
 int dp_k_resize_normalize_batch_ex(const uint8_t* images, int64_t num_images, int in_h, int in_w,
                                    const int64_t* order, int64_t first, int64_t rows, int64_t id_base,
                                    int64_t id_stride, int64_t id_block, int out_h, int out_w,

@@ -374,6 +374,10 @@ Lowered Lower(const DatasetGraph& g, const UdfRegistry& reg) {
       L.kind = BatchKind::kCrop;
       L.crop = st[0];
       L.norm = st[1];
+    } else if (st.size() == 2 && st[0].op == MapStep::Op::kCenterCrop && st[1].op == MapStep::Op::kNormalize) {
+      L.kind = BatchKind::kCrop;  // K3 with center offsets
+      L.crop = st[0];
+      L.norm = st[1];
     } else if (st.size() == 2 && st[0].op == MapStep::Op::kResizeBilinear && st[1].op == MapStep::Op::kNormalize) {
       L.kind = BatchKind::kResize;
       L.resize = st[0];

@@ -1047,7 +1047,13 @@ class DevicePipeline {
         const auto& src = *L_.source;
         const int oh = static_cast<int>(L_.kind == BatchKind::kCrop ? L_.crop.out_h : L_.resize.out_h);
         const int ow = static_cast<int>(L_.kind == BatchKind::kCrop ? L_.crop.out_w : L_.resize.out_w);
-        if (L_.kind == BatchKind::kCrop)
+        if (L_.kind == BatchKind::kCrop && L_.crop.op == MapStep::Op::kCenterCrop)
+          KCheck(dp_k_center_crop_normalize_batch_ex(P<uint8_t>(src.values), src.count, static_cast<int>(src.h),
+                                                     static_cast<int>(src.w), order, row0, rows_total, src.shard_index,
+                                                     src.shard_count, src.shard_block, oh, ow, mean, stdv,
+                                                     P<int64_t>(slot->a), P<float>(slot->b), stream_),
+                 "K3 center");
+        else if (L_.kind == BatchKind::kCrop)
           KCheck(dp_k_crop_flip_normalize_batch_ex(P<uint8_t>(src.values), src.count, static_cast<int>(src.h),
                                                    static_cast<int>(src.w), order, row0, rows_total, src.shard_index,
                                                    src.shard_count, src.shard_block, L_.crop.seed, oh, ow, L_.crop.flip ? 1 : 0, mean,

@@ -74,8 +74,9 @@ crop_generic_kernel(ImageArgs a, uint64_t seed, int do_flip, int sstride) {
   const int64_t row = a.order ? a.order[a.first + j] : a.first + j;
   if (row < 0 || row >= a.num_images) return;  // engine orders are in range by construction
   const int64_t id = a.ids.of(row);  // element id (sharded residency)
-  CropParams cp = crop_params(seed, id, a.in_h, a.in_w, a.out_h, a.out_w);
-  if (!do_flip) cp.flip = 0;
+  CropParams cp = do_flip < 0 ? CropParams{(a.in_h - a.out_h) / 2, (a.in_w - a.out_w) / 2, 0}  // center
+                              : crop_params(seed, id, a.in_h, a.in_w, a.out_h, a.out_w);
+  if (do_flip <= 0) cp.flip = 0;
   if (band == 0 && threadIdx.x == 0) a.out_ids[j] = id;
 
   const int y_begin = band * kCropBandRows;
@@ -311,6 +312,7 @@ struct FastArgs {
   int stage_stride, stage_bytes, stages;
   uint64_t seed;
   int do_flip;
+  int center;  // K3: center_crop offsets instead of Philox draws
   NormConsts nc;
   RowIds ids;  // element id of resident row r = ids.of(r)
 };
@@ -362,7 +364,10 @@ struct CropOp {
     p.id = valid ? a.ids.of(row) : -1;
     p.nrows = min(a.band_rows, a.out_h - p.band * a.band_rows);
     CropParams cp{0, 0, 0};
-    if (valid) cp = crop_params(a.seed, p.id, a.in_h, a.in_w, a.out_h, a.out_w);
+    if (valid) {
+      if (a.center) cp = CropParams{(a.in_h - a.out_h) / 2, (a.in_w - a.out_w) / 2, 0};  // center_crop
+      else cp = crop_params(a.seed, p.id, a.in_h, a.in_w, a.out_h, a.out_w);
+    }
     const int start = cp.ox * 3;
     p.shift = start & 15;
     p.src_row = cp.oy + p.band * a.band_rows;  // first source row
@@ -871,7 +876,8 @@ static int crop_impl(const uint8_t* images, int64_t num_images, int in_h, int in
                            out, env_int("DP_DEV_CROP_BAND", kFastCropBandRows), kCropStages);
     f.ids = ids;
     f.seed = udf_seed;
-    f.do_flip = do_flip;
+    f.do_flip = do_flip > 0 ? 1 : 0;
+    f.center = do_flip < 0 ? 1 : 0;
     f.stage_stride = ((crop_w * 3 + 15 + 15) / 16) * 16;
     f.stage_bytes = ((f.band_rows * f.stage_stride + 127) / 128) * 128;
     const size_t taps = static_cast<size_t>(crop_h) * sizeof(RowTap);
@@ -999,6 +1005,18 @@ extern "C" int dp_k_crop_flip_normalize_batch_ex(const uint8_t* images, int64_t 
     return fail(DP_ERR_INVALID_ATTR, "crop_flip_normalize: bad sharded residency (id_base/id_stride/id_block)");
   return crop_impl(images, num_images, in_h, in_w, order, first, rows, udf_seed, crop_h, crop_w, do_flip, mean, stdv,
                    out_ids, out, stream, RowIds{id_base, id_stride, id_block});
+}
+
+extern "C" int dp_k_center_crop_normalize_batch_ex(const uint8_t* images, int64_t num_images, int in_h, int in_w,
+                                                   const int64_t* order, int64_t first, int64_t rows, int64_t id_base,
+                                                   int64_t id_stride, int64_t id_block, int crop_h, int crop_w,
+                                                   const float mean[3], const float stdv[3], int64_t* out_ids,
+                                                   float* out, void* stream) {
+  if (id_stride < 1 || id_block < 1 || id_base < 0 || id_base >= id_stride)
+    return fail(DP_ERR_INVALID_ATTR, "center_crop_normalize: bad sharded residency (id_base/id_stride/id_block)");
+  // do_flip = -1 selects the center offsets inside crop_impl (no draws, no flip)
+  return crop_impl(images, num_images, in_h, in_w, order, first, rows, 0, crop_h, crop_w, -1, mean, stdv, out_ids,
+                   out, stream, RowIds{id_base, id_stride, id_block});
 }
 
 extern "C" int dp_k_resize_normalize_batch(const uint8_t* images, int64_t num_images, int in_h, int in_w,

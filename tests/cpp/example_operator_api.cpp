@@ -80,5 +80,31 @@ int main() {
     ++nb;
   }
   std::printf("bucket rows=%lld batches=%lld\n", static_cast<long long>(rows), static_cast<long long>(nb));
+
+  // (image, label) elements through RandomResizedCrop (crop >> resize >>
+  // normalize, K9), with per-node metrics and the tuner's state
+  std::vector<int64_t> labels(512);
+  for (size_t i = 0; i < labels.size(); ++i) labels[i] = static_cast<int64_t>(i % 10);
+  reg.RegisterRandomCropFlip("crop160", 160, 160, 3, true);
+  reg.RegisterResizeBilinear("resize224", 224, 224);
+  DatasetGraph rrc = ops::TensorSlices(WithLabels(SynthImages(512, 256, 256, 0x5EED), labels.data(), 512), reg);
+  rrc = ops::Map(ops::Map(ops::Map(ops::Shuffle(rrc, 128, 9, reg), "crop160", 1, reg), "resize224", 1, reg), "norm",
+                 1, reg);
+  rrc = ops::Prefetch(ops::Batch(rrc, 64, false, reg), kAutotune, reg);
+  auto rit = MakeIterator(Optimize(rrc, RuleSet::Default(), reg).first, reg, o);
+  int64_t label_sum = 0, imgs = 0;
+  std::vector<int64_t> lab(64);
+  while (auto e = rit->GetNext()) {
+    const Tensor& l = e->component(2).tensor();
+    cudaEventSynchronize(static_cast<cudaEvent_t>(l.ready));
+    cudaMemcpy(lab.data(), l.data, l.nbytes(), cudaMemcpyDeviceToHost);
+    for (int64_t k = 0; k < l.shape[0]; ++k) label_sum += lab[k];
+    imgs += e->component(1).tensor().shape[0];
+  }
+  std::printf("rrc images=%lld label_sum=%lld shape=%s\n", static_cast<long long>(imgs),
+              static_cast<long long>(label_sum), rrc.element_spec().ToString().c_str());
+  for (const auto& row : rit->Metrics())
+    std::printf("metrics %s %s self_ns=%lld produced=%lld\n", row.path.c_str(), row.label.c_str(),
+                static_cast<long long>(row.self_time_ns), static_cast<long long>(row.elements_produced));
   return ia == ib ? 0 : 1;
 }

@@ -92,7 +92,7 @@ def test_chain_equals_the_reference(dp, orc, name):
 
 def test_chain_kinds_lower_to_the_expected_kernels(dp):
     want = {"u8_batch": "K9 gather_copy", "crop_only": "K9 image_chain", "crop_resize_normalize": "K9 image_chain",
-            "crop_flip_normalize_labels": "K3", "resize_normalize_labels": "K4"}
+            "crop_flip_normalize_labels": "K3", "resize_normalize_labels": "K4", "center_crop_normalize_labels": "K3"}
     for name, kernel in want.items():
         case = [c for c in GOLD["cases"] if c["name"] == name][0]
         g, _ = build(dp, case)

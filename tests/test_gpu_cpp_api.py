@@ -28,3 +28,7 @@ def test_cpp_example_known_answers(tmp_path):
     golden = json.load(open(os.path.join(ROOT, "tests", "golden", "golden.json")))["serialize"][0]
     assert f"fingerprint={golden['fingerprint']} roundtrip=1" in out.stdout
     assert "bucket rows=5000" in out.stdout
+    # labels ride through the K9 chain: sum of i % 10 over 512 images
+    assert "rrc images=512 label_sum=2296 " in out.stdout, out.stdout
+    assert "float32[?,224,224,3]" in out.stdout or "224,224,3" in out.stdout
+    assert "metrics /prefetch@0" in out.stdout

@@ -94,3 +94,49 @@ def test_full_epoch_digest_independent_of_launch_tiling(dp):
     for opts in ({"launch_batches": 1}, {"launch_batches": 7, "first_launch_batches": 3}):
         _, _, id_dig, pix_dig = _epoch_digests(dp, g, **opts)
         assert (id_dig, pix_dig) == (c["ids"], c["pixels"]), opts
+
+
+TOK = json.load(open(os.path.join(HERE, "golden", "token_digests.json")))
+
+
+@pytest.mark.parametrize("case", ["cfg4", "cfg4r", "cfg4b"])
+def test_full_epoch_every_token_matches_the_oracle(dp, case):
+    """A whole epoch of 1M sequences: every output word of the padded /
+    ragged / bucketed batches (padding included) and every row length /
+    split, digested on the device, equals the oracle's digests
+    (tests/golden/token_digests.json)."""
+    import torch
+    from paper_2101_12127_b200 import _capi
+    c = TOK["cases"][case]
+    reg = dp.Registry()
+    reg.register_length_filter("keep", TOK["keep"])
+    src = dp.Source.synthetic_tokens(TOK["n"], TOK["max_len"], TOK["seed"], TOK["seed"])
+    g = dp.Dataset.token_sequences(reg, src).filter("keep")
+    if case == "cfg4":
+        g = g.padded_batch(128)
+    elif case == "cfg4r":
+        g = g.batch(128)
+    else:
+        g = g.shuffle(10000, 42).bucket_by_length([128, 256, 384], [256, 128, 96, 64])
+    it = dp.make_iterator(g.prefetch(-1), seed_override=1)
+    L = _capi.lib()
+    dig = torch.zeros(2, dtype=torch.int64, device="cuda")
+    p0 = p1 = n = 0
+    for b in it:
+        (_, s0, ptr0, _), (_, s1, ptr1, _) = b.components[:2]
+        w0 = s0[0] * (s0[1] if len(s0) > 1 else 1)
+        _capi.check(L.dp_k_word_digest(ctypes.c_void_p(ptr0), w0, p0, ctypes.c_void_p(dig.data_ptr()),
+                                       ctypes.c_void_p(it.stream)))
+        fn = L.dp_k_order_digest if case == "cfg4r" else L.dp_k_word_digest  # row splits are int64
+        _capi.check(fn(ctypes.c_void_p(ptr1), s1[0], p1, ctypes.c_void_p(dig.data_ptr() + 8), ctypes.c_void_p(it.stream)))
+        p0 += w0
+        p1 += s1[0]
+        n += 1
+        b.release()
+    torch.cuda.synchronize()
+    v = [f"{int(x) & (2 ** 64 - 1):016x}" for x in dig.cpu().tolist()]
+    assert n == c["batches"]
+    if case == "cfg4r":
+        assert p0 == c["tokens"] and v == [c["values"], c["splits"]]
+    else:
+        assert p0 == c["words"] and v == [c["tokens"], c["lengths"]]

@@ -352,3 +352,25 @@ def test_chain_goldens_equal_the_restatement(orc):
         assert f"{Oracle.order_digest(imgs.reshape(-1).view(np.uint32)):016x}" == case["images"], case["name"]
         b = gold["batch"]
         assert case["batch_sizes"] == [min(b, n - k) for k in range(0, n, b)]
+
+
+def test_token_digest_goldens_reproduce():
+    """tests/golden/token_digests.json (the GPU full-epoch token parity
+    target) recomputed from the oracle for the ragged case (~3 s)."""
+    import json
+    import os
+    import sys
+    here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    sys.path.insert(0, here)
+    import make_token_digests as m
+    from tests.oracle_lib import Oracle
+    gold = json.load(open(os.path.join(here, "token_digests.json")))["cases"]["cfg4r"]
+    orc = Oracle()
+    lens = orc.lengths(m.N, m.MAX_LEN, m.SEED)
+    kept = orc.filter_len_le(lens, m.KEEP)
+    acc = pos = 0
+    for k in range(0, kept.size, m.BATCH):
+        toks = m.row_tokens(kept[k:k + m.BATCH], lens)
+        acc = (acc + m.digest(toks, pos)) % 2 ** 64
+        pos += toks.size
+    assert pos == gold["tokens"] and f"{acc:016x}" == gold["values"]

@@ -334,6 +334,17 @@ int dp_image_chain_output(const dp_image_chain* chain, int* out_h, int* out_w, i
 int dp_k_image_chain_batch(const uint8_t* images, int64_t num_images, const int64_t* order, int64_t first,
                            int64_t rows, int64_t id_base, int64_t id_stride, int64_t id_block,
                            const dp_image_chain* chain, int64_t* out_ids, void* out, void* stream);
+/* Which kernel runs a chain on HBM-resident, 16-byte aligned buffers: 10  */
+/* (K10, below) or 9 (K9).                                                 */
+int dp_image_chain_kernel(const dp_image_chain* chain, int* kernel);
+/* K10 (k_roll.cu): the resize chains [crop A] -> resize -> [crop B] ->     */
+/*     [one pixel op] whose column map is periodic (win_w : mid_w = 10:7,   */
+/*     8:7, 5:7, 5:4), run by dp_k_image_chain_batch: horizontal blends     */
+/*     computed once per (source row, column) and rolled in registers.      */
+/* Whether normalize(mean, std)'s two-FMA division equals IEEE division    */
+/* for every fp32 in [+0, 255] (checked exhaustively on the device at first */
+/* use, cached); the kernels use IEEE division where it does not.          */
+int dp_fast_div_proven(const float mean[3], const float stdv[3], int* proven);
 /* Batch with no map (BatchIterator over (id, u8 image), runtime.cpp:579-
  * 637): out[j] = images[p_j] byte for byte (image_bytes each). */
 int dp_k_gather_copy_batch(const uint8_t* images, int64_t num_images, int64_t image_bytes, const int64_t* order,

@@ -46,6 +46,9 @@ _SIGS = {
     "dp_k_word_digest": (c_int, [c_vp, c_i64, c_i64, c_vp, c_vp]),
     "dp_k_synth_images": (c_int, [c_vp, c_u64, c_u64, c_u64, c_u64, c_vp]),
     "dp_k_synth_tokens": (c_int, [c_vp, c_vp, c_i64, c_u64, c_vp]),
+    "dp_k_image_chain_batch": (c_int, [c_vp, c_i64, c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "dp_image_chain_kernel": (c_int, [c_vp, ctypes.POINTER(c_int)]),
+    "dp_fast_div_proven": (c_int, [c_fp, c_fp, ctypes.POINTER(c_int)]),
 }
 
 
@@ -89,6 +92,51 @@ def declared_symbols() -> list[str]:
                 text = re.sub(r"/\*.*?\*/", "", f.read(), flags=re.S)
             names += re.findall(r"\b(dp_\w+)\s*\(", text)
     return sorted(set(names))
+
+
+class ImageChain(ctypes.Structure):
+    """dp_image_chain (include/dpcuda.h): [crop A][pixel ops][resize][crop B][pixel ops]."""
+    _fields_ = [("in_h", c_int), ("in_w", c_int),
+                ("pre_mode", c_int), ("pre_h", c_int), ("pre_w", c_int), ("pre_flip", c_int), ("pre_seed", c_u64),
+                ("resize", c_int), ("rs_h", c_int), ("rs_w", c_int),
+                ("post_mode", c_int), ("post_h", c_int), ("post_w", c_int), ("post_flip", c_int),
+                ("post_seed", c_u64),
+                ("num_pre_ops", c_int), ("num_post_ops", c_int), ("op_kind", c_int * 4),
+                ("op_a", (ctypes.c_float * 3) * 4), ("op_b", (ctypes.c_float * 3) * 4), ("out_f32", c_int)]
+
+    @classmethod
+    def from_steps(cls, steps, in_h, in_w):
+        """The descriptor of a chain given as oracle steps (tests/oracle_lib.steps_array's tuples), the
+        way the engine lowers map chains (csrc/engine/lowering.cpp LowerImageChain)."""
+        c = cls()
+        c.in_h, c.in_w = in_h, in_w
+        nops = 0
+        for st in steps:
+            kind = st[0]
+            if kind in ("random_crop", "center_crop"):
+                mode = 1 if kind == "random_crop" else 2
+                if not c.resize and not c.pre_mode:
+                    c.pre_mode, c.pre_h, c.pre_w = mode, st[1], st[2]
+                    if mode == 1:
+                        c.pre_seed, c.pre_flip = st[3], int(st[4])
+                else:
+                    c.post_mode, c.post_h, c.post_w = mode, st[1], st[2]
+                    if mode == 1:
+                        c.post_seed, c.post_flip = st[3], int(st[4])
+            elif kind == "resize":
+                c.resize, c.rs_h, c.rs_w = 1, st[1], st[2]
+            else:
+                a, b = ((0, 0, 0), (1, 1, 1)) if kind == "cast" else (st[1], st[2])
+                c.op_kind[nops] = 1 if kind == "affine" else 0
+                c.op_a[nops][:] = [float(x) for x in a]
+                c.op_b[nops][:] = [float(x) for x in b]
+                if c.resize:
+                    c.num_post_ops += 1
+                else:
+                    c.num_pre_ops += 1
+                nops += 1
+        c.out_f32 = 1 if (c.resize or nops) else 0
+        return c
 
 
 def floats3(vals) -> ctypes.Array:

@@ -25,6 +25,8 @@
 #include <string>
 
 #include "common.cuh"
+#include "fastdiv.hpp"
+#include "roll.hpp"
 #include "status.hpp"
 
 namespace dpk {
@@ -375,6 +377,12 @@ extern "C" int dp_k_image_chain_batch(const uint8_t* images, int64_t num_images,
     return fail(DP_ERR_INVALID_ATTR, "image_chain: bad sharded residency (id_base/id_stride/id_block)");
   if (rows == 0) return DP_OK;
   if (!images || !out_ids || !out || num_images < 1) return fail(DP_ERR_INVALID_ATTR, "image_chain: null buffer");
+  // resize chains over a periodic column map: K10 (k_roll.cu)
+  if (f32) {
+    const int rc = roll_chain_batch(images, num_images, order, first, rows, id_base, id_stride, id_block, chain, oh, ow,
+                                    out_ids, static_cast<float*>(out), as_stream(stream));
+    if (rc != 1) return rc;
+  }
   ChainArgs a{};
   a.images = images;
   a.order = order;
@@ -434,23 +442,15 @@ extern "C" int dp_k_image_chain_batch(const uint8_t* images, int64_t num_images,
   };
   if (qn > 1024) return fail(DP_ERR_INVALID_ATTR, "image_chain: output rows wider than 4096 values");
   // op 0 sees u8 taps (or their blend when it follows the resize): values
-  // in [0, 255]; fast division where tools/prove_fast_div.c covers the
-  // constants (the ImageNet mean / std per channel, and cast's 0 / 1)
+  // in [0, 255]; fast division where its equality with IEEE division is
+  // proven for the constants (the ImageNet mean / std and cast's 0 / 1
+  // offline by tools/prove_fast_div.c, anything else on the device at first
+  // use: fastdiv.hpp)
   {
-    const float M[3] = {123.675f, 116.28f, 103.53f}, S[3] = {58.395f, 57.12f, 57.375f};
     const int nops = chain->num_pre_ops + chain->num_post_ops;
     for (int k = 0; k < nops; ++k)
       for (int c = 0; c < 3; ++c) a.op_rcp[k][c] = 1.0f / chain->op_b[k][c];
-    if (nops > 0 && chain->op_kind[0] == 0) {
-      bool proven = true;
-      for (int c = 0; c < 3; ++c) {
-        const float m = chain->op_a[0][c], sd = chain->op_b[0][c];
-        const bool imagenet = std::memcmp(&m, &M[c], 4) == 0 && std::memcmp(&sd, &S[c], 4) == 0;
-        const bool cast = m == 0.0f && !std::signbit(m) && sd == 1.0f;
-        proven = proven && (imagenet || cast);
-      }
-      if (proven) a.fast_mask = 1u;
-    }
+    if (nops > 0 && chain->op_kind[0] == 0 && fast_div_proven(chain->op_a[0], chain->op_b[0])) a.fast_mask = 1u;
   }
   a.scale_y = static_cast<float>(a.win_h) / static_cast<float>(a.mid_h);
   a.scale_x = static_cast<float>(a.win_w) / static_cast<float>(a.mid_w);

@@ -19,6 +19,8 @@
 #include <tuple>
 
 #include "common.cuh"
+#include "fastdiv.hpp"
+#include "roll.hpp"
 #include "status.hpp"
 
 namespace dpk {
@@ -871,6 +873,26 @@ static int crop_impl(const uint8_t* images, int64_t num_images, int in_h, int in
     return fail(DP_ERR_INVALID_ATTR, "crop_flip_normalize: crop larger than the image");
   if (rows == 0) return DP_OK;
   cudaStream_t s = as_stream(stream);
+  if (!fast_div_proven(mean, stdv)) {
+    // the two-FMA division is not exact for these constants: the same chain
+    // through K9 with IEEE division
+    dp_image_chain c{};
+    c.in_h = in_h;
+    c.in_w = in_w;
+    c.pre_mode = do_flip < 0 ? 2 : 1;
+    c.pre_h = crop_h;
+    c.pre_w = crop_w;
+    c.pre_flip = do_flip > 0 ? 1 : 0;
+    c.pre_seed = udf_seed;
+    c.num_pre_ops = 1;
+    for (int ch = 0; ch < 3; ++ch) {
+      c.op_a[0][ch] = mean[ch];
+      c.op_b[0][ch] = stdv[ch];
+    }
+    c.out_f32 = 1;
+    return dp_k_image_chain_batch(images, num_images, order, first, rows, ids.base, ids.stride, ids.block, &c, out_ids,
+                                  out, stream);
+  }
   if (fast_ok(images, in_w, crop_w, out)) {
     FastArgs f = make_fast(images, num_images, in_h, in_w, order, first, rows, crop_h, crop_w, mean, stdv, out_ids,
                            out, env_int("DP_DEV_CROP_BAND", kFastCropBandRows), kCropStages);
@@ -912,6 +934,25 @@ static int resize_impl(const uint8_t* images, int64_t num_images, int in_h, int 
   if (st) return st;
   if (rows == 0) return DP_OK;
   cudaStream_t s = as_stream(stream);
+  const bool proven = fast_div_proven(mean, stdv);
+  if (!proven || env_int("DP_DEV_K4_ROLL", 0)) {
+    // the same chain as a descriptor: K10 (periodic column maps) or K9, both
+    // with IEEE division when the two-FMA division is not proven exact
+    dp_image_chain c{};
+    c.in_h = in_h;
+    c.in_w = in_w;
+    c.resize = 1;
+    c.rs_h = out_h;
+    c.rs_w = out_w;
+    c.num_post_ops = 1;
+    for (int ch = 0; ch < 3; ++ch) {
+      c.op_a[0][ch] = mean[ch];
+      c.op_b[0][ch] = stdv[ch];
+    }
+    c.out_f32 = 1;
+    return dp_k_image_chain_batch(images, num_images, order, first, rows, ids.base, ids.stride, ids.block, &c, out_ids,
+                                  out, stream);
+  }
   if (fast_ok(images, in_w, out_w, out)) {
     FastArgs f = make_fast(images, num_images, in_h, in_w, order, first, rows, out_h, out_w, mean, stdv, out_ids, out,
                            env_int("DP_DEV_RESIZE_BAND", kFastResizeBandRows), kResizeStages);

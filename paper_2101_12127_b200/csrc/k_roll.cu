@@ -53,7 +53,10 @@
 namespace dpk {
 namespace {
 
-constexpr int kRollMaxWarps = 11;  // consumer warps: + the producer = 3 warps per SM sub-partition (<= 168 registers)
+#ifndef DP_ROLL_WARPS
+#define DP_ROLL_WARPS 11  // consumer warps: + the producer = 3 warps per SM sub-partition (<= 168 registers)
+#endif
+constexpr int kRollMaxWarps = DP_ROLL_WARPS;
 constexpr int kRollMaxStages = 8;
 constexpr int kRollMaxStripes = 4;
 constexpr size_t kRollSmemMax = 224 * 1024;
@@ -150,7 +153,13 @@ struct Roll {
                                         : -((PO - (2 * c + 1) * PI + 2 * PO - 1) / (2 * PO));
   }
   static constexpr int kF = 3 * PO;                          // floats per period
-  static constexpr int kP = (kF + 1) / 2;                    // packed pairs
+  // Packed pairs: a pair is one channel of two neighbouring pixels, so
+  // every op constant is a per-channel scalar the FFMA2 broadcasts and the
+  // tap weights are one pair per pixel pair (an odd period leaves one
+  // half-used pair per channel).
+  static constexpr int kNPP = (PO + 1) / 2;  // pixel pairs
+  static constexpr int kP = 3 * kNPP;
+  static constexpr int kW = kNPP;  // weight pairs
   static constexpr int kSpan = 3 * (T(PO - 1) + 2 - T(0));  // window bytes of a period
   static constexpr int kNW = (kSpan + 3) / 4;       // shifted words used
   static constexpr int kNWL = (kSpan + 3 + 3) / 4;  // words loaded (any byte offset)
@@ -164,7 +173,13 @@ struct Roll {
   __host__ __device__ static constexpr int R(int e) {
     return kFlip ? L<kFlip>(e) - 3 : L<kFlip>(e) + 3;
   }
-  __host__ __device__ static constexpr int e1(int i) { return 2 * i + 1 < kF ? 2 * i + 1 : 2 * i; }
+  // values (e0, e1) of pair i (e1 == e0: a half-used pair) and its weight pair
+  __host__ __device__ static constexpr int e0(int i) { return 6 * (i % kNPP) + i / kNPP; }
+  __host__ __device__ static constexpr int e1(int i) { return 2 * (i % kNPP) + 1 < PO ? e0(i) + 3 : e0(i); }
+  __host__ __device__ static constexpr int wi(int i) { return i % kNPP; }
+  // the pair and half holding value e = 3 * pixel + channel
+  __host__ __device__ static constexpr int pair_of(int e) { return (e % 3) * kNPP + (e / 3) / 2; }
+  __host__ __device__ static constexpr bool hi_of(int e) { return (e / 3) % 2 == 1; }
 
   static __device__ __forceinline__ uint32_t pick(const uint32_t* w, int b) {
     return __byte_perm(w[b >> 2], 0x4B000000u, 0x7440u | static_cast<uint32_t>(b & 3));
@@ -175,7 +190,7 @@ struct Roll {
 
   // horizontal blends of one staged row for this lane's period
   template <bool kFlip>
-  static __device__ __forceinline__ void hrow(const uint8_t* row, int b, f32x2 (&H)[kP], const f32x2 (&wx2)[kP],
+  static __device__ __forceinline__ void hrow(const uint8_t* row, int b, f32x2 (&H)[kP], const f32x2 (&wx2)[kW],
                                               const PkK& k) {
     const uint32_t* src = reinterpret_cast<const uint32_t*>(row + (b & ~3));
     const int sh = (b & 3) * 8;
@@ -188,14 +203,172 @@ struct Roll {
     for (int i = 0; i < kNW; ++i) w[i] = __funnelshift_r(W[i], W[i + 1], sh);
 #pragma unroll
     for (int i = 0; i < kP; ++i)
-      H[i] = k.lerp_u8(raw2(w, L<kFlip>(2 * i), L<kFlip>(e1(i))), raw2(w, R<kFlip>(2 * i), R<kFlip>(e1(i))), wx2[i]);
+      H[i] = k.lerp_u8(raw2(w, L<kFlip>(e0(i)), L<kFlip>(e1(i))), raw2(w, R<kFlip>(e0(i)), R<kFlip>(e1(i))),
+                       wx2[wi(i)]);
+  }
+};
+
+// One consumer warp's state: its stripe and run, the op constants, and the
+// lane geometry (period, tap weights, output positions), a function of crop
+// B's (offset, flip), recomputed when they change.
+template <int PO, int PI, int kOp>
+struct RollWarp {
+  using RO = Roll<PO, PI, kOp>;
+  static constexpr int kP = RO::kP, kF = RO::kF, kW = RO::kW;
+  int lane, stripe, run, px_lo, px_hi, n4;
+  float* buf;
+  PkK k;
+  float sa[3], sb[3], sr_[3];  // op constants per channel (normalize: mean, -std, RN(1 / std))
+  int g_ox1, g_f1;
+  int p, pos[PO], vec_base;
+  bool vec;
+  f32x2 wx2[kW];
+
+  __device__ void init(const RollArgs& a, uint8_t* smem, int warp, int lane_) {
+    lane = lane_;
+    stripe = warp % a.stripes;
+    run = warp / a.stripes;
+    px_lo = a.stripe_px[stripe];
+    px_hi = a.stripe_px[stripe + 1];
+    n4 = 3 * (px_hi - px_lo) / 4;
+    buf = reinterpret_cast<float*>(smem + a.buf_offset) + static_cast<size_t>(warp) * (a.buf_floats + 128);
+    k = PkK(a.nc);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      sa[c] = a.op_a[c];
+      sb[c] = kOp == 1 ? -a.op_b[c] : a.op_b[c];
+      sr_[c] = a.op_r[c];
+    }
+    g_ox1 = g_f1 = -1;
+    p = vec_base = 0;
+    vec = false;
+  }
+
+  __device__ void geometry(const RollArgs& a, const RollMeta& m) {
+    g_ox1 = m.ox1;
+    g_f1 = m.f1;
+    // mid columns of this stripe, the lane's period and where its pixels land
+    const int m_lo = m.f1 ? m.ox1 + a.out_w - px_hi : m.ox1 + px_lo;
+    const int m_hi = m.f1 ? m.ox1 + a.out_w - px_lo : m.ox1 + px_hi;
+    p = m_lo / PO + lane;
+    const bool active = p * PO < m_hi;
+    if (!active) p = m_lo / PO;  // a valid period (reads stay in the stage); writes nothing
+#pragma unroll
+    for (int c = 0; c < PO; ++c) {
+      const int mc = p * PO + c - m.ox1;  // output pixel before crop B's flip
+      const int x = (m.f1 ? a.out_w - 1 - mc : mc) - px_lo;
+      // invalid pixels go to this lane's trash slot past the row (no predicated stores)
+      pos[c] = active && mc >= 0 && mc < a.out_w && x >= 0 && x < px_hi - px_lo ? 3 * x : a.buf_floats + 4 * lane;
+    }
+    // float4 stores straight from the pairs when every lane's pixels are
+    // all in the stripe or all out, in order (no crop-B flip) and 16-byte aligned
+    const int x0 = p * PO - m.ox1 - px_lo;
+    const bool whole = !active || (x0 >= 0 && x0 + PO <= px_hi - px_lo);
+    vec = kF % 4 == 0 && !m.f1 && __all_sync(0xffffffffu, whole && (3 * x0) % 4 == 0);
+    vec_base = active ? 3 * x0 : -1;
+    float wx[kF];
+#pragma unroll
+    for (int c = 0; c < PO; ++c) {
+      int xa, xb;
+      float w;
+      roll_coord(p * PO + c, a.win_w, a.scale_x, xa, xb, w);
+      // the periodic taps are (xf, xf + 1), xf = PI p + T(c); at the edges
+      // they differ from the clamped ones but give p00 exactly:
+      if (xb == xa) w = 0.0f;                          // right clamp: xf == x0, any right tap
+      else if (xa == p * PI + RO::T(c) + 1) w = 1.0f;  // left clamp: xf == -1, (p(-1), p(0)) at weight 1
+      wx[3 * c] = wx[3 * c + 1] = wx[3 * c + 2] = w;
+    }
+#pragma unroll
+    for (int i = 0; i < kW; ++i) wx2[i] = pk2(wx[RO::e0(i)], wx[RO::e1(i)]);
+  }
+
+  // one output row from the blends of its two window rows
+  template <bool kVec>
+  __device__ __forceinline__ void emit(const RollArgs& a, const RollTap* tp, int r, float4* orow, int row_f4,
+                                       const f32x2 (&A)[kP], const f32x2 (&B)[kP]) {
+    const f32x2 wy2 = splat2(tp[r].wy);
+    float2 f[kP];
+#pragma unroll
+    for (int i = 0; i < kP; ++i) {
+      f32x2 v = k.lerp(A[i], B[i], wy2);
+      const int c = RO::e0(i) % 3;
+      if (kOp == 1) v = k.normalize(v, splat2(sa[c]), splat2(sb[c]), splat2(sr_[c]));
+      if (kOp == 2) v = k.add(k.mul(v, splat2(sa[c])), splat2(sb[c]));
+      f[i] = up2(v);
+      if (kOp == 3) {
+        f[i].x = __fdiv_rn(__fsub_rn(f[i].x, a.op_a[RO::e0(i) % 3]), a.op_b[RO::e0(i) % 3]);
+        f[i].y = __fdiv_rn(__fsub_rn(f[i].y, a.op_a[RO::e1(i) % 3]), a.op_b[RO::e1(i) % 3]);
+      }
+    }
+    if constexpr (kVec && kF % 4 == 0) {
+      if (vec_base >= 0) {
+        float4* d = reinterpret_cast<float4*>(buf + vec_base);
+        auto val = [&](int e) { return RO::hi_of(e) ? f[RO::pair_of(e)].y : f[RO::pair_of(e)].x; };
+#pragma unroll
+        for (int q = 0; q < kF / 4; ++q) d[q] = make_float4(val(4 * q), val(4 * q + 1), val(4 * q + 2), val(4 * q + 3));
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < kP; ++i) {
+        const int e0 = RO::e0(i), e1 = RO::e1(i);
+        buf[pos[e0 / 3] + e0 % 3] = f[i].x;
+        if (e1 != e0) buf[pos[e1 / 3] + e1 % 3] = f[i].y;
+      }
+    }
+    __syncwarp();
+    float4* o = orow + static_cast<size_t>(r) * row_f4;
+    const float4* b4 = reinterpret_cast<const float4*>(buf);
+    for (int c = lane; c < n4; c += 32) st_cs_f4(o + c, b4[c]);
+    __syncwarp();
+  }
+
+  // walk the run: A / B hold the blends of window rows s and s + 1 (roles
+  // swap every source row), each computed once
+  template <bool kFlip, bool kVec>
+  __device__ void walk(const RollArgs& a, const RollMeta& m, const uint8_t* stage, const RollTap* tp, int r_lo,
+                       int r_hi) {
+    float4* orow = reinterpret_cast<float4*>(a.out + (static_cast<size_t>(m.j) * a.out_h +
+                                                       static_cast<size_t>(m.band) * a.band_rows) *
+                                                          (3 * a.out_w) + 3 * px_lo);
+    const int row_f4 = 3 * a.out_w / 4;
+    const int b = kFlip ? m.adj + 3 * (a.win_w - 1 - PI * p - (RO::T(PO - 1) + 1)) : m.adj + 3 * (PI * p + RO::T(0));
+    f32x2 A[kP], B[kP];
+#pragma unroll
+    for (int i = 0; i < kP; ++i) B[i] = splat2(0.0f);
+    int r = r_lo;
+    int sr = tp[r].y0;
+    const int s_last = tp[r_hi - 1].y1;
+    RO::template hrow<kFlip>(stage + (sr - m.wy_lo) * a.stage_stride, b, A, wx2, k);
+    for (;;) {
+      if (sr + 1 <= s_last) RO::template hrow<kFlip>(stage + (sr + 1 - m.wy_lo) * a.stage_stride, b, B, wx2, k);
+      while (r < r_hi && tp[r].y0 == sr) emit<kVec>(a, tp, r++, orow, row_f4, A, B);
+      if (r >= r_hi) break;
+      ++sr;
+      if (sr + 1 <= s_last) RO::template hrow<kFlip>(stage + (sr + 1 - m.wy_lo) * a.stage_stride, b, A, wx2, k);
+      while (r < r_hi && tp[r].y0 == sr) emit<kVec>(a, tp, r++, orow, row_f4, B, A);
+      if (r >= r_hi) break;
+      ++sr;
+    }
+  }
+
+  __device__ void item(const RollArgs& a, const RollMeta& m, const uint8_t* stage, const RollTap* taps) {
+    const int r_lo = static_cast<int>((static_cast<int64_t>(run) * m.nrows) / a.runs);
+    const int r_hi = static_cast<int>((static_cast<int64_t>(run + 1) * m.nrows) / a.runs);
+    if (r_lo >= r_hi) return;
+    if (m.ox1 != g_ox1 || m.f1 != g_f1) geometry(a, m);
+    const RollTap* tp = taps + m.oy1 + m.band * a.band_rows;
+    if (vec) {
+      if (m.f0) walk<true, true>(a, m, stage, tp, r_lo, r_hi);
+      else walk<false, true>(a, m, stage, tp, r_lo, r_hi);
+    } else {
+      if (m.f0) walk<true, false>(a, m, stage, tp, r_lo, r_hi);
+      else walk<false, false>(a, m, stage, tp, r_lo, r_hi);
+    }
   }
 };
 
 template <int PO, int PI, int kOp>
 __global__ void __launch_bounds__(kRollMaxWarps * 32 + 32, 1) roll_kernel(RollArgs a) {
-  using RO = Roll<PO, PI, kOp>;
-  constexpr int kP = RO::kP, kF = RO::kF;
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t full[kRollMaxStages], empty[kRollMaxStages];
   __shared__ RollMeta meta[kRollMaxStages];
@@ -293,119 +466,15 @@ __global__ void __launch_bounds__(kRollMaxWarps * 32 + 32, 1) roll_kernel(RollAr
   if (warp > a.cons_warps) return;
 
   // ---- consumer warps: warp = run * stripes + stripe ----
-  const int stripe = warp % a.stripes, run = warp / a.stripes;
-  const int px_lo = a.stripe_px[stripe], px_hi = a.stripe_px[stripe + 1];
-  const int n4 = 3 * (px_hi - px_lo) / 4;
-  float* buf = reinterpret_cast<float*>(smem + a.buf_offset) + static_cast<size_t>(warp) * a.buf_floats;
-  const PkK k(a.nc);
-  // op constants by pair pattern (channel of the pair's first value: 0, 2, 1)
-  f32x2 ca[3], cb[3], cr[3];
-#pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    const int c1 = (c + 1) % 3;
-    ca[c] = pk2(a.op_a[c], a.op_a[c1]);
-    cb[c] = kOp == 1 ? pk2(-a.op_b[c], -a.op_b[c1]) : pk2(a.op_b[c], a.op_b[c1]);
-    cr[c] = pk2(a.op_r[c], a.op_r[c1]);
-  }
-  // lane geometry, a function of (ox1, f1): recomputed when they change
-  int g_ox1 = -1, g_f1 = -1;
-  int p = 0, pos[PO];
-  f32x2 wx2[kP];
+  RollWarp<PO, PI, kOp> w;
+  w.init(a, smem, warp, lane);
   int kq = 0;
   for (int64_t item = blockIdx.x; item < total; item += gridDim.x, ++kq) {
     const int s = kq % a.stages;
     mbar_wait(&full[s], (kq / a.stages) & 1);
     const RollMeta m = meta[s];
-    const int r_lo = static_cast<int>((static_cast<int64_t>(run) * m.nrows) / a.runs);
-    const int r_hi = static_cast<int>((static_cast<int64_t>(run + 1) * m.nrows) / a.runs);
     if (m.id >= 0 && m.band == 0 && warp == 0 && lane == 0) a.out_ids[m.j] = m.id;
-    if (m.id >= 0 && r_lo < r_hi) {
-      if (m.ox1 != g_ox1 || m.f1 != g_f1) {
-        g_ox1 = m.ox1;
-        g_f1 = m.f1;
-        // mid columns of this stripe, the lane's period and where its pixels land
-        const int m_lo = m.f1 ? m.ox1 + a.out_w - px_hi : m.ox1 + px_lo;
-        const int m_hi = m.f1 ? m.ox1 + a.out_w - px_lo : m.ox1 + px_hi;
-        p = m_lo / PO + lane;
-        const bool active = p * PO < m_hi;
-        if (!active) p = m_lo / PO;  // a valid period (reads stay in the stage); writes nothing
-#pragma unroll
-        for (int c = 0; c < PO; ++c) {
-          const int mc = p * PO + c - m.ox1;  // output pixel before crop B's flip
-          const int x = (m.f1 ? a.out_w - 1 - mc : mc) - px_lo;
-          pos[c] = active && mc >= 0 && mc < a.out_w && x >= 0 && x < px_hi - px_lo ? 3 * x : -1;
-        }
-        float wx[kF];
-#pragma unroll
-        for (int c = 0; c < PO; ++c) {
-          int x0, x1;
-          float w;
-          roll_coord(p * PO + c, a.win_w, a.scale_x, x0, x1, w);
-          // the periodic taps are (xf, xf + 1), xf = PI p + T(c); at the
-          // edges they differ from the clamped ones but give p00 exactly:
-          if (x1 == x0) w = 0.0f;                      // right clamp: xf == x0, any right tap
-          else if (x0 == p * PI + RO::T(c) + 1) w = 1.0f;  // left clamp: xf == -1, (p(-1), p(0)) at weight 1
-          wx[3 * c] = wx[3 * c + 1] = wx[3 * c + 2] = w;
-        }
-#pragma unroll
-        for (int i = 0; i < kP; ++i) wx2[i] = pk2(wx[2 * i], wx[RO::e1(i)]);
-      }
-      const uint8_t* stage = smem + static_cast<size_t>(s) * a.stage_bytes + 16;
-      const RollTap* tp = taps + m.oy1 + m.band * a.band_rows;
-      float4* orow = reinterpret_cast<float4*>(a.out + (static_cast<size_t>(m.j) * a.out_h +
-                                                         static_cast<size_t>(m.band) * a.band_rows) *
-                                                            (3 * a.out_w) + 3 * px_lo);
-      const int row_f4 = 3 * a.out_w / 4;
-      // one output row from the blends of its two window rows
-      auto emit = [&](int r, const f32x2(&A)[kP], const f32x2(&B)[kP]) {
-        const f32x2 wy2 = splat2(tp[r].wy);
-#pragma unroll
-        for (int i = 0; i < kP; ++i) {
-          f32x2 v = k.lerp(A[i], B[i], wy2);
-          const int c = (2 * i) % 3;
-          if (kOp == 1) v = k.normalize(v, ca[c], cb[c], cr[c]);
-          if (kOp == 2) v = k.add(k.mul(v, ca[c]), cb[c]);
-          float2 f = up2(v);
-          if (kOp == 3) {
-            f.x = __fdiv_rn(__fsub_rn(f.x, a.op_a[(2 * i) % 3]), a.op_b[(2 * i) % 3]);
-            f.y = __fdiv_rn(__fsub_rn(f.y, a.op_a[RO::e1(i) % 3]), a.op_b[RO::e1(i) % 3]);
-          }
-          const int e0 = 2 * i, e1 = RO::e1(i);
-          if (pos[e0 / 3] >= 0) buf[pos[e0 / 3] + e0 % 3] = f.x;
-          if (e1 != e0 && pos[e1 / 3] >= 0) buf[pos[e1 / 3] + e1 % 3] = f.y;
-        }
-        __syncwarp();
-        float4* o = orow + static_cast<size_t>(r) * row_f4;
-        const float4* b4 = reinterpret_cast<const float4*>(buf);
-        for (int c = lane; c < n4; c += 32) st_cs_f4(o + c, b4[c]);
-        __syncwarp();
-      };
-      // walk the run: A / B hold the blends of window rows s and s + 1
-      // (roles swap every source row), each computed once
-      auto walk = [&](auto flip_tag) {
-        constexpr bool kFlip = decltype(flip_tag)::value;
-        const int b = kFlip ? m.adj + 3 * (a.win_w - 1 - PI * p - (RO::T(PO - 1) + 1)) : m.adj + 3 * (PI * p + RO::T(0));
-        f32x2 A[kP], B[kP];
-#pragma unroll
-        for (int i = 0; i < kP; ++i) B[i] = splat2(0.0f);
-        int r = r_lo;
-        int sr = tp[r].y0;
-        const int s_last = tp[r_hi - 1].y1;
-        RO::template hrow<kFlip>(stage + (sr - m.wy_lo) * a.stage_stride, b, A, wx2, k);
-        for (;;) {
-          if (sr + 1 <= s_last) RO::template hrow<kFlip>(stage + (sr + 1 - m.wy_lo) * a.stage_stride, b, B, wx2, k);
-          while (r < r_hi && tp[r].y0 == sr) emit(r++, A, B);
-          if (r >= r_hi) break;
-          ++sr;
-          if (sr + 1 <= s_last) RO::template hrow<kFlip>(stage + (sr + 1 - m.wy_lo) * a.stage_stride, b, A, wx2, k);
-          while (r < r_hi && tp[r].y0 == sr) emit(r++, B, A);
-          if (r >= r_hi) break;
-          ++sr;
-        }
-      };
-      if (m.f0) walk(std::true_type{});
-      else walk(std::false_type{});
-    }
+    if (m.id >= 0) w.item(a, m, smem + static_cast<size_t>(s) * a.stage_bytes + 16, taps);
     __syncwarp();
     if (lane == 0) roll_arrive(&empty[s]);
   }
@@ -519,7 +588,7 @@ bool roll_plan(const dp_image_chain* c, int out_h, int out_w, RollPlanHost& h) {
   if (periodic_map<7, 10>(a.win_w, a.mid_w)) PO = 7, PI = 10;
   else if (periodic_map<7, 8>(a.win_w, a.mid_w)) PO = 7, PI = 8;
   else if (periodic_map<7, 5>(a.win_w, a.mid_w)) PO = 7, PI = 5;
-  else if (periodic_map<4, 5>(a.win_w, a.mid_w)) PO = 4, PI = 5;
+  else if (periodic_map<8, 10>(a.win_w, a.mid_w)) PO = 8, PI = 10;  // 5:4 as two periods per lane (24 floats)
   else return false;
   // the pixel op
   int op = 0;
@@ -558,7 +627,7 @@ bool roll_plan(const dp_image_chain* c, int out_h, int out_w, RollPlanHost& h) {
   if (a.cons_warps > kRollMaxWarps) return false;
   // bands: ~run_rows output rows per run, spread evenly over the image
   const double scale = static_cast<double>(a.win_h) / a.mid_h;
-  const int run_rows = roll_env("DP_DEV_ROLL_RUN", scale > 1.2 ? 4 : 8);
+  const int run_rows = roll_env("DP_DEV_ROLL_RUN", 8);  // tools/dev sweep: 8 best for 160->224 and 320->256
   a.bands = std::max(1, (out_h + a.runs * run_rows - 1) / (a.runs * run_rows));
   a.band_rows = (out_h + a.bands - 1) / a.bands;
   a.bands = (out_h + a.band_rows - 1) / a.band_rows;
@@ -570,7 +639,7 @@ bool roll_plan(const dp_image_chain* c, int out_h, int out_w, RollPlanHost& h) {
   for (int st = 1; st < a.stripes; ++st)
     a.buf_floats = std::max(a.buf_floats, ((3 * (a.stripe_px[st + 1] - a.stripe_px[st]) + 3) / 4) * 4);
   const size_t taps = ((static_cast<size_t>(a.mid_h) * sizeof(RollTap) + 127) / 128) * 128;
-  const size_t bufs = static_cast<size_t>(a.cons_warps) * a.buf_floats * sizeof(float);
+  const size_t bufs = static_cast<size_t>(a.cons_warps) * (a.buf_floats + 128) * sizeof(float);  // + trash slots
   a.stages = roll_env("DP_DEV_ROLL_STAGES", kRollMaxStages);
   while (a.stages > 2 && static_cast<size_t>(a.stages) * a.stage_bytes + taps + bufs > kRollSmemMax) --a.stages;
   const size_t smem = static_cast<size_t>(a.stages) * a.stage_bytes + taps + bufs;
@@ -619,7 +688,7 @@ int roll_chain_batch(const uint8_t* images, int64_t num_images, const int64_t* o
   DP_ROLL(7, 10)
   DP_ROLL(7, 8)
   DP_ROLL(7, 5)
-  DP_ROLL(4, 5)
+  DP_ROLL(8, 10)
 #undef DP_ROLL
   return 1;
 }

@@ -632,6 +632,33 @@ def run_ours(args, cfg):
         distr.destroy_process_group()
 
 
+def pcie_gbs(local, h2d=False):
+    """Plain pinned-memory copy bandwidth, 512 MiB, best of 5, CUDA events (D2H, or H2D)."""
+    import torch
+    try:
+        n = 512 << 20
+        d = torch.empty(n, dtype=torch.uint8, device=f"cuda:{local}")
+        h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+        s = torch.cuda.Stream(device=local)
+        best = 0.0
+        with torch.cuda.stream(s):
+            for i in range(6):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(s)
+                if h2d:
+                    d.copy_(h, non_blocking=True)
+                else:
+                    h.copy_(d, non_blocking=True)
+                e1.record(s)
+                e1.synchronize()
+                if i:
+                    best = max(best, n / (e0.elapsed_time(e1) / 1e3) / 1e9)
+        del d, h
+        return round(best, 1)
+    except Exception:  # reported, not fatal
+        return None
+
+
 def pcie_d2h_gbs(local):
     """Plain pinned-memory D2H copy bandwidth (512 MiB, best of 5, CUDA events): the e2e roofline."""
     import torch
@@ -751,11 +778,29 @@ def run_e2e(dp, cfg, local, args, world=1, dev=None):
                 "how": "the same with every batch copied back into pinned host slots (host_output); PCIe D2H bound"}}
 
 
+def e2e_consumer():
+    """tools/bin/libdpe2e.so (tools/e2e_consumer.c, built by __graft_entry__.build()): the token e2e loop in C."""
+    import ctypes
+    path = os.path.join(ROOT, "tools", "bin", "libdpe2e.so")
+    if not os.path.exists(path):
+        import __graft_entry__
+        __graft_entry__._build_e2e_consumer()
+    lib = ctypes.CDLL(path)
+    lib.dpe2e_consume_host_batches.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
+                                               ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_uint64),
+                                               ctypes.POINTER(ctypes.c_int64)]
+    return lib
+
+
 def run_e2e_tokens(dp, cfg, local, args, world=1, dev=None):
     """Token configs end to end: the sequences live in pinned host memory
-    (lengths, offsets and tokens read by the kernels over PCIe) and every
-    batch is copied back into pinned host slots; host wall clock over whole
-    epochs of a 200,000-sequence host dataset."""
+    (each epoch plan stages the rows it consumes over PCIe) and every batch
+    is copied back into pinned host slots, waited on and read by the host.
+    The consumer loop is C over the C ABI (tools/e2e_consumer.c: GetNext,
+    wait, read, release -- what a C++ / FFI user writes); through ctypes the
+    ~10 us Python cost per 128-sequence batch would be the bound.  Host wall
+    clock over whole epochs of a 200,000-sequence host dataset."""
+    import ctypes
     import numpy as np
     n_host = 200_000
     rng = np.random.default_rng(1)
@@ -763,38 +808,41 @@ def run_e2e_tokens(dp, cfg, local, args, world=1, dev=None):
     toks = rng.integers(0, 2 ** 31 - 1, int(lens.sum()), dtype=np.int64).astype(np.int32)
     src = dp.Source.tokens_from_host(lens, toks, device=local, pinned=True)
     g, _ = build_other_graph(dp, cfg, local, 0, 1, src=src)
+    C = e2e_consumer()
+    ragged = 1 if cfg.get("ragged") else 0
 
-    def make():
-        return dp.make_iterator(g, seed_override=1, device=local, host_output=True)
+    def consume(it, n):
+        rows, chk, done = ctypes.c_int64(0), ctypes.c_uint64(0), ctypes.c_int64(0)
+        st = C.dpe2e_consume_host_batches(it.h, n, ragged, ctypes.byref(rows), ctypes.byref(chk),
+                                          ctypes.byref(done))
+        if st:
+            raise RuntimeError(f"e2e consumer: dp_status {st}")
+        return rows.value
 
-    it = make()
+    it = dp.make_iterator(g, seed_override=1, device=local, host_output=True)
     per_epoch = int(re.search(r"elements, (\d+) batches", it.describe()).group(1))
-    steps = per_epoch * 2
-    for _ in range(per_epoch):  # one warm-up epoch on the same iterator (slots allocated, plans built ahead)
-        it.get_next().wait().release()
-    # three timed windows of 2 epochs each on the same iterator; the median
-    # is reported (a window takes ~20 ms: one host hiccup would dominate it)
+    epochs = 4
+    steps = per_epoch * epochs
+    consume(it, per_epoch)  # one warm-up epoch on the same iterator (slots allocated, plans built ahead)
+    # three timed windows of 4 epochs each on the same iterator; the median is reported
     windows = []
     for _ in range(3):
         if world > 1:
             max_over_ranks(0.0, world, dev)  # barrier: start together
         t0 = time.perf_counter()
-        rows = 0
-        for _ in range(steps):
-            b = it.get_next().wait()
-            rows += b.components[1][1][0] - (1 if cfg.get("ragged") else 0)
-            b.release()
+        rows = consume(it, steps)
         secs = time.perf_counter() - t0
         if world > 1:
             secs = max_over_ranks(secs * 1e3, world, dev) / 1e3
         windows.append((secs, rows))
     secs, rows = sorted(windows)[1]
+    del it
     # bytes per step, from the same batches (untimed pass)
-    it = make()
+    it = dp.make_iterator(g, seed_override=1, device=local, host_output=True)
     for _ in range(per_epoch):
         it.get_next().release()
     b_in = b_out = 0
-    for _ in range(steps):
+    for _ in range(per_epoch):
         b = it.get_next().wait()
         if cfg.get("ragged"):
             splits = b.numpy(1)
@@ -807,15 +855,21 @@ def run_e2e_tokens(dp, cfg, local, args, world=1, dev=None):
             b_in += 4 * int(ln.sum()) + r * (8 + 4 + 8)
             b_out += 4 * r * lm + 4 * r
         b.release()
+    del it
+    b_in, b_out = b_in * epochs, b_out * epochs
+    h2d_meas = pcie_gbs(local, h2d=True)
     return {"value": round(rows * world / secs, 1), "unit": cfg["unit"],
             "h2d_bytes_per_step": int(b_in / steps) * world, "d2h_bytes_per_step": int(b_out / steps) * world,
             "steps": steps, "windows_ms": [round(w[0] * 1e3, 2) for w in windows],
             "pcie": {"h2d_gbs_achieved": round(b_in / secs / 1e9, 1), "d2h_gbs_achieved": round(b_out / secs / 1e9, 1),
-                     "d2h_gbs_measured": pcie_d2h_gbs(local)},
+                     "h2d_gbs_measured": h2d_meas, "d2h_gbs_measured": pcie_d2h_gbs(local),
+                     "h2d_frac": round(b_in / secs / 1e9 / h2d_meas, 3) if h2d_meas else None},
             "host_dataset": f"{n_host} sequences, len U[1,1024], pinned host memory",
-            "how": "pinned host token source read over PCIe by the kernels (lengths, offsets, tokens) + D2H of every "
-                   "batch into pinned host slots; host wall clock over 2 epochs after a warm-up epoch on the same "
-                   "iterator (median of 3 such windows), each batch waited on by the host",
+            "consumer": "C loop over the C ABI (tools/e2e_consumer.c): dp_iterator_get_next, dp_batch_wait, read "
+                        "the batch's first / last token on the host, dp_batch_release",
+            "how": "pinned host token source staged over PCIe by each epoch plan + D2H of every batch into pinned "
+                   "host slots, each batch waited on and read by the host; host wall clock over 4 epochs after a "
+                   "warm-up epoch on the same iterator (median of 3 such windows)",
             "bound": "PCIe: each epoch plan stages exactly the rows it consumes from pinned host memory into HBM "
                      "(dp_k_stage_rows, one pass), the batch kernels stream HBM, every batch is copied back"}
 

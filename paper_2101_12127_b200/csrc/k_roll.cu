@@ -625,24 +625,30 @@ bool roll_plan(const dp_image_chain* c, int out_h, int out_w, RollPlanHost& h) {
   a.runs = std::max(1, warps / a.stripes);
   a.cons_warps = a.runs * a.stripes;
   if (a.cons_warps > kRollMaxWarps) return false;
-  // bands: ~run_rows output rows per run, spread evenly over the image
+  // bands: ~run_rows output rows per run, spread evenly over the image;
+  // shorter runs when a ring of 2 stages does not fit
   const double scale = static_cast<double>(a.win_h) / a.mid_h;
-  const int run_rows = roll_env("DP_DEV_ROLL_RUN", 8);  // tools/dev sweep: 8 best for 160->224 and 320->256
-  a.bands = std::max(1, (out_h + a.runs * run_rows - 1) / (a.runs * run_rows));
-  a.band_rows = (out_h + a.bands - 1) / a.bands;
-  a.bands = (out_h + a.band_rows - 1) / a.band_rows;
   a.stage_stride = static_cast<int>(std::min<size_t>(row_bytes, ((3 * a.win_w + 15 + 15) / 16) * 16));
   if (a.win_w == c->in_w) a.stage_stride = static_cast<int>(row_bytes);
-  const int max_src = std::min(a.win_h, static_cast<int>(a.band_rows * scale) + 3);
-  a.stage_bytes = ((16 + max_src * a.stage_stride + 16 + 127) / 128) * 128;
   a.buf_floats = ((3 * (a.stripe_px[1] - a.stripe_px[0]) + 3) / 4) * 4;
   for (int st = 1; st < a.stripes; ++st)
     a.buf_floats = std::max(a.buf_floats, ((3 * (a.stripe_px[st + 1] - a.stripe_px[st]) + 3) / 4) * 4);
   const size_t taps = ((static_cast<size_t>(a.mid_h) * sizeof(RollTap) + 127) / 128) * 128;
   const size_t bufs = static_cast<size_t>(a.cons_warps) * (a.buf_floats + 128) * sizeof(float);  // + trash slots
-  a.stages = roll_env("DP_DEV_ROLL_STAGES", kRollMaxStages);
-  while (a.stages > 2 && static_cast<size_t>(a.stages) * a.stage_bytes + taps + bufs > kRollSmemMax) --a.stages;
-  const size_t smem = static_cast<size_t>(a.stages) * a.stage_bytes + taps + bufs;
+  const int want_stages = std::min(kRollMaxStages, std::max(2, roll_env("DP_DEV_ROLL_STAGES", kRollMaxStages)));
+  size_t smem = 0;
+  // tools/dev sweep: runs of 8 rows best for 160 -> 224 and 320 -> 256
+  for (int run_rows = roll_env("DP_DEV_ROLL_RUN", 8); run_rows >= 1; --run_rows) {
+    a.bands = std::max(1, (out_h + a.runs * run_rows - 1) / (a.runs * run_rows));
+    a.band_rows = (out_h + a.bands - 1) / a.bands;
+    a.bands = (out_h + a.band_rows - 1) / a.band_rows;
+    const int max_src = std::min(a.win_h, static_cast<int>(a.band_rows * scale) + 3);
+    a.stage_bytes = ((16 + max_src * a.stage_stride + 16 + 127) / 128) * 128;
+    a.stages = want_stages;
+    while (a.stages > 2 && static_cast<size_t>(a.stages) * a.stage_bytes + taps + bufs > kRollSmemMax) --a.stages;
+    smem = static_cast<size_t>(a.stages) * a.stage_bytes + taps + bufs;
+    if (smem <= kRollSmemMax && a.stages >= 2) break;
+  }
   if (smem > kRollSmemMax || a.stages < 2) return false;
   a.taps_offset = a.stages * a.stage_bytes;
   a.buf_offset = static_cast<int>(a.taps_offset + taps);

@@ -28,12 +28,16 @@ from tests.oracle_lib import MEAN, STD, Oracle  # noqa: E402
 
 CROP = [["random_crop", 224, 224, 7, True], ["normalize", list(MEAN), list(STD)]]
 RESIZE = [["resize", 224, 224], ["normalize", list(MEAN), list(STD)]]
+RRC = [["random_crop", 160, 160, 7, True], ["resize", 224, 224], ["normalize", list(MEAN), list(STD)]]
+EVAL = [["resize", 256, 256], ["center_crop", 224, 224], ["normalize", list(MEAN), list(STD)]]
 
 CASES = {
     # name: (source, n, hw, steps)
     "cfg2": ("tensor_slices", 65536, 256, CROP),
     "cfg3": ("tensor_slices", 65536, 320, RESIZE),
     "cfg5": ("interleave", 65536, 256, CROP),   # 32 files x 2048 records, cycle 4, parallel 4
+    "cfg2rrc": ("tensor_slices", 65536, 256, RRC),   # RandomResizedCrop (K10)
+    "cfg3e": ("tensor_slices", 65536, 320, EVAL),    # ResNet eval (K10)
 }
 
 
@@ -48,12 +52,19 @@ def epoch_ids(orc, source, n):
 
 def main():
     orc = Oracle()
+    only = sys.argv[1:]  # case names to (re)compute; the others are kept from the existing file
+    path = os.path.join(HERE, "epoch_digests.json")
+    old = json.load(open(path))["cases"] if only and os.path.exists(path) else {}
     out = {"generator": "tests/golden/make_epoch_digests.py (oracle restatement: shuffle / interleave order + "
                         "oracle/chain.c map chain)",
            "digest": "pixels: sum over the epoch's output u32 words w at running position p of "
                      "SplitMix64Next(w ^ p * 0x9E3779B97F4A7C15) mod 2^64; ids: the same over the int64 ids",
            "cases": {}}
     for name, (source, n, hw, steps) in CASES.items():
+        if only and name not in only:
+            if name in old:
+                out["cases"][name] = old[name]
+            continue
         t = time.time()
         ids = epoch_ids(orc, source, n)
         pix = orc.epoch_image_digest([tuple(s) for s in steps], ids, hw, hw)
@@ -61,7 +72,7 @@ def main():
                               "base_seed": 1, "batch": 256, "ids": f"{Oracle.order_digest(ids):016x}",
                               "pixels": f"{pix:016x}"}
         print(name, out["cases"][name]["ids"], out["cases"][name]["pixels"], f"{time.time() - t:.1f}s", flush=True)
-    with open(os.path.join(HERE, "epoch_digests.json"), "w") as f:
+    with open(path, "w") as f:
         json.dump(out, f, indent=1)
 
 

@@ -61,13 +61,15 @@ CFG = {
                              "(RandomResizedCrop at a fixed scale)",
                     in_hw=(256, 256), out_hw=(224, 224), batch=256, n=65536,
                     udfs=[("random_crop", 160, 160, 7, True), ("resize", 224, 224), ("normalize",)],
-                    bytes_per_elem=160 * 160 * 3 + IMG_BYTES_WRITE, kernel="K9 image_chain_batch"),
+                    bytes_per_elem=160 * 160 * 3 + IMG_BYTES_WRITE,
+                    kernel="K10 image_chain_roll (dp_k_image_chain_batch)"),
     "cfg3e": dict(workload="synthetic 320x320x3 u8 images -> Shuffle(10k, seed 42) -> Map(bilinear resize 256) -> "
                            "Map(center crop 224) -> Map(normalize fp32) -> Batch(256) (ResNet eval)",
                   in_hw=(320, 320), out_hw=(224, 224), batch=256, n=65536,
                   udfs=[("resize", 256, 256), ("center_crop", 224, 224), ("normalize",)],
                   # source rows / columns 20..299 feed the center window: 280 x 280 x 3 read
-                  bytes_per_elem=280 * 280 * 3 + IMG_BYTES_WRITE, kernel="K9 image_chain_batch"),
+                  bytes_per_elem=280 * 280 * 3 + IMG_BYTES_WRITE,
+                  kernel="K10 image_chain_roll (dp_k_image_chain_batch)"),
     "cfg1": dict(workload="Range(2^28) int64 -> Map(x*3+1) -> Batch(1024) (cfg1 shape at the roofline size "
                           "SURVEY.md 8(d) names; Range(1M) is the parity case)",
                  kind="range", batch=1024, n=1 << 28, bytes_per_elem=8, kernel="K1 range_affine_batch",

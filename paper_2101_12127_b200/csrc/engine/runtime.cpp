@@ -280,7 +280,12 @@ class DevicePipeline {
     const char* kinds[] = {"K1 gather_affine_batch", "K3 crop_flip_normalize_batch", "K4 resize_normalize_batch",
                            "K5 padded_batches",     "K1 gather_affine_batch",       "K9 image_chain_batch",
                            "K9 gather_copy_batch"};
-    os << "batch stage: " << kinds[static_cast<int>(L_.kind)] << " (batch " << L_.batch << (L_.drop ? ", drop" : "")
+    std::string kernel = kinds[static_cast<int>(L_.kind)];
+    int k10 = 0;  // a resize chain over a periodic column map on HBM-resident images: K10
+    if (L_.kind == BatchKind::kChain && L_.source->residency != Residency::kHost &&
+        dp_image_chain_kernel(&L_.img_chain, &k10) == DP_OK && k10 == 10)
+      kernel = "K10 image_chain_roll (via K9 image_chain_batch)";
+    os << "batch stage: " << kernel << " (batch " << L_.batch << (L_.drop ? ", drop" : "")
        << ", " << group_ << " batch(es) per launch, depth " << depth_ << (autotune_ ? " autotuned" : "") << ")\n";
     os << "index chain (bottom-up):";
     for (const auto& op : L_.chain) {

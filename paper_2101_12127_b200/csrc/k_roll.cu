@@ -287,32 +287,37 @@ struct RollWarp {
   __device__ __forceinline__ void emit(const RollArgs& a, const RollTap* tp, int r, float4* orow, int row_f4,
                                        const f32x2 (&A)[kP], const f32x2 (&B)[kP]) {
     const f32x2 wy2 = splat2(tp[r].wy);
+    // pixel-pair major: the values of pixels 2j, 2j + 1 are done after step
+    // j, so each float4 / word store issues as soon as its values exist and
+    // few results are live at once
     float2 f[kP];
+    float4* d = reinterpret_cast<float4*>(buf + (vec_base >= 0 ? vec_base : 0));
 #pragma unroll
-    for (int i = 0; i < kP; ++i) {
-      f32x2 v = k.lerp(A[i], B[i], wy2);
-      const int c = RO::e0(i) % 3;
-      if (kOp == 1) v = k.normalize(v, splat2(sa[c]), splat2(sb[c]), splat2(sr_[c]));
-      if (kOp == 2) v = k.add(k.mul(v, splat2(sa[c])), splat2(sb[c]));
-      f[i] = up2(v);
-      if (kOp == 3) {
-        f[i].x = __fdiv_rn(__fsub_rn(f[i].x, a.op_a[RO::e0(i) % 3]), a.op_b[RO::e0(i) % 3]);
-        f[i].y = __fdiv_rn(__fsub_rn(f[i].y, a.op_a[RO::e1(i) % 3]), a.op_b[RO::e1(i) % 3]);
+    for (int j = 0; j < RO::kNPP; ++j) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const int i = c * RO::kNPP + j;
+        f32x2 v = k.lerp(A[i], B[i], wy2);
+        if (kOp == 1) v = k.normalize(v, splat2(sa[c]), splat2(sb[c]), splat2(sr_[c]));
+        if (kOp == 2) v = k.add(k.mul(v, splat2(sa[c])), splat2(sb[c]));
+        f[i] = up2(v);
+        if (kOp == 3) {
+          f[i].x = __fdiv_rn(__fsub_rn(f[i].x, a.op_a[c]), a.op_b[c]);
+          f[i].y = __fdiv_rn(__fsub_rn(f[i].y, a.op_a[c]), a.op_b[c]);
+        }
+        if constexpr (!(kVec && kF % 4 == 0)) {
+          const int e0 = RO::e0(i), e1 = RO::e1(i);
+          buf[pos[e0 / 3] + e0 % 3] = f[i].x;
+          if (e1 != e0) buf[pos[e1 / 3] + e1 % 3] = f[i].y;
+        }
       }
-    }
-    if constexpr (kVec && kF % 4 == 0) {
-      if (vec_base >= 0) {
-        float4* d = reinterpret_cast<float4*>(buf + vec_base);
+      if constexpr (kVec && kF % 4 == 0) {
         auto val = [&](int e) { return RO::hi_of(e) ? f[RO::pair_of(e)].y : f[RO::pair_of(e)].x; };
+        const int done = 6 * j + 6;  // values [0, done) exist
 #pragma unroll
-        for (int q = 0; q < kF / 4; ++q) d[q] = make_float4(val(4 * q), val(4 * q + 1), val(4 * q + 2), val(4 * q + 3));
-      }
-    } else {
-#pragma unroll
-      for (int i = 0; i < kP; ++i) {
-        const int e0 = RO::e0(i), e1 = RO::e1(i);
-        buf[pos[e0 / 3] + e0 % 3] = f[i].x;
-        if (e1 != e0) buf[pos[e1 / 3] + e1 % 3] = f[i].y;
+        for (int q = 0; q < kF / 4; ++q)
+          if (4 * q + 4 <= done && 4 * q + 4 > done - 6 && vec_base >= 0)
+            d[q] = make_float4(val(4 * q), val(4 * q + 1), val(4 * q + 2), val(4 * q + 3));
       }
     }
     __syncwarp();

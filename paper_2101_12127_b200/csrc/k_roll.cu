@@ -323,7 +323,12 @@ struct RollWarp {
     __syncwarp();
     float4* o = orow + static_cast<size_t>(r) * row_f4;
     const float4* b4 = reinterpret_cast<const float4*>(buf);
-    for (int c = lane; c < n4; c += 32) st_cs_f4(o + c, b4[c]);
+    // a stripe is <= 32 periods = 24 * PO floats: ceil(3 PO / 4) float4 per lane
+#pragma unroll
+    for (int it = 0; it < (3 * PO + 3) / 4; ++it) {
+      const int c = lane + 32 * it;
+      if (c < n4) st_cs_f4(o + c, b4[c]);
+    }
     __syncwarp();
   }
 

@@ -45,7 +45,8 @@ CFG = {
     "cfg3": dict(workload="synthetic 320x320x3 u8 images -> Shuffle(10k, seed 42) -> Map(bilinear resize 320->224 + "
                           "normalize fp32) -> Batch(256) -> Prefetch(AUTOTUNE)",
                  in_hw=(320, 320), out_hw=(224, 224), mode=1, batch=256, n=65536,
-                 bytes_per_elem=320 * 320 * 3 + IMG_BYTES_WRITE, kernel="K4 resize_normalize_batch"),
+                 bytes_per_elem=320 * 320 * 3 + IMG_BYTES_WRITE,
+                 kernel="K10 image_chain_roll (dp_k_resize_normalize_batch)"),
     "cfg5": dict(workload="Shard(N) over 32*N synthetic record files of 2048 256x256x3 u8 images (each GPU holds "
                           "only its 32 files) -> Interleave(cycle 4, parallel 4) -> Shuffle(10k, seed 42) -> Map(random "
                           "crop 224 + flip + normalize fp32) -> Batch(256) -> Prefetch(AUTOTUNE)",

@@ -285,6 +285,22 @@ class DevicePipeline {
     if (L_.kind == BatchKind::kChain && L_.source->residency != Residency::kHost &&
         dp_image_chain_kernel(&L_.img_chain, &k10) == DP_OK && k10 == 10)
       kernel = "K10 image_chain_roll (via K9 image_chain_batch)";
+    if (L_.kind == BatchKind::kResize && L_.source->residency != Residency::kHost) {
+      dp_image_chain c{};  // resize + normalize as a chain: K10 when its column map is periodic
+      c.in_h = static_cast<int>(L_.source->h);
+      c.in_w = static_cast<int>(L_.source->w);
+      c.resize = 1;
+      c.rs_h = static_cast<int>(L_.resize.out_h);
+      c.rs_w = static_cast<int>(L_.resize.out_w);
+      c.num_post_ops = 1;
+      for (int ch = 0; ch < 3; ++ch) {
+        c.op_a[0][ch] = L_.norm.mean[ch];
+        c.op_b[0][ch] = L_.norm.stdv[ch];
+      }
+      c.out_f32 = 1;
+      if (dp_image_chain_kernel(&c, &k10) == DP_OK && k10 == 10)
+        kernel = "K10 image_chain_roll (via K4 resize_normalize_batch)";
+    }
     os << "batch stage: " << kernel << " (batch " << L_.batch << (L_.drop ? ", drop" : "")
        << ", " << group_ << " batch(es) per launch, depth " << depth_ << (autotune_ ? " autotuned" : "") << ")\n";
     os << "index chain (bottom-up):";

@@ -187,7 +187,11 @@ def test_k3_crop_only(K, orc, dev):
         assert np.array_equal(out[k], orc.crop_flip_normalize(host[k], k, do_flip=False))
 
 
-def test_k4_resize_normalize_within_1ulp(K, orc, dev):
+@pytest.mark.parametrize("roll", ["1", "0"])
+def test_k4_resize_normalize_within_1ulp(K, orc, dev, monkeypatch, roll):
+    """320 -> 224 runs on K10 (periodic column map, k_roll.cu) by default and
+    on K4's periodic-tap consumer with K10 disabled; both bit-exact."""
+    monkeypatch.setenv("DP_DEV_ROLL", roll)
     imgs = device_images(K, dev, 40, 320, 320)
     order = gpu_shuffle(K, 40, 16, orc.shuffle_seed(1, 42))
     ids, out = run_resize(K, imgs, order, 5, 30)
@@ -207,13 +211,18 @@ def test_k4_periodic_and_general_paths_agree(K, dev, monkeypatch):
     general ResizeOp (DP_DEV_RESIZE_PERIODIC=0) must give the same bits."""
     imgs = device_images(K, dev, 24, 320, 320)
     order = gpu_shuffle(K, 24, 8, 99)
+    _, k10 = run_resize(K, imgs, order, 0, 24)
+    monkeypatch.setenv("DP_DEV_ROLL", "0")
     _, a = run_resize(K, imgs, order, 0, 24)
     monkeypatch.setenv("DP_DEV_RESIZE_PERIODIC", "0")
     _, b = run_resize(K, imgs, order, 0, 24)
     assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    assert np.array_equal(a.view(np.uint32), k10.view(np.uint32))
 
 
-def test_k4_other_shapes(K, orc, dev):
+@pytest.mark.parametrize("roll", ["1", "0"])
+def test_k4_other_shapes(K, orc, dev, monkeypatch, roll):
+    monkeypatch.setenv("DP_DEV_ROLL", roll)
     # (256, 256) and (160, 160) -> periodic column taps (ResizePOp 7/8, 7/10
     # with 16 groups per row), the rest the general ResizeOp / generic kernel
     for (ih, iw, oh, ow) in ((100, 160, 224, 224), (480, 360, 224, 224), (33, 57, 17, 23), (256, 256, 224, 224),

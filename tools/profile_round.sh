@@ -7,7 +7,7 @@
 set -u
 out=gpurun_out/prof
 mkdir -p $out
-declare -A KREGEX=([cfg2]="regex:pipeline_kernel" [cfg3]="regex:pipeline_kernel" [cfg4]="regex:padded_batches_kernel" [cfg4b]="regex:bucket_rows_batches_kernel" [cfg4r]="regex:ragged_batches_kernel" [cfg1]="regex:range_affine" [cfg5]="regex:pipeline_kernel" [cfg2u8]="regex:gather_copy_kernel" [cfg2rrc]="regex:roll_kernel" [cfg3e]="regex:roll_kernel")
+declare -A KREGEX=([cfg2]="regex:pipeline_kernel" [cfg3]="regex:roll_kernel" [cfg4]="regex:padded_batches_kernel" [cfg4b]="regex:bucket_rows_batches_kernel" [cfg4r]="regex:ragged_batches_kernel" [cfg1]="regex:range_affine" [cfg5]="regex:pipeline_kernel" [cfg2u8]="regex:gather_copy_kernel" [cfg2rrc]="regex:roll_kernel" [cfg3e]="regex:roll_kernel")
 for c in ${CONFIGS:-cfg2 cfg3 cfg5 cfg4 cfg4r cfg4b cfg1 cfg2u8 cfg2rrc cfg3e}; do
   python bench.py --config $c --steps 64 --warmup 32 > $out/plain_$c.log 2>&1 || { echo "plain $c failed"; continue; }
   ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv --log-file $out/launches_$c.csv \

@@ -822,7 +822,9 @@ def run_e2e_tokens(dp, cfg, local, args, world=1, dev=None):
             raise RuntimeError(f"e2e consumer: dp_status {st}")
         return rows.value
 
-    it = dp.make_iterator(g, seed_override=1, device=local, host_output=True)
+    # launch group size: the iterator's default (a 16 / 64 / 512 MB sweep measured the same: PCIe bound)
+    launch = int(os.environ.get("DP_E2E_TOKEN_LAUNCH_BYTES", 0))
+    it = dp.make_iterator(g, seed_override=1, device=local, host_output=True, max_launch_bytes=launch)
     per_epoch = int(re.search(r"elements, (\d+) batches", it.describe()).group(1))
     epochs = 4
     steps = per_epoch * epochs
@@ -841,7 +843,7 @@ def run_e2e_tokens(dp, cfg, local, args, world=1, dev=None):
     secs, rows = sorted(windows)[len(windows) // 2]
     del it
     # bytes per step, from the same batches (untimed pass)
-    it = dp.make_iterator(g, seed_override=1, device=local, host_output=True)
+    it = dp.make_iterator(g, seed_override=1, device=local, host_output=True, max_launch_bytes=launch)
     for _ in range(per_epoch):
         it.get_next().release()
     b_in = b_out = 0

@@ -20,7 +20,8 @@
 // is computed once and kept in registers (two rows, ping-pong, no moves);
 // each output row is then one vertical lerp + the op per value.
 //
-// Horizontal taps are periodic: win_w = PI * G, mid_w = PO * G and every
+// Horizontal taps are periodic (instantiated window : mid ratios 10:7, 8:7,
+// 5:7, 5:4, 9:7, 12:7, 6:7, 4:7, 3:2, 2:1): win_w = PI * G, mid_w = PO * G and every
 // mid column x = PO p + c reads window columns PI p + T(c) and + 1 (the host
 // checks every column against the device tap formula; the right-edge clamp
 // x1 == x0 gets weight 0, which gives p00 exactly as the clamped blend does).
@@ -599,6 +600,12 @@ bool roll_plan(const dp_image_chain* c, int out_h, int out_w, RollPlanHost& h) {
   else if (periodic_map<7, 8>(a.win_w, a.mid_w)) PO = 7, PI = 8;
   else if (periodic_map<7, 5>(a.win_w, a.mid_w)) PO = 7, PI = 5;
   else if (periodic_map<8, 10>(a.win_w, a.mid_w)) PO = 8, PI = 10;  // 5:4 as two periods per lane (24 floats)
+  else if (periodic_map<7, 9>(a.win_w, a.mid_w)) PO = 7, PI = 9;     // 288 -> 224
+  else if (periodic_map<7, 12>(a.win_w, a.mid_w)) PO = 7, PI = 12;   // 384 -> 224
+  else if (periodic_map<7, 6>(a.win_w, a.mid_w)) PO = 7, PI = 6;     // 192 -> 224
+  else if (periodic_map<7, 4>(a.win_w, a.mid_w)) PO = 7, PI = 4;     // 128 -> 224
+  else if (periodic_map<8, 12>(a.win_w, a.mid_w)) PO = 8, PI = 12;   // 3:2, e.g. 384 -> 256
+  else if (periodic_map<8, 16>(a.win_w, a.mid_w)) PO = 8, PI = 16;   // 2:1
   else return false;
   // the pixel op
   int op = 0;
@@ -705,6 +712,12 @@ int roll_chain_batch(const uint8_t* images, int64_t num_images, const int64_t* o
   DP_ROLL(7, 8)
   DP_ROLL(7, 5)
   DP_ROLL(8, 10)
+  DP_ROLL(7, 9)
+  DP_ROLL(7, 12)
+  DP_ROLL(7, 6)
+  DP_ROLL(7, 4)
+  DP_ROLL(8, 12)
+  DP_ROLL(8, 16)
 #undef DP_ROLL
   return 1;
 }

@@ -87,6 +87,15 @@ CASES = {
     "two_stripes_random_post_crop": ((320, 320), [("resize", 256, 256), ("random_crop", 224, 224, 5, True),
                                                   ("normalize", MEAN, STD)], 16, 12),
     "k4_full_size": ((320, 320), [("resize", 224, 224), ("normalize", MEAN, STD)], 24, 20),
+    # the other instantiated ratios: 9:7, 12:7, 6:7, 4:7, 3:2, 2:1
+    "ratio_9to7": ((144, 144), [("resize", 112, 112), ("normalize", MEAN, STD)], 12, 11),
+    "ratio_12to7": ((48, 48), [("resize", 28, 28), ("normalize", MEAN, STD)], 16, 16),
+    "ratio_6to7_post_crop": ((96, 96), [("resize", 112, 112), ("random_crop", 96, 92, 2, True),
+                                        ("normalize", MEAN, STD)], 12, 12),
+    "ratio_4to7_pre_crop": ((64, 64), [("random_crop", 48, 48, 6, True), ("resize", 84, 84),
+                                       ("normalize", MEAN, STD)], 12, 12),
+    "ratio_3to2_center": ((96, 96), [("resize", 64, 64), ("center_crop", 48, 48), ("normalize", MEAN, STD)], 12, 12),
+    "ratio_2to1_affine": ((128, 128), [("resize", 64, 64), ("affine", (0.5, 0.25, 2.0), (1.0, -1.0, 0.0))], 12, 12),
 }
 
 

@@ -283,6 +283,12 @@ struct RollWarp {
     for (int i = 0; i < kW; ++i) wx2[i] = pk2(wx[RO::e0(i)], wx[RO::e1(i)]);
   }
 
+  // float4 slot swizzle of the row buffer on the float4 store path: lanes
+  // write 6 float4 apart (2-way bank conflicts in a quarter warp); flipping
+  // bit 0 of the slot in every odd group of 8 spreads them, and the readout's
+  // 8 consecutive slots stay one aligned group (a permutation within it)
+  static __device__ __forceinline__ int swz(int q) { return q ^ ((q >> 3) & 1); }
+
   // one output row from the blends of its two window rows
   template <bool kVec>
   __device__ __forceinline__ void emit(const RollArgs& a, const RollTap* tp, int r, float4* orow, int row_f4,
@@ -292,7 +298,6 @@ struct RollWarp {
     // j, so each float4 / word store issues as soon as its values exist and
     // few results are live at once
     float2 f[kP];
-    float4* d = reinterpret_cast<float4*>(buf + (vec_base >= 0 ? vec_base : 0));
 #pragma unroll
     for (int j = 0; j < RO::kNPP; ++j) {
 #pragma unroll
@@ -315,10 +320,12 @@ struct RollWarp {
       if constexpr (kVec && kF % 4 == 0) {
         auto val = [&](int e) { return RO::hi_of(e) ? f[RO::pair_of(e)].y : f[RO::pair_of(e)].x; };
         const int done = 6 * j + 6;  // values [0, done) exist
+        const int q4 = (vec_base >> 2);  // the lane's first float4 (vec_base is 16-byte aligned)
 #pragma unroll
         for (int q = 0; q < kF / 4; ++q)
           if (4 * q + 4 <= done && 4 * q + 4 > done - 6 && vec_base >= 0)
-            d[q] = make_float4(val(4 * q), val(4 * q + 1), val(4 * q + 2), val(4 * q + 3));
+            reinterpret_cast<float4*>(buf)[swz(q4 + q)] =
+                make_float4(val(4 * q), val(4 * q + 1), val(4 * q + 2), val(4 * q + 3));
       }
     }
     __syncwarp();
@@ -328,7 +335,7 @@ struct RollWarp {
 #pragma unroll
     for (int it = 0; it < (3 * PO + 3) / 4; ++it) {
       const int c = lane + 32 * it;
-      if (c < n4) st_cs_f4(o + c, b4[c]);
+      if (c < n4) st_cs_f4(o + c, b4[kVec && kF % 4 == 0 ? swz(c) : c]);
     }
     __syncwarp();
   }

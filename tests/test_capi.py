@@ -303,3 +303,14 @@ def test_image_chain_kernel_choice_without_gpu():
     assert kern([("random_crop", 28, 28, 3, True), ("resize", 24, 24)], 48, 48) == 9   # 7:6 is not instantiated
     assert kern([("random_crop", 24, 24, 3, True), ("normalize", mean, std)], 48, 48) == 9  # no resize
     assert kern([("random_crop", 24, 24, 3, True)], 48, 48) == 9
+
+
+def test_bench_e2e_consumer_builds_against_the_c_abi():
+    """tools/e2e_consumer.c (bench.py's token e2e loop) is plain C over
+    include/dpcuda_pipeline.h and links against libdpcuda.so."""
+    import __graft_entry__
+    import os
+    __graft_entry__._build_e2e_consumer()
+    path = os.path.join(os.path.dirname(_capi.LIB_PATH), "..", "..", "tools", "bin", "libdpe2e.so")
+    lib = ctypes.CDLL(os.path.abspath(path))
+    assert hasattr(lib, "dpe2e_consume_host_batches")

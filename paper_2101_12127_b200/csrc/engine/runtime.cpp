@@ -282,10 +282,9 @@ class DevicePipeline {
                            "K9 gather_copy_batch"};
     std::string kernel = kinds[static_cast<int>(L_.kind)];
     int k10 = 0;  // a resize chain over a periodic column map on HBM-resident images: K10
-    if (L_.kind == BatchKind::kChain && L_.source->residency != Residency::kHost &&
-        dp_image_chain_kernel(&L_.img_chain, &k10) == DP_OK && k10 == 10)
+    if (L_.kind == BatchKind::kChain && dp_image_chain_kernel(&L_.img_chain, &k10) == DP_OK && k10 == 10)
       kernel = "K10 image_chain_roll (via K9 image_chain_batch)";
-    if (L_.kind == BatchKind::kResize && L_.source->residency != Residency::kHost) {
+    if (L_.kind == BatchKind::kResize) {
       dp_image_chain c{};  // resize + normalize as a chain: K10 when its column map is periodic
       c.in_h = static_cast<int>(L_.source->h);
       c.in_w = static_cast<int>(L_.source->w);

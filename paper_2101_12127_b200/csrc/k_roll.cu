@@ -527,13 +527,17 @@ bool periodic_map(int win_w, int mid_w) {
   return true;
 }
 
+int roll_env(const char* name, int fallback);
+
 bool roll_in_device_memory(const void* p) {
   cudaPointerAttributes attr{};
   if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
     cudaGetLastError();
     return false;
   }
-  return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
+  // HBM, or pinned host memory: the TMA engine reads it over PCIe in bulk
+  return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged ||
+         (attr.type == cudaMemoryTypeHost && roll_env("DP_DEV_TMA_HOST", 1));
 }
 
 int roll_env(const char* name, int fallback) {  // development-only knob overrides (tools/dev)

@@ -39,6 +39,7 @@
 // mbarrier stages; W consumer warps split a band into runs x stripes and
 // release stages through "empty" mbarriers (no CTA barrier in the loop).
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
@@ -559,15 +560,15 @@ int roll_sm_count() {
 template <int PO, int PI, int kOp>
 int roll_launch(const RollArgs& a, size_t smem, cudaStream_t s) {
   auto kernel = roll_kernel<PO, PI, kOp>;
-  static int dev_set = -1;  // the smem attribute, once per process (single device per process here)
+  static std::atomic<int> dev_set{-1};  // the smem attribute, set again when the device changes
   int dev = 0;
   cudaGetDevice(&dev);
-  if (dev_set != dev) {
+  if (dev_set.load(std::memory_order_relaxed) != dev) {
     const int rc = cuda_status(
         cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kRollSmemMax)),
         "image_chain (roll) smem attribute");
     if (rc) return rc;
-    dev_set = dev;
+    dev_set.store(dev, std::memory_order_relaxed);
   }
   const int64_t items = a.rows * a.bands;
   const int grid = static_cast<int>(std::min<int64_t>(items, roll_sm_count()));

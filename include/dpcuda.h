@@ -362,6 +362,12 @@ int dp_k_order_digest(const int64_t* values, int64_t n, int64_t first,
 int dp_k_word_digest(const uint32_t* words, int64_t n, int64_t first,
                      uint64_t* digest_dev, void* stream);
 
+/* rows x width bytes of a pitched (device) source, packed into dst --    */
+/* typically mapped pinned host memory: an SM-side read-back that does not */
+/* queue behind the copy engines (the plan's small read-backs while a      */
+/* launch group's host_output copy is in flight).                          */
+int dp_k_copy_strided(const void* src, size_t src_pitch, size_t width, size_t rows, void* dst, void* stream);
+
 /* ---------------------------------------------------------------------- */
 /* Synthetic inputs (same generators as oracle/restate.c). */
 /* images[i, off] = top byte of SplitMix64Next(seed ^ ((first_id + i) *    */

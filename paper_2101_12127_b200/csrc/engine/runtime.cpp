@@ -196,6 +196,7 @@ class DevicePipeline {
     cudaStreamDestroy(stream_);
     cudaStreamDestroy(plan_stream_);
     if (copy_stream_) cudaStreamDestroy(copy_stream_);
+    if (rb_host_) cudaFreeHost(rb_host_);
   }
 
   // The per-batch fast path makes no CUDA call and takes one lock (in
@@ -484,6 +485,37 @@ class DevicePipeline {
     if (pending_plan_.valid()) pending_plan_.get();  // rethrows the helper's error
   }
 
+  // Plan read-backs (counts, batch shapes): a kernel on stream s writes the
+  // bytes into mapped pinned host memory and s is synchronised -- no copy
+  // engine involved, so they never queue behind a launch group's host_output
+  // D2H copy (which held every token epoch's next plan for the length of a
+  // 200 MB copy).  rows x width bytes at src_pitch (contiguous by default).
+  void ReadBack(void* dst, const void* src, size_t width, cudaStream_t s, size_t rows = 1, size_t src_pitch = 0) {
+    const size_t bytes = width * rows;
+    if (!bytes) return;
+    static const bool copy_engine = std::getenv("DP_DEV_RB_COPY") != nullptr;  // development A/B switch
+    if (copy_engine) {
+      CudaCheck(cudaMemcpy2DAsync(dst, width, src, src_pitch ? src_pitch : width, width, rows, cudaMemcpyDeviceToHost,
+                                  s),
+                "read-back");
+      CudaCheck(cudaStreamSynchronize(s), "read-back");
+      return;
+    }
+    std::lock_guard lk(rb_mu_);
+    if (bytes > rb_cap_) {
+      if (rb_host_) {
+        CudaCheck(cudaStreamSynchronize(s), "read-back");
+        cudaFreeHost(rb_host_);
+        rb_host_ = nullptr;
+      }
+      rb_cap_ = std::max<size_t>(bytes, size_t(1) << 20);
+      CudaCheck(cudaHostAlloc(&rb_host_, rb_cap_, cudaHostAllocMapped | cudaHostAllocPortable), "read-back buffer");
+    }
+    KCheck(dp_k_copy_strided(src, src_pitch ? src_pitch : width, width, rows, rb_host_, s), "read-back");
+    CudaCheck(cudaStreamSynchronize(s), "read-back");
+    std::memcpy(dst, rb_host_, bytes);
+  }
+
   // Builds epoch e's plan on a helper thread (plan stream); Plan() joins it.
   void PrefetchPlan(int64_t e) {
     JoinPendingPlan();
@@ -632,8 +664,7 @@ class DevicePipeline {
                  "filter");
           launches_ += 3;
           int64_t m = 0;
-          CudaCheck(cudaMemcpyAsync(&m, nk.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, s), "filter count");
-          CudaCheck(cudaStreamSynchronize(s), "filter count");
+          ReadBack(&m, nk.get(), sizeof(int64_t), s);
           cur = out;
           count = m;
           break;
@@ -680,8 +711,7 @@ class DevicePipeline {
         KCheck(dp_k_batch_max_len(P<int32_t>(L_.source->lengths), P<int64_t>(cur), count, L_.batch, P<int32_t>(lm), s),
                "batch_max_len");
         launches_++;
-        CudaCheck(cudaMemcpyAsync(p.lmax.data(), lm.get(), sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, s), "lmax");
-        CudaCheck(cudaStreamSynchronize(s), "lmax");
+        ReadBack(p.lmax.data(), lm.get(), sizeof(int32_t) * nb, s);
         for (int64_t j = 0; j < nb; ++j) {
           const int64_t rows = std::min<int64_t>(L_.batch, count - j * L_.batch);
           p.boff[j + 1] = p.boff[j] + rows * p.lmax[j];
@@ -720,8 +750,7 @@ class DevicePipeline {
       launches_ += 3;
     }
     int64_t total = 0;
-    CudaCheck(cudaMemcpyAsync(&total, P<int64_t>(prefix) + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s), "staged");
-    CudaCheck(cudaStreamSynchronize(s), "staged size");
+    ReadBack(&total, P<int64_t>(prefix) + n, sizeof(int64_t), s);
     p.st_tokens = dalloc(sizeof(int32_t) * std::max<int64_t>(total, 1));
     p.st_lengths = dalloc(sizeof(int32_t) * std::max<int64_t>(n, 1));
     p.st_offsets = prefix;
@@ -792,13 +821,8 @@ class DevicePipeline {
     const int64_t B = L_.batch, nb = L_.drop ? count / B : (count + B - 1) / B;
     p.boff.assign(nb + 1, 0);
     if (nb) {  // prefix[j * B] for j < nb, then the end of the last batch
-      CudaCheck(cudaMemcpy2DAsync(p.boff.data(), sizeof(int64_t), prefix.get(), sizeof(int64_t) * B, sizeof(int64_t),
-                                  nb, cudaMemcpyDeviceToHost, s),
-                "batch starts");
-      CudaCheck(cudaMemcpyAsync(&p.boff[nb], P<int64_t>(prefix) + std::min(nb * B, count), sizeof(int64_t),
-                                cudaMemcpyDeviceToHost, s),
-                "batch end");
-      CudaCheck(cudaStreamSynchronize(s), "batch starts");
+      ReadBack(p.boff.data(), prefix.get(), sizeof(int64_t), s, nb, sizeof(int64_t) * B);  // prefix[j * B]
+      ReadBack(&p.boff[nb], P<int64_t>(prefix) + std::min(nb * B, count), sizeof(int64_t), s);
     }
     p.lmax.assign(nb, 0);
     for (int64_t j = 0; j < nb; ++j) p.lmax[j] = static_cast<int32_t>(p.boff[j + 1] - p.boff[j]);  // tokens
@@ -823,14 +847,12 @@ class DevicePipeline {
            "bucket_plan");
     launches_ += 8;
     int64_t nb = 0;
-    CudaCheck(cudaMemcpyAsync(&nb, nbd.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, s), "bucket count");
-    CudaCheck(cudaStreamSynchronize(s), "bucket count");
+    ReadBack(&nb, nbd.get(), sizeof(int64_t), s);
     std::vector<int32_t> rows32(nb);
     p.lmax.assign(nb, 0);
     if (nb) {
-      CudaCheck(cudaMemcpyAsync(rows32.data(), brows.get(), sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, s), "rows");
-      CudaCheck(cudaMemcpyAsync(p.lmax.data(), blmax.get(), sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, s), "lmax");
-      CudaCheck(cudaStreamSynchronize(s), "bucket rows");
+      ReadBack(rows32.data(), brows.get(), sizeof(int32_t) * nb, s);
+      ReadBack(p.lmax.data(), blmax.get(), sizeof(int32_t) * nb, s);
     }
     p.rows.assign(rows32.begin(), rows32.end());
     p.boff.assign(nb + 1, 0);
@@ -1554,6 +1576,9 @@ class DevicePipeline {
   uint64_t base_seed_;
   IteratorOptions opt_;
   cudaStream_t stream_ = nullptr, plan_stream_ = nullptr, copy_stream_ = nullptr, consumer_ = nullptr;
+  std::mutex rb_mu_;  // the plan read-back buffer (mapped pinned host memory)
+  void* rb_host_ = nullptr;
+  size_t rb_cap_ = 0;
   int64_t depth_ = 2;
   int64_t max_depth_ = 2;  // AUTOTUNE ceiling: the slots pre-allocated within the budget
   bool autotune_ = false;

@@ -1,5 +1,6 @@
 // k_index.cu -- K1 range_affine_batch, K6 shard / interleave index mapping,
 // K7 order digest, synthetic input generators.  All HBM-bound integer work.
+#include <algorithm>
 #include <cstdint>
 #include <queue>
 #include <vector>
@@ -322,4 +323,32 @@ extern "C" int dp_k_synth_tokens(int32_t* tokens, const int64_t* offsets, int64_
   if (n <= 0) return DP_OK;
   synth_tokens_kernel<<<grid_for(n * 32, 1), kThreads, 0, as_stream(stream)>>>(tokens, offsets, n, seed);
   return launch_status("synth_tokens");
+}
+
+namespace dpk {
+namespace {
+// rows x width bytes from a pitched source into a packed destination; the
+// destination is typically mapped pinned host memory (an SM-side write over
+// PCIe that does not queue behind the copy engines)
+__global__ void copy_strided_kernel(const uint8_t* __restrict__ src, size_t pitch, size_t width, size_t rows,
+                                    uint8_t* __restrict__ dst) {
+  const size_t total = width * rows;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const size_t r = i / width, c = i - r * width;
+    dst[i] = src[r * pitch + c];
+  }
+}
+}  // namespace
+}  // namespace dpk
+
+extern "C" int dp_k_copy_strided(const void* src, size_t src_pitch, size_t width, size_t rows, void* dst,
+                                 void* stream) {
+  if (width == 0 || rows == 0) return DP_OK;
+  if (!src || !dst || src_pitch < width) return dpk::fail(DP_ERR_INVALID_ATTR, "copy_strided: bad arguments");
+  const size_t total = width * rows;
+  const int blocks = static_cast<int>(std::min<size_t>((total + 255) / 256, 148 * 4));
+  dpk::copy_strided_kernel<<<blocks, 256, 0, dpk::as_stream(stream)>>>(static_cast<const uint8_t*>(src), src_pitch,
+                                                                        width, rows, static_cast<uint8_t*>(dst));
+  return dpk::launch_status("copy_strided");
 }

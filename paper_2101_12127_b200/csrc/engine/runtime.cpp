@@ -51,6 +51,7 @@
 #include <set>
 #include <sstream>
 
+#include "../roll.hpp"
 #include "dpb200/datapipe.hpp"
 #include "dpcuda.h"
 #include "engine/device_util.hpp"
@@ -298,7 +299,7 @@ class DevicePipeline {
         c.op_b[0][ch] = L_.norm.stdv[ch];
       }
       c.out_f32 = 1;
-      if (dp_image_chain_kernel(&c, &k10) == DP_OK && k10 == 10)
+      if (dpk::roll_chain_eligible(&c, c.rs_h, c.rs_w, /*allow_general=*/false))  // as resize_normalize_batch
         kernel = "K10 image_chain_roll (via K4 resize_normalize_batch)";
     }
     os << "batch stage: " << kernel << " (batch " << L_.batch << (L_.drop ? ", drop" : "")

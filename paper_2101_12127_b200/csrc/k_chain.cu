@@ -380,7 +380,7 @@ extern "C" int dp_k_image_chain_batch(const uint8_t* images, int64_t num_images,
   // resize chains over a periodic column map: K10 (k_roll.cu)
   if (f32) {
     const int rc = roll_chain_batch(images, num_images, order, first, rows, id_base, id_stride, id_block, chain, oh, ow,
-                                    out_ids, static_cast<float*>(out), as_stream(stream));
+                                    out_ids, static_cast<float*>(out), as_stream(stream), true);
     if (rc != 1) return rc;
   }
   ChainArgs a{};

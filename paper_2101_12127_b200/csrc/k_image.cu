@@ -959,7 +959,7 @@ static int resize_impl(const uint8_t* images, int64_t num_images, int in_h, int 
       return dp_k_image_chain_batch(images, num_images, order, first, rows, ids.base, ids.stride, ids.block, &c,
                                     out_ids, out, stream);
     const int rc = roll_chain_batch(images, num_images, order, first, rows, ids.base, ids.stride, ids.block, &c, out_h,
-                                    out_w, out_ids, out, s);
+                                    out_w, out_ids, out, s, /*allow_general=*/false);
     if (rc != 1) return rc;
   }
   if (fast_ok(images, in_w, out_w, out)) {

@@ -287,8 +287,9 @@ def test_pipeline_spec_errors_carry_line_and_column():
 
 
 def test_image_chain_kernel_choice_without_gpu():
-    """dp_image_chain_kernel: resize chains over a periodic column map run on
-    K10 (k_roll.cu), the rest on K9; pure host logic."""
+    """dp_image_chain_kernel: resize chains (periodic column maps, or any
+    other with runtime taps) run on K10 (k_roll.cu), the rest on K9; pure
+    host logic."""
     mean, std = (123.675, 116.28, 103.53), (58.395, 57.12, 57.375)
 
     def kern(steps, h, w):
@@ -300,7 +301,8 @@ def test_image_chain_kernel_choice_without_gpu():
     assert kern([("random_crop", 160, 160, 7, True), ("resize", 224, 224), ("normalize", mean, std)], 256, 256) == 10
     assert kern([("resize", 256, 256), ("center_crop", 224, 224), ("normalize", mean, std)], 320, 320) == 10
     assert kern([("resize", 224, 224), ("normalize", mean, std)], 320, 320) == 10
-    assert kern([("random_crop", 28, 28, 3, True), ("resize", 24, 24)], 48, 48) == 9   # 7:6 is not instantiated
+    assert kern([("random_crop", 28, 28, 3, True), ("resize", 24, 24)], 48, 48) == 10  # 7:6: runtime taps
+    assert kern([("normalize", mean, std), ("resize", 24, 24)], 48, 48) == 9           # pixel op before the resize
     assert kern([("random_crop", 24, 24, 3, True), ("normalize", mean, std)], 48, 48) == 9  # no resize
     assert kern([("random_crop", 24, 24, 3, True)], 48, 48) == 9
 

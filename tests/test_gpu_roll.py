@@ -96,6 +96,16 @@ CASES = {
                                        ("normalize", MEAN, STD)], 12, 12),
     "ratio_3to2_center": ((96, 96), [("resize", 64, 64), ("center_crop", 48, 48), ("normalize", MEAN, STD)], 12, 12),
     "ratio_2to1_affine": ((128, 128), [("resize", 64, 64), ("affine", (0.5, 0.25, 2.0), (1.0, -1.0, 0.0))], 12, 12),
+    # any other downscaling ratio: the general column map (runtime taps per pixel)
+    "general_7to6_crop_flip": ((48, 48), [("random_crop", 28, 28, 3, True), ("resize", 24, 24),
+                                          ("normalize", MEAN, STD)], 16, 16),
+    "general_25to16": ((112, 112), [("resize", 72, 72), ("normalize", MEAN, STD)], 8, 8),
+    "general_8to5_affine": ((96, 96), [("resize", 60, 60), ("affine", (0.5, 0.25, 2.0), (1.0, -1.0, 0.0))], 8, 8),
+    "general_post_crop_flip": ((80, 80), [("resize", 72, 72), ("random_crop", 64, 60, 4, True),
+                                          ("normalize", MEAN, STD)], 8, 8),
+    "general_ieee": ((80, 48), [("random_crop", 66, 44, 1, False), ("resize", 50, 36),
+                                ("normalize", (0.0, 0.0, 0.0), ADV_STD)], 8, 8),
+    "general_wide_two_stripes": ((128, 512), [("resize", 96, 300), ("normalize", MEAN, STD)], 4, 4),
 }
 
 
@@ -141,12 +151,15 @@ def test_k10_sharded_ids_key_the_crops(K, orc):
 
 
 def test_k10_eligibility(K):
-    # periodic maps run on K10; others (and pre-resize pixel ops, two post ops) stay on K9
+    # resize chains run on K10 (periodic maps or runtime taps); pre-resize pixel ops, two post ops and
+    # output rows that are not whole float4 stay on K9
     assert kernel_of(K, [("random_crop", 160, 160, 7, True), ("resize", 224, 224), ("normalize", MEAN, STD)],
                      256, 256) == 10
     assert kernel_of(K, [("resize", 256, 256), ("center_crop", 224, 224), ("normalize", MEAN, STD)], 320, 320) == 10
     assert kernel_of(K, [("random_crop", 28, 28, 3, True), ("resize", 24, 24), ("normalize", MEAN, STD)],
-                     48, 48) == 9
+                     48, 48) == 10  # general column map
+    assert kernel_of(K, [("random_crop", 28, 28, 3, True), ("resize", 24, 26)], 48, 48) == 9  # 26 * 3 % 4 != 0
+    assert kernel_of(K, [("resize", 100, 100), ("normalize", MEAN, STD)], 64, 64) == 9  # a non-periodic upscale
     assert kernel_of(K, [("normalize", MEAN, STD), ("resize", 56, 56)], 80, 80) == 9
     assert kernel_of(K, [("resize", 56, 56), ("affine", (1, 1, 1), (0, 0, 0)), ("normalize", MEAN, STD)],
                      80, 80) == 9

@@ -192,15 +192,19 @@ struct Roll {
   // clamped ones of chain_coord (no periodic form needed)
   static constexpr bool kGen = PI == 0;
 
-  static __device__ __forceinline__ void hrow_gen(const uint8_t* row, const int (&offl)[PO], const int (&offr)[PO],
-                                                  f32x2 (&H)[kP], const f32x2 (&wx2)[kW], const PkK& k) {
+  // (the right tap is the next window column, 3 bytes on -- or 3 back when
+  // crop A flips; a right-edge clamp carries weight 0 instead)
+  template <bool kFlip>
+  static __device__ __forceinline__ void hrow_gen(const uint8_t* row, const int (&offl)[PO], f32x2 (&H)[kP],
+                                                  const f32x2 (&wx2)[kW], const PkK& k) {
+    constexpr int kR = kFlip ? -3 : 3;
 #pragma unroll
     for (int i = 0; i < kP; ++i) {
       const int c0 = e0(i) / 3, c1 = e1(i) / 3, ch = e0(i) % 3;
       const f32x2 pl = pk2(__uint_as_float(0x4B000000u | row[offl[c0] + ch]),
                            __uint_as_float(0x4B000000u | row[offl[c1] + ch]));
-      const f32x2 pr = pk2(__uint_as_float(0x4B000000u | row[offr[c0] + ch]),
-                           __uint_as_float(0x4B000000u | row[offr[c1] + ch]));
+      const f32x2 pr = pk2(__uint_as_float(0x4B000000u | row[offl[c0] + ch + kR]),
+                           __uint_as_float(0x4B000000u | row[offl[c1] + ch + kR]));
       H[i] = k.lerp_u8(pl, pr, wx2[wi(i)]);
     }
   }
@@ -245,7 +249,7 @@ struct RollWarp {
   float sa[3], sb[3], sr_[3];  // op constants per channel (normalize: mean, -std, RN(1 / std))
   int g_ox1, g_f1;
   int p, pos[PO], vec_base;
-  int xl[RO::kGen ? PO : 1], xr[RO::kGen ? PO : 1];  // general map: the window columns of each pixel's taps
+  int xl[RO::kGen ? PO : 1];  // general map: the window column of each pixel's left tap
   bool vec;
   f32x2 wx2[kW];
 
@@ -297,9 +301,9 @@ struct RollWarp {
       int xa, xb;
       float w;
       roll_coord(p * PO + c, a.win_w, a.scale_x, xa, xb, w);
-      if constexpr (RO::kGen) {  // the clamped taps themselves
+      if constexpr (RO::kGen) {  // the left tap; the right one is the next column
         xl[c] = xa;
-        xr[c] = xb;
+        if (xb == xa) w = 0.0f;  // right clamp: p00 exactly, whatever the next column holds
       } else if (xb == xa) {
         // the periodic taps are (xf, xf + 1), xf = PI p + T(c); at the edges
         // they differ from the clamped ones but give p00 exactly:
@@ -380,16 +384,13 @@ struct RollWarp {
                                                           (3 * a.out_w) + 3 * px_lo);
     const int row_f4 = 3 * a.out_w / 4;
     const int b = kFlip ? m.adj + 3 * (a.win_w - 1 - PI * p - (RO::T(PO - 1) + 1)) : m.adj + 3 * (PI * p + RO::T(0));
-    int offl[PO], offr[PO];  // general map: tap byte offsets in a staged row (crop A's flip mirrors them)
+    int offl[PO];  // general map: left-tap byte offsets in a staged row (crop A's flip mirrors them)
     if constexpr (RO::kGen) {
 #pragma unroll
-      for (int c = 0; c < PO; ++c) {
-        offl[c] = m.adj + 3 * (kFlip ? a.win_w - 1 - xl[c] : xl[c]);
-        offr[c] = m.adj + 3 * (kFlip ? a.win_w - 1 - xr[c] : xr[c]);
-      }
+      for (int c = 0; c < PO; ++c) offl[c] = m.adj + 3 * (kFlip ? a.win_w - 1 - xl[c] : xl[c]);
     }
     auto hrow = [&](const uint8_t* row, f32x2(&H)[kP]) {
-      if constexpr (RO::kGen) RO::hrow_gen(row, offl, offr, H, wx2, k);
+      if constexpr (RO::kGen) RO::template hrow_gen<kFlip>(row, offl, H, wx2, k);
       else RO::template hrow<kFlip>(row, b, H, wx2, k);
     };
     f32x2 A[kP], B[kP];
@@ -660,7 +661,7 @@ bool roll_plan(const dp_image_chain* c, int out_h, int out_w, RollPlanHost& h, b
   else if (periodic_map<8, 12>(a.win_w, a.mid_w)) PO = 8, PI = 12;   // 3:2, e.g. 384 -> 256
   else if (periodic_map<8, 16>(a.win_w, a.mid_w)) PO = 8, PI = 16;   // 2:1
   // any other ratio, for downscaling chains: runtime taps (measured against
-  // K9: 240 -> 176 5.70 vs 3.79 M img/s; upscales and the plain resize of
+  // K9: 240 -> 176 6.2 vs 3.8 M img/s; upscales and the plain resize of
   // dp_k_resize_normalize_batch stay on K9 / K4, which are faster there)
   else if (allow_general && a.win_w > a.mid_w && roll_env("DP_DEV_ROLL_GENERAL", 1)) PO = 8, PI = 0;
   else return false;

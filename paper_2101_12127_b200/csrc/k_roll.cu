@@ -660,10 +660,11 @@ bool roll_plan(const dp_image_chain* c, int out_h, int out_w, RollPlanHost& h, b
   else if (periodic_map<7, 4>(a.win_w, a.mid_w)) PO = 7, PI = 4;     // 128 -> 224
   else if (periodic_map<8, 12>(a.win_w, a.mid_w)) PO = 8, PI = 12;   // 3:2, e.g. 384 -> 256
   else if (periodic_map<8, 16>(a.win_w, a.mid_w)) PO = 8, PI = 16;   // 2:1
-  // any other ratio, for downscaling chains: runtime taps (measured against
-  // K9: 240 -> 176 6.2 vs 3.8 M img/s; upscales and the plain resize of
-  // dp_k_resize_normalize_batch stay on K9 / K4, which are faster there)
-  else if (allow_general && a.win_w > a.mid_w && roll_env("DP_DEV_ROLL_GENERAL", 1)) PO = 8, PI = 0;
+  // any other ratio of a chain: runtime taps (against K9: 240 -> 176 6.2 vs
+  // 3.8 M img/s, 176 -> 224 5.7 vs 4.7); dp_k_resize_normalize_batch keeps
+  // K4 for them (300 -> 224: K4 5.0, this form 4.1 M img/s)
+  else if ((allow_general || roll_env("DP_DEV_K4_GENERAL", 0)) && roll_env("DP_DEV_ROLL_GENERAL", 1))
+    PO = 8, PI = 0;
   else return false;
   // the pixel op
   int op = 0;

@@ -10,7 +10,7 @@
 namespace dpk {
 
 // Launches K10 for a chain with a resize and at most one pixel op after it
-// when the column map is periodic (or, with allow_general, any downscale)
+// when the column map is periodic (or, with allow_general, any other ratio)
 // and the buffers qualify (16-byte aligned, images in HBM or pinned host
 // memory); returns 1 (nothing launched) when the chain is not K10's, DP_OK
 // after the launch, or an error status.

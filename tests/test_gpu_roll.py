@@ -96,10 +96,13 @@ CASES = {
                                        ("normalize", MEAN, STD)], 12, 12),
     "ratio_3to2_center": ((96, 96), [("resize", 64, 64), ("center_crop", 48, 48), ("normalize", MEAN, STD)], 12, 12),
     "ratio_2to1_affine": ((128, 128), [("resize", 64, 64), ("affine", (0.5, 0.25, 2.0), (1.0, -1.0, 0.0))], 12, 12),
-    # any other downscaling ratio: the general column map (runtime taps per pixel)
+    # any other ratio: the general column map (runtime taps per pixel)
     "general_7to6_crop_flip": ((48, 48), [("random_crop", 28, 28, 3, True), ("resize", 24, 24),
                                           ("normalize", MEAN, STD)], 16, 16),
     "general_25to16": ((112, 112), [("resize", 72, 72), ("normalize", MEAN, STD)], 8, 8),
+    "general_16to25_up": ((64, 64), [("resize", 100, 100), ("normalize", MEAN, STD)], 8, 8),
+    "general_rrc_11to14_up": ((256, 256), [("random_crop", 176, 176, 5, True), ("resize", 224, 224),
+                                           ("normalize", MEAN, STD)], 12, 12),
     "general_8to5_affine": ((96, 96), [("resize", 60, 60), ("affine", (0.5, 0.25, 2.0), (1.0, -1.0, 0.0))], 8, 8),
     "general_post_crop_flip": ((80, 80), [("resize", 72, 72), ("random_crop", 64, 60, 4, True),
                                           ("normalize", MEAN, STD)], 8, 8),
@@ -159,7 +162,7 @@ def test_k10_eligibility(K):
     assert kernel_of(K, [("random_crop", 28, 28, 3, True), ("resize", 24, 24), ("normalize", MEAN, STD)],
                      48, 48) == 10  # general column map
     assert kernel_of(K, [("random_crop", 28, 28, 3, True), ("resize", 24, 26)], 48, 48) == 9  # 26 * 3 % 4 != 0
-    assert kernel_of(K, [("resize", 100, 100), ("normalize", MEAN, STD)], 64, 64) == 9  # a non-periodic upscale
+    assert kernel_of(K, [("resize", 100, 100), ("normalize", MEAN, STD)], 64, 64) == 10  # a non-periodic upscale
     assert kernel_of(K, [("normalize", MEAN, STD), ("resize", 56, 56)], 80, 80) == 9
     assert kernel_of(K, [("resize", 56, 56), ("affine", (1, 1, 1), (0, 0, 0)), ("normalize", MEAN, STD)],
                      80, 80) == 9

@@ -61,6 +61,7 @@ for name, hw, steps, entry in CASES:
     res = {}
     for mode, env in (("K10 general", "1"), ("fallback", "0")):
         os.environ["DP_DEV_ROLL_GENERAL"] = env
+        os.environ["DP_DEV_K4_GENERAL"] = env
         ms, ips, out = run(steps, hw, entry=entry)
         res[mode] = out.clone()
         print(f"{name:32s} {mode:12s}: {ms:.3f} ms per 4096 images, {ips / 1e6:.2f} M img/s", flush=True)

@@ -210,3 +210,51 @@ def test_unproven_constants_use_ieee_division(K, orc, which):
     for j in range(rows):
         want = orc.chain(imgs[order[j]], int(order[j]), steps)
         assert np.array_equal(got[j].view(np.uint32), want.view(np.uint32)), j
+
+
+def test_k10_random_chains_bit_exact(K, orc):
+    """40 seeded random resize chains (image sizes, crop A / B modes and
+    flips, output sizes of any ratio -- periodic or not, up or down --,
+    the pixel op and its constants), each on K10 when eligible, compared
+    value for value with the oracle's sequential chain."""
+    import torch
+    rng = np.random.default_rng(2024)
+    ran = 0
+    for case in range(40):
+        in_w = int(rng.choice([16, 32, 48, 64, 80, 96]))
+        in_h = int(rng.integers(8, 97))
+        steps = []
+        win_h, win_w = in_h, in_w
+        if rng.random() < 0.6:
+            win_h, win_w = int(rng.integers(4, in_h + 1)), int(rng.integers(4, in_w + 1))
+            if rng.random() < 0.7:
+                steps.append(("random_crop", win_h, win_w, int(rng.integers(0, 100)), bool(rng.random() < 0.5)))
+            else:
+                steps.append(("center_crop", win_h, win_w))
+        mid_h, mid_w = int(rng.integers(4, 2 * win_h + 4)), 4 * int(rng.integers(1, (2 * win_w + 8) // 4 + 1))
+        steps.append(("resize", mid_h, mid_w))
+        out_h, out_w = mid_h, mid_w
+        if rng.random() < 0.4:
+            out_h, out_w = int(rng.integers(1, mid_h + 1)), 4 * int(rng.integers(1, mid_w // 4 + 1))
+            if rng.random() < 0.5:
+                steps.append(("random_crop", out_h, out_w, int(rng.integers(0, 100)), bool(rng.random() < 0.5)))
+            else:
+                steps.append(("center_crop", out_h, out_w))
+        op = rng.integers(0, 4)
+        if op == 1:
+            steps.append(("normalize", MEAN, STD))
+        elif op == 2:
+            steps.append(("affine", tuple(rng.normal(size=3)), tuple(rng.normal(size=3))))
+        elif op == 3:
+            steps.append(("normalize", tuple(rng.uniform(0, 255, 3)), tuple(rng.uniform(0.5, 100, 3))))
+        if kernel_of(K, steps, in_h, in_w) != 10:
+            continue
+        ran += 1
+        n, rows = 6, 5
+        imgs = orc.images(case * 100, n, in_h, in_w)
+        order = rng.integers(0, n, size=rows).astype(np.int64)
+        ids, out = run_chain(K, steps, torch.from_numpy(imgs).cuda(), torch.from_numpy(order).cuda(), rows)
+        for j in range(rows):
+            want = orc.chain(imgs[order[j]], int(order[j]), steps)
+            assert np.array_equal(out[j].view(np.uint32), want.view(np.uint32)), (case, steps, j)
+    assert ran >= 25, ran

@@ -338,7 +338,7 @@ int dp_k_image_chain_batch(const uint8_t* images, int64_t num_images, const int6
 /* (K10, below) or 9 (K9).                                                 */
 int dp_image_chain_kernel(const dp_image_chain* chain, int* kernel);
 /* K10 (k_roll.cu): the resize chains [crop A] -> resize -> [crop B] ->     */
-/*     [one pixel op] whose column map is periodic (win_w : mid_w = 10:7,   */
+/*     [one or two pixel ops] whose column map is periodic (10:7,           */
 /*     8:7, 5:7, 5:4, 9:7, 12:7, 6:7, 4:7, 3:2, 2:1; any other ratio of a   */
 /*     chain with runtime taps), run by                                     */
 /*     dp_k_image_chain_batch / dp_k_resize_normalize_batch: horizontal blends */

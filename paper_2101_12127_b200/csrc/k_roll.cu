@@ -98,6 +98,7 @@ struct RollArgs {
   int stage_stride, stage_bytes, stages;
   int taps_offset, buf_offset, buf_floats;  // smem layout after the stages
   float op_a[3], op_b[3], op_r[3];           // the pixel op: normalize (mean, std, RN(1/std)) or affine (a, b)
+  float op2_a[3], op2_b[3];                  // a second pixel op (affine, or normalize with IEEE division)
   NormConsts nc;                             // opaque 1 / -1 / -0 / -2^23 for the packed ops
   RollIds ids;
 };
@@ -265,7 +266,7 @@ struct RollWarp {
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       sa[c] = a.op_a[c];
-      sb[c] = kOp == 1 ? -a.op_b[c] : a.op_b[c];
+      sb[c] = (kOp & 3) == 1 ? -a.op_b[c] : a.op_b[c];
       sr_[c] = a.op_r[c];
     }
     g_ox1 = g_f1 = -1;
@@ -337,13 +338,26 @@ struct RollWarp {
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         const int i = c * RO::kNPP + j;
+        // kOp = first op + 4 * second op (0 none, 1 proven normalize, 2
+        // affine, 3 IEEE normalize; the second op is never the proven form:
+        // its input is not a blend of bytes)
+        constexpr int kOp0 = kOp & 3, kOp1 = kOp >> 2;
         f32x2 v = k.lerp(A[i], B[i], wy2);
-        if (kOp == 1) v = k.normalize(v, splat2(sa[c]), splat2(sb[c]), splat2(sr_[c]));
-        if (kOp == 2) v = k.add(k.mul(v, splat2(sa[c])), splat2(sb[c]));
+        if (kOp0 == 1) v = k.normalize(v, splat2(sa[c]), splat2(sb[c]), splat2(sr_[c]));
+        if (kOp0 == 2) v = k.add(k.mul(v, splat2(sa[c])), splat2(sb[c]));
+        if (kOp1 == 2 && kOp0 != 3) v = k.add(k.mul(v, splat2(a.op2_a[c])), splat2(a.op2_b[c]));
         f[i] = up2(v);
-        if (kOp == 3) {
+        if (kOp0 == 3) {
           f[i].x = __fdiv_rn(__fsub_rn(f[i].x, a.op_a[c]), a.op_b[c]);
           f[i].y = __fdiv_rn(__fsub_rn(f[i].y, a.op_a[c]), a.op_b[c]);
+          if (kOp1 == 2) {
+            f[i].x = __fadd_rn(__fmul_rn(f[i].x, a.op2_a[c]), a.op2_b[c]);
+            f[i].y = __fadd_rn(__fmul_rn(f[i].y, a.op2_a[c]), a.op2_b[c]);
+          }
+        }
+        if (kOp1 == 3) {
+          f[i].x = __fdiv_rn(__fsub_rn(f[i].x, a.op2_a[c]), a.op2_b[c]);
+          f[i].y = __fdiv_rn(__fsub_rn(f[i].y, a.op2_a[c]), a.op2_b[c]);
         }
         if constexpr (!(kVec && kF % 4 == 0)) {
           const int e0 = RO::e0(i), e1 = RO::e1(i);
@@ -627,7 +641,7 @@ struct RollPlanHost {
 };
 
 bool roll_plan(const dp_image_chain* c, int out_h, int out_w, RollPlanHost& h, bool allow_general) {
-  if (!c->resize || c->num_pre_ops != 0 || c->num_post_ops > 1 || !roll_env("DP_DEV_ROLL", 1)) return false;
+  if (!c->resize || c->num_pre_ops != 0 || c->num_post_ops > 2 || !roll_env("DP_DEV_ROLL", 1)) return false;
   const size_t row_bytes = static_cast<size_t>(c->in_w) * 3;
   if (row_bytes % 16 || out_w % 4) return false;
   RollArgs& a = h.a;
@@ -666,6 +680,11 @@ bool roll_plan(const dp_image_chain* c, int out_h, int out_w, RollPlanHost& h, b
   else if ((allow_general || roll_env("DP_DEV_K4_GENERAL", 0)) && roll_env("DP_DEV_ROLL_GENERAL", 1))
     PO = 8, PI = 0;
   else return false;
+  // two pixel ops: the general form only (one instantiation set)
+  if (c->num_post_ops == 2) {
+    if (!allow_general || !roll_env("DP_DEV_ROLL_GENERAL", 1)) return false;
+    PO = 8, PI = 0;
+  }
   // the pixel op
   int op = 0;
   if (c->num_post_ops == 1) {
@@ -675,6 +694,16 @@ bool roll_plan(const dp_image_chain* c, int out_h, int out_w, RollPlanHost& h, b
       a.op_r[ch] = 1.0f / c->op_b[0][ch];  // RN(1 / std)
     }
     op = c->op_kind[0] == 1 ? 2 : (fast_div_proven(a.op_a, a.op_b) ? 1 : 3);
+  }
+  if (c->num_post_ops == 2) {
+    for (int ch = 0; ch < 3; ++ch) {
+      a.op_a[ch] = c->op_a[0][ch];
+      a.op_b[ch] = c->op_b[0][ch];
+      a.op_r[ch] = 1.0f / c->op_b[0][ch];
+      a.op2_a[ch] = c->op_a[1][ch];
+      a.op2_b[ch] = c->op_b[1][ch];
+    }
+    op = (c->op_kind[0] == 1 ? 2 : (fast_div_proven(a.op_a, a.op_b) ? 1 : 3)) + 4 * (c->op_kind[1] == 1 ? 2 : 3);
   }
   // stripes: output pixel ranges (multiples of 4) whose mid columns span <= 32 periods
   // for every crop-B offset the chain can draw
@@ -764,7 +793,8 @@ int roll_chain_batch(const uint8_t* images, int64_t num_images, const int64_t* o
       case 0: return roll_launch<PO_, PI_, 0>(a, h.smem, stream);                \
       case 1: return roll_launch<PO_, PI_, 1>(a, h.smem, stream);                \
       case 2: return roll_launch<PO_, PI_, 2>(a, h.smem, stream);                \
-      default: return roll_launch<PO_, PI_, 3>(a, h.smem, stream);               \
+      case 3: return roll_launch<PO_, PI_, 3>(a, h.smem, stream);                \
+      default: break;                                                            \
     }                                                                            \
   }
   DP_ROLL(7, 10)
@@ -779,6 +809,17 @@ int roll_chain_batch(const uint8_t* images, int64_t num_images, const int64_t* o
   DP_ROLL(8, 16)
   DP_ROLL(8, 0)
 #undef DP_ROLL
+  if (h.PO == 8 && h.PI == 0) {  // two pixel ops (general form)
+    switch (h.op) {
+      case 1 + 8: return roll_launch<8, 0, 1 + 8>(a, h.smem, stream);
+      case 2 + 8: return roll_launch<8, 0, 2 + 8>(a, h.smem, stream);
+      case 3 + 8: return roll_launch<8, 0, 3 + 8>(a, h.smem, stream);
+      case 1 + 12: return roll_launch<8, 0, 1 + 12>(a, h.smem, stream);
+      case 2 + 12: return roll_launch<8, 0, 2 + 12>(a, h.smem, stream);
+      case 3 + 12: return roll_launch<8, 0, 3 + 12>(a, h.smem, stream);
+      default: break;
+    }
+  }
   return 1;
 }
 

@@ -109,6 +109,17 @@ CASES = {
     "general_ieee": ((80, 48), [("random_crop", 66, 44, 1, False), ("resize", 50, 36),
                                 ("normalize", (0.0, 0.0, 0.0), ADV_STD)], 8, 8),
     "general_wide_two_stripes": ((128, 512), [("resize", 96, 300), ("normalize", MEAN, STD)], 4, 4),
+    # two pixel ops after the resize (general form): cast then affine, affine then normalize (IEEE), proven
+    # normalize then affine, IEEE normalize then IEEE normalize
+    "two_ops_cast_affine": ((80, 80), [("resize", 56, 56), ("normalize", (0, 0, 0), (1, 1, 1)),
+                                       ("affine", (1 / 255, 1 / 255, 1 / 255), (0.0, -0.5, 0.25))], 8, 8),
+    "two_ops_affine_normalize": ((64, 64), [("random_crop", 40, 40, 3, True), ("resize", 56, 56),
+                                            ("affine", (1 / 255, 2 / 255, 0.5), (-0.5, 0.25, 3.0)),
+                                            ("normalize", (0.5, 0.5, 0.5), (0.25, 0.5, 2.0))], 8, 8),
+    "two_ops_normalize_affine": ((96, 96), [("resize", 60, 60), ("normalize", MEAN, STD),
+                                            ("affine", (2.0, 0.5, -1.0), (0.1, 0.2, 0.3))], 8, 8),
+    "two_ops_ieee_ieee": ((80, 48), [("resize", 50, 36), ("normalize", (0.0, 0.0, 0.0), ADV_STD),
+                                     ("normalize", (0.5, 1.0, -2.0), (3.0, 0.75, 1.5))], 8, 8),
 }
 
 
@@ -165,7 +176,9 @@ def test_k10_eligibility(K):
     assert kernel_of(K, [("resize", 100, 100), ("normalize", MEAN, STD)], 64, 64) == 10  # a non-periodic upscale
     assert kernel_of(K, [("normalize", MEAN, STD), ("resize", 56, 56)], 80, 80) == 9
     assert kernel_of(K, [("resize", 56, 56), ("affine", (1, 1, 1), (0, 0, 0)), ("normalize", MEAN, STD)],
-                     80, 80) == 9
+                     80, 80) == 10  # two pixel ops: the general form
+    assert kernel_of(K, [("resize", 56, 56), ("affine", (1, 1, 1), (0, 0, 0)), ("normalize", MEAN, STD),
+                         ("affine", (1, 1, 1), (0, 0, 0))], 80, 80) == 9  # three
 
 
 def test_fast_division_proof_on_device(K):

@@ -480,14 +480,16 @@ def test_host_output_equals_device_output(dp):
         assert (a[0] == b[0]).all() and np.array_equal(a[1], b[1])
 
 
-@pytest.mark.parametrize("op", ["crop", "resize", "rrc"])
+@pytest.mark.parametrize("op", ["crop", "resize", "resize_k4", "rrc"])
 def test_pinned_host_source_equals_device_source(dp, orc, op):
     """Images in pinned host memory (end-to-end runs) go through the same
     TMA kernels as HBM-resident ones (K3 crop, K10 resize / RandomResizedCrop
     chain: cp.async.bulk reads host memory over PCIe) and give the same bits,
     also with the TMA path disabled (generic kernels' 16-byte loads)."""
     imgs = orc.images(0, 64, 80, 80)
-    reg = image_registry(dp, 0, crop=(48, 48)) if op == "crop" else image_registry(dp, 1, crop=(56, 56))
+    reg = (image_registry(dp, 0, crop=(48, 48)) if op == "crop" else
+           image_registry(dp, 1, crop=(60, 60)) if op == "resize_k4" else  # 4:3: K4's TMA path
+           image_registry(dp, 1, crop=(56, 56)))
     reg.register_random_crop_flip("c40", 40, 40, seed=3, flip=True)
     if op == "rrc":
         imgs = orc.images(0, 64, 64, 64)
@@ -498,7 +500,7 @@ def test_pinned_host_source_equals_device_source(dp, orc, op):
         os.environ["DP_DEV_TMA_HOST"] = tma
         try:
             d = dp.Dataset.tensor_slices(reg, src).shuffle(20, 1)
-            d = d.map("crop") if op == "crop" else d.map("resize") if op == "resize" else d.map("c40").map("resize")
+            d = d.map("crop") if op == "crop" else d.map("c40").map("resize") if op == "rrc" else d.map("resize")
             g, _ = d.map("norm").batch(10).optimize()
             out.append(drain(dp.make_iterator(g, seed_override=2), comps=(0, 1)))
         finally:

@@ -283,7 +283,7 @@ class DevicePipeline {
                            "K5 padded_batches",     "K1 gather_affine_batch",       "K9 image_chain_batch",
                            "K9 gather_copy_batch"};
     std::string kernel = kinds[static_cast<int>(L_.kind)];
-    int k10 = 0;  // a resize chain over a periodic column map on HBM-resident images: K10
+    int k10 = 0;  // resize chains K10 takes (dp_image_chain_kernel)
     if (L_.kind == BatchKind::kChain && dp_image_chain_kernel(&L_.img_chain, &k10) == DP_OK && k10 == 10)
       kernel = "K10 image_chain_roll (via K9 image_chain_batch)";
     if (L_.kind == BatchKind::kResize) {

@@ -40,5 +40,5 @@ for name, steps in [("center crop 224 (u8)", [("center_crop", 224, 224)]),
         e1.synchronize()
         best = min(best, e0.elapsed_time(e1))
     alg = rows * (oh.value * ow.value * 3 * (1 + el))
-    print(f"{name:32s} {best:.3f} ms  {rows / best / 1e3:.2f} M img/s  {alg / best / 1e9:.0f} GB/s  "
-          f"frac {alg / best / 1e9 / 6457:.2f}", flush=True)
+    print(f"{name:32s} {best:.3f} ms  {rows / best / 1e3:.2f} M img/s  {alg / best / 1e6:.0f} GB/s  "
+          f"frac {alg / best / 1e6 / 6457:.2f}", flush=True)

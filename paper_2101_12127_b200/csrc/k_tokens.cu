@@ -203,7 +203,17 @@ padded_batch_kernel(const int32_t* __restrict__ tokens, const int64_t* __restric
 // (position, length, offset, lmax, destination) once, in parallel, into
 // shared memory; then each warp streams its rows with kLoadsInFlight token
 // loads per lane issued before their stores.
-constexpr int kRowTile = 128;
+#ifndef DP_TOK_TILE
+#define DP_TOK_TILE 128
+#endif
+constexpr int kRowTile = DP_TOK_TILE;
+// padded batches: 64-row tiles (twice the CTAs, each preamble half as long;
+// tile sweep 64 / 128 / 256: 0.92 / 0.89 / 0.86 of HBM on cfg4, while the
+// ragged kernel stays best at 128)
+#ifndef DP_TOK_PAD_TILE
+#define DP_TOK_PAD_TILE 64
+#endif
+constexpr int kPadTile = DP_TOK_PAD_TILE;
 #ifndef DP_TOK_LOADS
 #define DP_TOK_LOADS 16
 #endif
@@ -217,10 +227,10 @@ padded_batches_kernel(const int32_t* __restrict__ tokens, const int64_t* __restr
                       const int32_t* __restrict__ lengths, const int64_t* __restrict__ order, int64_t first_row,
                       int64_t rows, int64_t batch, const int32_t* __restrict__ lmax, const int64_t* __restrict__ boff,
                       int32_t pad, int32_t* __restrict__ out, int32_t* __restrict__ out_lengths) {
-  __shared__ int64_t s_src[kRowTile], s_dst[kRowTile];
-  __shared__ int32_t s_len[kRowTile], s_lm[kRowTile];
-  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * kRowTile;
-  const int n = static_cast<int>(rows - r0 < kRowTile ? rows - r0 : kRowTile);
+  __shared__ int64_t s_src[kPadTile], s_dst[kPadTile];
+  __shared__ int32_t s_len[kPadTile], s_lm[kPadTile];
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * kPadTile;
+  const int n = static_cast<int>(rows - r0 < kPadTile ? rows - r0 : kPadTile);
   const int64_t j0 = first_row / batch;
   for (int t = threadIdx.x; t < n; t += kThreads) {
     const int64_t R = first_row + r0 + t, j = R / batch;
@@ -401,7 +411,7 @@ extern "C" int dp_k_padded_batches(const int32_t* tokens, const int64_t* offsets
                                    int32_t* out_lengths, void* stream) {
   if (rows < 0 || batch < 1) return fail(DP_ERR_INVALID_ATTR, "padded_batches: bad rows/batch");
   if (rows == 0) return DP_OK;
-  const int64_t blocks = (rows + kRowTile - 1) / kRowTile;
+  const int64_t blocks = (rows + kPadTile - 1) / kPadTile;
   if (blocks > 0x7fffffff) return fail(DP_ERR_INVALID_ATTR, "padded_batches: too many rows");
   padded_batches_kernel<<<static_cast<int>(blocks), kThreads, 0, as_stream(stream)>>>(
       tokens, offsets, lengths, order, first_row, rows, batch, lmax_dev, boff_dev, pad_value, out, out_lengths);

@@ -214,6 +214,13 @@ constexpr int kRowTile = DP_TOK_TILE;
 #define DP_TOK_PAD_TILE 64
 #endif
 constexpr int kPadTile = DP_TOK_PAD_TILE;
+#ifndef DP_TOK_RAGGED_THREADS
+#define DP_TOK_RAGGED_THREADS 256
+#endif
+#ifndef DP_TOK_RAGGED_TILE
+#define DP_TOK_RAGGED_TILE 128
+#endif
+constexpr int kRaggedThreads = DP_TOK_RAGGED_THREADS, kRaggedTile = DP_TOK_RAGGED_TILE;
 #ifndef DP_TOK_LOADS
 #define DP_TOK_LOADS 16
 #endif
@@ -319,17 +326,17 @@ len_prefix_apply_kernel(const int32_t* __restrict__ lengths, const int64_t* __re
 // row R's tokens go to values[prefix[R] - prefix[first_row]]; batch j's
 // row splits (rows_j + 1 int64, relative to the batch) follow the splits of
 // the batches before it in the launch group.  Row tiles as padded_batches.
-__global__ void __launch_bounds__(kThreads, DP_TOK_MINB)
+__global__ void __launch_bounds__(kRaggedThreads, DP_TOK_MINB)
 ragged_batches_kernel(const int32_t* __restrict__ tokens, const int64_t* __restrict__ offsets,
                       const int32_t* __restrict__ lengths, const int64_t* __restrict__ order, int64_t first_row,
                       int64_t rows, int64_t batch, int64_t n_rows, const int64_t* __restrict__ prefix,
                       int32_t* __restrict__ values, int64_t* __restrict__ splits) {
-  __shared__ int64_t s_src[kRowTile], s_dst[kRowTile];
-  __shared__ int32_t s_len[kRowTile];
-  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * kRowTile;
-  const int n = static_cast<int>(rows - r0 < kRowTile ? rows - r0 : kRowTile);
+  __shared__ int64_t s_src[kRaggedTile], s_dst[kRaggedTile];
+  __shared__ int32_t s_len[kRaggedTile];
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * kRaggedTile;
+  const int n = static_cast<int>(rows - r0 < kRaggedTile ? rows - r0 : kRaggedTile);
   const int64_t j0 = first_row / batch, base = prefix[first_row];
-  for (int t = threadIdx.x; t < n; t += kThreads) {
+  for (int t = threadIdx.x; t < n; t += kRaggedThreads) {
     const int64_t R = first_row + r0 + t, j = R / batch, r = R - j * batch;
     const int64_t p = order ? __ldcs(order + R) : R;
     const int32_t len = lengths[p];
@@ -343,7 +350,7 @@ ragged_batches_kernel(const int32_t* __restrict__ tokens, const int64_t* __restr
   }
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  constexpr int kW = kThreads / 32;
+  constexpr int kW = kRaggedThreads / 32;
   for (int t = threadIdx.x >> 5; t < n; t += 2 * kW) {  // rows t and t + kW
     const int b = t + kW, has_b = b < n;
     const int la = s_len[t], lb = has_b ? s_len[b] : 0;
@@ -517,9 +524,9 @@ extern "C" int dp_k_ragged_batches(const int32_t* tokens, const int64_t* offsets
   if (rows < 0 || batch < 1 || first_row < 0 || first_row + rows > n_rows)
     return fail(DP_ERR_INVALID_ATTR, "ragged_batches: bad rows/batch");
   if (rows == 0) return DP_OK;
-  const int64_t blocks = (rows + kRowTile - 1) / kRowTile;
+  const int64_t blocks = (rows + kRaggedTile - 1) / kRaggedTile;
   if (blocks > 0x7fffffff) return fail(DP_ERR_INVALID_ATTR, "ragged_batches: too many rows");
-  ragged_batches_kernel<<<static_cast<int>(blocks), kThreads, 0, as_stream(stream)>>>(
+  ragged_batches_kernel<<<static_cast<int>(blocks), kRaggedThreads, 0, as_stream(stream)>>>(
       tokens, offsets, lengths, order, first_row, rows, batch, n_rows, prefix, values, splits);
   return launch_status("ragged_batches");
 }

@@ -98,9 +98,11 @@ struct Slot {
   bool release_recorded = false;
   // group bookkeeping
   int64_t first_batch = 0, num_batches = 0;
-  std::atomic<int64_t> handed_out{0};
+  std::atomic<int64_t> handed_out{0};  // written by the GetNext thread only
   int64_t units = 0;  // what GetNext hands out from this slot: batches, or elements when unbatched
-  std::atomic<int64_t> outstanding{0};
+  // The group's lease: every handed-out unit holds a copy, the iterator holds
+  // one until the last unit goes out (see Lease); set at issue.
+  std::shared_ptr<void> lease;
   bool busy = false;
   std::vector<int64_t> batch_off_a, batch_off_b, batch_rows, batch_cols;
   ~Slot() {
@@ -172,6 +174,11 @@ class DevicePipeline {
 
   ~DevicePipeline() {
     DeviceGuard g(opt_.device);
+    {
+      std::lock_guard lk(shared_->mu);
+      shared_->alive = false;
+    }
+    for (auto& sl : slots_) sl->lease.reset();  // groups not fully handed out
     try {
       JoinPendingPlan();
     } catch (...) {  // an error of a plan nobody asked for: dropped with the pipeline
@@ -1025,7 +1032,19 @@ class DevicePipeline {
       slot->num_batches = nb;
       slot->units = nb;  // unbatched: set to the element count below
       slot->handed_out = 0;
-      slot->outstanding = 0;
+      slot->lease = std::shared_ptr<void>(
+          nullptr,
+          [slot_ref = slot, consumer = consumer_, shared = shared_](void*) {
+            // the last holder of the group is gone: every unit was handed out
+            // and dropped.  Record the release (one API call per group).
+            std::lock_guard lk(shared->mu);
+            if (shared->alive && !slot_ref->release_recorded) {
+              cudaEventRecord(slot_ref->release, consumer);
+              slot_ref->release_recorded = true;
+              shared->slots_freed.fetch_add(1, std::memory_order_release);
+            }
+          },
+          PoolAllocator<char>());
     }
     const auto tA = std::chrono::steady_clock::now();
     dbg_[3] += std::chrono::duration<double>(tA - t0).count();
@@ -1256,34 +1275,18 @@ class DevicePipeline {
     return 0;
   }
 
-  // A lease on `slot` for one handed-out unit.  Lock-free on the per-batch
-  // path: `outstanding` goes up before `handed_out`, so the drop that brings
-  // `outstanding` to 0 after the slot's last unit was handed out is the only
-  // one that sees both; it records the release event (one API call per
-  // group) under the lock.  The slot is reused only after that (TryIssueGroup),
-  // and the event orders every unit's consumer-stream work before the rewrite.
+  // A lease on `slot` for one handed-out unit: a copy of the group's lease,
+  // and for the group's last unit the iterator's own reference, moved.  The
+  // group's deleter therefore runs on the drop of whichever unit goes last,
+  // never before the last unit was handed out, and records the release event
+  // under the lock; the slot is reused only after that (FindFreeSlot /
+  // TryIssueGroup), and the event orders every unit's consumer-stream work
+  // before the rewrite.  Per unit: one refcount increment, no allocation.
   std::shared_ptr<void> Lease(const std::shared_ptr<Slot>& slot) {
-    slot->outstanding.fetch_add(1);
-    slot->handed_out.fetch_add(1);
-    return std::shared_ptr<void>(
-        nullptr,
-        [slot, consumer = consumer_, shared = shared_](void*) {
-          if (slot->outstanding.fetch_sub(1) == 1 && slot->handed_out.load() == slot->units) {
-            // Re-checked under the lock: a Lease() of the group's last unit
-            // may have run between the fetch_sub and the handed_out load (its
-            // outstanding++ precedes its handed_out++, so it is visible here);
-            // that unit's own drop releases the slot.  Every drop that reaches
-            // outstanding == 0 after the last hand-out gets here, and the
-            // first one under the lock records the event.
-            std::lock_guard lk(shared->mu);
-            if (shared->alive && !slot->release_recorded && slot->outstanding.load() == 0) {
-              cudaEventRecord(slot->release, consumer);
-              slot->release_recorded = true;
-              shared->slots_freed.fetch_add(1, std::memory_order_release);
-            }
-          }
-        },
-        PoolAllocator<char>());
+    const int64_t h = slot->handed_out.load(std::memory_order_relaxed) + 1;
+    slot->handed_out.store(h, std::memory_order_relaxed);
+    if (h >= slot->units) return std::move(slot->lease);
+    return slot->lease;
   }
 
   Element MakeElement(const std::shared_ptr<Slot>& slot, int64_t i) {

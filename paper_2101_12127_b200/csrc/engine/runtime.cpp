@@ -26,7 +26,7 @@
 // consecutive batches (a power of two near 3.2 GB of output -- 16 cfg2
 // batches; padded kinds: the whole epoch).  GetNext keeps `depth` groups in
 // flight on the iterator's stream and returns batch i as an Element of device
-// Tensor views whose owner is a lease on the slot; the slot is rewritten only
+// Tensor views whose owner is the group's lease on the slot; the slot is rewritten only
 // after every batch of its group was handed out and dropped, and after
 // consumer-stream work queued before the drop (one release event per group).
 // `depth` = the prefetch buffer_size, or for AUTOTUNE a value chosen from the
@@ -207,8 +207,8 @@ class DevicePipeline {
     if (rb_host_) cudaFreeHost(rb_host_);
   }
 
-  // The per-batch fast path makes no CUDA call and takes one lock (in
-  // MakeElement): issuing, slot reuse, autotuning and the consumer-stream wait
+  // The per-batch fast path makes no CUDA call and takes no lock (the
+  // group's lease is copied, see Lease): issuing, slot reuse, autotuning and the consumer-stream wait
   // happen at group boundaries, or when a released slot may let the next
   // group go out (Shared::slots_freed).
   std::optional<Element> Next() {

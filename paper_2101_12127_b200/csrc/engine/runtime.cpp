@@ -266,15 +266,17 @@ class DevicePipeline {
   }
 
   double dbg_[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int64_t plans_built_ = 0;
   void PrintDebugTiming() const {
     if (!std::getenv("DP_DEBUG_TIMING") || produced_ == 0) return;
     std::fprintf(stderr,
                  "[dp timing] per GetNext (us): issue %.1f autotune %.1f element %.1f | per group: find %.1f plan %.1f "
-                 "launch %.1f events %.1f (%lld groups)\n",
+                 "launch %.1f events %.1f (%lld groups) | prefetched plan build %.1f (%lld plans)\n",
                  1e6 * dbg_[0] / produced_, 1e6 * dbg_[1] / produced_, 1e6 * dbg_[2] / produced_,
                  1e6 * dbg_[3] / std::max<int64_t>(issued_count_, 1), 1e6 * dbg_[4] / std::max<int64_t>(issued_count_, 1),
                  1e6 * dbg_[5] / std::max<int64_t>(issued_count_, 1), 1e6 * dbg_[6] / std::max<int64_t>(issued_count_, 1),
-                 static_cast<long long>(issued_count_));
+                 static_cast<long long>(issued_count_), 1e6 * dbg_[7] / std::max<int64_t>(plans_built_, 1),
+                 static_cast<long long>(plans_built_));
   }
 
   int64_t delivered() const { return produced_; }
@@ -533,8 +535,12 @@ class DevicePipeline {
       DeviceGuard g(opt_.device);
       EpochPlan p;
       p.epoch = e;
+      const auto t0 = std::chrono::steady_clock::now();
       BuildPlan(p, e);
+      const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
       std::lock_guard lk(plans_mu_);
+      dbg_[7] += dt;  // helper-thread plan build time (DP_DEBUG_TIMING)
+      plans_built_++;
       plans_.emplace(e, std::move(p));
     });
   }

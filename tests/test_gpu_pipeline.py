@@ -356,6 +356,33 @@ def test_consumer_may_hold_batches(dp):
     assert ids.tolist() == list(range(300))
 
 
+@pytest.mark.parametrize("launch_batches", [1, 3, 4])
+def test_group_lease_keeps_held_batches_intact(dp, launch_batches):
+    """One lease per launch group: a batch held anywhere in a group (first,
+    middle, last) keeps the whole group's slot from being rewritten while
+    the iterator runs on through later groups and a second epoch; the other
+    batches are dropped as they come, so the rest of the ring is reused."""
+    reg = image_registry(dp, 0, crop=(24, 24))
+    src = dp.Source.synthetic_images(640, 32, 32)
+    g, _ = dp.Dataset.tensor_slices(reg, src).shuffle(200, 9).map("crop").map("norm").batch(16).repeat(2).prefetch(2).optimize()
+    ref = drain(dp.make_iterator(g, seed_override=3, launch_batches=launch_batches), comps=(0, 1))
+    assert len(ref) == 80
+    it = dp.make_iterator(g, seed_override=3, launch_batches=launch_batches)
+    held, k = {}, 0
+    while (b := it.get_next()) is not None:
+        if k % 7 in (0, 3) or k == 39:
+            held[k] = b
+        else:
+            np.testing.assert_array_equal(b.numpy(1), ref[k][1])
+            b.release()
+        k += 1
+    assert k == 80
+    for k, b in held.items():  # read only now, after 80 batches went past
+        np.testing.assert_array_equal(b.numpy(0), ref[k][0])
+        np.testing.assert_array_equal(b.numpy(1), ref[k][1])
+        b.release()
+
+
 def test_concurrent_get_next_callers(dp):
     """PipelineIterator::GetNext is thread-safe for concurrent callers
     (runtime.hpp:53-55): 4 threads draining one iterator get every batch

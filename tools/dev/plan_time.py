@@ -24,3 +24,15 @@ for name in sys.argv[1:] or ["cfg4", "cfg4r", "cfg4b"]:
     print(name, "us per epoch", round((time.perf_counter() - t0) / 10 * 1e6, 1), flush=True)
     del it
     sys.stderr.flush()
+
+# per-node self time (CUDA events) over the epochs above: which plan op dominates
+for name in sys.argv[1:] or ["cfg4b"]:
+    cfg = dict(bench.CFG[name])
+    g, _ = bench.build_other_graph(dp, cfg, 0, 0, 1)
+    it = dp.make_iterator(g, seed_override=1)
+    per = int(re.search(r"elements, (\d+) batches", it.describe()).group(1))
+    it.skip(12 * per)
+    torch.cuda.synchronize()
+    for row in it.metrics():
+        print(name, row[1], "self us per epoch", round(row[2] / 12 / 1e3, 1))
+    del it
